@@ -1,0 +1,500 @@
+#!/usr/bin/env python
+"""Benchmark of the SpMxV hot path (arXiv 1203.2739) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c5|c4|c3|c2|c1]
+                    [--impl ours|reference] [--quick]
+
+One JSON line on rank 0.  A "step" is one pass of the whole hot path over the
+workload:
+  c5/c4 (power iterations, BJ configs 5/4): y^ = A^ x^ with the fused max-abs
+        (+ NCCL border-x allgather when N > 1), max all-reduce, x-update;
+  c3    (multiple-SpMxV, BJ config 3): y = sum_k A^k x, fused split pass;
+  c2/c1: one SpMxV with L2 flushed before each call (their matrices fit L2).
+`value` = 2 nnz / step time (GFLOP/s, whole job); `roofline` is the SpMxV
+kernel's algorithmic bytes / its average CUDA-event duration against the
+measured HBM copy peak; `cpu_baseline` times the CPU oracle (test
+infrastructure) on a bounded sample; `e2e` repeats the step through the C ABI
+with the input x copied from pinned host memory and y read back every step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SpMxV GFLOP/s and achieved HBM GB/s (fraction of ~8 TB/s) at 1/2/4/8 B200"
+WORKLOAD_DESC = {
+    "c1": "tiny irregular 2,000^2, U{4..16} nnz/row, identity perms (BJ configs[0])",
+    "c2": "SB 200,000^2, 16 blocks x 12,500 rows, 5% border, hidden perm (BJ configs[1])",
+    "c3": "DB 500,000^2, K=8 nonzero-disjoint 2D-block split, fused multiple-SpMxV (BJ configs[2])",
+    "c4": "power-law 4,000,000^2, Zipf-Mandelbrot rows, 70% +-2,000 band, 100 power iterations (BJ configs[3])",
+    "c5": "SB 64,000,000^2, 64 blocks x 1M rows, 2% border, hidden perm, power iterations (BJ configs[4])",
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# --------------------------------------------------------------------------
+# clocks during the timed region (pynvml sampling thread)
+# --------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, device_index: int, period_s: float = 0.02):
+        self.idx, self.period = device_index, period_s
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:   # pragma: no cover
+            log("clock sampler unavailable:", e)
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------------
+# workload
+# --------------------------------------------------------------------------
+def make_problem(name: str, rank: int, world: int):
+    """Generate (or, for world > 1, share via /dev/shm) the synthetic problem."""
+    import synth
+    if world == 1:
+        return synth.make(name)
+    import pickle
+    import torch.distributed as dist
+    cache = f"/dev/shm/spmv_bench_{name}_{os.environ.get('MASTER_PORT', '0')}"
+    if rank == 0:
+        p = synth.make(name)
+        os.makedirs(cache, exist_ok=True)
+        meta = {}
+        for k in ("row_ptr", "col", "val", "row_perm", "col_perm", "parts", "owner"):
+            a = getattr(p, k)
+            if a is not None:
+                np.save(os.path.join(cache, k + ".npy"), a)
+                meta[k] = True
+        with open(os.path.join(cache, "meta.pkl"), "wb") as f:
+            pickle.dump({"p": {k: v for k, v in p.__dict__.items() if not isinstance(v, np.ndarray)}}, f)
+        dist.barrier()
+        dist.barrier()
+        import shutil
+        shutil.rmtree(cache, ignore_errors=True)
+        return p
+    dist.barrier()
+    with open(os.path.join(cache, "meta.pkl"), "rb") as f:
+        d = pickle.load(f)["p"]
+    for k in ("row_ptr", "col", "val", "row_perm", "col_perm", "parts", "owner"):
+        fn = os.path.join(cache, k + ".npy")
+        d[k] = np.load(fn, mmap_mode="r") if os.path.exists(fn) else None
+    import synth as S
+    p = S.Problem(**d)
+    # touch before the cache dir is removed (pages stay mapped)
+    dist.barrier()
+    return p
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+def load_traffic(workload: str):
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get(workload)
+    except Exception:
+        return None
+
+
+# --------------------------------------------------------------------------
+# CPU baseline: the oracle on a bounded sample (test infrastructure)
+# --------------------------------------------------------------------------
+_XCACHE = {}
+
+
+def oracle_sample(p, target_s: float, nthreads: int, start_row: int = 0, max_rows=None):
+    import oracle
+    if id(p) not in _XCACHE:
+        _XCACHE[id(p)] = p.x()
+    x = _XCACHE[id(p)]
+    rows = min(p.m, 1 << 16) if max_rows is None else max_rows
+    while True:
+        r0 = start_row % p.m
+        r1 = min(p.m, r0 + rows)
+        a, b = int(p.row_ptr[r0]), int(p.row_ptr[r1])
+        rp = np.asarray(p.row_ptr[r0:r1 + 1]) - a
+        col, val = np.asarray(p.col[a:b]), np.asarray(p.val[a:b])
+        t0 = time.perf_counter()
+        oracle.spmv(rp, col, val, x, nthreads=nthreads)
+        dt = time.perf_counter() - t0
+        if dt >= target_s or r1 - r0 >= p.m or max_rows is not None:
+            return {"rows": r1 - r0, "nnz": b - a, "seconds": dt, "gflops": 2.0 * (b - a) / dt / 1e9,
+                    "row_range": [r0, r1]}
+        rows = int(min(p.m, max(rows * 2, rows * target_s / max(dt, 1e-3) * 1.1)))
+
+
+def cpu_leg(args, p, split, x_gpu, y_gpu):
+    """The only place the timed arm touches oracle/: the CPU baseline and the
+    sampled, teacher-forced parity check of the last timed step."""
+    import oracle
+    cpu = parity = None
+    if not args.no_cpu_baseline:
+        nthreads = os.cpu_count() or 1
+        r = oracle_sample(p, args.cpu_seconds, nthreads)
+        cpu = {"value": r["gflops"], "unit": "GFLOP/s", "cores": nthreads, "kind": "oracle",
+               "sample": f"{r['rows']} consecutive original-order rows ({r['nnz']} nnz) of {args.workload}, "
+                         f"oracle.spmv (serial per-row fp64, rows over {nthreads} threads), {r['seconds']:.1f} s"}
+    if not args.no_parity and x_gpu is not None:
+        rng = np.random.default_rng(1234)
+        nsamp = min(p.m, args.parity_rows)
+        prow = np.sort(rng.choice(p.m, nsamp, replace=False))          # permuted rows checked
+        x_orig = x_gpu[p.col_perm] if p.col_perm is not None else x_gpu  # x[j] = x^[col_perm[j]]
+        if p.row_perm is not None:
+            inv = np.empty_like(p.row_perm)
+            inv[p.row_perm] = np.arange(p.m, dtype=p.row_perm.dtype)
+            orow = inv[prow]
+        else:
+            orow = prow
+        yref, S = oracle.spmv_rows(orow, p.row_ptr, p.col, p.val, x_orig)
+        if split:
+            yref = oracle.split(p.row_ptr, p.col, p.val, p.parts, p.n_parts, x_orig)[orow]
+        nbad, worst, _ = oracle.check(y_gpu[prow], yref, S)
+        parity = {"rows_checked": int(nsamp), "failures": int(nbad), "max_err_over_S": worst,
+                  "tol": 1e-12, "teacher_forced": True}
+    return cpu, parity
+
+
+# --------------------------------------------------------------------------
+# reference arm: the oracle as it stands, on the host cores
+# --------------------------------------------------------------------------
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    p = make_problem(args.workload, 0, 1)
+    nthreads = os.cpu_count() or 1
+    import oracle
+    # calibrate a per-step sample of ~1 s (bounded), then time W + K steps
+    cal = oracle_sample(p, 1.0, nthreads)
+    rows = cal["rows"]
+    for w in range(args.warmup):
+        oracle_sample(p, 0, nthreads, start_row=w * rows, max_rows=rows)
+    tot_nnz, tot_s = 0, 0.0
+    for k in range(args.steps):
+        r = oracle_sample(p, 0, nthreads, start_row=(args.warmup + k) * rows, max_rows=rows)
+        tot_nnz += r["nnz"]
+        tot_s += r["seconds"]
+    gf = 2.0 * tot_nnz / tot_s / 1e9
+    sample = f"{args.steps} steps x {rows} consecutive original-order rows of {args.workload} (oracle.spmv, {nthreads} threads)"
+    line = {"impl": "reference", "metric": METRIC, "value": gf, "unit": "GFLOP/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_s / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": args.workload, "desc": WORKLOAD_DESC[args.workload]},
+            "cpu_baseline": {"value": gf, "unit": "GFLOP/s", "cores": nthreads, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": gf, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    del oracle
+    return 0
+
+
+# --------------------------------------------------------------------------
+# our arm
+# --------------------------------------------------------------------------
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import paper_1203_2739_b200 as sp
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+    t0 = time.time()
+    p = make_problem(args.workload, rank, world)
+    t_gen = time.time() - t0
+    uid = None
+    if world > 1:
+        obj = [sp.spmv_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    t0 = time.time()
+    split = p.parts is not None
+    h = sp.spmv_create(p.m, p.n, p.row_ptr, p.col, p.val, row_perm=p.row_perm, col_perm=p.col_perm,
+                       blocks=p.blocks, parts=p.parts, n_parts=p.n_parts,
+                       dist=None if world == 1 else dict(rank=rank, world=world, device=local_rank,
+                                                         nccl_unique_id=uid))
+    t_create = time.time() - t0
+    info = sp.spmv_get_info(h)
+    log(f"[rank {rank}] gen {t_gen:.1f}s create {t_create:.1f}s nnz {p.nnz} local {info['nnz_local']} "
+        f"tiles {info['n_tiles']} long {info['n_long_rows']}")
+
+    # x^ (permuted, this rank's layout)
+    x = p.x()
+    xhat = np.empty_like(x)                 # input preparation: x^[col_perm[j]] = x[j]
+    if p.col_perm is not None:
+        xhat[p.col_perm] = x
+    else:
+        xhat[:] = x
+    if world > 1:
+        a, L = info["x_interior_begin"], info["x_interior_len"]
+        b, Lb = info["x_border_begin"], info["x_border_len"]
+        xloc = np.concatenate([xhat[a:a + L], xhat[b:b + Lb]])
+    else:
+        xloc = xhat
+    xd = torch.from_numpy(np.ascontiguousarray(xloc)).to(dev)
+    x_in = xd.clone()
+    yd = torch.empty(info["m_local"], dtype=torch.float64, device=dev)
+    md = torch.zeros(1, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream()
+    power = args.workload in ("c4", "c5") and info["has_owner_map"]
+    l2_flush = args.workload in ("c1", "c2", "c3")
+    flush_buf = torch.empty(512 * 1024 * 1024 // 8, dtype=torch.float64, device=dev) if l2_flush else None
+    xbuf = [xd, torch.empty_like(xd)]
+    launches_per_step = 0
+
+    def apply(xcur):
+        if split:
+            sp.spmv_split_apply(h, xcur, yd, sp.SPMV_FUSE_MAXABS if power else 0, stream=stream)
+        else:
+            sp.spmv_apply(h, xcur, yd, sp.SPMV_FUSE_MAXABS if power else 0, stream=stream)
+
+    def glue(xcur, xnext):
+        sp.spmv_maxabs(h, md, stream=stream)
+        sp.spmv_normalize(h, yd, md, xnext, stream=stream)
+
+    launches_per_step = 1 + (2 if power else 0)
+    cur = 0
+    for _ in range(args.warmup):
+        if l2_flush:
+            flush_buf.fill_(1.0)
+        apply(xbuf[cur])
+        if power:
+            glue(xbuf[cur], xbuf[1 - cur])
+            cur = 1 - cur
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    K = args.steps
+    ev_a = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    ev_b = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    st_all = torch.cuda.Event(enable_timing=True)
+    en_all = torch.cuda.Event(enable_timing=True)
+    x_last = None
+    with ClockSampler(local_rank) as clk:
+        st_all.record(stream)
+        for k in range(K):
+            if l2_flush:
+                flush_buf.fill_(1.0)
+            ev_a[k].record(stream)
+            apply(xbuf[cur])
+            ev_b[k].record(stream)
+            if power:
+                if k == K - 1:
+                    x_last = xbuf[cur]
+                glue(xbuf[cur], xbuf[1 - cur])
+                cur = 1 - cur
+        en_all.record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    spmv_ms = [a.elapsed_time(b) for a, b in zip(ev_a, ev_b)]
+    total_ms = st_all.elapsed_time(en_all)
+    if l2_flush:   # the flush is not part of the path: step time = SpMxV time
+        total_ms = sum(spmv_ms)
+    avg_spmv_ms = sum(spmv_ms) / K
+    if dist:
+        t = torch.tensor([total_ms, avg_spmv_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, avg_spmv_max = t.tolist()
+    else:
+        avg_spmv_max = avg_spmv_ms
+    ms_per_step = total_ms / K
+    gflops = 2.0 * p.nnz / (ms_per_step * 1e-3) / 1e9
+
+    # device copies of the last step's x_t and y_t for the CPU leg's parity check
+    if not power:
+        x_last = xbuf[cur]
+    y_gpu = yd.cpu().numpy() if world == 1 else None
+    x_gpu = x_last.cpu().numpy() if world == 1 else None
+
+    # ---------------- e2e through the C ABI with host buffers
+    e2e = None
+    if not args.no_e2e:
+        hx = torch.from_numpy(np.ascontiguousarray(xloc)).pin_memory()
+        hy = torch.empty(info["m_local"], dtype=torch.float64).pin_memory()
+        hm = torch.empty(1, dtype=torch.float64).pin_memory()
+        Ke = max(3, min(K, args.e2e_steps))
+        for _ in range(2):
+            xbuf[0].copy_(hx, non_blocking=True)
+            apply(xbuf[0])
+            if power:
+                glue(xbuf[0], xbuf[1])
+            hy.copy_(yd, non_blocking=True)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(Ke):
+            xbuf[0].copy_(hx, non_blocking=True)
+            apply(xbuf[0])
+            if power:
+                glue(xbuf[0], xbuf[1])
+                hm.copy_(md, non_blocking=True)
+            hy.copy_(yd, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1) / Ke
+        if dist:
+            t = torch.tensor([ems], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = t.item()
+        e2e = {"value": 2.0 * p.nnz / (ems * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": ems,
+               "h2d_bytes_per_step": int(hx.numel() * 8), "d2h_bytes_per_step": int(hy.numel() * 8 + (8 if power else 0)),
+               "steps": Ke}
+
+    # ---------------- roofline of the SpMxV kernel
+    peaks, peak_src = load_peaks()
+    bytes_alg = info["bytes_alg_split"] if split else info["bytes_alg"]
+    if dist:
+        t = torch.tensor([bytes_alg], dtype=torch.float64, device=dev)
+        dist.all_reduce(t)
+        bytes_tot = t.item()
+    else:
+        bytes_tot = bytes_alg
+    achieved = bytes_alg / (avg_spmv_ms * 1e-3) / 1e9       # this rank's kernel
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    tr = load_traffic(args.workload)
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved / hbm_peak, "traffic": tr.get("dram_bytes_per_launch") if tr else None,
+                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src}, copy read+write)",
+                "bytes_alg_per_launch": bytes_alg, "kernel_ms": avg_spmv_ms,
+                "frac_of_8TBs": achieved / 8000.0}
+
+    # ---------------- CPU leg (rank 0, N = 1 only): oracle baseline + sampled parity
+    cpu, parity = None, None
+    if rank == 0 and world == 1:
+        cpu, parity = cpu_leg(args, p, split, x_gpu, y_gpu)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": gflops, "unit": "GFLOP/s", "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.workload, "desc": WORKLOAD_DESC[args.workload],
+                       "m": p.m, "n": p.n, "nnz": p.nnz,
+                       "step": ("SpMxV+maxabs+x-update (power iteration)" if power else
+                                "fused multiple-SpMxV" if split else "SpMxV"),
+                       "l2": ("flushed (512 MB write) before every SpMxV; step time = SpMxV time" if l2_flush
+                              else f"inputs larger than L2 ({bytes_tot / 1e9:.1f} GB vs 126 MB)"),
+                       "parallelism": f"sb-rowblock{world}" if world > 1 else "1gpu"},
+            "hbm_gbs": bytes_tot / (avg_spmv_max * 1e-3) / 1e9,
+            "spmv_ms": avg_spmv_max,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches_per_step * K,
+            "clocks": clk.summary(),
+            "parity": parity,
+            "setup_s": {"generate": t_gen, "create": t_create},
+        }
+        print(json.dumps(line), flush=True)
+    sp.spmv_destroy(h)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=None)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="c5", choices=sorted(WORKLOAD_DESC))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--parity-rows", type=int, default=200000)
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    args = ap.parse_args()
+    if args.steps is None:
+        args.steps = {"c5": 50, "c4": 100, "c3": 100, "c2": 100, "c1": 100}[args.workload]
+    if args.warmup < 3:
+        raise SystemExit("--warmup must be >= 3")
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if world != args.gpus:
+        log(f"note: WORLD_SIZE={world} but --gpus {args.gpus}; using WORLD_SIZE")
+        args.gpus = world
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        if args.impl == "reference":
+            rc = run_reference(args, rank, world)
+        else:
+            rc = run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+    return rc
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,94 @@
+"""Build libspmv_b200.so in-tree (nvcc for sm_100a + g++), no torch involved.
+
+    python -m paper_1203_2739_b200.build [--force] [--verbose]
+
+The CUDA runtime is linked statically (the library is built with nvcc 12.9;
+torch in the same process carries its own 12.8 runtime), NCCL is the venv's
+libnccl.so.2 that torch itself loads (one NCCL per process), found by rpath.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+import sysconfig
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+BUILD = os.path.join(HERE, "_build")
+LIB = os.path.join(HERE, "libspmv_b200.so")
+CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+NVCC = os.path.join(CUDA, "bin", "nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _nccl_dir() -> str:
+    for base in [sysconfig.get_paths()["purelib"], sysconfig.get_paths()["platlib"]]:
+        d = os.path.join(base, "nvidia", "nccl")
+        if os.path.exists(os.path.join(d, "include", "nccl.h")):
+            return d
+    raise RuntimeError("venv NCCL (nvidia/nccl) not found")
+
+
+SOURCES = {
+    "kernels.cu": "cu",
+    "host.cpp": "cpp",
+}
+HEADERS = ["internal.h", os.path.join("..", "..", "include", "spmv.h")]
+
+
+def _newer(target: str, deps) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    os.makedirs(BUILD, exist_ok=True)
+    nccl = _nccl_dir()
+    inc = ["-I" + CSRC, "-I" + os.path.join(ROOT, "include"), "-I" + os.path.join(nccl, "include"),
+           "-I" + os.path.join(CUDA, "include")]
+    hdrs = [os.path.join(CSRC, h) for h in HEADERS]
+    objs = []
+    for src, kind in SOURCES.items():
+        s = os.path.join(CSRC, src)
+        o = os.path.join(BUILD, src + ".o")
+        objs.append(o)
+        if not force and not _newer(o, [s, __file__] + hdrs):
+            continue
+        if kind == "cu":
+            cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+                   "--expt-relaxed-constexpr", "-Xptxas", "-v", "-c", s, "-o", o, *inc]
+        else:
+            cmd = ["g++", "-O2", "-std=c++17", "-fPIC", "-fopenmp", "-Wall", "-Wno-unused-function",
+                   "-c", s, "-o", o, *inc]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if verbose or r.returncode:
+            sys.stdout.write(r.stdout)
+            sys.stdout.write(r.stderr)
+        if r.returncode:
+            raise RuntimeError(f"compile failed: {src}")
+    if force or _newer(LIB, objs):
+        tmp = LIB + f".tmp{os.getpid()}"
+        nccl_lib = os.path.join(nccl, "lib")
+        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs,
+               "-Xcompiler", "-fopenmp", "-lgomp",
+               "-L" + nccl_lib, "-Xlinker", "-l:libnccl.so.2",
+               "-Xlinker", "-rpath," + nccl_lib]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode:
+            sys.stdout.write(r.stdout + r.stderr)
+            raise RuntimeError("link failed")
+        os.replace(tmp, LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose="--verbose" in sys.argv or "-v" in sys.argv)
+    print(LIB)

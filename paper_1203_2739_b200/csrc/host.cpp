@@ -1,0 +1,833 @@
+// host.cpp -- the C ABI of include/spmv.h: ingest, validation, permutation,
+// planning, device upload, apply orchestration and the NCCL border exchange.
+//
+// Paper: Akbudak, Kayaaslan & Aykanat, arXiv 1203.2739 (P:Lnn = PAPER.md line).
+//   a1 ingest  : A^ = P_r A P_c, old->new arrays
+//   a2 plan    : SB/DB envelope of Eq.(1)/(5); row tiles;
+//                split segments of Pi; shard of the row-slice
+//                decomposition y_k <- R_k x
+//   a3/a4      : x preparation; border-x exchange over NCCL (coupling columns
+//                are the only input shared between row slices)
+//   a5-a7      : one tile-kernel launch (kernels.cu)
+//   a8         : fused multiple-SpMxV
+//   a9         : max-abs and x-update glue for the power iterations
+#include <algorithm>
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <omp.h>
+
+#include "../../include/spmv.h"
+#include "internal.h"
+
+using spmvb::kTileNnz;
+using spmvb::kTileRows;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+spmv_status_t fail(spmv_status_t s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return s;
+}
+
+#define CUDA_TRY(expr)                                                                        \
+    do {                                                                                      \
+        cudaError_t e_ = (expr);                                                              \
+        if (e_ != cudaSuccess)                                                                \
+            return fail(SPMV_ERR_INTERNAL, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_),  \
+                        __FILE__, __LINE__);                                                  \
+    } while (0)
+
+#define NCCL_TRY(expr)                                                                        \
+    do {                                                                                      \
+        ncclResult_t r_ = (expr);                                                             \
+        if (r_ != ncclSuccess)                                                                \
+            return fail(SPMV_ERR_INTERNAL, "%s: %s (%s:%d)", #expr, ncclGetErrorString(r_),   \
+                        __FILE__, __LINE__);                                                  \
+    } while (0)
+
+constexpr uint32_t kMagic = 0x53504d56u;   // "SPMV"
+constexpr int64_t kPad = 8;                // col/val padding (128-bit quad loads past the end)
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+};
+
+}  // namespace
+
+struct spmv_plan_s {
+    uint32_t magic = kMagic;
+    int device = 0;
+    int rank = 0, world = 1;
+    int kind = 0;                     // 0 none, 1 SB, 2 DB
+    int64_t m = 0, n = 0, nnz = 0;    // global
+    int64_t m_loc = 0, nnz_loc = 0, row_begin = 0;
+    int64_t x_int_begin = 0, x_int_len = 0;     // interior columns (global permuted range)
+    int64_t x_bord_begin = 0, x_bord_len = 0;   // owned border slice (global permuted)
+    int64_t border_begin = 0, border_total = 0; // C_B
+    int64_t x_local_len = 0;
+    int64_t n_tiles = 0, n_long = 0;
+    int32_t n_parts = 0;
+    int64_t n_seg = 0;
+    int64_t bytes_alg = 0, bytes_alg_split = 0;
+    bool has_perm = false;
+    bool has_owner = false;
+
+    // device arrays (one allocation each)
+    int32_t* d_rowptr = nullptr;      // [m_loc+1]
+    int32_t* d_col = nullptr;         // [nnz_loc + pad] local column ids
+    double* d_val = nullptr;          // [nnz_loc + pad]
+    int32_t* d_tile_row = nullptr;    // [T+1]
+    int32_t* d_tile_seg = nullptr;    // [T*K+1]
+    int32_t* d_seg_ptr = nullptr;     // [S+1]
+    int32_t* d_seg_row = nullptr;     // [S]
+    int32_t* d_scol = nullptr;        // [nnz_loc + pad] split stream
+    double* d_sval = nullptr;
+    int32_t* d_colinv = nullptr;      // ORIGINAL mode: x^[c] = x[colinv[c]]
+    int32_t* d_rowperm = nullptr;     // ORIGINAL mode: y[i] = y^[row_perm[i]]
+    double* d_xhat = nullptr;
+    double* d_yhat = nullptr;
+    int32_t* d_owner = nullptr;       // [x_local_len] local col -> local row
+    unsigned long long* d_slots = nullptr;
+    double* d_xborder = nullptr;      // [border_total] gathered x(C_B) (world > 1)
+    double* d_mscratch = nullptr;
+
+    // exchange
+    ncclComm_t comm = nullptr;
+    std::vector<int64_t> bord_off, bord_cnt;   // per rank, offsets inside C_B
+    bool equal_slices = true;
+    std::vector<void*> allocs;
+};
+
+namespace {
+
+template <class T>
+spmv_status_t dalloc(spmv_plan_s* h, T** out, size_t count) {
+    void* p = nullptr;
+    size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess)
+        return fail(SPMV_ERR_INTERNAL, "cudaMalloc(%zu bytes): %s", bytes, cudaGetErrorString(e));
+    h->allocs.push_back(p);
+    *out = static_cast<T*>(p);
+    return SPMV_OK;
+}
+
+template <class T>
+spmv_status_t upload(spmv_plan_s* h, T** out, const T* src, size_t count, size_t alloc_count = 0) {
+    spmv_status_t s = dalloc(h, out, std::max(count, alloc_count));
+    if (s) return s;
+    if (alloc_count > count) CUDA_TRY(cudaMemset(*out, 0, std::max(count, alloc_count) * sizeof(T)));
+    if (count) CUDA_TRY(cudaMemcpy(*out, src, count * sizeof(T), cudaMemcpyHostToDevice));
+    return SPMV_OK;
+}
+
+void free_plan(spmv_plan_s* h) {
+    if (!h) return;
+    cudaSetDevice(h->device);
+    cudaDeviceSynchronize();
+    for (void* p : h->allocs) cudaFree(p);
+    h->allocs.clear();
+    if (h->comm) ncclCommDestroy(h->comm);
+    h->comm = nullptr;
+    h->magic = 0;
+    delete h;
+}
+
+bool valid(spmv_handle_t h) { return h && h->magic == kMagic; }
+
+// Row-tile plan: greedy over rows; a tile holds whole
+// rows with <= kTileNnz nonzeros and <= kTileRows rows; a longer row is a tile
+// of its own (long-row path).  Tiles never cross an SB block boundary
+// (block_row_ptr), so tiles are identical at every world size.
+void plan_tiles(const std::vector<int64_t>& rp, int64_t m_loc, const std::vector<int64_t>& cuts,
+                std::vector<int32_t>& tile_row, int64_t& n_long) {
+    tile_row.clear();
+    n_long = 0;
+    size_t ci = 0;
+    int64_t r = 0;
+    tile_row.push_back(0);
+    while (r < m_loc) {
+        while (ci < cuts.size() && cuts[ci] <= r) ++ci;
+        const int64_t lim = ci < cuts.size() ? std::min<int64_t>(cuts[ci], m_loc) : m_loc;
+        const int64_t len0 = rp[r + 1] - rp[r];
+        if (len0 > kTileNnz) {
+            ++r;
+            ++n_long;
+        } else {
+            const int64_t base = rp[r];
+            int64_t e = r;
+            while (e < lim && e - r < kTileRows && rp[e + 1] - base <= kTileNnz) ++e;
+            r = e;
+        }
+        tile_row.push_back((int32_t)r);
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* spmv_status_string(spmv_status_t s) {
+    switch (s) {
+    case SPMV_OK: return "ok";
+    case SPMV_ERR_USAGE: return "usage error";
+    case SPMV_ERR_DATA: return "data error";
+    case SPMV_ERR_INTERNAL: return "internal error";
+    case SPMV_ERR_UNSUPPORTED: return "unsupported";
+    }
+    return "unknown status";
+}
+
+const char* spmv_last_error(void) { return g_last_error.c_str(); }
+
+int32_t spmv_version(void) { return 100; }
+
+spmv_status_t spmv_nccl_unique_id(void* out, size_t len) {
+    if (!out || len < sizeof(ncclUniqueId)) return fail(SPMV_ERR_USAGE, "nccl_unique_id: buffer too small");
+    ncclUniqueId id;
+    NCCL_TRY(ncclGetUniqueId(&id));
+    memcpy(out, &id, sizeof id);
+    return SPMV_OK;
+}
+
+spmv_status_t spmv_shard_plan(const spmv_blocks_t* blocks, int64_t m, int64_t n, int32_t rank, int32_t world,
+                              spmv_shard_t* out) {
+    if (!blocks || !out || world < 1 || rank < 0 || rank >= world) return fail(SPMV_ERR_USAGE, "shard_plan: bad arguments");
+    const int K = blocks->K;
+    if (K < 1 || !blocks->row_block_ptr || !blocks->col_block_ptr) return fail(SPMV_ERR_USAGE, "shard_plan: bad blocks");
+    if (world > K) return fail(SPMV_ERR_UNSUPPORTED, "fewer blocks than ranks");
+    const int64_t* rbp = blocks->row_block_ptr;
+    const int64_t* cbp = blocks->col_block_ptr;
+    if (rbp[K + 1] != m || cbp[K + 1] != n) return fail(SPMV_ERR_DATA, "block descriptor does not cover the matrix");
+    const int64_t CB = cbp[K + 1] - cbp[K];
+    auto bo = [&](int k) -> int64_t {
+        return blocks->border_owner_ptr ? blocks->border_owner_ptr[k] : cbp[K] + (CB * k) / K;
+    };
+    auto first_block = [&](int r) { return (int)((int64_t)K * r / world); };
+    memset(out, 0, sizeof *out);
+    out->border_begin = cbp[K];
+    out->border_total = CB;
+    if (world == 1) {
+        out->row_begin = 0;
+        out->row_end = m;
+        out->x_interior_begin = 0;
+        out->x_interior_len = n;
+        out->x_border_begin = cbp[K];
+        out->x_border_len = 0;
+        out->x_local_len = n;
+        out->block_begin = 0;
+        out->block_end = K;
+        return SPMV_OK;
+    }
+    const int b0 = first_block(rank), b1 = first_block(rank + 1);
+    out->block_begin = b0;
+    out->block_end = b1;
+    out->row_begin = rbp[b0];
+    out->row_end = rbp[b1];
+    out->x_interior_begin = cbp[b0];
+    out->x_interior_len = cbp[b1] - cbp[b0];
+    out->x_border_begin = bo(b0);
+    out->x_border_len = bo(b1) - bo(b0);
+    out->x_local_len = out->x_interior_len + out->x_border_len;
+    return SPMV_OK;
+}
+
+static spmv_status_t create_impl(int64_t m, int64_t n, int64_t nnz, const int64_t* row_ptr,
+                                 const int32_t* col_idx, const double* val, const int32_t* row_perm,
+                                 const int32_t* col_perm, const spmv_blocks_t* blocks, int32_t n_parts,
+                                 const int32_t* part_of_nnz, const spmv_dist_t* dist, spmv_plan_s* h) {
+    // ---------------------------------------------------------- arguments
+    if (m < 0 || n < 0 || nnz < 0) return fail(SPMV_ERR_USAGE, "negative dimension");
+    if (!row_ptr) return fail(SPMV_ERR_USAGE, "row_ptr is NULL");
+    if (nnz > 0 && (!col_idx || !val)) return fail(SPMV_ERR_USAGE, "col_idx/val is NULL");
+    if (n_parts < 0 || (n_parts > 0 && !part_of_nnz)) return fail(SPMV_ERR_USAGE, "bad split arguments");
+    if (m > INT32_MAX - 1 || n > INT32_MAX - 1) return fail(SPMV_ERR_UNSUPPORTED, "dimension beyond int32");
+    const int world = dist ? dist->world : 1;
+    const int rank = dist ? dist->rank : 0;
+    if (dist && (world < 1 || rank < 0 || rank >= world || !dist->nccl_unique_id))
+        return fail(SPMV_ERR_USAGE, "bad dist descriptor");
+    if (world > 1 && (!blocks || blocks->kind != SPMV_SB))
+        return fail(SPMV_ERR_UNSUPPORTED, "world > 1 needs an SB block descriptor (DB split sharding is NEXT f1)");
+    h->rank = rank;
+    h->world = world;
+    h->m = m; h->n = n; h->nnz = nnz;
+    h->n_parts = n_parts;
+    h->has_perm = row_perm || col_perm;
+
+    // ------------------------------------------------ CSR structure (a1)
+    if (row_ptr[0] != 0 || row_ptr[m] != nnz) return fail(SPMV_ERR_DATA, "row_ptr[0] != 0 or row_ptr[m] != nnz");
+    {
+        std::atomic<int> bad{0};
+#pragma omp parallel for schedule(static)
+        for (int64_t i = 0; i < m; ++i)
+            if (row_ptr[i + 1] < row_ptr[i]) bad = 1;
+        if (bad) return fail(SPMV_ERR_DATA, "row_ptr not nondecreasing");
+#pragma omp parallel for schedule(static)
+        for (int64_t t = 0; t < nnz; ++t)
+            if (col_idx[t] < 0 || (int64_t)col_idx[t] >= n) bad = 2;
+        if (bad) return fail(SPMV_ERR_DATA, "column index out of range");
+        if (n_parts > 0) {
+#pragma omp parallel for schedule(static)
+            for (int64_t t = 0; t < nnz; ++t)
+                if (part_of_nnz[t] < 0 || part_of_nnz[t] >= n_parts) bad = 3;
+            if (bad) return fail(SPMV_ERR_DATA, "part id outside [0, K)");
+        }
+    }
+    // permutations must be bijections
+    std::vector<int32_t> row_inv(m), col_inv(n);
+    for (int pass = 0; pass < 2; ++pass) {
+        const int32_t* p = pass ? col_perm : row_perm;
+        const int64_t len = pass ? n : m;
+        std::vector<int32_t>& inv = pass ? col_inv : row_inv;
+        if (!p) {
+#pragma omp parallel for schedule(static)
+            for (int64_t i = 0; i < len; ++i) inv[i] = (int32_t)i;
+            continue;
+        }
+        std::fill(inv.begin(), inv.end(), -1);
+        for (int64_t i = 0; i < len; ++i) {
+            if (p[i] < 0 || (int64_t)p[i] >= len || inv[p[i]] != -1)
+                return fail(SPMV_ERR_DATA, "%s permutation is not a bijection", pass ? "column" : "row");
+            inv[p[i]] = (int32_t)i;
+        }
+    }
+
+    // ------------------------------------------------ block descriptor (a2)
+    int K = 0;
+    std::vector<int64_t> rbp, cbp, bop;
+    if (blocks) {
+        K = blocks->K;
+        if ((blocks->kind != SPMV_SB && blocks->kind != SPMV_DB) || K < 1 || !blocks->row_block_ptr ||
+            !blocks->col_block_ptr)
+            return fail(SPMV_ERR_USAGE, "bad block descriptor");
+        rbp.assign(blocks->row_block_ptr, blocks->row_block_ptr + K + 2);
+        cbp.assign(blocks->col_block_ptr, blocks->col_block_ptr + K + 2);
+        if (rbp[0] != 0 || rbp[K + 1] != m || cbp[0] != 0 || cbp[K + 1] != n)
+            return fail(SPMV_ERR_DATA, "block descriptor does not cover the matrix");
+        for (int k = 0; k <= K; ++k)
+            if (rbp[k + 1] < rbp[k] || cbp[k + 1] < cbp[k])
+                return fail(SPMV_ERR_DATA, "block descriptor not nondecreasing");
+        if (blocks->kind == SPMV_SB && rbp[K] != rbp[K + 1])
+            return fail(SPMV_ERR_DATA, "SB form with a non-empty row border");
+        h->kind = blocks->kind;
+        h->border_begin = cbp[K];
+        h->border_total = cbp[K + 1] - cbp[K];
+        bop.resize(K + 1);
+        if (blocks->border_owner_ptr) {
+            for (int k = 0; k <= K; ++k) bop[k] = blocks->border_owner_ptr[k];
+            if (bop[0] != cbp[K] || bop[K] != cbp[K + 1])
+                return fail(SPMV_ERR_DATA, "border_owner_ptr does not cover C_B");
+            for (int k = 0; k < K; ++k)
+                if (bop[k + 1] < bop[k]) return fail(SPMV_ERR_DATA, "border_owner_ptr not nondecreasing");
+        } else {
+            for (int k = 0; k <= K; ++k) bop[k] = cbp[K] + (h->border_total * k) / K;
+        }
+    }
+
+    // --------------------------------------------------- shard
+    spmv_shard_t sh;
+    if (blocks) {
+        spmv_status_t ss = spmv_shard_plan(blocks, m, n, rank, world, &sh);
+        if (ss) return ss;
+    } else {
+        memset(&sh, 0, sizeof sh);
+        sh.row_end = m;
+        sh.x_interior_len = n;
+        sh.x_local_len = n;
+    }
+    if (world > 1) {
+        h->bord_off.resize(world);
+        h->bord_cnt.resize(world);
+        for (int r = 0; r < world; ++r) {
+            spmv_shard_t o;
+            spmv_shard_plan(blocks, m, n, r, world, &o);
+            h->bord_off[r] = o.x_border_begin - o.border_begin;
+            h->bord_cnt[r] = o.x_border_len;
+            if (h->bord_cnt[r] != h->bord_cnt[0]) h->equal_slices = false;
+        }
+    }
+    const int64_t R0 = sh.row_begin, R1 = sh.row_end;
+    h->row_begin = R0;
+    h->m_loc = R1 - R0;
+    h->x_int_begin = sh.x_interior_begin;
+    h->x_int_len = sh.x_interior_len;
+    h->x_bord_begin = sh.x_border_begin;
+    h->x_bord_len = sh.x_border_len;
+    h->x_local_len = sh.x_local_len;
+
+    // ---------------------------------------------- NCCL bootstrap (a4)
+    if (world > 1) {
+        h->device = dist->device;
+        CUDA_TRY(cudaSetDevice(h->device));
+        ncclUniqueId id;
+        memcpy(&id, dist->nccl_unique_id, sizeof id);
+        NCCL_TRY(ncclCommInitRank(&h->comm, world, id, rank));
+    }
+
+    // --------------------------------------- permute the local rows (a1)
+    // new row p has the entries of old row row_inv[p], columns mapped through
+    // col_perm, sorted by new column; duplicates rejected (reading A3).
+    const int64_t m_loc = h->m_loc;
+    std::vector<int64_t> rp(m_loc + 1);
+    rp[0] = 0;
+    for (int64_t p = 0; p < m_loc; ++p) {
+        const int64_t i = row_inv[R0 + p];
+        rp[p + 1] = rp[p] + (row_ptr[i + 1] - row_ptr[i]);
+    }
+    const int64_t nnz_loc = rp[m_loc];
+    h->nnz_loc = nnz_loc;
+    spmv_status_t local_status = SPMV_OK;
+    if (nnz_loc + kPad >= INT32_MAX) local_status = fail(SPMV_ERR_UNSUPPORTED, "shard nnz beyond int32");
+
+    std::vector<int32_t> pcol, lcol;
+    std::vector<double> pval;
+    std::vector<int32_t> ppart;
+    std::vector<int64_t> n_long_rows;
+    if (local_status == SPMV_OK) {
+        pcol.resize(nnz_loc);
+        pval.resize(nnz_loc);
+        if (n_parts) ppart.resize(nnz_loc);
+        std::atomic<int> dup{0}, env{0};
+        const bool sb_env = blocks != nullptr;
+#pragma omp parallel
+        {
+            std::vector<int64_t> idx;
+            std::vector<int32_t> key;
+#pragma omp for schedule(dynamic, 2048)
+            for (int64_t p = 0; p < m_loc; ++p) {
+                const int64_t i = row_inv[R0 + p];
+                const int64_t a = row_ptr[i], L = row_ptr[i + 1] - a;
+                const int64_t o = rp[p];
+                key.resize(L);
+                idx.resize(L);
+                for (int64_t t = 0; t < L; ++t) {
+                    key[t] = col_perm ? col_perm[col_idx[a + t]] : col_idx[a + t];
+                    idx[t] = t;
+                }
+                bool sorted = true;
+                for (int64_t t = 1; t < L; ++t)
+                    if (key[t] < key[t - 1]) { sorted = false; break; }
+                if (!sorted) {
+                    if (L <= 32) {   // insertion sort (stable)
+                        for (int64_t t = 1; t < L; ++t) {
+                            int64_t j = t;
+                            const int64_t v = idx[t];
+                            while (j > 0 && key[idx[j - 1]] > key[v]) { idx[j] = idx[j - 1]; --j; }
+                            idx[j] = v;
+                        }
+                    } else {
+                        std::stable_sort(idx.begin(), idx.end(),
+                                         [&](int64_t u, int64_t v) { return key[u] < key[v]; });
+                    }
+                }
+                for (int64_t t = 0; t < L; ++t) {
+                    const int64_t s = idx[t];
+                    pcol[o + t] = key[s];
+                    pval[o + t] = val[a + s];
+                    if (n_parts) ppart[o + t] = part_of_nnz[a + s];
+                    if (t && pcol[o + t] == pcol[o + t - 1]) dup = 1;
+                }
+                if (sb_env) {   // envelope of Eq.(1)/(5)
+                    const int64_t gp = R0 + p;
+                    const int64_t k = std::upper_bound(rbp.begin(), rbp.begin() + K + 1, gp) - rbp.begin() - 1;
+                    if (k < K) {
+                        for (int64_t t = 0; t < L; ++t) {
+                            const int64_t c = pcol[o + t];
+                            if (!((c >= cbp[k] && c < cbp[k + 1]) || c >= cbp[K])) { env = 1; break; }
+                        }
+                    }
+                }
+            }
+        }
+        if (dup) local_status = fail(SPMV_ERR_DATA, "duplicate (i, j) entry");
+        else if (env) local_status = fail(SPMV_ERR_DATA, "nonzero outside the SB/DB envelope");
+    }
+    if (world > 1) {   // every rank returns the same status
+        int* d_st = nullptr;
+        int st = (int)local_status;
+        CUDA_TRY(cudaMalloc(&d_st, sizeof(int)));
+        CUDA_TRY(cudaMemcpy(d_st, &st, sizeof(int), cudaMemcpyHostToDevice));
+        NCCL_TRY(ncclAllReduce(d_st, d_st, 1, ncclInt32, ncclMax, h->comm, 0));
+        CUDA_TRY(cudaMemcpy(&st, d_st, sizeof(int), cudaMemcpyDeviceToHost));
+        cudaFree(d_st);
+        if (st != SPMV_OK && local_status == SPMV_OK)
+            local_status = fail((spmv_status_t)st, "create failed on another rank");
+    }
+    if (local_status != SPMV_OK) return local_status;
+    if (world == 1) {
+        if (dist) h->device = dist->device;
+        else CUDA_TRY(cudaGetDevice(&h->device));
+        CUDA_TRY(cudaSetDevice(h->device));
+    }
+
+    // -------------------------------------- local column ids (x layout)
+    // world 1: global permuted ids.  world > 1: [interior | full C_B] where
+    // the kernel reads c < x_int_len from the user's x and the rest from the
+    // gathered border buffer.
+    if (world > 1) {
+        const int64_t Q0 = h->x_int_begin, B0 = h->border_begin, nint = h->x_int_len;
+#pragma omp parallel for schedule(static)
+        for (int64_t t = 0; t < nnz_loc; ++t) {
+            const int64_t c = pcol[t];
+            pcol[t] = (int32_t)(c >= B0 ? nint + (c - B0) : c - Q0);
+        }
+    }
+
+    // ------------------------------------------------------ tiles (a2)
+    std::vector<int64_t> cuts;
+    if (blocks)
+        for (int k = 1; k <= K; ++k)
+            if (rbp[k] > R0 && rbp[k] < R1) cuts.push_back(rbp[k] - R0);
+    std::vector<int32_t> tile_row;
+    plan_tiles(rp, m_loc, cuts, tile_row, h->n_long);
+    const int64_t T = (int64_t)tile_row.size() - 1;
+    h->n_tiles = T;
+    if (T >= INT32_MAX) return fail(SPMV_ERR_UNSUPPORTED, "too many tiles");
+
+    // algorithmic bytes: 12 nnz + 4 (m+1) + 8 m + 8 n_touched
+    {
+        const int64_t xl = world > 1 ? h->x_int_len + h->border_total : n;
+        std::vector<char> touched(std::max<int64_t>(xl, 1), 0);
+#pragma omp parallel for schedule(static)
+        for (int64_t t = 0; t < nnz_loc; ++t) touched[pcol[t]] = 1;
+        int64_t nt = 0;
+#pragma omp parallel for reduction(+ : nt)
+        for (int64_t c = 0; c < xl; ++c) nt += touched[c];
+        h->bytes_alg = 12 * nnz_loc + 4 * (m_loc + 1) + 8 * m_loc + 8 * nt;
+        h->bytes_alg_split = 0;
+        if (n_parts) h->bytes_alg_split = 12 * nnz_loc + 8 * m_loc + 8 * nt;   // + segment metadata below
+    }
+
+    // ------------------------------------------------ device upload
+    std::vector<int32_t> rp32(m_loc + 1);
+#pragma omp parallel for schedule(static)
+    for (int64_t p = 0; p <= m_loc; ++p) rp32[p] = (int32_t)rp[p];
+    spmv_status_t s;
+    if ((s = upload(h, &h->d_rowptr, rp32.data(), m_loc + 1))) return s;
+    if ((s = upload(h, &h->d_col, pcol.data(), nnz_loc, nnz_loc + kPad))) return s;
+    if ((s = upload(h, &h->d_val, pval.data(), nnz_loc, nnz_loc + kPad))) return s;
+    if ((s = upload(h, &h->d_tile_row, tile_row.data(), T + 1))) return s;
+
+    // -------------------------------------------- split layout (a8)
+    // Within each row tile the nonzeros are regrouped part-major: for k = 0..K-1,
+    // the tile's rows' part-k runs ("segments") in row order.  This is the
+    // access order that Pi defines, executed tile by tile.
+    if (n_parts) {
+        const int KP = n_parts;
+        std::vector<int64_t> seg_cnt(T * KP, 0), nz_cnt(T * KP, 0);
+#pragma omp parallel for schedule(dynamic, 64)
+        for (int64_t t = 0; t < T; ++t) {
+            std::vector<int64_t> stamp(KP, -1);   // last row that opened a part-k segment
+            for (int64_t r = tile_row[t]; r < tile_row[t + 1]; ++r) {
+                for (int64_t e = rp[r]; e < rp[r + 1]; ++e) {
+                    const int k = ppart[e];
+                    nz_cnt[t * KP + k]++;
+                    if (stamp[k] != r) { stamp[k] = r; seg_cnt[t * KP + k]++; }
+                }
+            }
+        }
+        std::vector<int32_t> tile_seg(T * KP + 1);
+        std::vector<int64_t> seg_off(T * KP + 1), nz_off(T * KP + 1);
+        seg_off[0] = 0;
+        nz_off[0] = 0;
+        for (int64_t q = 0; q < T * KP; ++q) {
+            seg_off[q + 1] = seg_off[q] + seg_cnt[q];
+            nz_off[q + 1] = nz_off[q] + nz_cnt[q];
+        }
+        const int64_t S = seg_off[T * KP];
+        if (S >= INT32_MAX) return fail(SPMV_ERR_UNSUPPORTED, "too many split segments");
+        h->n_seg = S;
+        for (int64_t q = 0; q <= T * KP; ++q) tile_seg[q] = (int32_t)seg_off[q];
+        std::vector<int32_t> seg_ptr(S + 1), seg_row(S), scol(nnz_loc);
+        std::vector<double> sval(nnz_loc);
+        seg_ptr[S] = (int32_t)nnz_loc;
+#pragma omp parallel for schedule(dynamic, 64)
+        for (int64_t t = 0; t < T; ++t) {
+            for (int k = 0; k < KP; ++k) {
+                int64_t sg = seg_off[t * KP + k];
+                int64_t nz = nz_off[t * KP + k];
+                for (int64_t r = tile_row[t]; r < tile_row[t + 1]; ++r) {
+                    bool has = false;
+                    for (int64_t e = rp[r]; e < rp[r + 1]; ++e) {
+                        if (ppart[e] != k) continue;
+                        if (!has) {
+                            seg_ptr[sg] = (int32_t)nz;
+                            seg_row[sg] = (int32_t)(r - tile_row[t]);
+                            ++sg;
+                            has = true;
+                        }
+                        scol[nz] = pcol[e];
+                        sval[nz] = pval[e];
+                        ++nz;
+                    }
+                }
+            }
+        }
+        h->bytes_alg_split += 8 * S + 4 * (T * KP + 1);
+        if ((s = upload(h, &h->d_tile_seg, tile_seg.data(), T * KP + 1))) return s;
+        if ((s = upload(h, &h->d_seg_ptr, seg_ptr.data(), S + 1))) return s;
+        if ((s = upload(h, &h->d_seg_row, seg_row.data(), S))) return s;
+        if ((s = upload(h, &h->d_scol, scol.data(), nnz_loc, nnz_loc + kPad))) return s;
+        if ((s = upload(h, &h->d_sval, sval.data(), nnz_loc, nnz_loc + kPad))) return s;
+    }
+
+    // -------------------------------------- ORIGINAL-mode maps (a3, a7)
+    if (world == 1 && h->has_perm) {
+        if ((s = upload(h, &h->d_colinv, col_inv.data(), n))) return s;
+        std::vector<int32_t> rperm(m);
+#pragma omp parallel for schedule(static)
+        for (int64_t i = 0; i < m; ++i) rperm[i] = row_perm ? row_perm[i] : (int32_t)i;
+        if ((s = upload(h, &h->d_rowperm, rperm.data(), m))) return s;
+        if ((s = dalloc(h, &h->d_xhat, n))) return s;
+        if ((s = dalloc(h, &h->d_yhat, m))) return s;
+    }
+
+    // ------------------------------- owner map r(c) for the x-update (a9)
+    // Square A: column c (new) is old column j = col_inv[c]; as a row, old j
+    // is new row row_perm[j].  x^_{t+1}[c] = y^_t[row_perm[col_inv[c]]] / m.
+    if (m == n && m > 0) {
+        std::vector<int32_t> owner(h->x_local_len);
+        std::atomic<int> outside{0};
+#pragma omp parallel for schedule(static)
+        for (int64_t l = 0; l < h->x_local_len; ++l) {
+            const int64_t c = (world > 1) ? (l < h->x_int_len ? h->x_int_begin + l
+                                                              : h->x_bord_begin + (l - h->x_int_len))
+                                          : l;
+            const int64_t j = col_inv[c];
+            const int64_t r = row_perm ? row_perm[j] : j;
+            if (r < R0 || r >= R1) { outside = 1; owner[l] = 0; }
+            else owner[l] = (int32_t)(r - R0);
+        }
+        if (!outside) {
+            if ((s = upload(h, &h->d_owner, owner.data(), h->x_local_len))) return s;
+            h->has_owner = true;
+        }
+    }
+
+    // ------------------------------------------------- misc buffers
+    if ((s = dalloc(h, &h->d_slots, spmvb::kMaxSlots * spmvb::kSlotStride))) return s;
+    CUDA_TRY(cudaMemset(h->d_slots, 0, spmvb::kMaxSlots * spmvb::kSlotStride * sizeof(unsigned long long)));
+    if ((s = dalloc(h, &h->d_mscratch, 2))) return s;
+    if (world > 1) {
+        if ((s = dalloc(h, &h->d_xborder, h->border_total))) return s;
+        CUDA_TRY(cudaMemset(h->d_xborder, 0, std::max<int64_t>(h->border_total, 1) * sizeof(double)));
+    }
+    CUDA_TRY(cudaDeviceSynchronize());
+    return SPMV_OK;
+}
+
+spmv_status_t spmv_create(int64_t m, int64_t n, int64_t nnz, const int64_t* row_ptr, const int32_t* col_idx,
+                          const double* val, const int32_t* row_perm, const int32_t* col_perm,
+                          const spmv_blocks_t* blocks, int32_t n_parts, const int32_t* part_of_nnz,
+                          const spmv_dist_t* dist, spmv_handle_t* out) {
+    if (!out) return fail(SPMV_ERR_USAGE, "out is NULL");
+    *out = nullptr;
+    spmv_plan_s* h = new (std::nothrow) spmv_plan_s();
+    if (!h) return fail(SPMV_ERR_INTERNAL, "out of host memory");
+    spmv_status_t s;
+    try {
+        s = create_impl(m, n, nnz, row_ptr, col_idx, val, row_perm, col_perm, blocks, n_parts, part_of_nnz,
+                        dist, h);
+    } catch (const std::bad_alloc&) {
+        s = fail(SPMV_ERR_INTERNAL, "out of host memory");
+    } catch (...) {
+        s = fail(SPMV_ERR_INTERNAL, "unexpected exception");
+    }
+    if (s != SPMV_OK) {
+        free_plan(h);
+        return s;
+    }
+    *out = h;
+    return SPMV_OK;
+}
+
+spmv_status_t spmv_destroy(spmv_handle_t h) {
+    if (!h) return SPMV_OK;
+    if (!valid(h)) return fail(SPMV_ERR_USAGE, "invalid handle");
+    free_plan(h);
+    return SPMV_OK;
+}
+
+// --------------------------------------------------------------- apply
+static spmv_status_t check_vectors(spmv_handle_t h, const double* x, int64_t x_len, double* y, int64_t y_len,
+                                   uint32_t flags) {
+    if (!valid(h)) return fail(SPMV_ERR_USAGE, "invalid handle");
+    if (flags & ~(uint32_t)(SPMV_VEC_ORIGINAL | SPMV_FUSE_MAXABS | SPMV_SPLIT_LITERAL))
+        return fail(SPMV_ERR_USAGE, "unknown flag");
+    if ((!x && x_len) || (!y && y_len)) return fail(SPMV_ERR_USAGE, "NULL vector");
+    if ((const void*)x == (const void*)y && x) return fail(SPMV_ERR_USAGE, "x and y alias");
+    if (((uintptr_t)x & 7) || ((uintptr_t)y & 7)) return fail(SPMV_ERR_USAGE, "x/y not 8-byte aligned");
+    const bool orig = flags & SPMV_VEC_ORIGINAL;
+    if (orig && h->world > 1) return fail(SPMV_ERR_UNSUPPORTED, "ORIGINAL index space with world > 1");
+    const int64_t xl = orig ? h->n : h->x_local_len;
+    const int64_t yl = orig ? h->m : h->m_loc;
+    if (x_len != xl || y_len != yl)
+        return fail(SPMV_ERR_DATA, "dimension mismatch: x_len %lld (want %lld), y_len %lld (want %lld)",
+                    (long long)x_len, (long long)xl, (long long)y_len, (long long)yl);
+    return SPMV_OK;
+}
+
+static spmv_status_t run(spmv_handle_t h, const double* x, double* y, uint32_t flags, cudaStream_t st,
+                         bool split) {
+    CUDA_TRY(cudaSetDevice(h->device));
+    const bool orig = (flags & SPMV_VEC_ORIGINAL) && h->has_perm;
+    const double* xk = x;
+    double* yk = y;
+    if (orig) {   // a3: x^[c] = x[col_inv[c]]
+        CUDA_TRY(spmvb::launch_gather(x, h->d_colinv, h->d_xhat, h->n, st));
+        xk = h->d_xhat;
+        yk = h->d_yhat;
+    }
+    spmvb::TileArgs A{};
+    A.tile_row = h->d_tile_row;
+    A.n_tiles = (int32_t)h->n_tiles;
+    A.y = yk;
+    A.x_lo = xk;
+    A.x_hi = xk;
+    A.x_split = INT32_MAX;
+    bool xsplit = false;
+    if (h->world > 1) {   // a4: border-x exchange over NCCL
+        if (h->x_bord_len)
+            CUDA_TRY(cudaMemcpyAsync(h->d_xborder + h->bord_off[h->rank], x + h->x_int_len,
+                                     h->x_bord_len * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        if (h->equal_slices) {
+            NCCL_TRY(ncclAllGather(h->d_xborder + h->bord_off[h->rank], h->d_xborder, h->bord_cnt[0], ncclFloat64,
+                                   h->comm, st));
+        } else {
+            NCCL_TRY(ncclGroupStart());
+            for (int r = 0; r < h->world; ++r)
+                if (h->bord_cnt[r])
+                    NCCL_TRY(ncclBroadcast(h->d_xborder + h->bord_off[r], h->d_xborder + h->bord_off[r],
+                                           h->bord_cnt[r], ncclFloat64, r, h->comm, st));
+            NCCL_TRY(ncclGroupEnd());
+        }
+        A.x_hi = h->d_xborder;
+        A.x_split = (int32_t)h->x_int_len;
+        xsplit = true;
+    }
+    if (flags & SPMV_FUSE_MAXABS) {
+        CUDA_TRY(cudaMemsetAsync(h->d_slots, 0,
+                                 spmvb::kMaxSlots * spmvb::kSlotStride * sizeof(unsigned long long), st));
+        A.maxabs_slots = h->d_slots;
+    }
+    if (!split) {
+        A.tile_seg = h->d_tile_row;
+        A.seg_ptr = h->d_rowptr;
+        A.seg_row = nullptr;
+        A.col = h->d_col;
+        A.val = h->d_val;
+        A.K = 1; A.k_begin = 0; A.k_end = 1;
+        CUDA_TRY(spmvb::launch_tiles(A, false, xsplit, st));
+    } else {
+        A.tile_seg = h->d_tile_seg;
+        A.seg_ptr = h->d_seg_ptr;
+        A.seg_row = h->d_seg_row;
+        A.col = h->d_scol;
+        A.val = h->d_sval;
+        A.K = h->n_parts;
+        if (flags & SPMV_SPLIT_LITERAL) {   // y = 0; y <- y + A^k x, one pass per k
+            CUDA_TRY(cudaMemsetAsync(yk, 0, h->m_loc * sizeof(double), st));
+            for (int k = 0; k < h->n_parts; ++k) {
+                spmvb::TileArgs B = A;
+                B.k_begin = k; B.k_end = k + 1;
+                B.accumulate = 1;
+                if (k != h->n_parts - 1) B.maxabs_slots = nullptr;
+                CUDA_TRY(spmvb::launch_tiles(B, true, xsplit, st));
+            }
+        } else {
+            A.k_begin = 0; A.k_end = h->n_parts;
+            CUDA_TRY(spmvb::launch_tiles(A, true, xsplit, st));
+        }
+    }
+    if (orig)   // a7: y[i] = y^[row_perm[i]]
+        CUDA_TRY(spmvb::launch_gather(h->d_yhat, h->d_rowperm, y, h->m, st));
+    return SPMV_OK;
+}
+
+spmv_status_t spmv_apply(spmv_handle_t h, const double* x, int64_t x_len, double* y, int64_t y_len, uint32_t flags,
+                         void* stream) {
+    spmv_status_t s = check_vectors(h, x, x_len, y, y_len, flags);
+    if (s) return s;
+    if (flags & SPMV_SPLIT_LITERAL) return fail(SPMV_ERR_USAGE, "SPLIT_LITERAL is a split_apply flag");
+    return run(h, x, y, flags, (cudaStream_t)stream, false);
+}
+
+spmv_status_t spmv_split_apply(spmv_handle_t h, const double* x, int64_t x_len, double* y, int64_t y_len,
+                               uint32_t flags, void* stream) {
+    spmv_status_t s = check_vectors(h, x, x_len, y, y_len, flags);
+    if (s) return s;
+    if (!h->n_parts) return fail(SPMV_ERR_UNSUPPORTED, "handle has no split");
+    return run(h, x, y, flags, (cudaStream_t)stream, true);
+}
+
+spmv_status_t spmv_get_info(spmv_handle_t h, spmv_info_t* info) {
+    if (!valid(h) || !info) return fail(SPMV_ERR_USAGE, "invalid handle or info");
+    memset(info, 0, sizeof *info);
+    info->m = h->m; info->n = h->n; info->nnz = h->nnz;
+    info->m_local = h->m_loc; info->nnz_local = h->nnz_loc; info->row_begin = h->row_begin;
+    info->x_local_len = h->x_local_len;
+    info->x_interior_begin = h->x_int_begin; info->x_interior_len = h->x_int_len;
+    info->x_border_begin = h->x_bord_begin; info->x_border_len = h->x_bord_len;
+    info->border_total = h->border_total;
+    info->n_tiles = h->n_tiles; info->n_long_rows = h->n_long;
+    info->bytes_alg = h->bytes_alg; info->bytes_alg_split = h->bytes_alg_split;
+    info->split_segments = h->n_seg;
+    info->n_parts = h->n_parts; info->rank = h->rank; info->world = h->world; info->kind = h->kind;
+    info->has_owner_map = h->has_owner ? 1 : 0;
+    return SPMV_OK;
+}
+
+spmv_status_t spmv_maxabs(spmv_handle_t h, double* m_dev, void* stream) {
+    if (!valid(h) || !m_dev) return fail(SPMV_ERR_USAGE, "invalid handle or pointer");
+    cudaStream_t st = (cudaStream_t)stream;
+    CUDA_TRY(cudaSetDevice(h->device));
+    CUDA_TRY(spmvb::launch_maxabs_finish(h->d_slots, m_dev, st));
+    if (h->world > 1) NCCL_TRY(ncclAllReduce(m_dev, m_dev, 1, ncclFloat64, ncclMax, h->comm, st));
+    return SPMV_OK;
+}
+
+spmv_status_t spmv_normalize(spmv_handle_t h, const double* y, const double* m_dev, double* x_next, void* stream) {
+    if (!valid(h) || !y || !m_dev || !x_next) return fail(SPMV_ERR_USAGE, "invalid handle or pointer");
+    if (!h->has_owner) return fail(SPMV_ERR_UNSUPPORTED, "no owner-aligned column->row map (A17)");
+    CUDA_TRY(cudaSetDevice(h->device));
+    CUDA_TRY(spmvb::launch_normalize(y, h->d_owner, m_dev, x_next, h->x_local_len, (cudaStream_t)stream));
+    return SPMV_OK;
+}
+
+spmv_status_t spmv_debug_copy_csr(spmv_handle_t h, int64_t* row_ptr, int32_t* col, double* val) {
+    if (!valid(h) || !row_ptr || (h->nnz_loc && (!col || !val))) return fail(SPMV_ERR_USAGE, "bad arguments");
+    CUDA_TRY(cudaSetDevice(h->device));
+    CUDA_TRY(cudaDeviceSynchronize());
+    std::vector<int32_t> rp(h->m_loc + 1);
+    CUDA_TRY(cudaMemcpy(rp.data(), h->d_rowptr, rp.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < rp.size(); ++i) row_ptr[i] = rp[i];
+    if (h->nnz_loc) {
+        CUDA_TRY(cudaMemcpy(col, h->d_col, h->nnz_loc * sizeof(int32_t), cudaMemcpyDeviceToHost));
+        CUDA_TRY(cudaMemcpy(val, h->d_val, h->nnz_loc * sizeof(double), cudaMemcpyDeviceToHost));
+        if (h->world > 1) {   // back to global permuted ids
+            const int64_t Q0 = h->x_int_begin, B0 = h->border_begin, nint = h->x_int_len;
+            for (int64_t t = 0; t < h->nnz_loc; ++t)
+                col[t] = (int32_t)(col[t] >= nint ? B0 + (col[t] - nint) : Q0 + col[t]);
+        }
+    }
+    return SPMV_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,51 @@
+// internal.h -- shared between the host library (host.cpp) and the kernels
+// (kernels.cu).  Not part of the ABI (include/spmv.h is).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace spmvb {
+
+// Row-tile geometry of the SpMxV kernels.
+//   kThreads : threads per CTA
+//   kTileNnz : max nonzeros of a multi-row tile; rows longer than this get a
+//              tile of their own and take the long-row path
+//   kTileRows: max rows of a tile (bounds the shared-memory row arrays)
+constexpr int kThreads = 256;
+constexpr int kTileNnz = 2048;
+constexpr int kTileRows = 512;
+constexpr int kMaxSlots = 64;      // max-abs accumulator slots (spread atomics)
+constexpr int kSlotStride = 16;    // 16 x 8 B = 128 B apart
+
+// A "segment" is the run of nonzeros of one row inside one split part
+// (P:L107): with no split, segments are the rows.  Tile t covers local rows
+// [tile_row[t], tile_row[t+1]); its part-k segments are
+// [tile_seg[t*K+k], tile_seg[t*K+k+1]) with nonzeros [seg_ptr[s], seg_ptr[s+1]).
+struct TileArgs {
+    const int32_t* tile_row;   // [T+1]
+    const int32_t* tile_seg;   // [T*K+1]  (plain: == tile_row, K = 1)
+    const int32_t* seg_ptr;    // [S+1]    (plain: row_ptr)
+    const int32_t* seg_row;    // [S] tile-local row of each segment (plain: unused)
+    const int32_t* col;        // [nnz + pad] local column ids
+    const double* val;         // [nnz + pad]
+    const double* x_lo;        // x for columns < x_split
+    const double* x_hi;        // x_hi[c - x_split] for columns >= x_split
+    int32_t x_split;
+    int32_t n_tiles;
+    double* y;                 // local rows
+    int32_t K, k_begin, k_end; // parts processed in this pass
+    int32_t accumulate;        // 1: y <- y + (sum over parts) (literal split pass)
+    unsigned long long* maxabs_slots;   // nullptr or kMaxSlots*kSlotStride
+};
+
+cudaError_t launch_tiles(const TileArgs& a, bool split, bool xsplit, cudaStream_t s);
+// x^[c] = x[colinv[c]]   (ORIGINAL-mode x preparation, a3)
+cudaError_t launch_gather(const double* src, const int32_t* idx, double* dst, int64_t n, cudaStream_t s);
+// max over slots -> *out
+cudaError_t launch_maxabs_finish(const unsigned long long* slots, double* out, cudaStream_t s);
+// x_next[c] = y[owner[c]] / *m   (power-iteration glue, a9)
+cudaError_t launch_normalize(const double* y, const int32_t* owner, const double* m, double* x_next,
+                             int64_t n, cudaStream_t s);
+int kernel_num_sms();
+
+}  // namespace spmvb
