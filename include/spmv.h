@@ -202,6 +202,21 @@ spmv_status_t spmv_normalize(spmv_handle_t h, const double* y, const double* m_d
  * Synchronous.  Used by tests to check the ingest bit-exactly. */
 spmv_status_t spmv_debug_copy_csr(spmv_handle_t h, int64_t* row_ptr, int32_t* col, double* val);
 
+/* Diagnostics for the measurement harness: roofline
+ * microkernels, asynchronous on `stream`, results written to *out_dev only to
+ * keep the loads alive.  They bound what the SpMxV kernel can reach:
+ *   spmv_diag_read   : 128-bit read stream over `bytes` of device memory (HBM read peak)
+ *   spmv_diag_gather : `count` random 8-byte gathers from x[0..n) (x-gather rate)
+ *   spmv_diag_csr    : over the handle's device CSR (world 1): mode 0 streams
+ *                      col/val only; mode 1 also gathers x[col] (no row sums);
+ *                      mode 2 gathers x[col mod 2^20] (8 MB window); mode 3
+ *                      gathers independent of col (no load-to-load dependency). */
+spmv_status_t spmv_diag_read(const void* buf, int64_t bytes, int32_t blocks_per_sm, double* out_dev, void* stream);
+spmv_status_t spmv_diag_gather(const double* x, int64_t n, int64_t count, double* out_dev, void* stream);
+spmv_status_t spmv_diag_gather_mode(const double* x, int64_t n, int64_t count, int32_t mode, int32_t blocks_per_sm,
+                                    double* out_dev, void* stream);   /* gather flavours 0..7, see diag.cu */
+spmv_status_t spmv_diag_csr(spmv_handle_t h, const double* x, int32_t mode, double* out_dev, void* stream);
+
 /* Writes a fresh 128-byte NCCL unique id into out (len >= 128). */
 spmv_status_t spmv_nccl_unique_id(void* out, size_t len);
 

@@ -33,7 +33,8 @@ SPMV_SPLIT_LITERAL = 4
 
 EXPORTED = ["spmv_create", "spmv_apply", "spmv_split_apply", "spmv_destroy", "spmv_get_info",
             "spmv_maxabs", "spmv_normalize", "spmv_debug_copy_csr", "spmv_nccl_unique_id",
-            "spmv_status_string", "spmv_last_error", "spmv_version"]
+            "spmv_status_string", "spmv_last_error", "spmv_version", "spmv_shard_plan",
+            "spmv_diag_read", "spmv_diag_gather", "spmv_diag_csr", "spmv_diag_gather_mode"]
 
 
 class SpmvError(RuntimeError):
@@ -86,6 +87,11 @@ def lib():
         L.spmv_normalize.argtypes = [vp, vp, vp, vp, vp]
         L.spmv_debug_copy_csr.argtypes = [vp, vp, vp, vp]
         L.spmv_nccl_unique_id.argtypes = [vp, ctypes.c_size_t]
+        L.spmv_diag_read.argtypes = [vp, i64, i32, vp, vp]
+        L.spmv_diag_gather.argtypes = [vp, i64, i64, vp, vp]
+        L.spmv_diag_csr.argtypes = [vp, vp, i32, vp, vp]
+        L.spmv_diag_gather_mode.argtypes = [vp, i64, i64, i32, i32, vp, vp]
+        L.spmv_shard_plan.argtypes = [vp, i64, i64, i32, i32, vp]
         L.spmv_status_string.argtypes = [i32]
         L.spmv_status_string.restype = ctypes.c_char_p
         L.spmv_last_error.argtypes = []
@@ -258,6 +264,27 @@ def spmv_nccl_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     _check(lib().spmv_nccl_unique_id(buf, 128), "spmv_nccl_unique_id")
     return buf.raw
+
+
+def spmv_diag_read(buf, nbytes: int, out, blocks_per_sm: int = 4, stream=None):
+    _check(lib().spmv_diag_read(ctypes.c_void_p(buf.data_ptr()), nbytes, blocks_per_sm, ctypes.c_void_p(_dev(out)),
+                                ctypes.c_void_p(_stream(stream))), "spmv_diag_read")
+
+
+def spmv_diag_gather(x, count: int, out, stream=None):
+    _check(lib().spmv_diag_gather(ctypes.c_void_p(_dev(x)), x.numel(), count, ctypes.c_void_p(_dev(out)),
+                                  ctypes.c_void_p(_stream(stream))), "spmv_diag_gather")
+
+
+def spmv_diag_gather_mode(x, count: int, mode: int, out, blocks_per_sm: int = 8, stream=None):
+    _check(lib().spmv_diag_gather_mode(ctypes.c_void_p(_dev(x)), x.numel(), count, mode, blocks_per_sm,
+                                       ctypes.c_void_p(_dev(out)), ctypes.c_void_p(_stream(stream))),
+           "spmv_diag_gather_mode")
+
+
+def spmv_diag_csr(h, x, mode: int, out, stream=None):
+    _check(lib().spmv_diag_csr(_h(h), ctypes.c_void_p(_dev(x)), mode, ctypes.c_void_p(_dev(out)),
+                               ctypes.c_void_p(_stream(stream))), "spmv_diag_csr")
 
 
 def spmv_status_string(s: int) -> str:

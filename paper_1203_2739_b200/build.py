@@ -33,6 +33,8 @@ def _nccl_dir() -> str:
 
 SOURCES = {
     "kernels.cu": "cu",
+    "diag.cu": "cu",
+    "pipe.cu": "cu",
     "host.cpp": "cpp",
 }
 HEADERS = ["internal.h", os.path.join("..", "..", "include", "spmv.h")]

@@ -15,6 +15,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -94,6 +95,8 @@ struct spmv_plan_s {
     int32_t* d_col = nullptr;         // [nnz_loc + pad] local column ids
     double* d_val = nullptr;          // [nnz_loc + pad]
     int32_t* d_tile_row = nullptr;    // [T+1]
+    int32_t* d_tile_nnz = nullptr;    // [T+1] row_ptr[tile_row[t]]
+    bool use_pipe = true;             // persistent pipelined kernel (pipe.cu)
     int32_t* d_tile_seg = nullptr;    // [T*K+1]
     int32_t* d_seg_ptr = nullptr;     // [S+1]
     int32_t* d_seg_row = nullptr;     // [S]
@@ -166,12 +169,13 @@ void plan_tiles(const std::vector<int64_t>& rp, int64_t m_loc, const std::vector
     while (r < m_loc) {
         while (ci < cuts.size() && cuts[ci] <= r) ++ci;
         const int64_t lim = ci < cuts.size() ? std::min<int64_t>(cuts[ci], m_loc) : m_loc;
-        const int64_t len0 = rp[r + 1] - rp[r];
-        if (len0 > kTileNnz) {
+        // a tile's nonzeros sit at positions [(a & 3), (a & 3) + n) of a
+        // 16-byte aligned kTileNnz-slot stage buffer (pipe.cu)
+        const int64_t base = rp[r] & ~int64_t(3);
+        if (rp[r + 1] - base > kTileNnz) {
             ++r;
             ++n_long;
         } else {
-            const int64_t base = rp[r];
             int64_t e = r;
             while (e < lim && e - r < kTileRows && rp[e + 1] - base <= kTileNnz) ++e;
             r = e;
@@ -520,10 +524,17 @@ static spmv_status_t create_impl(int64_t m, int64_t n, int64_t nnz, const int64_
 #pragma omp parallel for schedule(static)
     for (int64_t p = 0; p <= m_loc; ++p) rp32[p] = (int32_t)rp[p];
     spmv_status_t s;
-    if ((s = upload(h, &h->d_rowptr, rp32.data(), m_loc + 1))) return s;
+    if ((s = upload(h, &h->d_rowptr, rp32.data(), m_loc + 1, m_loc + 1 + kPad))) return s;
     if ((s = upload(h, &h->d_col, pcol.data(), nnz_loc, nnz_loc + kPad))) return s;
     if ((s = upload(h, &h->d_val, pval.data(), nnz_loc, nnz_loc + kPad))) return s;
     if ((s = upload(h, &h->d_tile_row, tile_row.data(), T + 1))) return s;
+    {
+        std::vector<int32_t> tile_nnz(T + 1);
+        for (int64_t t = 0; t <= T; ++t) tile_nnz[t] = (int32_t)rp[tile_row[t]];
+        if ((s = upload(h, &h->d_tile_nnz, tile_nnz.data(), T + 1))) return s;
+        const char* kenv = getenv("SPMV_KERNEL");
+        h->use_pipe = !(kenv && strcmp(kenv, "tile") == 0);
+    }
 
     // -------------------------------------------- split layout (a8)
     // Within each row tile the nonzeros are regrouped part-major: for k = 0..K-1,
@@ -727,7 +738,21 @@ static spmv_status_t run(spmv_handle_t h, const double* x, double* y, uint32_t f
                                  spmvb::kMaxSlots * spmvb::kSlotStride * sizeof(unsigned long long), st));
         A.maxabs_slots = h->d_slots;
     }
-    if (!split) {
+    if (!split && h->use_pipe) {
+        spmvb::PipeArgs P{};
+        P.tile_row = h->d_tile_row;
+        P.tile_nnz = h->d_tile_nnz;
+        P.rowptr = h->d_rowptr;
+        P.col = h->d_col;
+        P.val = h->d_val;
+        P.x_lo = A.x_lo;
+        P.x_hi = A.x_hi;
+        P.x_split = A.x_split;
+        P.n_tiles = A.n_tiles;
+        P.y = A.y;
+        P.maxabs_slots = A.maxabs_slots;
+        CUDA_TRY(spmvb::launch_pipe(P, xsplit, st));
+    } else if (!split) {
         A.tile_seg = h->d_tile_row;
         A.seg_ptr = h->d_rowptr;
         A.seg_row = nullptr;
@@ -827,6 +852,35 @@ spmv_status_t spmv_debug_copy_csr(spmv_handle_t h, int64_t* row_ptr, int32_t* co
                 col[t] = (int32_t)(col[t] >= nint ? B0 + (col[t] - nint) : Q0 + col[t]);
         }
     }
+    return SPMV_OK;
+}
+
+// ------------------------------------------------------------ diagnostics
+spmv_status_t spmv_diag_read(const void* buf, int64_t bytes, int32_t blocks_per_sm, double* out_dev, void* stream) {
+    if (!buf || bytes < 16 || !out_dev || blocks_per_sm < 1) return fail(SPMV_ERR_USAGE, "diag_read: bad arguments");
+    CUDA_TRY(spmvb::diag_read(buf, bytes, out_dev, blocks_per_sm, (cudaStream_t)stream));
+    return SPMV_OK;
+}
+
+spmv_status_t spmv_diag_gather(const double* x, int64_t n, int64_t count, double* out_dev, void* stream) {
+    if (!x || n < 1 || count < 1 || !out_dev) return fail(SPMV_ERR_USAGE, "diag_gather: bad arguments");
+    CUDA_TRY(spmvb::diag_gather(x, n, count, out_dev, (cudaStream_t)stream));
+    return SPMV_OK;
+}
+
+spmv_status_t spmv_diag_gather_mode(const double* x, int64_t n, int64_t count, int32_t mode, int32_t blocks_per_sm,
+                                    double* out_dev, void* stream) {
+    if (!x || n < 2 || count < 1 || !out_dev || blocks_per_sm < 1) return fail(SPMV_ERR_USAGE, "diag_gather_mode: bad arguments");
+    CUDA_TRY(spmvb::diag_gather_mode(x, n, count, mode, blocks_per_sm, out_dev, (cudaStream_t)stream));
+    return SPMV_OK;
+}
+
+spmv_status_t spmv_diag_csr(spmv_handle_t h, const double* x, int32_t mode, double* out_dev, void* stream) {
+    if (!valid(h) || !out_dev || (mode >= 1 && !x) || mode < 0 || mode > 3)
+        return fail(SPMV_ERR_USAGE, "diag_csr: bad arguments");
+    if (h->world > 1) return fail(SPMV_ERR_UNSUPPORTED, "diag_csr: world 1 only");
+    CUDA_TRY(cudaSetDevice(h->device));
+    CUDA_TRY(spmvb::diag_csr(h->d_col, h->d_val, x, h->nnz_loc, mode, out_dev, (cudaStream_t)stream));
     return SPMV_OK;
 }
 

@@ -39,6 +39,23 @@ struct TileArgs {
 };
 
 cudaError_t launch_tiles(const TileArgs& a, bool split, bool xsplit, cudaStream_t s);
+
+// Persistent warp-specialised single-SpMxV kernel (pipe.cu).
+struct PipeArgs {
+    const int32_t* tile_row;   // [T+1]
+    const int32_t* tile_nnz;   // [T+1] = row_ptr[tile_row[t]]
+    const int32_t* rowptr;     // [m+1+4]
+    const int32_t* col;        // [nnz+pad]
+    const double* val;         // [nnz+pad]
+    const double* x_lo;
+    const double* x_hi;
+    int32_t x_split;
+    int32_t n_tiles;
+    double* y;
+    unsigned long long* maxabs_slots;
+};
+cudaError_t launch_pipe(const PipeArgs& a, bool xsplit, cudaStream_t s);
+size_t pipe_smem_bytes();
 // x^[c] = x[colinv[c]]   (ORIGINAL-mode x preparation, a3)
 cudaError_t launch_gather(const double* src, const int32_t* idx, double* dst, int64_t n, cudaStream_t s);
 // max over slots -> *out
@@ -47,5 +64,13 @@ cudaError_t launch_maxabs_finish(const unsigned long long* slots, double* out, c
 cudaError_t launch_normalize(const double* y, const int32_t* owner, const double* m, double* x_next,
                              int64_t n, cudaStream_t s);
 int kernel_num_sms();
+
+// roofline microkernels (diag.cu)
+cudaError_t diag_read(const void* buf, int64_t bytes, double* out, int blocks_per_sm, cudaStream_t s);
+cudaError_t diag_gather(const double* x, int64_t n, int64_t count, double* out, cudaStream_t s);
+cudaError_t diag_gather_mode(const double* x, int64_t n, int64_t count, int mode, int blocks_per_sm, double* out,
+                             cudaStream_t s);
+cudaError_t diag_csr(const int32_t* col, const double* val, const double* x, int64_t nnz, int mode, double* out,
+                     cudaStream_t s);
 
 }  // namespace spmvb

@@ -32,7 +32,7 @@ def test_exports_every_declared_symbol():
     L = ctypes.CDLL(sp.LIB_PATH)
     for n in names:
         assert hasattr(L, n), n
-    assert set(names) <= set(sp.EXPORTED) | {"spmv_shard_plan"}
+    assert set(names) <= set(sp.EXPORTED)
 
 
 def test_status_strings_and_version():
