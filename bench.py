@@ -405,6 +405,28 @@ def run_ours(args, rank, world, local_rank):
                "h2d_bytes_per_step": int(hx.numel() * 8), "d2h_bytes_per_step": int(hy.numel() * 8 + (8 if power else 0)),
                "steps": Ke}
 
+    # ---------------- second roofline: the LSU x-gather rate, measured live
+    gather = None
+    if not args.no_gather_peak:
+        gx = torch.rand(4 << 20, dtype=torch.float64, device=dev)      # 32 MB, L2-resident
+        sink = torch.zeros(1, dtype=torch.float64, device=dev)
+        cnt = 1 << 29
+        for _ in range(2):
+            sp.spmv_diag_gather_mode(gx, cnt, 0, sink)
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(3):
+            sp.spmv_diag_gather_mode(gx, cnt, 0, sink)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        gpeak = 3 * cnt / (g0.elapsed_time(g1) * 1e-3) / 1e9
+        nnz_loc = info["nnz_local"]
+        gach = nnz_loc / (avg_spmv_ms * 1e-3) / 1e9
+        gather = {"bound": "lsu_gather", "achieved": gach, "peak": gpeak, "unit": "Ggathers/s", "frac": gach / gpeak,
+                  "note": "one x gather per nonzero; peak = random 8-byte __ldg gathers from a 32 MB L2-resident "
+                          "vector, measured in this run (spmv_diag_gather_mode)"}
+        del gx
+
     # ---------------- roofline of the SpMxV kernel
     peaks, peak_src = load_peaks()
     bytes_alg = info["bytes_alg_split"] if split else info["bytes_alg"]
@@ -443,6 +465,7 @@ def run_ours(args, rank, world, local_rank):
             "hbm_gbs": bytes_tot / (avg_spmv_max * 1e-3) / 1e9,
             "spmv_ms": avg_spmv_max,
             "roofline": roofline,
+            "roofline_gather": gather,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches_per_step * K,
@@ -465,6 +488,7 @@ def main():
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-gather-peak", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--parity-rows", type=int, default=200000)
     ap.add_argument("--e2e-steps", type=int, default=10)

@@ -35,6 +35,8 @@ SOURCES = {
     "kernels.cu": "cu",
     "diag.cu": "cu",
     "pipe.cu": "cu",
+    "rowtile.cu": "cu",
+    "split.cu": "cu",
     "host.cpp": "cpp",
 }
 HEADERS = ["internal.h", os.path.join("..", "..", "include", "spmv.h")]

@@ -165,10 +165,11 @@ __global__ void __launch_bounds__(256) gather_smem_kernel(const double* __restri
 template <int MODE>
 __global__ void __launch_bounds__(256) csr_stream_kernel(const int32_t* __restrict__ col, const double* __restrict__ val,
                                                          const double* __restrict__ x, int64_t nq, double* out) {
+    // one CTA per 512 consecutive quads, launched in order (no drift)
     const uint64_t pol = pol_first();
     double acc = 0.0;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq; q += 2 * stride) {
+    const int64_t stride = blockDim.x;
+    for (int64_t q = blockIdx.x * 512ll + threadIdx.x; q < nq && q < blockIdx.x * 512ll + 512; q += 2 * stride) {
         const bool two = q + stride < nq;
         const int4 c0 = ldv4(col + 4 * q, pol);
         const int4 a0 = ldv4(val + 4 * q, pol), b0 = ldv4(val + 4 * q + 2, pol);
@@ -258,7 +259,7 @@ cudaError_t diag_gather_mode(const double* x, int64_t n, int64_t count, int mode
 cudaError_t diag_csr(const int32_t* col, const double* val, const double* x, int64_t nnz, int mode, double* out,
                      cudaStream_t s) {
     const int64_t nq = (nnz + 3) / 4;
-    const int grid = sms() * 8;
+    const int grid = (int)((nq + 511) / 512);
     switch (mode) {
     case 0: csr_stream_kernel<0><<<grid, 256, 0, s>>>(col, val, x, nq, out); break;
     case 1: csr_stream_kernel<1><<<grid, 256, 0, s>>>(col, val, x, nq, out); break;

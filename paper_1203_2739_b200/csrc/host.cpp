@@ -96,7 +96,9 @@ struct spmv_plan_s {
     double* d_val = nullptr;          // [nnz_loc + pad]
     int32_t* d_tile_row = nullptr;    // [T+1]
     int32_t* d_tile_nnz = nullptr;    // [T+1] row_ptr[tile_row[t]]
-    bool use_pipe = true;             // persistent pipelined kernel (pipe.cu)
+    int* d_counter = nullptr;         // tile-claim counter of the pipe kernel
+    int32_t* d_tile_cls = nullptr;    // [T] tile class (internal.h)
+    int kernel = 0;                   // 0 rowtile.cu (default), 1 pipe.cu, 2 kernels.cu tile kernel
     int32_t* d_tile_seg = nullptr;    // [T*K+1]
     int32_t* d_seg_ptr = nullptr;     // [S+1]
     int32_t* d_seg_row = nullptr;     // [S]
@@ -262,6 +264,7 @@ static spmv_status_t create_impl(int64_t m, int64_t n, int64_t nnz, const int64_
     if (!row_ptr) return fail(SPMV_ERR_USAGE, "row_ptr is NULL");
     if (nnz > 0 && (!col_idx || !val)) return fail(SPMV_ERR_USAGE, "col_idx/val is NULL");
     if (n_parts < 0 || (n_parts > 0 && !part_of_nnz)) return fail(SPMV_ERR_USAGE, "bad split arguments");
+    if (n_parts > spmvb::kMaxParts) return fail(SPMV_ERR_UNSUPPORTED, "more than %d split parts", spmvb::kMaxParts);
     if (m > INT32_MAX - 1 || n > INT32_MAX - 1) return fail(SPMV_ERR_UNSUPPORTED, "dimension beyond int32");
     const int world = dist ? dist->world : 1;
     const int rank = dist ? dist->rank : 0;
@@ -532,8 +535,28 @@ static spmv_status_t create_impl(int64_t m, int64_t n, int64_t nnz, const int64_
         std::vector<int32_t> tile_nnz(T + 1);
         for (int64_t t = 0; t <= T; ++t) tile_nnz[t] = (int32_t)rp[tile_row[t]];
         if ((s = upload(h, &h->d_tile_nnz, tile_nnz.data(), T + 1))) return s;
-        const char* kenv = getenv("SPMV_KERNEL");
-        h->use_pipe = !(kenv && strcmp(kenv, "tile") == 0);
+        std::vector<int32_t> tile_cls(std::max<int64_t>(T, 1), spmvb::kTileGeneral);
+#pragma omp parallel for schedule(static)
+        for (int64_t t = 0; t < T; ++t) {
+            int64_t mx = 0;
+            for (int64_t r = tile_row[t]; r < tile_row[t + 1]; ++r) mx = std::max(mx, rp[r + 1] - rp[r]);
+            // short tiles: lanes per row V = largest power of two with
+            // rows * V <= 512 (rowtile.cu CTA), capped at 32 and at the
+            // longest row rounded up to a power of two
+            int32_t cls = spmvb::kTileGeneral;
+            if (mx <= spmvb::kShortRow) {
+                const int64_t nr = tile_row[t + 1] - tile_row[t];
+                int32_t V = 1;
+                while (V < 32 && nr * (2 * V) <= 512 && V < mx) V *= 2;
+                cls = V;
+            }
+            tile_cls[t] = cls;
+        }
+        if ((s = upload(h, &h->d_tile_cls, tile_cls.data(), T))) return s;
+        const char* kenv = getenv("SPMV_KERNEL");   // A/B switch for measurements only
+        h->kernel = 0;
+        if (kenv && strcmp(kenv, "pipe") == 0) h->kernel = 1;
+        if (kenv && strcmp(kenv, "tile") == 0) h->kernel = 2;
     }
 
     // -------------------------------------------- split layout (a8)
@@ -636,6 +659,7 @@ static spmv_status_t create_impl(int64_t m, int64_t n, int64_t nnz, const int64_
     if ((s = dalloc(h, &h->d_slots, spmvb::kMaxSlots * spmvb::kSlotStride))) return s;
     CUDA_TRY(cudaMemset(h->d_slots, 0, spmvb::kMaxSlots * spmvb::kSlotStride * sizeof(unsigned long long)));
     if ((s = dalloc(h, &h->d_mscratch, 2))) return s;
+    if ((s = dalloc(h, &h->d_counter, 4))) return s;
     if (world > 1) {
         if ((s = dalloc(h, &h->d_xborder, h->border_total))) return s;
         CUDA_TRY(cudaMemset(h->d_xborder, 0, std::max<int64_t>(h->border_total, 1) * sizeof(double)));
@@ -738,10 +762,11 @@ static spmv_status_t run(spmv_handle_t h, const double* x, double* y, uint32_t f
                                  spmvb::kMaxSlots * spmvb::kSlotStride * sizeof(unsigned long long), st));
         A.maxabs_slots = h->d_slots;
     }
-    if (!split && h->use_pipe) {
+    if (!split && h->kernel != 2) {
         spmvb::PipeArgs P{};
         P.tile_row = h->d_tile_row;
         P.tile_nnz = h->d_tile_nnz;
+        P.tile_cls = h->d_tile_cls;
         P.rowptr = h->d_rowptr;
         P.col = h->d_col;
         P.val = h->d_val;
@@ -751,7 +776,9 @@ static spmv_status_t run(spmv_handle_t h, const double* x, double* y, uint32_t f
         P.n_tiles = A.n_tiles;
         P.y = A.y;
         P.maxabs_slots = A.maxabs_slots;
-        CUDA_TRY(spmvb::launch_pipe(P, xsplit, st));
+        P.tile_counter = h->d_counter;
+        if (h->kernel == 1) CUDA_TRY(spmvb::launch_pipe(P, xsplit, st));
+        else CUDA_TRY(spmvb::launch_rowtile(P, xsplit, st));
     } else if (!split) {
         A.tile_seg = h->d_tile_row;
         A.seg_ptr = h->d_rowptr;
@@ -774,11 +801,13 @@ static spmv_status_t run(spmv_handle_t h, const double* x, double* y, uint32_t f
                 B.k_begin = k; B.k_end = k + 1;
                 B.accumulate = 1;
                 if (k != h->n_parts - 1) B.maxabs_slots = nullptr;
-                CUDA_TRY(spmvb::launch_tiles(B, true, xsplit, st));
+                if (h->kernel == 2) CUDA_TRY(spmvb::launch_tiles(B, true, xsplit, st));
+                else CUDA_TRY(spmvb::launch_split(B, xsplit, st));
             }
         } else {
             A.k_begin = 0; A.k_end = h->n_parts;
-            CUDA_TRY(spmvb::launch_tiles(A, true, xsplit, st));
+            if (h->kernel == 2) CUDA_TRY(spmvb::launch_tiles(A, true, xsplit, st));
+            else CUDA_TRY(spmvb::launch_split(A, xsplit, st));
         }
     }
     if (orig)   // a7: y[i] = y^[row_perm[i]]

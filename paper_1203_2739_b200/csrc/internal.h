@@ -14,6 +14,9 @@ namespace spmvb {
 constexpr int kThreads = 256;
 constexpr int kTileNnz = 2048;
 constexpr int kTileRows = 512;
+constexpr int kTileShort = 1;      // >= 1: every row has <= kShortRow nonzeros; value = lanes per row
+constexpr int kTileGeneral = 0;
+constexpr int kShortRow = 32;
 constexpr int kMaxSlots = 64;      // max-abs accumulator slots (spread atomics)
 constexpr int kSlotStride = 16;    // 16 x 8 B = 128 B apart
 
@@ -44,6 +47,7 @@ cudaError_t launch_tiles(const TileArgs& a, bool split, bool xsplit, cudaStream_
 struct PipeArgs {
     const int32_t* tile_row;   // [T+1]
     const int32_t* tile_nnz;   // [T+1] = row_ptr[tile_row[t]]
+    const int32_t* tile_cls;   // [T] kTileShort / kTileGeneral
     const int32_t* rowptr;     // [m+1+4]
     const int32_t* col;        // [nnz+pad]
     const double* val;         // [nnz+pad]
@@ -53,8 +57,15 @@ struct PipeArgs {
     int32_t n_tiles;
     double* y;
     unsigned long long* maxabs_slots;
+    int* tile_counter;         // zeroed by launch_pipe before every launch
 };
 cudaError_t launch_pipe(const PipeArgs& a, bool xsplit, cudaStream_t s);
+// Default single-SpMxV kernel (rowtile.cu): one 512-thread CTA per row tile.
+using RowTileArgs = PipeArgs;
+cudaError_t launch_rowtile(const RowTileArgs& a, bool xsplit, cudaStream_t s);
+// Fused / literal multiple-SpMxV kernel (split.cu), K <= 64 parts.
+constexpr int kMaxParts = 64;
+cudaError_t launch_split(const TileArgs& a, bool xsplit, cudaStream_t s);
 size_t pipe_smem_bytes();
 // x^[c] = x[colinv[c]]   (ORIGINAL-mode x preparation, a3)
 cudaError_t launch_gather(const double* src, const int32_t* idx, double* dst, int64_t n, cudaStream_t s);

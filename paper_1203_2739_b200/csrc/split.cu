@@ -1,0 +1,206 @@
+// split.cu -- multiple-SpMxV y = 0; y <- y + A^k x, k = 1..K,
+// fused per row tile, sm_100a.
+//
+// Layout (host.cpp, "split layout"): within each row tile the nonzeros are
+// regrouped part-major -- for k = 0..K-1 the part-k runs ("segments") of the
+// tile's rows, in row order.  That is the access order the splitting Pi
+// defines, executed tile by tile: the whole GPU sweeps the tiles in
+// order, and inside a tile the parts are visited in order.
+//
+// One CTA of 512 threads per tile (same geometry as rowtile.cu):
+//   1. one 128-bit quad of the tile's part-major (col, val) stream per
+//      thread, L2 evict-first; x gathered through the read-only path; products
+//      staged in shared memory; the tile's segment offsets and rows alongside;
+//   2. for k = 0..K-1: every part-k segment of <= 32 nonzeros is summed
+//      serially by one thread (the per-(row, part) temporary), longer ones by
+//      a warp with a fixed tree; then ysum[row] += tmp -- y accumulated on
+//      chip "on the fly" in part order, one y store per row.
+//      Short segments reproduce the oracle's order bit for bit.
+// Literal mode (SPMV_SPLIT_LITERAL) runs the same kernel once per part with
+// ysum initialised from y: the unfused sequence of K passes.
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "internal.h"
+
+namespace spmvb {
+namespace {
+
+constexpr int kST = 512;
+static_assert(kST * 4 == kTileNnz, "one quad per thread");
+
+__device__ __forceinline__ uint64_t pol_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ int4 ld_v4(const int32_t* ptr, uint64_t pol) {
+    int4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(ptr), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ double2 ld_v2d(const double* ptr, uint64_t pol) {
+    double2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+                 : "=d"(r.x), "=d"(r.y)
+                 : "l"(ptr), "l"(pol));
+    return r;
+}
+
+template <bool XSPLIT>
+__device__ __forceinline__ double ldx(const TileArgs& A, int c) {
+    if (XSPLIT) return c < A.x_split ? __ldg(A.x_lo + c) : __ldg(A.x_hi + (c - A.x_split));
+    return __ldg(A.x_lo + c);
+}
+
+struct SplitSmem {
+    double prod[kTileNnz];
+    double ysum[kTileRows];
+    int32_t so[kTileNnz + 1];       // segment offsets (positions from a4), all parts of the tile
+    int32_t srow[kTileNnz];         // tile-local row of each segment
+    int32_t kseg[65];               // first segment of part k (relative), K <= 64
+    int32_t longsegs[kTileNnz];
+    int32_t nlong;
+    double red[kST / 32];
+};
+
+// sum of positions [p0, p1) of a long segment by one warp (fixed order)
+__device__ __forceinline__ double warp_sum(const SplitSmem& sm, int p0, int p1, int lane) {
+    double acc = 0.0;
+    for (int p = p0 + lane; p < p1; p += 32) acc += sm.prod[p];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    return acc;
+}
+
+template <bool XSPLIT>
+__global__ void __launch_bounds__(kST, 2) spmv_split_kernel(const TileArgs A) {
+    __shared__ __align__(16) SplitSmem sm;
+    const int t = blockIdx.x;
+    const int tid = threadIdx.x;
+    const int K = A.K;
+    const int kb = A.k_begin, ke = A.k_end;
+    const int s_lo = A.tile_seg[t * K + kb], s_hi = A.tile_seg[t * K + ke];
+    if (A.accumulate && s_lo == s_hi) return;           // literal pass: no part-k rows here
+    const int r0 = A.tile_row[t];
+    const int nr = A.tile_row[t + 1] - r0;
+    const int a = A.seg_ptr[s_lo], b = A.seg_ptr[s_hi];
+    const int a4 = a & ~3;
+    const uint64_t pol = pol_evict_first();
+
+    for (int j = tid; j < nr; j += kST) sm.ysum[j] = A.accumulate ? A.y[r0 + j] : 0.0;
+
+    if (b - a4 > kTileNnz) {
+        // one long row (the tile is a single row): per part, fixed-assignment
+        // partials + fixed block tree, accumulated in part order
+        __syncthreads();
+        for (int k = kb; k < ke; ++k) {
+            const int s0 = A.tile_seg[t * K + k], s1 = A.tile_seg[t * K + k + 1];
+            if (s0 == s1) continue;
+            const int64_t pa = A.seg_ptr[s0], pb = A.seg_ptr[s1];
+            double acc = 0.0;
+            for (int64_t q = (pa >> 2) + tid; q < ((pb + 3) >> 2); q += kST) {
+                const int4 c = ld_v4(A.col + 4 * q, pol);
+                const double2 v0 = ld_v2d(A.val + 4 * q, pol);
+                const double2 v1 = ld_v2d(A.val + 4 * q + 2, pol);
+                const int64_t g = 4 * q;
+                if (g + 0 >= pa && g + 0 < pb) acc += v0.x * ldx<XSPLIT>(A, c.x);
+                if (g + 1 >= pa && g + 1 < pb) acc += v0.y * ldx<XSPLIT>(A, c.y);
+                if (g + 2 >= pa && g + 2 < pb) acc += v1.x * ldx<XSPLIT>(A, c.z);
+                if (g + 3 >= pa && g + 3 < pb) acc += v1.y * ldx<XSPLIT>(A, c.w);
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+            if ((tid & 31) == 0) sm.red[tid >> 5] = acc;
+            __syncthreads();
+            if (tid == 0) {
+                double tot = 0.0;
+                for (int w = 0; w < kST / 32; ++w) tot += sm.red[w];
+                sm.ysum[0] += tot;
+            }
+            __syncthreads();
+        }
+    } else {
+        // ------------------------------------------- stage products, segments
+        const int nseg = s_hi - s_lo;
+        for (int j = tid; j <= nseg; j += kST) sm.so[j] = A.seg_ptr[s_lo + j] - a4;
+        for (int j = tid; j < nseg; j += kST) sm.srow[j] = A.seg_row[s_lo + j];
+        for (int k = kb + tid; k <= ke; k += kST) sm.kseg[k - kb] = A.tile_seg[t * K + k] - s_lo;
+        if (tid == 0) sm.nlong = 0;
+        {
+            const int p = 4 * tid;
+            if (a4 + p < b) {
+                const int4 c = ld_v4(A.col + a4 + p, pol);
+                const double2 v0 = ld_v2d(A.val + a4 + p, pol);
+                const double2 v1 = ld_v2d(A.val + a4 + p + 2, pol);
+                const int lo = a - a4, hi = b - a4;
+                const double x0 = (p + 0 >= lo && p + 0 < hi) ? ldx<XSPLIT>(A, c.x) : 0.0;
+                const double x1 = (p + 1 >= lo && p + 1 < hi) ? ldx<XSPLIT>(A, c.y) : 0.0;
+                const double x2 = (p + 2 >= lo && p + 2 < hi) ? ldx<XSPLIT>(A, c.z) : 0.0;
+                const double x3 = (p + 3 >= lo && p + 3 < hi) ? ldx<XSPLIT>(A, c.w) : 0.0;
+                double2 w0, w1;
+                w0.x = v0.x * x0; w0.y = v0.y * x1;
+                w1.x = v1.x * x2; w1.y = v1.y * x3;
+                *reinterpret_cast<double2*>(&sm.prod[p]) = w0;
+                *reinterpret_cast<double2*>(&sm.prod[p + 2]) = w1;
+            }
+        }
+        __syncthreads();
+        // ------------------------------------------- parts in order
+        const int warp = tid >> 5, lane = tid & 31;
+        for (int k = 0; k < ke - kb; ++k) {
+            const int j0 = sm.kseg[k], j1 = sm.kseg[k + 1];
+            if (j0 == j1) continue;                                 // CTA-uniform
+            bool any_long = false;
+            for (int j = j0 + tid; j < j1; j += kST) {
+                const int p0 = sm.so[j], p1 = sm.so[j + 1];
+                if (p1 - p0 <= kShortRow) {
+                    double tmp = 0.0;
+                    for (int p = p0; p < p1; ++p) tmp += sm.prod[p];
+                    sm.ysum[sm.srow[j]] += tmp;                     // one segment per row per part
+                } else {
+                    sm.longsegs[atomicAdd(&sm.nlong, 1)] = j;
+                    any_long = true;
+                }
+            }
+            if (__syncthreads_or(any_long)) {
+                for (int i = warp; i < sm.nlong; i += kST / 32) {
+                    const int j = sm.longsegs[i];
+                    const double tmp = warp_sum(sm, sm.so[j], sm.so[j + 1], lane);
+                    if (lane == 0) sm.ysum[sm.srow[j]] += tmp;
+                }
+                __syncthreads();
+                if (tid == 0) sm.nlong = 0;
+            }
+            __syncthreads();
+        }
+    }
+
+    double mx = 0.0;
+    for (int j = tid; j < nr; j += kST) {
+        const double v = sm.ysum[j];
+        A.y[r0 + j] = v;
+        mx = fmax(mx, fabs(v));
+    }
+    if (A.maxabs_slots) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+        if ((tid & 31) == 0 && mx > 0.0)
+            atomicMax(A.maxabs_slots + (t & (kMaxSlots - 1)) * kSlotStride,
+                      (unsigned long long)__double_as_longlong(mx));
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_split(const TileArgs& a, bool xsplit, cudaStream_t s) {
+    if (a.n_tiles <= 0) return cudaSuccess;
+    if (a.K > 64) return cudaErrorInvalidValue;
+    if (xsplit) spmv_split_kernel<true><<<a.n_tiles, kST, 0, s>>>(a);
+    else spmv_split_kernel<false><<<a.n_tiles, kST, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace spmvb
