@@ -98,7 +98,7 @@ struct spmv_plan_s {
     int32_t* d_tile_nnz = nullptr;    // [T+1] row_ptr[tile_row[t]]
     int* d_counter = nullptr;         // tile-claim counter of the pipe kernel
     int32_t* d_tile_cls = nullptr;    // [T] tile class (internal.h)
-    int kernel = 0;                   // 0 rowtile.cu (default), 1 pipe.cu, 2 kernels.cu tile kernel
+    int kernel = 0;                   // 0 rowtile/256 (default), 1 pipe, 2 tile, 3 rowtile/512, 4 rowseg
     int32_t* d_tile_seg = nullptr;    // [T*K+1]
     int32_t* d_seg_ptr = nullptr;     // [S+1]
     int32_t* d_seg_row = nullptr;     // [S]
@@ -557,6 +557,9 @@ static spmv_status_t create_impl(int64_t m, int64_t n, int64_t nnz, const int64_
         h->kernel = 0;
         if (kenv && strcmp(kenv, "pipe") == 0) h->kernel = 1;
         if (kenv && strcmp(kenv, "tile") == 0) h->kernel = 2;
+        if (kenv && strcmp(kenv, "rowtile512") == 0) h->kernel = 3;
+        if (kenv && strcmp(kenv, "rowseg") == 0) h->kernel = 4;
+        if (kenv && strcmp(kenv, "rowtile128") == 0) h->kernel = 5;
     }
 
     // -------------------------------------------- split layout (a8)
@@ -778,7 +781,10 @@ static spmv_status_t run(spmv_handle_t h, const double* x, double* y, uint32_t f
         P.maxabs_slots = A.maxabs_slots;
         P.tile_counter = h->d_counter;
         if (h->kernel == 1) CUDA_TRY(spmvb::launch_pipe(P, xsplit, st));
-        else CUDA_TRY(spmvb::launch_rowtile(P, xsplit, st));
+        else if (h->kernel == 3) CUDA_TRY(spmvb::launch_rowtile(P, xsplit, 512, st));
+        else if (h->kernel == 4) CUDA_TRY(spmvb::launch_rowseg(P, xsplit, st));
+        else if (h->kernel == 5) CUDA_TRY(spmvb::launch_rowtile(P, xsplit, 128, st));
+        else CUDA_TRY(spmvb::launch_rowtile(P, xsplit, 256, st));
     } else if (!split) {
         A.tile_seg = h->d_tile_row;
         A.seg_ptr = h->d_rowptr;

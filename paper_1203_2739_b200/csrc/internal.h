@@ -17,7 +17,7 @@ constexpr int kTileRows = 512;
 constexpr int kTileShort = 1;      // >= 1: every row has <= kShortRow nonzeros; value = lanes per row
 constexpr int kTileGeneral = 0;
 constexpr int kShortRow = 32;
-constexpr int kMaxSlots = 64;      // max-abs accumulator slots (spread atomics)
+constexpr int kMaxSlots = 1024;      // max-abs accumulator slots (spread atomics)
 constexpr int kSlotStride = 16;    // 16 x 8 B = 128 B apart
 
 // A "segment" is the run of nonzeros of one row inside one split part
@@ -62,7 +62,8 @@ struct PipeArgs {
 cudaError_t launch_pipe(const PipeArgs& a, bool xsplit, cudaStream_t s);
 // Default single-SpMxV kernel (rowtile.cu): one 512-thread CTA per row tile.
 using RowTileArgs = PipeArgs;
-cudaError_t launch_rowtile(const RowTileArgs& a, bool xsplit, cudaStream_t s);
+cudaError_t launch_rowtile(const RowTileArgs& a, bool xsplit, int threads, cudaStream_t s);
+cudaError_t launch_rowseg(const RowTileArgs& a, bool xsplit, cudaStream_t s);
 // Fused / literal multiple-SpMxV kernel (split.cu), K <= 64 parts.
 constexpr int kMaxParts = 64;
 cudaError_t launch_split(const TileArgs& a, bool xsplit, cudaStream_t s);

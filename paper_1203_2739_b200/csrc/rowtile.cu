@@ -65,22 +65,185 @@ __device__ __forceinline__ double ldx(const RowTileArgs& A, int c) {
     return __ldg(A.x_lo + c);
 }
 
-struct RTSmem {
+
+
+template <int NT>
+struct RTSmemT {
     double prod[kTileNnz];          // product of position p (nonzero a4 + p)
     int32_t so[kTileRows + 1];      // row_ptr[r0 + j] - a4
     int32_t longrows[kTileRows];    // general tiles: rows with > 32 nonzeros
     int32_t nlong;
-    double red[kRT / 32];
+    double red[NT / 32];
 };
 
-template <bool XSPLIT>
-__global__ void __launch_bounds__(kRT, 3) spmv_rowtile_kernel(const RowTileArgs A) {
-    __shared__ __align__(16) RTSmem sm;
+// NT threads per tile CTA; each thread streams QPT = 512/NT quads.
+template <bool XSPLIT, int NT>
+__global__ void __launch_bounds__(NT, (NT == 512 ? 3 : NT == 256 ? 6 : 8)) spmv_rowtile_kernel(const RowTileArgs A) {
+    constexpr int QPT = 512 / NT;
+    __shared__ __align__(16) RTSmemT<NT> sm;
     const int t = blockIdx.x;
     const int tid = threadIdx.x;
     const int r0 = A.tile_row[t], r1 = A.tile_row[t + 1];
     const int a = A.tile_nnz[t], b = A.tile_nnz[t + 1];
     const int cls = A.tile_cls[t];
+    const int nr = r1 - r0;
+    const int a4 = a & ~3;
+    const uint64_t pol = pol_evict_first();
+    double mx = 0.0;
+
+    if (b - a4 > kTileNnz) {
+        // ------------------------------------------- one long row (> a tile)
+        const int64_t qa = a >> 2, qb = ((int64_t)b + 3) >> 2;
+        double acc = 0.0;
+        for (int64_t q = qa + tid; q < qb; q += NT) {
+            const int4 c = ld_v4(A.col + 4 * q, pol);
+            const double2 v0 = ld_v2d(A.val + 4 * q, pol);
+            const double2 v1 = ld_v2d(A.val + 4 * q + 2, pol);
+            const int64_t g = 4 * q;
+            if (g + 0 >= a && g + 0 < b) acc += v0.x * ldx<XSPLIT>(A, c.x);
+            if (g + 1 >= a && g + 1 < b) acc += v0.y * ldx<XSPLIT>(A, c.y);
+            if (g + 2 >= a && g + 2 < b) acc += v1.x * ldx<XSPLIT>(A, c.z);
+            if (g + 3 >= a && g + 3 < b) acc += v1.y * ldx<XSPLIT>(A, c.w);
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+        if ((tid & 31) == 0) sm.red[tid >> 5] = acc;
+        __syncthreads();
+        if (tid == 0) {
+            double tot = 0.0;
+            for (int w = 0; w < NT / 32; ++w) tot += sm.red[w];
+            A.y[r0] = tot;
+            if (A.maxabs_slots && tot != 0.0)
+                atomicMax(A.maxabs_slots + (t & (kMaxSlots - 1)) * kSlotStride,
+                          (unsigned long long)__double_as_longlong(fabs(tot)));
+        }
+        return;
+    }
+
+    // ------------------------------------------------ stage products, so[]
+    for (int j = tid; j <= nr; j += NT) sm.so[j] = A.rowptr[r0 + j] - a4;
+    if (tid == 0) sm.nlong = 0;
+    {
+        const int lo = a - a4, hi = b - a4;
+        int4 c[QPT];
+        double2 v0[QPT], v1[QPT];
+#pragma unroll
+        for (int k = 0; k < QPT; ++k) {
+            const int p = 4 * (tid + k * NT);
+            if (a4 + p < b) {
+                c[k] = ld_v4(A.col + a4 + p, pol);
+                v0[k] = ld_v2d(A.val + a4 + p, pol);
+                v1[k] = ld_v2d(A.val + a4 + p + 2, pol);
+            }
+        }
+        double xv[QPT][4];
+#pragma unroll
+        for (int k = 0; k < QPT; ++k) {
+            const int p = 4 * (tid + k * NT);
+            if (a4 + p < b) {
+                xv[k][0] = (p + 0 >= lo && p + 0 < hi) ? ldx<XSPLIT>(A, c[k].x) : 0.0;
+                xv[k][1] = (p + 1 >= lo && p + 1 < hi) ? ldx<XSPLIT>(A, c[k].y) : 0.0;
+                xv[k][2] = (p + 2 >= lo && p + 2 < hi) ? ldx<XSPLIT>(A, c[k].z) : 0.0;
+                xv[k][3] = (p + 3 >= lo && p + 3 < hi) ? ldx<XSPLIT>(A, c[k].w) : 0.0;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < QPT; ++k) {
+            const int p = 4 * (tid + k * NT);
+            if (a4 + p < b) {
+                double2 w0, w1;
+                w0.x = v0[k].x * xv[k][0]; w0.y = v0[k].y * xv[k][1];
+                w1.x = v1[k].x * xv[k][2]; w1.y = v1[k].y * xv[k][3];
+                *reinterpret_cast<double2*>(&sm.prod[p]) = w0;
+                *reinterpret_cast<double2*>(&sm.prod[p + 2]) = w1;
+            }
+        }
+    }
+    __syncthreads();
+
+    // ------------------------------------------------------- row sums
+    if (cls >= kTileShort) {
+        // every row <= 32 nonzeros: V lanes per row (vector-per-row, V chosen
+        // at plan time for 512 threads; halved per halving of NT, >= 1).
+        int V = cls * NT / 512;
+        if (V < 1) V = 1;
+        for (int rb = 0; rb < nr; rb += NT / V) {
+            const int r = rb + tid / V;
+            const int j = tid % V;
+            double acc = 0.0;
+            if (r < nr) {
+                const int p1 = sm.so[r + 1];
+                for (int p = sm.so[r] + j; p < p1; p += V) acc += sm.prod[p];
+            }
+            for (int off = V >> 1; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+            if (r < nr && j == 0) {
+                A.y[r0 + r] = acc;
+                mx = fmax(mx, fabs(acc));
+            }
+        }
+    } else {
+        // short rows: one thread each; long rows: listed, then one warp each
+        for (int r = tid; r < nr; r += NT) {
+            const int p0 = sm.so[r], p1 = sm.so[r + 1];
+            if (p1 - p0 <= kShortRow) {
+                double acc = 0.0;
+                for (int p = p0; p < p1; ++p) acc += sm.prod[p];
+                A.y[r0 + r] = acc;
+                mx = fmax(mx, fabs(acc));
+            } else {
+                sm.longrows[atomicAdd(&sm.nlong, 1)] = r;    // order irrelevant: each row is summed
+            }                                                // by one warp in a fixed order
+        }
+        __syncthreads();
+        const int warp = tid >> 5, lane = tid & 31;
+        for (int k = warp; k < sm.nlong; k += NT / 32) {
+            const int r = sm.longrows[k];
+            const int p0 = sm.so[r], p1 = sm.so[r + 1];
+            double acc = 0.0;
+            for (int p = p0 + lane; p < p1; p += 32) acc += sm.prod[p];
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+            if (lane == 0) {
+                A.y[r0 + r] = acc;
+                mx = fmax(mx, fabs(acc));
+            }
+        }
+    }
+    if (A.maxabs_slots) {   // one atomicMax per warp, no extra barrier
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+        if ((tid & 31) == 0 && mx > 0.0)
+            atomicMax(A.maxabs_slots + ((t * (NT / 32) + (tid >> 5)) & (kMaxSlots - 1)) * kSlotStride,
+                      (unsigned long long)__double_as_longlong(mx));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// spmv_rowseg_kernel: same tile geometry and streaming as above, but the
+// products never touch shared memory (the L1TEX pipe is shared by the x
+// gathers and shared-memory wavefronts; ncu: 69 % busy on C5 with staging).
+// Thread q keeps the products of positions 4q..4q+3 in registers and walks
+// them against the tile's row offsets: rows that start and end inside its
+// quad are stored at once; a row running across threads is completed with a
+// segmented inclusive scan over the threads (warp shuffles, then one carry
+// per warp through shared memory), in a fixed order -- deterministic.
+// ---------------------------------------------------------------------------
+struct SegSmem {
+    int32_t so[kTileRows + 1];
+    double wv[kRT / 32];            // per warp: scan value at lane 31
+    int32_t wf[kRT / 32];           // per warp: a chain reset happened in the warp
+    int32_t wh[kRT / 32];           // per warp: lane 31 carries a row into the next warp
+    double red[kRT / 32];
+};
+
+template <bool XSPLIT>
+__global__ void __launch_bounds__(kRT, 3) spmv_rowseg_kernel(const RowTileArgs A) {
+    __shared__ __align__(16) SegSmem sm;
+    const int t = blockIdx.x;
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int r0 = A.tile_row[t], r1 = A.tile_row[t + 1];
+    const int a = A.tile_nnz[t], b = A.tile_nnz[t + 1];
     const int nr = r1 - r0;
     const int a4 = a & ~3;
     const uint64_t pol = pol_evict_first();
@@ -102,7 +265,7 @@ __global__ void __launch_bounds__(kRT, 3) spmv_rowtile_kernel(const RowTileArgs 
         }
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-        if ((tid & 31) == 0) sm.red[tid >> 5] = acc;
+        if (lane == 0) sm.red[warp] = acc;
         __syncthreads();
         if (tid == 0) {
             double tot = 0.0;
@@ -115,98 +278,137 @@ __global__ void __launch_bounds__(kRT, 3) spmv_rowtile_kernel(const RowTileArgs 
         return;
     }
 
-    // ------------------------------------------------ stage products, so[]
+    // -------------------------------------------- stream, gather, products
     for (int j = tid; j <= nr; j += kRT) sm.so[j] = A.rowptr[r0 + j] - a4;
-    if (tid == 0) sm.nlong = 0;
-    {
-        const int q = tid;                               // quad of positions 4q..4q+3
-        const int p = 4 * q;
-        if (a4 + p < b) {
-            const int4 c = ld_v4(A.col + a4 + p, pol);
-            const double2 v0 = ld_v2d(A.val + a4 + p, pol);
-            const double2 v1 = ld_v2d(A.val + a4 + p + 2, pol);
-            const int lo = a - a4, hi = b - a4;
-            const double x0 = (p + 0 >= lo && p + 0 < hi) ? ldx<XSPLIT>(A, c.x) : 0.0;
-            const double x1 = (p + 1 >= lo && p + 1 < hi) ? ldx<XSPLIT>(A, c.y) : 0.0;
-            const double x2 = (p + 2 >= lo && p + 2 < hi) ? ldx<XSPLIT>(A, c.z) : 0.0;
-            const double x3 = (p + 3 >= lo && p + 3 < hi) ? ldx<XSPLIT>(A, c.w) : 0.0;
-            double2 w0, w1;
-            w0.x = v0.x * x0; w0.y = v0.y * x1;
-            w1.x = v1.x * x2; w1.y = v1.y * x3;
-            *reinterpret_cast<double2*>(&sm.prod[p]) = w0;
-            *reinterpret_cast<double2*>(&sm.prod[p + 2]) = w1;
-        }
+    const int pq = 4 * tid;
+    const int lo = a - a4, hi = b - a4;
+    const int e_lo = max(pq, lo), e_hi = min(pq + 4, hi);
+    const bool act = e_lo < e_hi;
+    double pv[4] = {0.0, 0.0, 0.0, 0.0};
+    if (a4 + pq < b) {
+        const int4 c = ld_v4(A.col + a4 + pq, pol);
+        const double2 v0 = ld_v2d(A.val + a4 + pq, pol);
+        const double2 v1 = ld_v2d(A.val + a4 + pq + 2, pol);
+        const double x0 = (pq + 0 >= lo && pq + 0 < hi) ? ldx<XSPLIT>(A, c.x) : 0.0;
+        const double x1 = (pq + 1 >= lo && pq + 1 < hi) ? ldx<XSPLIT>(A, c.y) : 0.0;
+        const double x2 = (pq + 2 >= lo && pq + 2 < hi) ? ldx<XSPLIT>(A, c.z) : 0.0;
+        const double x3 = (pq + 3 >= lo && pq + 3 < hi) ? ldx<XSPLIT>(A, c.w) : 0.0;
+        pv[0] = v0.x * x0; pv[1] = v0.y * x1; pv[2] = v1.x * x2; pv[3] = v1.y * x3;
     }
-    __syncthreads();
+    __syncthreads();                                     // so[] staged
 
-    // ------------------------------------------------------- row sums
-    if (cls >= kTileShort) {
-        // every row <= 32 nonzeros: V = cls lanes per row (vector-per-row,
-        // V chosen at plan time so nr*V <= 512); lane j sums positions
-        // p0+j, p0+j+V, ... serially, then a fixed xor-shuffle tree.
-        const int V = cls;
-        const int r = tid / V;
-        const int j = tid - r * V;
-        double acc = 0.0;
-        if (r < nr) {
-            const int p1 = sm.so[r + 1];
-            for (int p = sm.so[r] + j; p < p1; p += V) acc += sm.prod[p];
+    for (int r = tid; r < nr; r += kRT)                  // empty rows: y = +0 (A5)
+        if (sm.so[r] == sm.so[r + 1]) A.y[r0 + r] = 0.0;
+
+    // ------------------------------------------------ walk the quad
+    double v = 0.0;          // scan input: chain value leaving this thread
+    bool f = true;           // chain reset at this thread
+    bool carry = false;      // this thread's last row continues in the next thread
+    int head_row = -1;
+    double head_sum = 0.0;
+    bool head_ends = false;
+    if (act) {
+        int lo_r = 0, hi_r = nr - 1;                     // last row with so(r) <= e_lo
+        while (lo_r < hi_r) {
+            const int mid = (lo_r + hi_r + 1) >> 1;
+            if (sm.so[mid] <= e_lo) lo_r = mid; else hi_r = mid - 1;
         }
-        for (int off = V >> 1; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-        if (r < nr && j == 0) {
-            A.y[r0 + r] = acc;
-            mx = acc < 0 ? -acc : acc;
-        }
-    } else {
-        // short rows: one thread each; long rows: listed, then one warp each
-        for (int r = tid; r < nr; r += kRT) {
-            const int p0 = sm.so[r], p1 = sm.so[r + 1];
-            if (p1 - p0 <= kShortRow) {
-                double acc = 0.0;
-                for (int p = p0; p < p1; ++p) acc += sm.prod[p];
-                A.y[r0 + r] = acc;
-                mx = fmax(mx, fabs(acc));
-            } else {
-                sm.longrows[atomicAdd(&sm.nlong, 1)] = r;    // order irrelevant: each row is summed
-            }                                                // by one warp in a fixed order
-        }
-        __syncthreads();
-        const int warp = tid >> 5, lane = tid & 31;
-        for (int k = warp; k < sm.nlong; k += kRT / 32) {
-            const int r = sm.longrows[k];
-            const int p0 = sm.so[r], p1 = sm.so[r + 1];
-            double acc = 0.0;
-            for (int p = p0 + lane; p < p1; p += 32) acc += sm.prod[p];
+        int row = lo_r;
+        int end = sm.so[row + 1];
+        head_row = row;
+        bool in_head = true;
+        double cur = 0.0;
 #pragma unroll
-            for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-            if (lane == 0) {
-                A.y[r0 + r] = acc;
-                mx = fmax(mx, fabs(acc));
+        for (int u = 0; u < 4; ++u) {
+            const int p = pq + u;
+            if (p >= e_lo && p < e_hi) {
+                while (p >= end) {
+                    if (in_head) { head_sum = cur; head_ends = true; in_head = false; }
+                    else { A.y[r0 + row] = cur; mx = fmax(mx, fabs(cur)); }   // row inside the quad
+                    cur = 0.0;
+                    ++row;
+                    end = sm.so[row + 1];
+                }
+                cur += pv[u];
             }
         }
+        if (in_head) {                                   // one row covers the whole quad
+            head_sum = cur;
+            if (end <= e_hi) head_ends = true;           // ... and ends here
+            else { f = false; carry = true; v = cur; }   // ... and runs on: pass the chain
+        } else if (end <= e_hi) {                        // last row also ends here
+            A.y[r0 + row] = cur;
+            mx = fmax(mx, fabs(cur));
+        } else {                                         // last row runs on: start a chain
+            carry = true;
+            v = cur;
+        }
+    }
+
+    // -------------------------- segmented inclusive scan of chain values
+    double S = v;
+    bool F = f;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const double Su = __shfl_up_sync(0xffffffffu, S, d);
+        const bool Fu = __shfl_up_sync(0xffffffffu, F ? 1 : 0, d) != 0;
+        if (lane >= d) {
+            if (!F) S = Su + S;
+            F = F || Fu;
+        }
+    }
+    if (lane == 31) {
+        sm.wv[warp] = S;
+        sm.wf[warp] = F ? 1 : 0;
+        sm.wh[warp] = carry ? 1 : 0;
+    }
+    __syncthreads();
+    // carry into this warp's lane 0: out_k = wf[k] ? wv[k] : c + wv[k],
+    // c = wh[k] ? out_k : 0, over earlier warps in order (fixed order)
+    double cin = 0.0;
+    for (int k = 0; k < warp; ++k) {
+        const double out = sm.wf[k] ? sm.wv[k] : cin + sm.wv[k];
+        cin = sm.wh[k] ? out : 0.0;
+    }
+    const double Sfull = F ? S : cin + S;
+    const double Sprev = __shfl_up_sync(0xffffffffu, Sfull, 1);
+    const bool cprev = __shfl_up_sync(0xffffffffu, carry ? 1 : 0, 1) != 0;
+    const double carry_in = (lane == 0) ? cin : (cprev ? Sprev : 0.0);
+    if (act && head_ends) {
+        const double tot = carry_in + head_sum;
+        A.y[r0 + head_row] = tot;
+        mx = fmax(mx, fabs(tot));
     }
     if (A.maxabs_slots) {
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-        __syncthreads();
-        if ((tid & 31) == 0) sm.red[tid >> 5] = mx;
-        __syncthreads();
-        if (tid == 0) {
-            double m = 0.0;
-            for (int w = 0; w < kRT / 32; ++w) m = fmax(m, sm.red[w]);
-            if (m > 0.0)
-                atomicMax(A.maxabs_slots + (t & (kMaxSlots - 1)) * kSlotStride,
-                          (unsigned long long)__double_as_longlong(m));
-        }
+        if (lane == 0 && mx > 0.0)
+            atomicMax(A.maxabs_slots + ((t * (kRT / 32) + warp) & (kMaxSlots - 1)) * kSlotStride,
+                      (unsigned long long)__double_as_longlong(mx));
     }
 }
 
 }  // namespace
 
-cudaError_t launch_rowtile(const RowTileArgs& a, bool xsplit, cudaStream_t s) {
+cudaError_t launch_rowtile(const RowTileArgs& a, bool xsplit, int nt, cudaStream_t s) {
     if (a.n_tiles <= 0) return cudaSuccess;
-    if (xsplit) spmv_rowtile_kernel<true><<<a.n_tiles, kRT, 0, s>>>(a);
-    else spmv_rowtile_kernel<false><<<a.n_tiles, kRT, 0, s>>>(a);
+    if (nt == 256) {
+        if (xsplit) spmv_rowtile_kernel<true, 256><<<a.n_tiles, 256, 0, s>>>(a);
+        else spmv_rowtile_kernel<false, 256><<<a.n_tiles, 256, 0, s>>>(a);
+    } else if (nt == 128) {
+        if (xsplit) spmv_rowtile_kernel<true, 128><<<a.n_tiles, 128, 0, s>>>(a);
+        else spmv_rowtile_kernel<false, 128><<<a.n_tiles, 128, 0, s>>>(a);
+    } else {
+        if (xsplit) spmv_rowtile_kernel<true, 512><<<a.n_tiles, 512, 0, s>>>(a);
+        else spmv_rowtile_kernel<false, 512><<<a.n_tiles, 512, 0, s>>>(a);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rowseg(const RowTileArgs& a, bool xsplit, cudaStream_t s) {
+    if (a.n_tiles <= 0) return cudaSuccess;
+    if (xsplit) spmv_rowseg_kernel<true><<<a.n_tiles, kRT, 0, s>>>(a);
+    else spmv_rowseg_kernel<false><<<a.n_tiles, kRT, 0, s>>>(a);
     return cudaGetLastError();
 }
 

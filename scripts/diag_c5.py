@@ -21,7 +21,7 @@ for mode in range(4):
 out["spmv_ms"] = timeit(lambda: sp.spmv_apply(h, x, y), reps=5)
 if os.environ.get("AB"):
     q = synth.make(w)
-    for k in ("pipe", "tile"):
+    for k in ("rowtile512", "rowtile128"):
         os.environ["SPMV_KERNEL"] = k
         h2 = sp.spmv_create(q.m, q.n, q.row_ptr, q.col, q.val, row_perm=q.row_perm, col_perm=q.col_perm, blocks=q.blocks)
         out[f"spmv_{k}_ms"] = timeit(lambda: sp.spmv_apply(h2, x, y), reps=5)
