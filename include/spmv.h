@@ -216,6 +216,15 @@ spmv_status_t spmv_diag_gather(const double* x, int64_t n, int64_t count, double
 spmv_status_t spmv_diag_gather_mode(const double* x, int64_t n, int64_t count, int32_t mode, int32_t blocks_per_sm,
                                     double* out_dev, void* stream);   /* gather flavours 0..7, see diag.cu */
 spmv_status_t spmv_diag_csr(spmv_handle_t h, const double* x, int32_t mode, double* out_dev, void* stream);
+/* Design microbenchmarks (diag2.cu): kind 1 L2->SM LDG.128 bandwidth over the
+ * L2-resident `buf` (`bytes` long, `count` bytes read in total); kind 2 bulk-copy
+ * L2->shared bandwidth, param = cluster size 1/2/4/8 (multicast when > 1),
+ * `count` bytes delivered per launch over all CTAs; kind 3 shared-memory
+ * y[r] += v*x[c] updates (`buf` unused, `count` updates, param 0 random /
+ * 1 conflict-free); kind 4 L2 gathers with `param` lanes per 128-byte line
+ * (`buf` = x of `bytes`, `count` gathers).  USAGE on bad arguments. */
+spmv_status_t spmv_diag_micro(int32_t kind, int32_t param, const void* buf, int64_t bytes, int64_t count,
+                              double* out_dev, void* stream);
 
 /* Writes a fresh 128-byte NCCL unique id into out (len >= 128). */
 spmv_status_t spmv_nccl_unique_id(void* out, size_t len);

@@ -34,7 +34,7 @@ SPMV_SPLIT_LITERAL = 4
 EXPORTED = ["spmv_create", "spmv_apply", "spmv_split_apply", "spmv_destroy", "spmv_get_info",
             "spmv_maxabs", "spmv_normalize", "spmv_debug_copy_csr", "spmv_nccl_unique_id",
             "spmv_status_string", "spmv_last_error", "spmv_version", "spmv_shard_plan",
-            "spmv_diag_read", "spmv_diag_gather", "spmv_diag_csr", "spmv_diag_gather_mode"]
+            "spmv_diag_read", "spmv_diag_gather", "spmv_diag_csr", "spmv_diag_gather_mode", "spmv_diag_micro"]
 
 
 class SpmvError(RuntimeError):
@@ -91,6 +91,7 @@ def lib():
         L.spmv_diag_gather.argtypes = [vp, i64, i64, vp, vp]
         L.spmv_diag_csr.argtypes = [vp, vp, i32, vp, vp]
         L.spmv_diag_gather_mode.argtypes = [vp, i64, i64, i32, i32, vp, vp]
+        L.spmv_diag_micro.argtypes = [i32, i32, vp, i64, i64, vp, vp]
         L.spmv_shard_plan.argtypes = [vp, i64, i64, i32, i32, vp]
         L.spmv_status_string.argtypes = [i32]
         L.spmv_status_string.restype = ctypes.c_char_p
@@ -280,6 +281,11 @@ def spmv_diag_gather_mode(x, count: int, mode: int, out, blocks_per_sm: int = 8,
     _check(lib().spmv_diag_gather_mode(ctypes.c_void_p(_dev(x)), x.numel(), count, mode, blocks_per_sm,
                                        ctypes.c_void_p(_dev(out)), ctypes.c_void_p(_stream(stream))),
            "spmv_diag_gather_mode")
+
+
+def spmv_diag_micro(kind: int, param: int, buf, nbytes: int, count: int, out, stream=None):
+    _check(lib().spmv_diag_micro(kind, param, ctypes.c_void_p(_dev(buf) if buf is not None else 0), nbytes, count,
+                                 ctypes.c_void_p(_dev(out)), ctypes.c_void_p(_stream(stream))), "spmv_diag_micro")
 
 
 def spmv_diag_csr(h, x, mode: int, out, stream=None):

@@ -34,6 +34,7 @@ def _nccl_dir() -> str:
 SOURCES = {
     "kernels.cu": "cu",
     "diag.cu": "cu",
+    "diag2.cu": "cu",
     "pipe.cu": "cu",
     "rowtile.cu": "cu",
     "split.cu": "cu",

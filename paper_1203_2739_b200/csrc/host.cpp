@@ -919,4 +919,11 @@ spmv_status_t spmv_diag_csr(spmv_handle_t h, const double* x, int32_t mode, doub
     return SPMV_OK;
 }
 
+spmv_status_t spmv_diag_micro(int32_t kind, int32_t param, const void* buf, int64_t bytes, int64_t count,
+                              double* out_dev, void* stream) {
+    if (!out_dev || count < 1 || (kind != 3 && (!buf || bytes < 16))) return fail(SPMV_ERR_USAGE, "diag_micro: bad arguments");
+    CUDA_TRY(spmvb::diag_micro(kind, param, buf, bytes, count, out_dev, (cudaStream_t)stream));
+    return SPMV_OK;
+}
+
 }  // extern "C"

@@ -84,5 +84,7 @@ cudaError_t diag_gather_mode(const double* x, int64_t n, int64_t count, int mode
                              cudaStream_t s);
 cudaError_t diag_csr(const int32_t* col, const double* val, const double* x, int64_t nnz, int mode, double* out,
                      cudaStream_t s);
+cudaError_t diag_micro(int kind, int param, const void* buf, int64_t bytes, int64_t count, double* out,
+                       cudaStream_t s);
 
 }  // namespace spmvb
