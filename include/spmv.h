@@ -159,9 +159,15 @@ typedef struct {
     int64_t bytes_alg;            /* 12 nnz + 4 (m+1) + 8 m + 8 n_touched, local */
     int64_t bytes_alg_split;      /* same for the fused split pass (0 without a split) */
     int64_t split_segments;       /* (row, part) segments of the split layout */
+    int64_t xs_panels;            /* x-staged kernel: panels (0 when that kernel is not used) */
+    int64_t xs_groups;            /* x-staged kernel: 32-entry groups (interior + border) */
+    int64_t xs_pad_slots;         /* x-staged kernel: padding slots among them */
+    int64_t bytes_stream;         /* device bytes the apply kernel actually reads + writes (no x reuse) */
     int32_t n_parts, rank, world, kind;
     int32_t has_owner_map;        /* spmv_normalize is available */
-    int32_t reserved[3];
+    int32_t kernel;               /* single-SpMxV kernel: 6 x-staged (SB default), 0 row-tile (default
+                                     otherwise); 1-5 measurement variants (SPMV_KERNEL env) */
+    int32_t reserved[2];
 } spmv_info_t;
 
 spmv_status_t spmv_get_info(spmv_handle_t h, spmv_info_t* info);
@@ -216,6 +222,17 @@ spmv_status_t spmv_diag_gather(const double* x, int64_t n, int64_t count, double
 spmv_status_t spmv_diag_gather_mode(const double* x, int64_t n, int64_t count, int32_t mode, int32_t blocks_per_sm,
                                     double* out_dev, void* stream);   /* gather flavours 0..7, see diag.cu */
 spmv_status_t spmv_diag_csr(spmv_handle_t h, const double* x, int32_t mode, double* out_dev, void* stream);
+/* Host-only test hook of the x-staged kernel's planner (plan_xs.cpp): packs a
+ * PERMUTED CSR (rows sorted by column, world-1 column ids) with an SB
+ * descriptor into panels/groups exactly as spmv_create does, decodes the
+ * packed streams again and compares them with the CSR bit for bit (and the
+ * format's invariants).  stats[6] = panels, interior groups, border groups,
+ * interior padding slots, border padding slots, nonzeros packed.  OK when the
+ * round trip is exact; INTERNAL (message in spmv_last_error) when not;
+ * UNSUPPORTED when the matrix does not fit the format. */
+spmv_status_t spmv_xs_plan_check(int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
+                                 const spmv_blocks_t* blocks, int64_t rows_target, int64_t* stats);
+
 /* Design microbenchmarks (diag2.cu): kind 1 L2->SM LDG.128 bandwidth over the
  * L2-resident `buf` (`bytes` long, `count` bytes read in total); kind 2 bulk-copy
  * L2->shared bandwidth, param = cluster size 1/2/4/8 (multicast when > 1),

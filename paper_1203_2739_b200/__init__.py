@@ -34,7 +34,8 @@ SPMV_SPLIT_LITERAL = 4
 EXPORTED = ["spmv_create", "spmv_apply", "spmv_split_apply", "spmv_destroy", "spmv_get_info",
             "spmv_maxabs", "spmv_normalize", "spmv_debug_copy_csr", "spmv_nccl_unique_id",
             "spmv_status_string", "spmv_last_error", "spmv_version", "spmv_shard_plan",
-            "spmv_diag_read", "spmv_diag_gather", "spmv_diag_csr", "spmv_diag_gather_mode", "spmv_diag_micro"]
+            "spmv_diag_read", "spmv_diag_gather", "spmv_diag_csr", "spmv_diag_gather_mode", "spmv_diag_micro",
+            "spmv_xs_plan_check"]
 
 
 class SpmvError(RuntimeError):
@@ -58,9 +59,10 @@ class spmv_info_t(ctypes.Structure):
     _fields_ = [(k, ctypes.c_int64) for k in (
         "m", "n", "nnz", "m_local", "nnz_local", "row_begin", "x_local_len", "x_interior_begin",
         "x_interior_len", "x_border_begin", "x_border_len", "border_total", "n_tiles", "n_long_rows",
-        "bytes_alg", "bytes_alg_split", "split_segments")] + [
-        (k, ctypes.c_int32) for k in ("n_parts", "rank", "world", "kind", "has_owner_map")] + [
-        ("reserved", ctypes.c_int32 * 3)]
+        "bytes_alg", "bytes_alg_split", "split_segments", "xs_panels", "xs_groups", "xs_pad_slots",
+        "bytes_stream")] + [
+        (k, ctypes.c_int32) for k in ("n_parts", "rank", "world", "kind", "has_owner_map", "kernel")] + [
+        ("reserved", ctypes.c_int32 * 2)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
@@ -92,6 +94,7 @@ def lib():
         L.spmv_diag_csr.argtypes = [vp, vp, i32, vp, vp]
         L.spmv_diag_gather_mode.argtypes = [vp, i64, i64, i32, i32, vp, vp]
         L.spmv_diag_micro.argtypes = [i32, i32, vp, i64, i64, vp, vp]
+        L.spmv_xs_plan_check.argtypes = [i64, i64, vp, vp, vp, vp, i64, vp]
         L.spmv_shard_plan.argtypes = [vp, i64, i64, i32, i32, vp]
         L.spmv_status_string.argtypes = [i32]
         L.spmv_status_string.restype = ctypes.c_char_p
@@ -210,6 +213,20 @@ def spmv_create(m: int, n: int, row_ptr, col_idx, val, row_perm=None, col_perm=N
                            int(n_parts if pa is not None else 0), _addr(pa), dptr, ctypes.byref(out))
     _check(st, "spmv_create")
     return Handle(out.value)
+
+
+def spmv_xs_plan_check(m: int, n: int, row_ptr, col, val, blocks, rows_target: int) -> dict:
+    """Host-only round trip of the x-staged planner (see spmv.h); raises on mismatch."""
+    rp = _np(row_ptr, np.int64)
+    ci = _np(col, np.int32)
+    va = _np(val, np.float64)
+    rbp = _np(blocks["row_block_ptr"], np.int64)
+    cbp = _np(blocks["col_block_ptr"], np.int64)
+    b = _Blocks(int(blocks["kind"]), int(blocks["K"]), rbp.ctypes.data, cbp.ctypes.data, None)
+    stats = np.zeros(6, dtype=np.int64)
+    _check(lib().spmv_xs_plan_check(m, n, _addr(rp), _addr(ci), _addr(va), ctypes.byref(b), rows_target,
+                                    stats.ctypes.data), "spmv_xs_plan_check")
+    return dict(zip(("panels", "groups_i", "groups_b", "pad_i", "pad_b", "entries"), (int(v) for v in stats)))
 
 
 def spmv_apply(h, x, y, flags: int = 0, stream=None, x_len: int | None = None, y_len: int | None = None):

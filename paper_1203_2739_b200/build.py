@@ -38,9 +38,11 @@ SOURCES = {
     "pipe.cu": "cu",
     "rowtile.cu": "cu",
     "split.cu": "cu",
+    "xstage.cu": "cu",
+    "plan_xs.cpp": "cpp",
     "host.cpp": "cpp",
 }
-HEADERS = ["internal.h", os.path.join("..", "..", "include", "spmv.h")]
+HEADERS = ["internal.h", "plan_xs.h", os.path.join("..", "..", "include", "spmv.h")]
 
 
 def _newer(target: str, deps) -> bool:

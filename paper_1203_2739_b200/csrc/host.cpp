@@ -28,6 +28,7 @@
 
 #include "../../include/spmv.h"
 #include "internal.h"
+#include "plan_xs.h"
 
 using spmvb::kTileNnz;
 using spmvb::kTileRows;
@@ -98,7 +99,20 @@ struct spmv_plan_s {
     int32_t* d_tile_nnz = nullptr;    // [T+1] row_ptr[tile_row[t]]
     int* d_counter = nullptr;         // tile-claim counter of the pipe kernel
     int32_t* d_tile_cls = nullptr;    // [T] tile class (internal.h)
-    int kernel = 0;                   // 0 rowtile/256 (default), 1 pipe, 2 tile, 3 rowtile/512, 4 rowseg
+    int kernel = 0;                   // 0 rowtile/256, 1 pipe, 2 tile, 3 rowtile/512, 4 rowseg, 5 rowtile/128,
+                                      // 6 x-staged (default for SB handles)
+    // x-staged kernel (xstage.cu)
+    spmvb::XsPanel* d_xs_panel = nullptr;
+    int32_t* d_xs_wg = nullptr;
+    int32_t* d_xs_wb = nullptr;
+    int32_t* d_xs_U = nullptr;
+    double* d_xs_gval = nullptr;
+    uint32_t* d_xs_gidx = nullptr;
+    double* d_xs_bval = nullptr;
+    uint32_t* d_xs_bidx = nullptr;
+    int32_t xs_cbits = 0;
+    int64_t xs_panels = 0, xs_groups = 0, xs_pad = 0, xs_gb = 0;
+    int64_t bytes_stream = 0;
     int32_t* d_tile_seg = nullptr;    // [T*K+1]
     int32_t* d_seg_ptr = nullptr;     // [S+1]
     int32_t* d_seg_row = nullptr;     // [S]
@@ -252,6 +266,89 @@ spmv_status_t spmv_shard_plan(const spmv_blocks_t* blocks, int64_t m, int64_t n,
     out->x_border_begin = bo(b0);
     out->x_border_len = bo(b1) - bo(b0);
     out->x_local_len = out->x_interior_len + out->x_border_len;
+    return SPMV_OK;
+}
+
+// Builds and uploads the x-staged kernel's panels (plan_xs.cpp).  Leaves the
+// handle on the row-tile kernel when the matrix does not fit the format.
+static spmv_status_t plan_xs(spmv_plan_s* h, const std::vector<int64_t>& rp, const std::vector<int32_t>& pcol,
+                             const std::vector<double>& pval, const std::vector<int64_t>& rbp,
+                             const std::vector<int64_t>& cbp) {
+    const int K = (int)rbp.size() - 2;
+    const int64_t R0 = h->row_begin, R1 = h->row_begin + h->m_loc;
+    std::vector<spmvb::XsBlockIn> bl;
+    for (int k = 0; k < K; ++k) {
+        if (rbp[k + 1] <= R0 || rbp[k] >= R1) continue;
+        spmvb::XsBlockIn b;
+        b.r0 = rbp[k] - R0;
+        b.r1 = rbp[k + 1] - R0;
+        const int64_t q0 = h->world > 1 ? h->x_int_begin : 0;
+        b.c0 = cbp[k] - q0;
+        b.c1 = cbp[k + 1] - q0;
+        bl.push_back(b);
+    }
+    const int64_t gb = h->world > 1 ? h->x_int_len : cbp[K];
+    h->xs_gb = gb;
+    const int64_t target = std::min<int64_t>(spmvb::kXsRowsMax,
+                                             std::max<int64_t>(256, h->m / (3 * (int64_t)spmvb::kernel_num_sms())));
+    std::vector<spmvb::XsPanelData> pd;
+    spmvb::XsPlanStats st;
+    std::string why;
+    int cbits = 0;
+    if (!spmvb::plan_xstage(rp, pcol, pval, bl, gb, h->border_total, target, pd, cbits, st, why)) return SPMV_OK;
+    if (st.entries != h->nnz_loc) return fail(SPMV_ERR_INTERNAL, "x-staged plan lost nonzeros (%lld of %lld)",
+                                              (long long)st.entries, (long long)h->nnz_loc);
+    const int NW = spmvb::kXsWarps;
+    const int64_t P = (int64_t)pd.size();
+    std::vector<spmvb::XsPanel> desc(P);
+    std::vector<int32_t> wg(P * NW + 1), wb(P * NW + 1);
+    int64_t gi = 0, gbn = 0, nu = 0;
+    for (int64_t p = 0; p < P; ++p) {
+        desc[p] = pd[p].desc;
+        for (int w = 0; w < NW; ++w) {
+            wg[p * NW + w] = (int32_t)gi;
+            wb[p * NW + w] = (int32_t)gbn;
+            gi += pd[p].g_cnt[w];
+            gbn += pd[p].b_cnt[w];
+        }
+        nu += (int64_t)NW * pd[p].desc.nch;
+    }
+    wg[P * NW] = (int32_t)gi;
+    wb[P * NW] = (int32_t)gbn;
+    spmv_status_t s;
+    if ((s = upload(h, &h->d_xs_panel, desc.data(), P))) return s;
+    if ((s = upload(h, &h->d_xs_wg, wg.data(), P * NW + 1))) return s;
+    if ((s = upload(h, &h->d_xs_wb, wb.data(), P * NW + 1))) return s;
+    if ((s = dalloc(h, &h->d_xs_U, std::max<int64_t>(nu, 1)))) return s;
+    if ((s = dalloc(h, &h->d_xs_gval, gi * 32))) return s;
+    if ((s = dalloc(h, &h->d_xs_gidx, gi * 32))) return s;
+    if ((s = dalloc(h, &h->d_xs_bval, gbn * 32))) return s;
+    if ((s = dalloc(h, &h->d_xs_bidx, gbn * 32))) return s;
+    for (int64_t p = 0; p < P; ++p) {
+        spmvb::XsPanelData& D = pd[p];
+        const int64_t go = wg[p * NW], bo = wb[p * NW];
+        if (!D.u_rel.empty() && D.desc.nch)
+            CUDA_TRY(cudaMemcpy(h->d_xs_U + D.desc.u_base, D.u_rel.data(), (size_t)NW * D.desc.nch * 4,
+                                cudaMemcpyHostToDevice));
+        if (!D.gval.empty()) {
+            CUDA_TRY(cudaMemcpy(h->d_xs_gval + go * 32, D.gval.data(), D.gval.size() * 8, cudaMemcpyHostToDevice));
+            CUDA_TRY(cudaMemcpy(h->d_xs_gidx + go * 32, D.gidx.data(), D.gidx.size() * 4, cudaMemcpyHostToDevice));
+        }
+        if (!D.bval.empty()) {
+            CUDA_TRY(cudaMemcpy(h->d_xs_bval + bo * 32, D.bval.data(), D.bval.size() * 8, cudaMemcpyHostToDevice));
+            CUDA_TRY(cudaMemcpy(h->d_xs_bidx + bo * 32, D.bidx.data(), D.bidx.size() * 4, cudaMemcpyHostToDevice));
+        }
+        std::vector<double>().swap(D.gval);
+        std::vector<uint32_t>().swap(D.gidx);
+        std::vector<double>().swap(D.bval);
+        std::vector<uint32_t>().swap(D.bidx);
+    }
+    h->xs_cbits = cbits;
+    h->xs_panels = P;
+    h->xs_groups = gi + gbn;
+    h->xs_pad = st.pad_i + st.pad_b;
+    h->bytes_stream = 12 * 32 * (gi + gbn) + 8 * (P * NW + 1) * 2 + 4 * nu + 8 * h->m_loc;
+    h->kernel = 6;
     return SPMV_OK;
 }
 
@@ -561,6 +658,7 @@ static spmv_status_t create_impl(int64_t m, int64_t n, int64_t nnz, const int64_
         if (kenv && strcmp(kenv, "rowseg") == 0) h->kernel = 4;
         if (kenv && strcmp(kenv, "rowtile128") == 0) h->kernel = 5;
     }
+    h->bytes_stream = 12 * nnz_loc + 4 * (m_loc + 1) + 8 * m_loc;
 
     // -------------------------------------------- split layout (a8)
     // Within each row tile the nonzeros are regrouped part-major: for k = 0..K-1,
@@ -623,6 +721,15 @@ static spmv_status_t create_impl(int64_t m, int64_t n, int64_t nnz, const int64_
         if ((s = upload(h, &h->d_seg_row, seg_row.data(), S))) return s;
         if ((s = upload(h, &h->d_scol, scol.data(), nnz_loc, nnz_loc + kPad))) return s;
         if ((s = upload(h, &h->d_sval, sval.data(), nnz_loc, nnz_loc + kPad))) return s;
+    }
+
+    // ------------------------------------ x-staged plan (SB handles, a5/a6)
+    {
+        const char* kenv = getenv("SPMV_KERNEL");
+        const bool want = blocks && h->kind == SPMV_SB && (!kenv || strcmp(kenv, "xstage") == 0) && nnz_loc > 0;
+        if (want) {
+            if ((s = plan_xs(h, rp, pcol, pval, rbp, cbp))) return s;
+        }
     }
 
     // -------------------------------------- ORIGINAL-mode maps (a3, a7)
@@ -712,6 +819,8 @@ static spmv_status_t check_vectors(spmv_handle_t h, const double* x, int64_t x_l
     if ((!x && x_len) || (!y && y_len)) return fail(SPMV_ERR_USAGE, "NULL vector");
     if ((const void*)x == (const void*)y && x) return fail(SPMV_ERR_USAGE, "x and y alias");
     if (((uintptr_t)x & 7) || ((uintptr_t)y & 7)) return fail(SPMV_ERR_USAGE, "x/y not 8-byte aligned");
+    if (h->kernel == 6 && !(flags & SPMV_VEC_ORIGINAL) && ((uintptr_t)x & 15))
+        return fail(SPMV_ERR_USAGE, "x not 16-byte aligned (the x-staged kernel bulk-copies x)");
     const bool orig = flags & SPMV_VEC_ORIGINAL;
     if (orig && h->world > 1) return fail(SPMV_ERR_UNSUPPORTED, "ORIGINAL index space with world > 1");
     const int64_t xl = orig ? h->n : h->x_local_len;
@@ -765,7 +874,24 @@ static spmv_status_t run(spmv_handle_t h, const double* x, double* y, uint32_t f
                                  spmvb::kMaxSlots * spmvb::kSlotStride * sizeof(unsigned long long), st));
         A.maxabs_slots = h->d_slots;
     }
-    if (!split && h->kernel != 2) {
+    if (!split && h->kernel == 6) {
+        spmvb::XsArgs X{};
+        X.panel = h->d_xs_panel;
+        X.n_panels = (int32_t)h->xs_panels;
+        X.cbits = h->xs_cbits;
+        X.wg = h->d_xs_wg;
+        X.wb = h->d_xs_wb;
+        X.U = h->d_xs_U;
+        X.gval = h->d_xs_gval;
+        X.gidx = h->d_xs_gidx;
+        X.bval = h->d_xs_bval;
+        X.bidx = h->d_xs_bidx;
+        X.x = xk;
+        X.xg = xsplit ? A.x_hi : xk + h->xs_gb;
+        X.y = yk;
+        X.maxabs_slots = A.maxabs_slots;
+        CUDA_TRY(spmvb::launch_xstage(X, st));
+    } else if (!split && h->kernel != 2) {
         spmvb::PipeArgs P{};
         P.tile_row = h->d_tile_row;
         P.tile_nnz = h->d_tile_nnz;
@@ -851,6 +977,11 @@ spmv_status_t spmv_get_info(spmv_handle_t h, spmv_info_t* info) {
     info->split_segments = h->n_seg;
     info->n_parts = h->n_parts; info->rank = h->rank; info->world = h->world; info->kind = h->kind;
     info->has_owner_map = h->has_owner ? 1 : 0;
+    info->xs_panels = h->xs_panels;
+    info->xs_groups = h->xs_groups;
+    info->xs_pad_slots = h->xs_pad;
+    info->bytes_stream = h->bytes_stream;
+    info->kernel = h->kernel;
     return SPMV_OK;
 }
 
@@ -916,6 +1047,42 @@ spmv_status_t spmv_diag_csr(spmv_handle_t h, const double* x, int32_t mode, doub
     if (h->world > 1) return fail(SPMV_ERR_UNSUPPORTED, "diag_csr: world 1 only");
     CUDA_TRY(cudaSetDevice(h->device));
     CUDA_TRY(spmvb::diag_csr(h->d_col, h->d_val, x, h->nnz_loc, mode, out_dev, (cudaStream_t)stream));
+    return SPMV_OK;
+}
+
+spmv_status_t spmv_xs_plan_check(int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
+                                 const spmv_blocks_t* blocks, int64_t rows_target, int64_t* stats) {
+    if (m < 0 || n < 0 || !row_ptr || !blocks || !stats || blocks->kind != SPMV_SB || blocks->K < 1 ||
+        !blocks->row_block_ptr || !blocks->col_block_ptr)
+        return fail(SPMV_ERR_USAGE, "xs_plan_check: bad arguments");
+    const int K = blocks->K;
+    const int64_t nnz = row_ptr[m];
+    if (nnz > 0 && (!col || !val)) return fail(SPMV_ERR_USAGE, "xs_plan_check: NULL col/val");
+    try {
+        std::vector<int64_t> rp(row_ptr, row_ptr + m + 1);
+        std::vector<int32_t> c(col, col + nnz);
+        std::vector<double> v(val, val + nnz);
+        std::vector<spmvb::XsBlockIn> bl;
+        for (int k = 0; k < K; ++k)
+            bl.push_back({blocks->row_block_ptr[k], blocks->row_block_ptr[k + 1], blocks->col_block_ptr[k],
+                          blocks->col_block_ptr[k + 1]});
+        const int64_t gb = blocks->col_block_ptr[K];
+        const int64_t glen = blocks->col_block_ptr[K + 1] - gb;
+        std::vector<spmvb::XsPanelData> pd;
+        spmvb::XsPlanStats st;
+        std::string why;
+        int cbits = 0;
+        if (!spmvb::plan_xstage(rp, c, v, bl, gb, glen, rows_target, pd, cbits, st, why))
+            return fail(SPMV_ERR_UNSUPPORTED, "xs_plan_check: %s", why.c_str());
+        stats[0] = st.panels; stats[1] = st.groups_i; stats[2] = st.groups_b;
+        stats[3] = st.pad_i; stats[4] = st.pad_b; stats[5] = st.entries;
+        if (st.entries != nnz) return fail(SPMV_ERR_INTERNAL, "xs_plan_check: plan holds %lld of %lld nonzeros",
+                                           (long long)st.entries, (long long)nnz);
+        if (!spmvb::verify_xstage(rp, c, v, gb, cbits, pd, why))
+            return fail(SPMV_ERR_INTERNAL, "xs_plan_check: %s", why.c_str());
+    } catch (const std::bad_alloc&) {
+        return fail(SPMV_ERR_INTERNAL, "out of host memory");
+    }
     return SPMV_OK;
 }
 

@@ -77,6 +77,51 @@ cudaError_t launch_normalize(const double* y, const int32_t* owner, const double
                              int64_t n, cudaStream_t s);
 int kernel_num_sms();
 
+// ---------------------------------------------------------------------------
+// x-staged single-SpMxV (xstage.cu, plan_xs.cpp).  A panel is a
+// run of rows of one SB block; its interior columns C_k are streamed through
+// shared memory in chunks of kXsW columns by the bulk-copy engine, its y rows
+// live in shared memory, and its nonzeros are pre-packed into 32-entry groups
+// (one per lane) with distinct rows and spread shared-memory banks.  Border
+// (C_B) nonzeros are gathered from L2.
+constexpr int kXsWarps = 16;                 // consumer warps; each owns a row range
+constexpr int kXsStages = 3;                 // x chunk ring
+constexpr int kXsW = 2048;                   // columns per chunk (multiple of 16)
+constexpr int kXsStageStride = kXsW + 16;    // doubles per stage buffer
+constexpr int kXsRowsMax = 22528;            // y rows per panel (shared memory)
+constexpr uint32_t kXsDummy = 0xFFFFFFFFu;   // padding slot
+static_assert(kXsW % 16 == 0, "chunk width must keep the bank map shift-invariant");
+
+struct XsPanel {
+    int32_t row0;      // first local row
+    int32_t nrows;     // rows in the panel (<= kXsRowsMax)
+    int32_t col0;      // first interior column (local id); chunk j starts at col0 + j*kXsW
+    int32_t col_end;   // one past the last interior column
+    int32_t nch;       // chunks
+    int32_t u_base;    // offset of this panel's per-warp chunk tables in XsArgs::U
+    int32_t rw;        // rows per warp (warp w owns [w*rw, min((w+1)*rw, nrows)))
+    int32_t pad;
+};
+
+struct XsArgs {
+    const XsPanel* panel;
+    int32_t n_panels;
+    int32_t cbits;            // border index: (row_in_warp << cbits) | border column
+    const int32_t* wg;        // [P*NW+1] interior groups of (panel, warp), contiguous
+    const int32_t* wb;        // [P*NW+1] border groups of (panel, warp)
+    const int32_t* U;         // per (panel, warp): nch entries, U[j] = first group with min chunk >= j
+    const double* gval;       // [groups*32]
+    const uint32_t* gidx;     // [groups*32] (row_in_panel << 16) | offset from its group's first chunk
+    const double* bval;
+    const uint32_t* bidx;
+    const double* x;          // interior columns: x[col]
+    const double* xg;         // border columns: xg[border column]
+    double* y;                // local rows
+    unsigned long long* maxabs_slots;
+};
+cudaError_t launch_xstage(const XsArgs& a, cudaStream_t s);
+size_t xstage_smem_bytes();
+
 // roofline microkernels (diag.cu)
 cudaError_t diag_read(const void* buf, int64_t bytes, double* out, int blocks_per_sm, cudaStream_t s);
 cudaError_t diag_gather(const double* x, int64_t n, int64_t count, double* out, cudaStream_t s);

@@ -1,0 +1,57 @@
+"""Host-only checks of the x-staged kernel's planner (plan_xs.cpp): the packed
+panel/group streams decode back to the permuted CSR bit for bit, with the
+format's invariants (distinct rows per group, <= 2 consecutive chunks per
+group, zero-valued padding).  The kernel itself is checked on the GPU
+(test_gpu_parity.py)."""
+import numpy as np
+import pytest
+
+import paper_1203_2739_b200 as sp
+import synth
+
+
+@pytest.mark.parametrize("name,target", [("c5s", 2000), ("c5s", 700), ("c2s", 300), ("c2s", 5000)])
+def test_plan_round_trip_presets(name, target):
+    p = synth.make(name, scramble=0)          # SB form in permuted order (rows sorted)
+    st = sp.spmv_xs_plan_check(p.m, p.n, p.row_ptr, p.col, p.val, p.blocks, target)
+    assert st["entries"] == p.nnz
+    assert st["panels"] >= p.blocks["K"]
+
+
+def _random_sb(seed, K, rows, cols, border, dens_int, dens_b):
+    """SB form with uneven, odd-sized blocks (chunk starts at odd columns)."""
+    rng = np.random.default_rng(seed)
+    rb = np.concatenate([[0], np.cumsum(rows)])
+    cb = np.concatenate([[0], np.cumsum(cols)])
+    m, nint = int(rb[-1]), int(cb[-1])
+    n = nint + border
+    rp = [0]
+    col, val = [], []
+    for k in range(K):
+        for r in range(rb[k], rb[k + 1]):
+            ci = np.flatnonzero(rng.random(cols[k]) < dens_int) + cb[k]
+            cbo = np.flatnonzero(rng.random(border) < dens_b) + nint if border else np.array([], dtype=np.int64)
+            c = np.concatenate([ci, cbo]).astype(np.int32)
+            col.append(c)
+            val.append(rng.standard_normal(len(c)))
+            rp.append(rp[-1] + len(c))
+    blocks = {"kind": 1, "K": K, "row_block_ptr": np.array(list(rb) + [m], dtype=np.int64),
+              "col_block_ptr": np.array(list(cb) + [n], dtype=np.int64)}
+    return m, n, np.array(rp, dtype=np.int64), np.concatenate(col), np.concatenate(val), blocks
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_plan_round_trip_random_sb(seed):
+    # block widths straddle chunk boundaries (kXsW = 2048): 1, 2047, 2049, 5001 columns
+    m, n, rp, col, val, blocks = _random_sb(seed, 4, [37, 600, 1201, 90], [1, 2047, 2049, 5001], 333, 0.01, 0.01)
+    st = sp.spmv_xs_plan_check(m, n, rp, col, val, blocks, 256)
+    assert st["entries"] == len(col)
+
+
+def test_plan_dense_rows_and_empty_rows():
+    # rows with many entries per chunk (each row's entries land in distinct groups)
+    # and empty rows/blocks without border columns
+    m, n, rp, col, val, blocks = _random_sb(5, 3, [40, 1, 300], [3000, 17, 4100], 0, 0.3, 0.0)
+    st = sp.spmv_xs_plan_check(m, n, rp, col, val, blocks, 512)
+    assert st["entries"] == len(col)
+    assert st["groups_b"] == 0
