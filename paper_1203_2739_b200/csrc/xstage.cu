@@ -125,6 +125,9 @@ __global__ void __launch_bounds__(kT, 1) spmv_xstage_kernel(const XsArgs A) {
         int jcur = 0, jw = 0, jr = 0;
         int nextU = nch > 1 ? __ldg(U + 1) : 0x7fffffff;
 
+        auto release = [&](int j) {
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sptr(&empty[j % NS])) : "memory");
+        };
         double rv[kD];
         uint32_t ri[kD];
         double rx[kGD];
@@ -162,17 +165,18 @@ __global__ void __launch_bounds__(kT, 1) spmv_xstage_kernel(const XsArgs A) {
                         ++jcur;
                         nextU = (jcur + 1 < nch) ? __ldg(U + jcur + 1) : 0x7fffffff;
                     }
+                    // release chunks this warp is done with before waiting for
+                    // new ones (the producer refills a stage only after every
+                    // warp has released it)
                     const int need = min(jcur + 1, nch - 1);
-                    while (jw <= need) {
-                        mbar_wait(sptr(&full[jw % NS]), (uint32_t)((jw / NS) & 1));
-                        ++jw;
-                    }
-                    if (jr < jcur) {
+                    if (jr < jcur || jw <= need) {
                         __syncwarp();
-                        do {
-                            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sptr(&empty[jr % NS])) : "memory");
-                            ++jr;
-                        } while (jr < jcur);
+                        while (jw <= need) {
+                            while (jr < jcur && jr < jw) release(jr++);
+                            mbar_wait(sptr(&full[jw % NS]), (uint32_t)((jw / NS) & 1));
+                            ++jw;
+                        }
+                        while (jr < jcur) release(jr++);
                     }
                     if (i != kXsDummy) {
                         const int r = (int)(i >> 16);
@@ -196,15 +200,15 @@ __global__ void __launch_bounds__(kT, 1) spmv_xstage_kernel(const XsArgs A) {
                 }
             }
         }
-        // every chunk is waited for and released exactly once per warp
-        while (jw < nch) {
-            mbar_wait(sptr(&full[jw % NS]), (uint32_t)((jw / NS) & 1));
-            ++jw;
-        }
+        // every chunk is waited for and released exactly once per warp, in order
         __syncwarp();
         while (jr < nch) {
-            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sptr(&empty[jr % NS])) : "memory");
-            ++jr;
+            if (jr < jw) {
+                release(jr++);
+            } else {
+                mbar_wait(sptr(&full[jw % NS]), (uint32_t)((jw / NS) & 1));
+                ++jw;
+            }
         }
     }
     __syncthreads();
