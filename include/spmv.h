@@ -159,14 +159,14 @@ typedef struct {
     int64_t bytes_alg;            /* 12 nnz + 4 (m+1) + 8 m + 8 n_touched, local */
     int64_t bytes_alg_split;      /* same for the fused split pass (0 without a split) */
     int64_t split_segments;       /* (row, part) segments of the split layout */
-    int64_t xs_panels;            /* x-staged kernel: panels (0 when that kernel is not used) */
-    int64_t xs_groups;            /* x-staged kernel: 32-entry groups (interior + border) */
-    int64_t xs_pad_slots;         /* x-staged kernel: padding slots among them */
+    int64_t xs_panels;            /* panel kernels (7, 6): panels (0 when the row-tile kernel is used) */
+    int64_t xs_groups;            /* panel kernels: 32-entry groups */
+    int64_t xs_pad_slots;         /* panel kernels: padding slots among them */
     int64_t bytes_stream;         /* device bytes the apply kernel actually reads + writes (no x reuse) */
     int32_t n_parts, rank, world, kind;
     int32_t has_owner_map;        /* spmv_normalize is available */
-    int32_t kernel;               /* single-SpMxV kernel: 6 x-staged (SB default), 0 row-tile (default
-                                     otherwise); 1-5 measurement variants (SPMV_KERNEL env) */
+    int32_t kernel;               /* single-SpMxV kernel: 7 column-sorted panels (SB default), 0 row-tile
+                                     (default otherwise); 1-6 measurement variants (SPMV_KERNEL env) */
     int32_t reserved[2];
 } spmv_info_t;
 
@@ -231,6 +231,16 @@ spmv_status_t spmv_diag_csr(spmv_handle_t h, const double* x, int32_t mode, doub
  * round trip is exact; INTERNAL (message in spmv_last_error) when not;
  * UNSUPPORTED when the matrix does not fit the format. */
 spmv_status_t spmv_xs_plan_check(int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
+                                 const spmv_blocks_t* blocks, int64_t rows_target, int64_t* stats);
+
+/* Host-only test hook of the column-sorted panel kernel's planner
+ * (plan_panel.cpp): packs a PERMUTED CSR (world-1 column ids) into panels
+ * (the row ranges of `blocks`, or the whole matrix when blocks is NULL) of
+ * about rows_target rows, decodes the groups again and compares them with the
+ * CSR bit for bit, checking that no row repeats within an epoch.
+ * stats[6] = panels, groups, padding slots, deferred nonzeros, epochs,
+ * nonzeros packed.  OK on an exact round trip; INTERNAL otherwise. */
+spmv_status_t spmv_pn_plan_check(int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
                                  const spmv_blocks_t* blocks, int64_t rows_target, int64_t* stats);
 
 /* Design microbenchmarks (diag2.cu): kind 1 L2->SM LDG.128 bandwidth over the

@@ -35,7 +35,7 @@ EXPORTED = ["spmv_create", "spmv_apply", "spmv_split_apply", "spmv_destroy", "sp
             "spmv_maxabs", "spmv_normalize", "spmv_debug_copy_csr", "spmv_nccl_unique_id",
             "spmv_status_string", "spmv_last_error", "spmv_version", "spmv_shard_plan",
             "spmv_diag_read", "spmv_diag_gather", "spmv_diag_csr", "spmv_diag_gather_mode", "spmv_diag_micro",
-            "spmv_xs_plan_check"]
+            "spmv_xs_plan_check", "spmv_pn_plan_check"]
 
 
 class SpmvError(RuntimeError):
@@ -95,6 +95,7 @@ def lib():
         L.spmv_diag_gather_mode.argtypes = [vp, i64, i64, i32, i32, vp, vp]
         L.spmv_diag_micro.argtypes = [i32, i32, vp, i64, i64, vp, vp]
         L.spmv_xs_plan_check.argtypes = [i64, i64, vp, vp, vp, vp, i64, vp]
+        L.spmv_pn_plan_check.argtypes = [i64, i64, vp, vp, vp, vp, i64, vp]
         L.spmv_shard_plan.argtypes = [vp, i64, i64, i32, i32, vp]
         L.spmv_status_string.argtypes = [i32]
         L.spmv_status_string.restype = ctypes.c_char_p
@@ -227,6 +228,25 @@ def spmv_xs_plan_check(m: int, n: int, row_ptr, col, val, blocks, rows_target: i
     _check(lib().spmv_xs_plan_check(m, n, _addr(rp), _addr(ci), _addr(va), ctypes.byref(b), rows_target,
                                     stats.ctypes.data), "spmv_xs_plan_check")
     return dict(zip(("panels", "groups_i", "groups_b", "pad_i", "pad_b", "entries"), (int(v) for v in stats)))
+
+
+def spmv_pn_plan_check(m: int, n: int, row_ptr, col, val, blocks, rows_target: int) -> dict:
+    """Host-only round trip of the column-sorted panel planner (see spmv.h); raises on mismatch."""
+    rp = _np(row_ptr, np.int64)
+    ci = _np(col, np.int32)
+    va = _np(val, np.float64)
+    keep = []
+    bptr = None
+    if blocks is not None:
+        rbp = _np(blocks["row_block_ptr"], np.int64)
+        cbp = _np(blocks["col_block_ptr"], np.int64)
+        b = _Blocks(int(blocks["kind"]), int(blocks["K"]), rbp.ctypes.data, cbp.ctypes.data, None)
+        keep += [rbp, cbp, b]
+        bptr = ctypes.byref(b)
+    stats = np.zeros(6, dtype=np.int64)
+    _check(lib().spmv_pn_plan_check(m, n, _addr(rp), _addr(ci), _addr(va), bptr, rows_target, stats.ctypes.data),
+           "spmv_pn_plan_check")
+    return dict(zip(("panels", "groups", "pads", "deferred", "epochs", "entries"), (int(v) for v in stats)))
 
 
 def spmv_apply(h, x, y, flags: int = 0, stream=None, x_len: int | None = None, y_len: int | None = None):

@@ -39,10 +39,12 @@ SOURCES = {
     "rowtile.cu": "cu",
     "split.cu": "cu",
     "xstage.cu": "cu",
+    "panel.cu": "cu",
+    "plan_panel.cpp": "cpp",
     "plan_xs.cpp": "cpp",
     "host.cpp": "cpp",
 }
-HEADERS = ["internal.h", "plan_xs.h", os.path.join("..", "..", "include", "spmv.h")]
+HEADERS = ["internal.h", "plan_xs.h", "plan_panel.h", os.path.join("..", "..", "include", "spmv.h")]
 
 
 def _newer(target: str, deps) -> bool:

@@ -29,6 +29,7 @@
 #include "../../include/spmv.h"
 #include "internal.h"
 #include "plan_xs.h"
+#include "plan_panel.h"
 
 using spmvb::kTileNnz;
 using spmvb::kTileRows;
@@ -100,7 +101,7 @@ struct spmv_plan_s {
     int* d_counter = nullptr;         // tile-claim counter of the pipe kernel
     int32_t* d_tile_cls = nullptr;    // [T] tile class (internal.h)
     int kernel = 0;                   // 0 rowtile/256, 1 pipe, 2 tile, 3 rowtile/512, 4 rowseg, 5 rowtile/128,
-                                      // 6 x-staged (default for SB handles)
+                                      // 6 x-staged, 7 column-sorted panels (default for SB handles)
     // x-staged kernel (xstage.cu)
     spmvb::XsPanel* d_xs_panel = nullptr;
     int32_t* d_xs_wg = nullptr;
@@ -113,6 +114,12 @@ struct spmv_plan_s {
     int32_t xs_cbits = 0;
     int64_t xs_panels = 0, xs_groups = 0, xs_pad = 0, xs_gb = 0;
     int64_t bytes_stream = 0;
+    // column-sorted panel kernel (panel.cu)
+    spmvb::PnPanel* d_pn_panel = nullptr;
+    double* d_pn_gval = nullptr;
+    uint32_t* d_pn_gidx = nullptr;
+    int32_t* d_pn_gbase = nullptr;
+    int64_t pn_panels = 0, pn_groups = 0, pn_pad = 0;
     int32_t* d_tile_seg = nullptr;    // [T*K+1]
     int32_t* d_seg_ptr = nullptr;     // [S+1]
     int32_t* d_seg_row = nullptr;     // [S]
@@ -349,6 +356,69 @@ static spmv_status_t plan_xs(spmv_plan_s* h, const std::vector<int64_t>& rp, con
     h->xs_pad = st.pad_i + st.pad_b;
     h->bytes_stream = 12 * 32 * (gi + gbn) + 8 * (P * NW + 1) * 2 + 4 * nu + 8 * h->m_loc;
     h->kernel = 6;
+    return SPMV_OK;
+}
+
+// Builds and uploads the column-sorted panel kernel's plan (plan_panel.cpp).
+// Leaves the handle on the row-tile kernel when the plan would be poor.
+static spmv_status_t plan_pn(spmv_plan_s* h, const std::vector<int64_t>& rp, const std::vector<int32_t>& pcol,
+                             const std::vector<double>& pval, const std::vector<int64_t>& rbp) {
+    const int K = (int)rbp.size() - 2;
+    const int64_t R0 = h->row_begin, R1 = h->row_begin + h->m_loc;
+    std::vector<std::pair<int64_t, int64_t>> ranges;
+    for (int k = 0; k < K; ++k) {
+        const int64_t a = std::max(rbp[k], R0), b = std::min(rbp[k + 1], R1);
+        if (b > a) ranges.push_back({a - R0, b - R0});
+    }
+    // panels: about kPnRowsMax rows, their count a multiple of the SM count
+    // when possible (whole waves of one CTA per SM)
+    const int64_t sms = spmvb::kernel_num_sms();
+    int64_t target = spmvb::kPnRowsMax;
+    for (int64_t k = 1; k <= 64; ++k) {
+        const int64_t r = (h->m_loc + sms * k - 1) / (sms * k);
+        if (r <= spmvb::kPnRowsMax) {
+            target = r;
+            break;
+        }
+    }
+    target = std::max<int64_t>(target, 1024);
+    if (const char* e = getenv("SPMV_PN_ROWS")) target = std::max<int64_t>(1, atoll(e));   // tests / measurements
+    const int64_t xs = h->world > 1 ? h->x_int_len : INT32_MAX;
+    std::vector<spmvb::PnPanelData> pd;
+    spmvb::PnPlanStats st;
+    std::string why;
+    if (!spmvb::plan_panel(rp, pcol, pval, ranges, xs, target, pd, st, why)) return SPMV_OK;
+    if (st.entries != h->nnz_loc)
+        return fail(SPMV_ERR_INTERNAL, "panel plan lost nonzeros (%lld of %lld)", (long long)st.entries,
+                    (long long)h->nnz_loc);
+    const char* kenv = getenv("SPMV_KERNEL");
+    const bool forced = kenv && strcmp(kenv, "panel") == 0;
+    if (!forced && st.pads > st.entries / 4) return SPMV_OK;   // > 25 % padding: the row-tile kernel is cheaper
+    const int64_t P = (int64_t)pd.size(), G = st.groups;
+    std::vector<spmvb::PnPanel> desc(P);
+    for (int64_t p = 0; p < P; ++p) desc[p] = pd[p].desc;
+    spmv_status_t s;
+    if ((s = upload(h, &h->d_pn_panel, desc.data(), P))) return s;
+    if ((s = dalloc(h, &h->d_pn_gval, G * 32))) return s;
+    if ((s = dalloc(h, &h->d_pn_gidx, G * 32))) return s;
+    if ((s = dalloc(h, &h->d_pn_gbase, G))) return s;
+    for (int64_t p = 0; p < P; ++p) {
+        spmvb::PnPanelData& D = pd[p];
+        const int64_t g0 = D.desc.g0, ng = (int64_t)D.gbase.size();
+        if (ng) {
+            CUDA_TRY(cudaMemcpy(h->d_pn_gval + g0 * 32, D.gval.data(), ng * 32 * 8, cudaMemcpyHostToDevice));
+            CUDA_TRY(cudaMemcpy(h->d_pn_gidx + g0 * 32, D.gidx.data(), ng * 32 * 4, cudaMemcpyHostToDevice));
+            CUDA_TRY(cudaMemcpy(h->d_pn_gbase + g0, D.gbase.data(), ng * 4, cudaMemcpyHostToDevice));
+        }
+        std::vector<double>().swap(D.gval);
+        std::vector<uint32_t>().swap(D.gidx);
+        std::vector<int32_t>().swap(D.gbase);
+    }
+    h->pn_panels = P;
+    h->pn_groups = G;
+    h->pn_pad = st.pads;
+    h->bytes_stream = (12 * 32 + 4) * G + 8 * h->m_loc;
+    h->kernel = 7;
     return SPMV_OK;
 }
 
@@ -726,9 +796,11 @@ static spmv_status_t create_impl(int64_t m, int64_t n, int64_t nnz, const int64_
     // ------------------------------------ x-staged plan (SB handles, a5/a6)
     {
         const char* kenv = getenv("SPMV_KERNEL");
-        const bool want = blocks && h->kind == SPMV_SB && (!kenv || strcmp(kenv, "xstage") == 0) && nnz_loc > 0;
-        if (want) {
+        const bool sb = blocks && h->kind == SPMV_SB && nnz_loc > 0;
+        if (sb && kenv && strcmp(kenv, "xstage") == 0) {
             if ((s = plan_xs(h, rp, pcol, pval, rbp, cbp))) return s;
+        } else if (sb && (!kenv || strcmp(kenv, "panel") == 0)) {
+            if ((s = plan_pn(h, rp, pcol, pval, rbp))) return s;
         }
     }
 
@@ -874,7 +946,20 @@ static spmv_status_t run(spmv_handle_t h, const double* x, double* y, uint32_t f
                                  spmvb::kMaxSlots * spmvb::kSlotStride * sizeof(unsigned long long), st));
         A.maxabs_slots = h->d_slots;
     }
-    if (!split && h->kernel == 6) {
+    if (!split && h->kernel == 7) {
+        spmvb::PnArgs X{};
+        X.panel = h->d_pn_panel;
+        X.n_panels = (int32_t)h->pn_panels;
+        X.x_split = A.x_split;
+        X.gval = h->d_pn_gval;
+        X.gidx = h->d_pn_gidx;
+        X.gbase = h->d_pn_gbase;
+        X.x_lo = A.x_lo;
+        X.x_hi = A.x_hi;
+        X.y = yk;
+        X.maxabs_slots = A.maxabs_slots;
+        CUDA_TRY(spmvb::launch_panel(X, st));
+    } else if (!split && h->kernel == 6) {
         spmvb::XsArgs X{};
         X.panel = h->d_xs_panel;
         X.n_panels = (int32_t)h->xs_panels;
@@ -977,9 +1062,9 @@ spmv_status_t spmv_get_info(spmv_handle_t h, spmv_info_t* info) {
     info->split_segments = h->n_seg;
     info->n_parts = h->n_parts; info->rank = h->rank; info->world = h->world; info->kind = h->kind;
     info->has_owner_map = h->has_owner ? 1 : 0;
-    info->xs_panels = h->xs_panels;
-    info->xs_groups = h->xs_groups;
-    info->xs_pad_slots = h->xs_pad;
+    info->xs_panels = h->kernel == 7 ? h->pn_panels : h->xs_panels;
+    info->xs_groups = h->kernel == 7 ? h->pn_groups : h->xs_groups;
+    info->xs_pad_slots = h->kernel == 7 ? h->pn_pad : h->xs_pad;
     info->bytes_stream = h->bytes_stream;
     info->kernel = h->kernel;
     return SPMV_OK;
@@ -1080,6 +1165,40 @@ spmv_status_t spmv_xs_plan_check(int64_t m, int64_t n, const int64_t* row_ptr, c
                                            (long long)st.entries, (long long)nnz);
         if (!spmvb::verify_xstage(rp, c, v, gb, cbits, pd, why))
             return fail(SPMV_ERR_INTERNAL, "xs_plan_check: %s", why.c_str());
+    } catch (const std::bad_alloc&) {
+        return fail(SPMV_ERR_INTERNAL, "out of host memory");
+    }
+    return SPMV_OK;
+}
+
+spmv_status_t spmv_pn_plan_check(int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
+                                 const spmv_blocks_t* blocks, int64_t rows_target, int64_t* stats) {
+    if (m < 0 || n < 0 || !row_ptr || !stats) return fail(SPMV_ERR_USAGE, "pn_plan_check: bad arguments");
+    const int64_t nnz = row_ptr[m];
+    if (nnz > 0 && (!col || !val)) return fail(SPMV_ERR_USAGE, "pn_plan_check: NULL col/val");
+    try {
+        std::vector<int64_t> rp(row_ptr, row_ptr + m + 1);
+        std::vector<int32_t> c(col, col + nnz);
+        std::vector<double> v(val, val + nnz);
+        std::vector<std::pair<int64_t, int64_t>> ranges;
+        if (blocks && blocks->K > 0 && blocks->row_block_ptr) {
+            for (int k = 0; k <= blocks->K; ++k)
+                if (blocks->row_block_ptr[k + 1] > blocks->row_block_ptr[k])
+                    ranges.push_back({blocks->row_block_ptr[k], blocks->row_block_ptr[k + 1]});
+        } else {
+            ranges.push_back({0, m});
+        }
+        std::vector<spmvb::PnPanelData> pd;
+        spmvb::PnPlanStats st;
+        std::string why;
+        if (!spmvb::plan_panel(rp, c, v, ranges, INT32_MAX, rows_target, pd, st, why))
+            return fail(SPMV_ERR_UNSUPPORTED, "pn_plan_check: %s", why.c_str());
+        stats[0] = st.panels; stats[1] = st.groups; stats[2] = st.pads;
+        stats[3] = st.deferred; stats[4] = st.epochs; stats[5] = st.entries;
+        if (st.entries != nnz) return fail(SPMV_ERR_INTERNAL, "pn_plan_check: plan holds %lld of %lld nonzeros",
+                                           (long long)st.entries, (long long)nnz);
+        if (!spmvb::verify_panel(rp, c, v, INT32_MAX, pd, why))
+            return fail(SPMV_ERR_INTERNAL, "pn_plan_check: %s", why.c_str());
     } catch (const std::bad_alloc&) {
         return fail(SPMV_ERR_INTERNAL, "out of host memory");
     }

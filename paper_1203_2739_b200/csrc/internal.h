@@ -122,6 +122,44 @@ struct XsArgs {
 cudaError_t launch_xstage(const XsArgs& a, cudaStream_t s);
 size_t xstage_smem_bytes();
 
+// ---------------------------------------------------------------------------
+// Column-sorted panel SpMxV (panel.cu, plan_panel.cpp): the
+// default kernel of SB handles.  A panel is a run of <= kPnRowsMax rows of one
+// SB block whose y lives in shared memory.  Its nonzeros are sorted by column
+// and cut into 32-entry groups, so one warp-wide x gather touches few 128-byte
+// lines (the L1TEX cost is per line, not per lane).  Groups are issued in
+// epochs of kPnB groups per warp; the rows of an epoch are distinct, so the
+// shared-memory y updates of one epoch never race, and a CTA barrier
+// separates epochs.
+constexpr int kPnWarps = 16;                 // warps per panel CTA
+constexpr int kPnB = 4;                      // groups per warp per epoch
+constexpr int kPnEpoch = kPnWarps * kPnB;    // groups per epoch
+constexpr int kPnRowsMax = 28672;            // y rows per panel (224 KB of shared memory)
+constexpr int kPnRowBits = 15;               // idx = (row_in_panel << 17) | (col - group base)
+constexpr int kPnDeltaBits = 17;
+constexpr uint32_t kPnDummy = 0xFFFFFFFFu;
+
+struct PnPanel {
+    int32_t row0;      // first local row
+    int32_t nrows;     // rows (<= kPnRowsMax)
+    int32_t g0;        // first group of the panel (groups of epoch e, step b, warp w: g0 + (e*kPnB + b)*16 + w)
+    int32_t ne;        // epochs
+};
+
+struct PnArgs {
+    const PnPanel* panel;
+    int32_t n_panels;
+    int32_t x_split;          // columns >= x_split read x_hi[c - x_split]
+    const double* gval;       // [groups*32]
+    const uint32_t* gidx;     // [groups*32]
+    const int32_t* gbase;     // [groups] first column of the group (local id)
+    const double* x_lo;
+    const double* x_hi;
+    double* y;
+    unsigned long long* maxabs_slots;
+};
+cudaError_t launch_panel(const PnArgs& a, cudaStream_t s);
+
 // roofline microkernels (diag.cu)
 cudaError_t diag_read(const void* buf, int64_t bytes, double* out, int blocks_per_sm, cudaStream_t s);
 cudaError_t diag_gather(const double* x, int64_t n, int64_t count, double* out, cudaStream_t s);

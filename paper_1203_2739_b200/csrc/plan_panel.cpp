@@ -1,0 +1,260 @@
+// plan_panel.cpp -- host planner of the column-sorted panel kernel (panel.cu).
+//
+// Why this layout (measured, profiles/r01_micro.json): a warp-wide 8-byte
+// gather from L2 costs one L1TEX wavefront per distinct 128-byte line, so the
+// row-ordered CSR loop pays one wavefront per nonzero (C5's columns are
+// random within a 980,000-column SB block, Eq.(1)).  The temporal
+// locality the SB reordering creates (rows of one block only touch
+// x(C_k) and x(C_B)) is exploited here by processing a large panel of rows
+// of one block together: sorted by column, the panel's nonzeros hit each x
+// line several times in a row, so 32 consecutive nonzeros touch only a few
+// lines.  y of the panel lives in shared memory (the per-row temporary of
+// P:L41-49 becomes a shared-memory accumulator written to HBM once).
+//
+// Plan of one panel:
+//   1. its nonzeros, sorted by (column, row-major position);
+//   2. epochs: runs of kPnEpoch groups whose rows are all distinct, filled in
+//      column order; a nonzero whose row is already in the epoch is deferred
+//      to the next epoch (taken first there);
+//   3. groups: 32 consecutive nonzeros of an epoch sharing a base column
+//      (column - base < 2^17) and one side of x_split; within a group the
+//      lanes alternate between the half-warps by y bank (row mod 16) so that
+//      the shared-memory y updates spread over the banks;
+//   4. padding: kPnDummy slots (the lane does nothing) and all-dummy groups
+//      completing the last epoch.
+// Row sums therefore accumulate in column order (ascending, except deferred
+// nonzeros); any order is within the oracle tolerance (reading A6), and the
+// plan is deterministic.
+#include "plan_panel.h"
+
+#include <algorithm>
+#include <cstring>
+#include <omp.h>
+
+namespace spmvb {
+namespace {
+
+struct Ent {
+    int32_t row;   // row in panel
+    int32_t col;   // local column id
+    double v;
+};
+
+class Emitter {
+  public:
+    explicit Emitter(PnPanelData& P) : P_(P) {}
+    void add(const Ent& e) { cur_[n_++] = e; }
+    int size() const { return n_; }
+    int32_t base() const { return cur_[0].col; }
+    void close() {
+        // lanes: entries sorted by y bank alternate between the half-warps
+        Ent s[32];
+        std::copy(cur_, cur_ + n_, s);
+        std::stable_sort(s, s + n_, [](const Ent& a, const Ent& b) { return (a.row & 15) < (b.row & 15); });
+        uint32_t idx[32];
+        double val[32];
+        for (int l = 0; l < 32; ++l) {
+            idx[l] = kPnDummy;
+            val[l] = 0.0;
+        }
+        const int32_t base = n_ ? cur_[0].col : 0;
+        for (int k = 0; k < n_; ++k) {
+            const int lane = (k & 1) * 16 + (k >> 1);
+            idx[lane] = ((uint32_t)s[k].row << kPnDeltaBits) | (uint32_t)(s[k].col - base);
+            val[lane] = s[k].v;
+        }
+        P_.gval.insert(P_.gval.end(), val, val + 32);
+        P_.gidx.insert(P_.gidx.end(), idx, idx + 32);
+        P_.gbase.push_back(base);
+        P_.pads += 32 - n_;
+        n_ = 0;
+    }
+
+  private:
+    PnPanelData& P_;
+    Ent cur_[32];
+    int n_ = 0;
+};
+
+void build_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col, const std::vector<double>& val,
+                 int64_t x_split, PnPanelData& P) {
+    const int64_t r0 = P.desc.row0, nr = P.desc.nrows;
+    const int64_t a = rp[r0], n = rp[r0 + nr] - a;
+    std::vector<Ent> ents(n);
+    std::vector<uint64_t> keys(n);
+    for (int64_t r = 0; r < nr; ++r)
+        for (int64_t e = rp[r0 + r]; e < rp[r0 + r + 1]; ++e) {
+            const int64_t i = e - a;
+            ents[i] = {(int32_t)r, col[e], val[e]};
+            keys[i] = ((uint64_t)(uint32_t)col[e] << 32) | (uint64_t)i;
+        }
+    std::sort(keys.begin(), keys.end());
+    P.entries = n;
+
+    const int64_t kMaxDelta = int64_t(1) << kPnDeltaBits;
+    auto side = [&](int32_t c) { return (int64_t)c >= x_split; };
+    std::vector<int32_t> stamp(nr, -1);
+    std::vector<int64_t> deferred, nd;
+    Emitter em(P);
+    int64_t pos = 0;
+    int32_t epoch = 0;
+    while (pos < n || !deferred.empty()) {
+        int ng = 0;
+        bool full = false;
+        // returns false when the epoch is full (entry not taken)
+        auto take = [&](int64_t i) -> bool {
+            const Ent& e = ents[i];
+            if (em.size() > 0 && (em.size() == 32 || (int64_t)e.col - em.base() >= kMaxDelta ||
+                                  side(e.col) != side(em.base()))) {
+                em.close();
+                if (++ng == kPnEpoch) return false;
+            }
+            em.add(e);
+            stamp[e.row] = epoch;
+            return true;
+        };
+        nd.clear();
+        for (int64_t i : deferred) {
+            if (full || stamp[ents[i].row] == epoch) {
+                nd.push_back(i);
+                continue;
+            }
+            if (!take(i)) {
+                full = true;
+                nd.push_back(i);
+            }
+        }
+        deferred.swap(nd);
+        while (!full && pos < n) {
+            const int64_t i = (int64_t)(keys[pos] & 0xFFFFFFFFu);
+            if (stamp[ents[i].row] == epoch) {
+                deferred.push_back(i);
+                ++P.deferred;
+                ++pos;
+                continue;
+            }
+            if (!take(i)) break;
+            ++pos;
+        }
+        if (em.size() > 0) {
+            em.close();
+            ++ng;
+        }
+        while (ng < kPnEpoch) {   // all-dummy groups complete the epoch
+            em.close();
+            ++ng;
+        }
+        ++epoch;
+    }
+    P.desc.ne = epoch;
+}
+
+}  // namespace
+
+bool plan_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col, const std::vector<double>& val,
+                const std::vector<std::pair<int64_t, int64_t>>& ranges, int64_t x_split, int64_t rows_target,
+                std::vector<PnPanelData>& out, PnPlanStats& st, std::string& why) {
+    out.clear();
+    st = PnPlanStats{};
+    const int64_t R = std::min<int64_t>(std::max<int64_t>(rows_target, 1), kPnRowsMax);
+    for (const auto& rg : ranges) {
+        const int64_t L = rg.second - rg.first;
+        if (L <= 0) continue;
+        int64_t np = (L + R - 1) / R;
+        while ((L + np - 1) / np > kPnRowsMax) ++np;
+        for (int64_t p = 0; p < np; ++p) {
+            const int64_t a = rg.first + L * p / np, e = rg.first + L * (p + 1) / np;
+            if (e - a > (int64_t(1) << kPnRowBits) - 1) {
+                why = "panel rows beyond the packed row field";
+                return false;
+            }
+            if (rp[e] - rp[a] >= (int64_t(1) << 32)) {
+                why = "panel nonzeros beyond 2^32";
+                return false;
+            }
+            PnPanelData d;
+            d.desc.row0 = (int32_t)a;
+            d.desc.nrows = (int32_t)(e - a);
+            out.push_back(std::move(d));
+        }
+    }
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t p = 0; p < (int64_t)out.size(); ++p) build_panel(rp, col, val, x_split, out[p]);
+    int64_t g = 0;
+    for (PnPanelData& P : out) {
+        P.desc.g0 = (int32_t)g;
+        g += (int64_t)P.gbase.size();
+        if (g >= INT32_MAX / 32) {
+            why = "too many groups for int32 group ids";
+            return false;
+        }
+        st.panels++;
+        st.entries += P.entries;
+        st.pads += P.pads;
+        st.deferred += P.deferred;
+        st.epochs += P.desc.ne;
+    }
+    st.groups = g;
+    return true;
+}
+
+bool verify_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col, const std::vector<double>& val,
+                  int64_t x_split, const std::vector<PnPanelData>& pd, std::string& why) {
+    bool ok = true;
+    std::string err;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t p = 0; p < (int64_t)pd.size(); ++p) {
+        const PnPanelData& P = pd[p];
+        const PnPanel& d = P.desc;
+        std::string e;
+        if ((int64_t)P.gbase.size() != (int64_t)d.ne * kPnEpoch) e = "group count != epochs * kPnEpoch";
+        std::vector<std::vector<std::pair<int32_t, double>>> got(d.nrows);
+        std::vector<int32_t> stamp(d.nrows, -1);
+        for (int64_t ep = 0; ep < d.ne && e.empty(); ++ep)
+            for (int k = 0; k < kPnEpoch && e.empty(); ++k) {
+                const int64_t g = ep * kPnEpoch + k;
+                const int32_t base = P.gbase[g];
+                int s = -1;
+                for (int l = 0; l < 32; ++l) {
+                    const uint32_t i = P.gidx[g * 32 + l];
+                    const double v = P.gval[g * 32 + l];
+                    if (i == kPnDummy) {
+                        if (v != 0.0) e = "dummy slot with a value";
+                        continue;
+                    }
+                    const int32_t r = (int32_t)(i >> kPnDeltaBits);
+                    const int64_t c = (int64_t)base + (i & ((1u << kPnDeltaBits) - 1));
+                    if (r >= d.nrows) { e = "row outside the panel"; break; }
+                    if (stamp[r] == ep) { e = "row repeated within an epoch"; break; }
+                    stamp[r] = (int32_t)ep;
+                    const int sd = c >= x_split;
+                    if (s >= 0 && sd != s) { e = "group mixes both sides of x_split"; break; }
+                    s = sd;
+                    got[r].push_back({(int32_t)c, v});
+                }
+            }
+        for (int64_t r = 0; r < d.nrows && e.empty(); ++r) {
+            auto& gr = got[r];
+            std::sort(gr.begin(), gr.end(),
+                      [](const std::pair<int32_t, double>& a, const std::pair<int32_t, double>& b) { return a.first < b.first; });
+            const int64_t R = d.row0 + r;
+            if ((int64_t)gr.size() != rp[R + 1] - rp[R]) { e = "row nonzero count differs"; break; }
+            for (int64_t t = 0; t < (int64_t)gr.size(); ++t)
+                if (gr[t].first != col[rp[R] + t] || std::memcmp(&gr[t].second, &val[rp[R] + t], 8) != 0) {
+                    e = "decoded (column, value) differs from the CSR";
+                    break;
+                }
+        }
+        if (!e.empty()) {
+#pragma omp critical
+            {
+                ok = false;
+                err = e + " (panel " + std::to_string(p) + ")";
+            }
+        }
+    }
+    if (!ok) why = err;
+    return ok;
+}
+
+}  // namespace spmvb

@@ -1,0 +1,36 @@
+// plan_panel.h -- host planner of the column-sorted panel kernel (panel.cu).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+namespace spmvb {
+
+struct PnPanelData {
+    PnPanel desc{};
+    std::vector<double> gval;      // [groups*32]
+    std::vector<uint32_t> gidx;    // [groups*32]
+    std::vector<int32_t> gbase;    // [groups]
+    int64_t entries = 0, pads = 0, deferred = 0;
+};
+
+struct PnPlanStats {
+    int64_t panels = 0, groups = 0, entries = 0, pads = 0, deferred = 0, epochs = 0;
+};
+
+// Row ranges [r0, r1) (local rows; e.g. the SB blocks of this rank) are cut
+// into panels of about rows_target rows.  Columns >= x_split come from the
+// second x pointer; a group never mixes the two sides.  Returns false (and
+// why) when the plan would be poor (caller falls back to the row-tile kernel).
+bool plan_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col, const std::vector<double>& val,
+                const std::vector<std::pair<int64_t, int64_t>>& ranges, int64_t x_split, int64_t rows_target,
+                std::vector<PnPanelData>& out, PnPlanStats& st, std::string& why);
+
+// Test hook: decode the groups back into (row, column, value) and compare with
+// the CSR bit for bit; checks the epoch invariant (distinct rows per epoch).
+bool verify_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col, const std::vector<double>& val,
+                  int64_t x_split, const std::vector<PnPanelData>& pd, std::string& why);
+
+}  // namespace spmvb

@@ -1,7 +1,11 @@
-"""GPU parity of the x-staged SB kernel (xstage.cu, the default for SB
-handles): odd block widths and chunk-straddling blocks, blocks without a
-border, empty rows, dense rows, bit-exact integer data, alignment errors,
-and run-to-run determinism.  Oracle: the CPU reference (oracle/)."""
+"""GPU parity of the SB panel kernels against the CPU oracle (oracle/):
+  panel  (panel.cu, kernel 7, the SB default): column-sorted panels, y in
+         shared memory, epoch barriers;
+  xstage (xstage.cu, kernel 6): x chunks streamed through shared memory.
+Odd block widths and chunk-straddling blocks, blocks without a border, empty
+and dense rows, bit-exact integer data, alignment errors, determinism."""
+import os
+
 import numpy as np
 import pytest
 
@@ -9,10 +13,12 @@ import oracle
 import paper_1203_2739_b200 as sp
 import synth
 from gpu_util import assert_parity, create, gpu_apply, oracle_permuted
-from test_xs_plan_cpu import _random_sb
+from test_xs_plan_cpu import _c5_like, _random_sb
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
+
+KERNEL_ID = {"xstage": 6, "panel": 7}
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -22,17 +28,22 @@ def cuda():
     sp.lib()
 
 
-def _run(m, n, rp, col, val, blocks, x, flags=0):
+@pytest.fixture(params=["panel", "xstage"])
+def kernel(request, monkeypatch):
+    monkeypatch.setenv("SPMV_KERNEL", request.param)
+    monkeypatch.setenv("SPMV_PN_ROWS", "700")
+    return request.param
+
+
+def _run(kernel, m, n, rp, col, val, blocks, x, flags=0):
     h = sp.spmv_create(m, n, rp, col, val, blocks=blocks)
-    info = sp.spmv_get_info(h)
-    assert info["kernel"] == 6, "SB handles use the x-staged kernel"
-    y = gpu_apply(h, x, m, flags=flags)
-    return h, y
+    assert sp.spmv_get_info(h)["kernel"] == KERNEL_ID[kernel]
+    return h, gpu_apply(h, x, m, flags=flags)
 
 
 @pytest.mark.parametrize("seed", [0, 1])
 @pytest.mark.parametrize("variant", ["int", "real"])
-def test_random_sb_odd_blocks(seed, variant):
+def test_random_sb_odd_blocks(kernel, seed, variant):
     m, n, rp, col, val, blocks = _random_sb(seed, 4, [37, 600, 1201, 90], [1, 2047, 2049, 5001], 333, 0.01, 0.01)
     rng = np.random.default_rng(seed + 10)
     if variant == "int":
@@ -41,43 +52,61 @@ def test_random_sb_odd_blocks(seed, variant):
     else:
         x = rng.uniform(-1, 1, n)
     yref, S = oracle.spmv(rp, col, val, x)
-    _, y = _run(m, n, rp, col, val, blocks, x)
-    assert_parity(y, yref, S, exact=(variant == "int"), what=f"random_sb/{seed}/{variant}")
+    _, y = _run(kernel, m, n, rp, col, val, blocks, x)
+    assert_parity(y, yref, S, exact=(variant == "int"), what=f"{kernel}/random_sb/{seed}/{variant}")
 
 
-def test_no_border_dense_and_empty_rows():
+def test_no_border_dense_rows(kernel):
     m, n, rp, col, val, blocks = _random_sb(5, 3, [40, 1, 300], [3000, 17, 4100], 0, 0.3, 0.0)
-    # make some rows empty
     x = np.random.default_rng(3).uniform(-1, 1, n)
     yref, S = oracle.spmv(rp, col, val, x)
-    _, y = _run(m, n, rp, col, val, blocks, x)
-    assert_parity(y, yref, S, what="no_border")
+    _, y = _run(kernel, m, n, rp, col, val, blocks, x)
+    assert_parity(y, yref, S, what=f"{kernel}/no_border")
 
 
 @pytest.mark.parametrize("name", ["c5s", "c2s"])
-@pytest.mark.parametrize("variant", ["int", "dyadic"])
-def test_presets_bit_exact(name, variant):
+@pytest.mark.parametrize("variant", ["int", "dyadic", "real"])
+def test_presets(kernel, name, variant):
     p = synth.make(name, variant=variant)
     x = p.x()
-    xh, yh_ref, _ = oracle_permuted(p, x)
+    xh, yh_ref, S = oracle_permuted(p, x)
     h = create(p)
-    assert sp.spmv_get_info(h)["kernel"] == 6
+    assert sp.spmv_get_info(h)["kernel"] == KERNEL_ID[kernel]
     yh = gpu_apply(h, xh, p.m)
-    assert_parity(yh, yh_ref, None, exact=True, what=f"{name}/{variant}")
+    assert_parity(yh, yh_ref, S, exact=(variant != "real"), what=f"{kernel}/{name}/{variant}")
 
 
-def test_misaligned_x_rejected_and_deterministic():
+@pytest.mark.parametrize("variant", ["int", "real"])
+def test_c5_like_default_geometry(monkeypatch, variant):
+    """The SB default (panel kernel) at its own panel size on a C5-shaped block pair."""
+    monkeypatch.delenv("SPMV_KERNEL", raising=False)
+    monkeypatch.setenv("SPMV_PN_ROWS", "30000")
+    p = _c5_like(seed=3)
+    if variant == "int":
+        rng = np.random.default_rng(1)
+        p.val[:] = rng.integers(-4, 5, p.nnz)
+    x = synth.vector(p.n, 3, 0, variant)
+    yref, S = oracle.spmv(p.row_ptr, p.col, p.val, x, nthreads=oracle.max_threads())
+    h = create(p)
+    info = sp.spmv_get_info(h)
+    assert info["kernel"] == 7 and info["xs_pad_slots"] < 0.05 * 32 * info["xs_groups"]
+    y = gpu_apply(h, x, p.m)
+    assert_parity(y, yref, S, exact=(variant == "int"), what=f"c5_like/{variant}")
+
+
+def test_misaligned_x_and_deterministic(kernel):
     p = synth.make("c5s")
     h = create(p)
     x = torch.from_numpy(oracle.permute_x(p.col_perm, p.x())).cuda()
-    buf = torch.zeros(p.n + 1, dtype=torch.float64, device="cuda")
-    buf[1:].copy_(x)
     y = torch.empty(p.m, dtype=torch.float64, device="cuda")
-    with pytest.raises(sp.SpmvError):
-        sp.spmv_apply(h, buf[1:], y)           # 8-byte aligned only
+    if kernel == "xstage":
+        buf = torch.zeros(p.n + 1, dtype=torch.float64, device="cuda")
+        buf[1:].copy_(x)
+        with pytest.raises(sp.SpmvError):
+            sp.spmv_apply(h, buf[1:], y)           # 8-byte aligned only: the bulk copy needs 16
     sp.spmv_apply(h, x, y)
     y1 = y.clone()
     for _ in range(3):
         sp.spmv_apply(h, x, y)
     torch.cuda.synchronize()
-    assert torch.equal(y, y1), "x-staged kernel must be run-to-run deterministic"
+    assert torch.equal(y, y1), "run-to-run deterministic"

@@ -55,3 +55,36 @@ def test_plan_dense_rows_and_empty_rows():
     st = sp.spmv_xs_plan_check(m, n, rp, col, val, blocks, 512)
     assert st["entries"] == len(col)
     assert st["groups_b"] == 0
+
+
+# ---------------------------------------------------------------- panel planner
+def _c5_like(K=2, rows=60_000, cols=58_800, border=1_200, seed=0):
+    synth.PRESETS["_c5like"] = lambda **kw: synth._sb(K, rows, cols, border // K, 12, 20, 0, 3, **kw)
+    return synth.make("_c5like", scramble=0, seed=seed)
+
+
+@pytest.mark.parametrize("target", [30_000, 7_000])
+def test_panel_plan_round_trip_c5_like(target):
+    p = _c5_like()
+    st = sp.spmv_pn_plan_check(p.m, p.n, p.row_ptr, p.col, p.val, p.blocks, target)
+    assert st["entries"] == p.nnz
+    assert st["epochs"] * 64 == st["groups"]
+    # big panels: little padding, few deferred nonzeros (the kernel's premise)
+    if target == 30_000:
+        assert st["pads"] < 0.05 * 32 * st["groups"]
+        assert st["deferred"] < 0.1 * p.nnz
+
+
+@pytest.mark.parametrize("name,target", [("c5s", 2000), ("c2s", 300), ("c4s", 5000)])
+def test_panel_plan_round_trip_small(name, target):
+    # small panels pad heavily (the library then keeps the row-tile kernel),
+    # but the round trip must still be exact; c4s has rows of up to 3,000 nonzeros
+    p = synth.make(name) if name == "c4s" else synth.make(name, scramble=0)
+    st = sp.spmv_pn_plan_check(p.m, p.n, p.row_ptr, p.col, p.val, p.blocks if name != "c4s" else None, target)
+    assert st["entries"] == p.nnz
+
+
+def test_panel_plan_random_sb_odd_blocks():
+    m, n, rp, col, val, blocks = _random_sb(7, 4, [37, 600, 1201, 90], [1, 2047, 2049, 5001], 333, 0.01, 0.01)
+    st = sp.spmv_pn_plan_check(m, n, rp, col, val, blocks, 400)
+    assert st["entries"] == len(col)
