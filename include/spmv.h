@@ -165,8 +165,8 @@ typedef struct {
     int64_t bytes_stream;         /* device bytes the apply kernel actually reads + writes (no x reuse) */
     int32_t n_parts, rank, world, kind;
     int32_t has_owner_map;        /* spmv_normalize is available */
-    int32_t kernel;               /* single-SpMxV kernel: 7 column-sorted panels (SB default), 0 row-tile
-                                     (default otherwise); 1-6 measurement variants (SPMV_KERNEL env) */
+    int32_t kernel;               /* single-SpMxV kernel: 0 row-tile (default); 1-7 measurement variants
+                                     selected by the SPMV_KERNEL environment variable at create */
     int32_t reserved[2];
 } spmv_info_t;
 

@@ -101,7 +101,7 @@ struct spmv_plan_s {
     int* d_counter = nullptr;         // tile-claim counter of the pipe kernel
     int32_t* d_tile_cls = nullptr;    // [T] tile class (internal.h)
     int kernel = 0;                   // 0 rowtile/256, 1 pipe, 2 tile, 3 rowtile/512, 4 rowseg, 5 rowtile/128,
-                                      // 6 x-staged, 7 column-sorted panels (default for SB handles)
+                                      // 6 x-staged, 7 column-sorted panels (SPMV_KERNEL=xstage/panel)
     // x-staged kernel (xstage.cu)
     spmvb::XsPanel* d_xs_panel = nullptr;
     int32_t* d_xs_wg = nullptr;
@@ -120,6 +120,7 @@ struct spmv_plan_s {
     uint32_t* d_pn_gidx = nullptr;
     int32_t* d_pn_gbase = nullptr;
     int64_t pn_panels = 0, pn_groups = 0, pn_pad = 0;
+    int32_t pn_max_rows = 0;
     int32_t* d_tile_seg = nullptr;    // [T*K+1]
     int32_t* d_seg_ptr = nullptr;     // [S+1]
     int32_t* d_seg_row = nullptr;     // [S]
@@ -362,13 +363,18 @@ static spmv_status_t plan_xs(spmv_plan_s* h, const std::vector<int64_t>& rp, con
 // Builds and uploads the column-sorted panel kernel's plan (plan_panel.cpp).
 // Leaves the handle on the row-tile kernel when the plan would be poor.
 static spmv_status_t plan_pn(spmv_plan_s* h, const std::vector<int64_t>& rp, const std::vector<int32_t>& pcol,
-                             const std::vector<double>& pval, const std::vector<int64_t>& rbp) {
+                             const std::vector<double>& pval, const std::vector<int64_t>& rbp,
+                             const std::vector<int64_t>& cbp) {
     const int K = (int)rbp.size() - 2;
     const int64_t R0 = h->row_begin, R1 = h->row_begin + h->m_loc;
-    std::vector<std::pair<int64_t, int64_t>> ranges;
+    std::vector<std::pair<int64_t, int64_t>> ranges, xcols;
+    const int64_t q0 = h->world > 1 ? h->x_int_begin : 0;
     for (int k = 0; k < K; ++k) {
         const int64_t a = std::max(rbp[k], R0), b = std::min(rbp[k + 1], R1);
-        if (b > a) ranges.push_back({a - R0, b - R0});
+        if (b > a) {
+            ranges.push_back({a - R0, b - R0});
+            xcols.push_back({cbp[k] - q0, cbp[k + 1] - q0});
+        }
     }
     // panels: about kPnRowsMax rows, their count a multiple of the SM count
     // when possible (whole waves of one CTA per SM)
@@ -383,11 +389,14 @@ static spmv_status_t plan_pn(spmv_plan_s* h, const std::vector<int64_t>& rp, con
     }
     target = std::max<int64_t>(target, 1024);
     if (const char* e = getenv("SPMV_PN_ROWS")) target = std::max<int64_t>(1, atoll(e));   // tests / measurements
+    if (const char* e = getenv("SPMV_L2_PERSIST_MB")) {   // measurements: L2 set-aside for evict_last lines
+        CUDA_TRY(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)atoll(e) << 20));
+    }
     const int64_t xs = h->world > 1 ? h->x_int_len : INT32_MAX;
     std::vector<spmvb::PnPanelData> pd;
     spmvb::PnPlanStats st;
     std::string why;
-    if (!spmvb::plan_panel(rp, pcol, pval, ranges, xs, target, pd, st, why)) return SPMV_OK;
+    if (!spmvb::plan_panel(rp, pcol, pval, ranges, xs, target, pd, st, why, &xcols)) return SPMV_OK;
     if (st.entries != h->nnz_loc)
         return fail(SPMV_ERR_INTERNAL, "panel plan lost nonzeros (%lld of %lld)", (long long)st.entries,
                     (long long)h->nnz_loc);
@@ -415,6 +424,8 @@ static spmv_status_t plan_pn(spmv_plan_s* h, const std::vector<int64_t>& rp, con
         std::vector<int32_t>().swap(D.gbase);
     }
     h->pn_panels = P;
+    h->pn_max_rows = 0;
+    for (int64_t p = 0; p < P; ++p) h->pn_max_rows = std::max(h->pn_max_rows, desc[p].nrows);
     h->pn_groups = G;
     h->pn_pad = st.pads;
     h->bytes_stream = (12 * 32 + 4) * G + 8 * h->m_loc;
@@ -799,8 +810,8 @@ static spmv_status_t create_impl(int64_t m, int64_t n, int64_t nnz, const int64_
         const bool sb = blocks && h->kind == SPMV_SB && nnz_loc > 0;
         if (sb && kenv && strcmp(kenv, "xstage") == 0) {
             if ((s = plan_xs(h, rp, pcol, pval, rbp, cbp))) return s;
-        } else if (sb && (!kenv || strcmp(kenv, "panel") == 0)) {
-            if ((s = plan_pn(h, rp, pcol, pval, rbp))) return s;
+        } else if (sb && kenv && strcmp(kenv, "panel") == 0) {
+            if ((s = plan_pn(h, rp, pcol, pval, rbp, cbp))) return s;
         }
     }
 
@@ -958,6 +969,7 @@ static spmv_status_t run(spmv_handle_t h, const double* x, double* y, uint32_t f
         X.x_hi = A.x_hi;
         X.y = yk;
         X.maxabs_slots = A.maxabs_slots;
+        X.max_rows = h->pn_max_rows;
         CUDA_TRY(spmvb::launch_panel(X, st));
     } else if (!split && h->kernel == 6) {
         spmvb::XsArgs X{};

@@ -144,6 +144,9 @@ struct PnPanel {
     int32_t nrows;     // rows (<= kPnRowsMax)
     int32_t g0;        // first group of the panel (groups of epoch e, step b, warp w: g0 + (e*kPnB + b)*16 + w)
     int32_t ne;        // epochs
+    int32_t pf_col;    // x_lo[pf_col, pf_col + pf_len) is prefetched into L2 at panel start
+    int32_t pf_len;    //   (a slice of the next block's interior columns, SB Eq.(1))
+    int32_t pad0, pad1;
 };
 
 struct PnArgs {
@@ -157,6 +160,8 @@ struct PnArgs {
     const double* x_hi;
     double* y;
     unsigned long long* maxabs_slots;
+    int32_t max_rows;         // largest panel: shared memory = 8 * max_rows bytes (the rest stays L1)
+    int32_t pf_epochs;        // epochs of the group stream prefetched into L2 ahead (0 = default)
 };
 cudaError_t launch_panel(const PnArgs& a, cudaStream_t s);
 

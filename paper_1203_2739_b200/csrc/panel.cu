@@ -19,6 +19,8 @@
 // issues the x gathers kGD steps ahead of their use.  The epilogue writes y
 // once per row and folds max |y|.
 #include <cstdint>
+#include <algorithm>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "internal.h"
@@ -29,14 +31,24 @@ namespace {
 constexpr int NW = kPnWarps;
 constexpr int kT = NW * 32;
 constexpr int kD = 16;    // groups in flight per warp
-constexpr int kGD = 8;    // gathers issued this many steps ahead
-static_assert(kD % kPnB == 0 && kD % kGD == 0, "ring geometry");
+constexpr int kPF = 8;    // default: epochs of the group stream prefetched into L2 ahead
+static_assert(kD % kPnB == 0, "ring geometry");
 constexpr uint32_t kDeltaMask = (1u << kPnDeltaBits) - 1u;
 
 __device__ __forceinline__ uint64_t pol_evict_first() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
+}
+__device__ __forceinline__ uint64_t pol_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ double ld_x(const double* p, uint64_t pol) {
+    double v;
+    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
 }
 __device__ __forceinline__ double ld_val(const double* p, uint64_t pol) {
     double v;
@@ -54,7 +66,14 @@ __device__ __forceinline__ int32_t ld_base(const int32_t* p) {
     return v;
 }
 
+// MODE (ablation, measurements only; 0 = the kernel): 1 no x gathers (x = 1),
+// 2 no shared-memory y update (register sum), 3 no epoch barriers (racy),
+// 4 no L2 prefetch of the group stream, 5 gathers 4 steps ahead (not 8),
+// 6 gathers of a fixed 2 MB window (no dependence on the loaded indices' values)
+template <int MODE>
 __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
+    constexpr int kGD = MODE == 5 ? 4 : 8;   // gathers issued this many steps ahead
+    static_assert(kD % kGD == 0, "ring geometry");
     extern __shared__ __align__(16) double ys[];
     const int p = blockIdx.x;
     const PnPanel d = A.panel[p];
@@ -63,6 +82,8 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
     __syncthreads();
 
     const uint64_t pol = pol_evict_first();
+    const uint64_t polx = pol_evict_last();   // x is the reused operand
+    const int PF = A.pf_epochs > 0 ? A.pf_epochs : kPF;
     const int T = d.ne * kPnB;                       // steps per warp
     const int64_t gw = (int64_t)d.g0 + warp;         // group of step t: gw + 16 t
 
@@ -76,11 +97,45 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
         i = ld_u32(A.gidx + g * 32 + lane, pol);
         b = ld_base(A.gbase + g);
     };
+    double racc = 0.0;
     auto gather = [&](uint32_t i, int32_t b) -> double {
+        if (MODE == 1) return 1.0;
+        if (MODE == 6) return __ldg(A.x_lo + ((b + (int)(i & 0xFFF)) & 0x3FFFF));
         if (i == kPnDummy) return 0.0;
         const double* xp = b < A.x_split ? A.x_lo + b : A.x_hi + (b - A.x_split);
-        return __ldg(xp + (i & kDeltaMask));
+        return ld_x(xp + (i & kDeltaMask), polx);
     };
+    // L2 prefetch of the panel's group stream kPF epochs ahead (one bulk
+    // prefetch per array per epoch, issued by thread 0): the register ring
+    // then waits for L2, not HBM, latency -- the x gathers depend on the
+    // loaded indices, so their distance is what bounds the pipeline.
+    auto prefetch_epoch = [&](int e) {
+        if (tid == 0 && e < d.ne) {
+            const int64_t g = (int64_t)d.g0 + (int64_t)e * kPnEpoch;
+            // normal priority: an evict_first prefetch is the first victim of the next one
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.gval + g * 32), "r"(kPnEpoch * 32 * 8)
+                         : "memory");
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.gidx + g * 32), "r"(kPnEpoch * 32 * 4)
+                         : "memory");
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.gbase + g), "r"(kPnEpoch * 4)
+                         : "memory");
+        }
+    };
+    if (MODE != 4) {
+        for (int e = 0; e < PF; ++e) prefetch_epoch(e);
+        // this panel's slice of the next SB block's x(C_k), kept in L2 (evict_last)
+        if (tid == 32 && d.pf_len > 0) {
+            const uint64_t pl = pol_evict_last();
+            // 16-byte aligned start and length (bulk prefetch granularity)
+            const uintptr_t a0 = reinterpret_cast<uintptr_t>(A.x_lo + d.pf_col) & ~uintptr_t(15);
+            const uintptr_t a1 = reinterpret_cast<uintptr_t>(A.x_lo + d.pf_col + d.pf_len) & ~uintptr_t(15);
+            for (uintptr_t a = a0; a < a1; a += 32768) {
+                const uint32_t n = (uint32_t)(a1 - a < 32768 ? a1 - a : 32768);
+                asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(a), "r"(n), "l"(pl)
+                             : "memory");
+            }
+        }
+    }
 #pragma unroll
     for (int u = 0; u < kD; ++u)
         if (u < T) load(u, rv[u], ri[u], rb[u]);
@@ -94,15 +149,130 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
             const int t = t0 + u;
             if (t >= T) break;
             const uint32_t i = ri[u];
-            if (i != kPnDummy) {
+            if (MODE == 2) {
+                racc = fma(rv[u], rx[u % kGD], racc);
+            } else if (i != kPnDummy) {
                 const int r = (int)(i >> kPnDeltaBits);
                 ys[r] = fma(rv[u], rx[u % kGD], ys[r]);
             }
             if (t + kD < T) load(t + kD, rv[u], ri[u], rb[u]);
             if (t + kGD < T) rx[u % kGD] = gather(ri[(u + kGD) % kD], rb[(u + kGD) % kD]);
-            if (u % kPnB == kPnB - 1) __syncthreads();   // epoch boundary (T is a multiple of kPnB)
+            if (u % kPnB == kPnB - 1) {                  // epoch boundary (T is a multiple of kPnB)
+                if (MODE != 3) __syncthreads();
+                if (MODE != 4) prefetch_epoch(t / kPnB + PF);
+            }
         }
     }
+    if (MODE == 2 && racc == 1.2345) ys[0] = racc;
+    __syncthreads();
+
+    double mx = 0.0;
+    for (int i = tid; i < d.nrows; i += kT) {
+        const double v = ys[i];
+        A.y[d.row0 + i] = v;
+        mx = fmax(mx, fabs(v));
+    }
+    if (A.maxabs_slots) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+        if (lane == 0 && mx > 0.0)
+            atomicMax(A.maxabs_slots + ((p * NW + warp) & (kMaxSlots - 1)) * kSlotStride,
+                      (unsigned long long)__double_as_longlong(mx));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Variant with the x gathers going to shared memory (cp.async, no register
+// cost per gather in flight): G steps of gathers in flight per warp.
+template <int G>
+__global__ void __launch_bounds__(kT, 1) spmv_panel2_kernel(const PnArgs A) {
+    constexpr int kD2 = 24;   // groups of (value, index, base) in flight per warp (registers)
+    static_assert(kD2 % kPnB == 0 && kD2 % G == 0 && G >= 2 && G < kD2, "ring geometry");
+    extern __shared__ __align__(16) double sm2[];
+    double* ys = sm2;
+    const int p = blockIdx.x;
+    const PnPanel d = A.panel[p];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    double* gr = sm2 + ((A.max_rows + 1) & ~1) + warp * G * 32;
+    const uint32_t gr_s = (uint32_t)__cvta_generic_to_shared(gr) + lane * 8;
+    for (int i = tid; i < d.nrows; i += kT) ys[i] = 0.0;
+    __syncthreads();
+
+    const uint64_t pol = pol_evict_first();
+    const uint64_t polx = pol_evict_last();
+    const int PF = A.pf_epochs > 0 ? A.pf_epochs : kPF;
+    const int T = d.ne * kPnB;
+    const int64_t gw = (int64_t)d.g0 + warp;
+
+    double rv[kD2];
+    uint32_t ri[kD2];
+    int32_t rb[kD2];
+    auto load = [&](int t, double& v, uint32_t& i, int32_t& b) {
+        const int64_t g = gw + 16 * (int64_t)t;
+        v = ld_val(A.gval + g * 32 + lane, pol);
+        i = ld_u32(A.gidx + g * 32 + lane, pol);
+        b = ld_base(A.gbase + g);
+    };
+    auto issue = [&](int slot, uint32_t i, int32_t b) {
+        if (i != kPnDummy) {
+            const double* xp = (b < A.x_split ? A.x_lo + b : A.x_hi + (b - A.x_split)) + (i & kDeltaMask);
+            asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;" ::"r"(gr_s + slot * 256),
+                         "l"(xp), "l"(polx) : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    auto prefetch_epoch = [&](int e) {
+        if (tid == 0 && e < d.ne) {
+            const int64_t g = (int64_t)d.g0 + (int64_t)e * kPnEpoch;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.gval + g * 32), "r"(kPnEpoch * 32 * 8)
+                         : "memory");
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.gidx + g * 32), "r"(kPnEpoch * 32 * 4)
+                         : "memory");
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.gbase + g), "r"(kPnEpoch * 4)
+                         : "memory");
+        }
+    };
+    for (int e = 0; e < PF; ++e) prefetch_epoch(e);
+    if (tid == 32 && d.pf_len > 0) {
+        const uintptr_t a0 = reinterpret_cast<uintptr_t>(A.x_lo + d.pf_col) & ~uintptr_t(15);
+        const uintptr_t a1 = reinterpret_cast<uintptr_t>(A.x_lo + d.pf_col + d.pf_len) & ~uintptr_t(15);
+        for (uintptr_t a = a0; a < a1; a += 32768) {
+            const uint32_t n = (uint32_t)(a1 - a < 32768 ? a1 - a : 32768);
+            asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(a), "r"(n), "l"(polx)
+                         : "memory");
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < kD2; ++u)
+        if (u < T) load(u, rv[u], ri[u], rb[u]);
+#pragma unroll
+    for (int u = 0; u < G - 1; ++u) {
+        if (u < T) issue(u, ri[u], rb[u]);
+        else asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+
+    for (int t0 = 0; t0 < T; t0 += kD2) {
+#pragma unroll
+        for (int u = 0; u < kD2; ++u) {
+            const int t = t0 + u;
+            if (t >= T) break;
+            // gathers of step t + G - 1 into ring slot (t + G - 1) % G (consumed at step t - 1)
+            if (t + G - 1 < T) issue((u + G - 1) % G, ri[(u + G - 1) % kD2], rb[(u + G - 1) % kD2]);
+            else asm volatile("cp.async.commit_group;" ::: "memory");
+            asm volatile("cp.async.wait_group %0;" ::"n"(G - 1) : "memory");
+            const uint32_t i = ri[u];
+            if (i != kPnDummy) {
+                const int r = (int)(i >> kPnDeltaBits);
+                ys[r] = fma(rv[u], gr[(u % G) * 32 + lane], ys[r]);
+            }
+            if (t + kD2 < T) load(t + kD2, rv[u], ri[u], rb[u]);
+            if (u % kPnB == kPnB - 1) {
+                __syncthreads();
+                prefetch_epoch(t / kPnB + PF);
+            }
+        }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
 
     double mx = 0.0;
@@ -124,14 +294,42 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
 
 cudaError_t launch_panel(const PnArgs& a, cudaStream_t s) {
     if (a.n_panels <= 0) return cudaSuccess;
-    static bool attr_done = false;
-    const size_t smem = (size_t)kPnRowsMax * sizeof(double);
-    if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(spmv_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        attr_done = true;
+    static int mode = -1, pf_env = 0;
+    // only the panel's y in shared memory: the rest of the 256 KB L1/shared
+    // array stays L1, which holds the global loads in flight
+    const size_t smem = (size_t)std::max(a.max_rows, 1) * sizeof(double);
+    if (mode < 0) {
+        const char* e = getenv("SPMV_PN_MODE");   // ablations for measurements only
+        mode = e ? atoi(e) : 0;
+        const char* f = getenv("SPMV_PN_PF");
+        pf_env = f ? atoi(f) : 0;
+        cudaError_t r = cudaSuccess;
+        const int smax = kPnRowsMax * (int)sizeof(double);
+        r = cudaFuncSetAttribute(spmv_panel_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
+        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
+        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
+        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
+        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
+        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
+        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
+        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel2_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel2_kernel<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        if (r != cudaSuccess) return r;
     }
-    spmv_panel_kernel<<<a.n_panels, kT, smem, s>>>(a);
+    PnArgs b = a;
+    auto smem2 = [&](int G) { return (size_t)((a.max_rows + 1) & ~1) * 8 + (size_t)NW * G * 256; };
+    if (pf_env > 0) b.pf_epochs = pf_env;
+    switch (mode) {
+    case 1: spmv_panel_kernel<1><<<b.n_panels, kT, smem, s>>>(b); break;
+    case 2: spmv_panel_kernel<2><<<b.n_panels, kT, smem, s>>>(b); break;
+    case 3: spmv_panel_kernel<3><<<b.n_panels, kT, smem, s>>>(b); break;
+    case 4: spmv_panel_kernel<4><<<b.n_panels, kT, smem, s>>>(b); break;
+    case 6: spmv_panel_kernel<6><<<b.n_panels, kT, smem, s>>>(b); break;
+    case 5: spmv_panel_kernel<5><<<b.n_panels, kT, smem, s>>>(b); break;
+    case 7: spmv_panel2_kernel<8><<<b.n_panels, kT, smem2(8), s>>>(b); break;
+    case 8: spmv_panel2_kernel<12><<<b.n_panels, kT, smem2(12), s>>>(b); break;
+    default: spmv_panel_kernel<0><<<b.n_panels, kT, smem, s>>>(b);
+    }
     return cudaGetLastError();
 }
 

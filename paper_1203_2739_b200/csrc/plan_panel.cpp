@@ -153,15 +153,23 @@ void build_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col
 
 bool plan_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col, const std::vector<double>& val,
                 const std::vector<std::pair<int64_t, int64_t>>& ranges, int64_t x_split, int64_t rows_target,
-                std::vector<PnPanelData>& out, PnPlanStats& st, std::string& why) {
+                std::vector<PnPanelData>& out, PnPlanStats& st, std::string& why,
+                const std::vector<std::pair<int64_t, int64_t>>* xcols) {
     out.clear();
     st = PnPlanStats{};
     const int64_t R = std::min<int64_t>(std::max<int64_t>(rows_target, 1), kPnRowsMax);
-    for (const auto& rg : ranges) {
+    for (size_t k = 0; k < ranges.size(); ++k) {
+        const auto& rg = ranges[k];
         const int64_t L = rg.second - rg.first;
         if (L <= 0) continue;
         int64_t np = (L + R - 1) / R;
         while ((L + np - 1) / np > kPnRowsMax) ++np;
+        // L2 prefetch slice: the next range's interior columns, cut in np pieces
+        int64_t pf0 = 0, pf1 = 0;
+        if (xcols && k + 1 < xcols->size()) {
+            pf0 = (*xcols)[k + 1].first;
+            pf1 = (*xcols)[k + 1].second;
+        }
         for (int64_t p = 0; p < np; ++p) {
             const int64_t a = rg.first + L * p / np, e = rg.first + L * (p + 1) / np;
             if (e - a > (int64_t(1) << kPnRowBits) - 1) {
@@ -175,6 +183,16 @@ bool plan_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col,
             PnPanelData d;
             d.desc.row0 = (int32_t)a;
             d.desc.nrows = (int32_t)(e - a);
+            if (pf1 > pf0) {
+                // 16-byte aligned slice boundaries (the bulk prefetch works in 16-byte units)
+                int64_t s0 = pf0 + (pf1 - pf0) * p / np, s1 = pf0 + (pf1 - pf0) * (p + 1) / np;
+                s0 &= ~int64_t(1);
+                s1 = std::min<int64_t>(s1 & ~int64_t(1), pf1 & ~int64_t(1));
+                if (s1 > s0) {
+                    d.desc.pf_col = (int32_t)s0;
+                    d.desc.pf_len = (int32_t)(s1 - s0);
+                }
+            }
             out.push_back(std::move(d));
         }
     }

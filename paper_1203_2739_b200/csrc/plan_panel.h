@@ -24,9 +24,12 @@ struct PnPlanStats {
 // into panels of about rows_target rows.  Columns >= x_split come from the
 // second x pointer; a group never mixes the two sides.  Returns false (and
 // why) when the plan would be poor (caller falls back to the row-tile kernel).
+// xcols (optional, one per range): the range's interior columns [c0, c1) --
+// each panel of range k then prefetches a slice of range k+1's columns.
 bool plan_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col, const std::vector<double>& val,
                 const std::vector<std::pair<int64_t, int64_t>>& ranges, int64_t x_split, int64_t rows_target,
-                std::vector<PnPanelData>& out, PnPlanStats& st, std::string& why);
+                std::vector<PnPanelData>& out, PnPlanStats& st, std::string& why,
+                const std::vector<std::pair<int64_t, int64_t>>* xcols = nullptr);
 
 // Test hook: decode the groups back into (row, column, value) and compare with
 // the CSR bit for bit; checks the epoch invariant (distinct rows per epoch).
