@@ -396,7 +396,7 @@ static spmv_status_t plan_pn(spmv_plan_s* h, const std::vector<int64_t>& rp, con
     std::vector<spmvb::PnPanelData> pd;
     spmvb::PnPlanStats st;
     std::string why;
-    if (!spmvb::plan_panel(rp, pcol, pval, ranges, xs, target, pd, st, why, &xcols)) return SPMV_OK;
+    if (!spmvb::plan_panel(rp, pcol, pval, ranges, xs, target, pd, st, why, &xcols, sms)) return SPMV_OK;
     if (st.entries != h->nnz_loc)
         return fail(SPMV_ERR_INTERNAL, "panel plan lost nonzeros (%lld of %lld)", (long long)st.entries,
                     (long long)h->nnz_loc);
@@ -1003,6 +1003,10 @@ static spmv_status_t run(spmv_handle_t h, const double* x, double* y, uint32_t f
         P.y = A.y;
         P.maxabs_slots = A.maxabs_slots;
         P.tile_counter = h->d_counter;
+        // x gathers: L1 no-allocate (a gathered line is not reused by the tile) and
+        // L2 evict-last (x is the reused operand; the matrix streams evict-first)
+        P.gmode = 2;
+        if (const char* g = getenv("SPMV_RT_GMODE")) P.gmode = atoi(g);   // measurements only
         if (h->kernel == 1) CUDA_TRY(spmvb::launch_pipe(P, xsplit, st));
         else if (h->kernel == 3) CUDA_TRY(spmvb::launch_rowtile(P, xsplit, 512, st));
         else if (h->kernel == 4) CUDA_TRY(spmvb::launch_rowseg(P, xsplit, st));

@@ -58,6 +58,8 @@ struct PipeArgs {
     double* y;
     unsigned long long* maxabs_slots;
     int* tile_counter;         // zeroed by launch_pipe before every launch
+    int32_t gmode;             // x gather flavour (measurements): 0 ld.global.nc, 1 + L2 evict_last,
+                               // 2 + L1 no_allocate and L2 evict_last
 };
 cudaError_t launch_pipe(const PipeArgs& a, bool xsplit, cudaStream_t s);
 // Default single-SpMxV kernel (rowtile.cu): one 512-thread CTA per row tile.

@@ -290,6 +290,146 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel2_kernel(const PnArgs A) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Variant 3: the group stream goes HBM -> L2 (bulk prefetch) -> shared memory
+// (bulk copies, one per array per epoch, mbarrier-tracked) instead of
+// through registers, so the LSU queue carries only the x gathers (L2 hits)
+// and the shared-memory traffic.  NS epochs of stream staged, G steps of
+// gathers in flight per warp.
+constexpr int kStage3 = kPnEpoch * 32 * 8 + kPnEpoch * 32 * 4 + kPnEpoch * 4;   // 24,832 B per epoch
+
+template <int NS, int G>
+__global__ void __launch_bounds__(kT, 1) spmv_panel3_kernel(const PnArgs A) {
+    static_assert(G % kPnB == 0 && G / kPnB <= NS - 1, "gathers read stages loaded ahead");
+    constexpr int U = G;   // unroll (multiple of kPnB)
+    extern __shared__ __align__(128) unsigned char sm3[];
+    const int p = blockIdx.x;
+    const PnPanel d = A.panel[p];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int yb = ((A.max_rows * 8 + 127) / 128) * 128;
+    double* ys = reinterpret_cast<double*>(sm3);
+    unsigned char* st = sm3 + yb;
+    uint64_t* full = reinterpret_cast<uint64_t*>(st + NS * kStage3);
+    auto sval = [&](int e) { return reinterpret_cast<const double*>(st + (e % NS) * kStage3); };
+    auto sidx = [&](int e) { return reinterpret_cast<const uint32_t*>(st + (e % NS) * kStage3 + kPnEpoch * 32 * 8); };
+    auto sbase = [&](int e) { return reinterpret_cast<const int32_t*>(st + (e % NS) * kStage3 + kPnEpoch * 32 * 12); };
+
+    const uint64_t polx = pol_evict_last();
+    const uint64_t pol = pol_evict_first();
+    const int PF = A.pf_epochs > 0 ? A.pf_epochs : kPF;
+    const int ne = d.ne, T = ne * kPnB;
+    auto bulk = [&](void* dst, const void* src, int bytes, uint64_t* bar) {
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+                     ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src), "r"(bytes),
+                     "r"((uint32_t)__cvta_generic_to_shared(bar)), "l"(pol) : "memory");
+    };
+    auto load_epoch = [&](int e) {   // thread 0 only
+        if (e >= ne) return;
+        uint64_t* bar = &full[e % NS];
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)),
+                     "r"(kStage3) : "memory");
+        const int64_t g = (int64_t)d.g0 + (int64_t)e * kPnEpoch;
+        unsigned char* dst = st + (e % NS) * kStage3;
+        bulk(dst, A.gval + g * 32, kPnEpoch * 32 * 8, bar);
+        bulk(dst + kPnEpoch * 32 * 8, A.gidx + g * 32, kPnEpoch * 32 * 4, bar);
+        bulk(dst + kPnEpoch * 32 * 12, A.gbase + g, kPnEpoch * 4, bar);
+    };
+    auto prefetch_epoch = [&](int e) {   // thread 0 only
+        if (e >= ne) return;
+        const int64_t g = (int64_t)d.g0 + (int64_t)e * kPnEpoch;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.gval + g * 32), "r"(kPnEpoch * 32 * 8) : "memory");
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.gidx + g * 32), "r"(kPnEpoch * 32 * 4) : "memory");
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.gbase + g), "r"(kPnEpoch * 4) : "memory");
+    };
+    auto wait_epoch = [&](int e) {
+        const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&full[e % NS]);
+        const uint32_t par = (uint32_t)((e / NS) & 1);
+        asm volatile("{\n.reg .pred q;\nW3: mbarrier.try_wait.parity.shared::cta.b64 q, [%0], %1;\n@!q bra W3;\n}"
+                     ::"r"(bar), "r"(par) : "memory");
+    };
+
+    if (tid == 0) {
+        for (int s = 0; s < NS; ++s)
+            asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&full[s])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    for (int i = tid; i < d.nrows; i += kT) ys[i] = 0.0;
+    __syncthreads();
+    if (tid == 0) {
+        for (int e = 0; e < NS; ++e) load_epoch(e);
+        for (int e = NS; e < NS + PF; ++e) prefetch_epoch(e);
+    }
+    if (tid == 32 && d.pf_len > 0) {
+        const uintptr_t a0 = reinterpret_cast<uintptr_t>(A.x_lo + d.pf_col) & ~uintptr_t(15);
+        const uintptr_t a1 = reinterpret_cast<uintptr_t>(A.x_lo + d.pf_col + d.pf_len) & ~uintptr_t(15);
+        for (uintptr_t a = a0; a < a1; a += 32768) {
+            const uint32_t n = (uint32_t)(a1 - a < 32768 ? a1 - a : 32768);
+            asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(a), "r"(n), "l"(polx)
+                         : "memory");
+        }
+    }
+
+    double rx[G];
+    uint32_t ri[G];
+    // gather of step t: group k = (t % kPnB) * 16 + warp of epoch t / kPnB
+    auto issue = [&](int t, double& xv, uint32_t& iv) {
+        const int e = t / kPnB, k = (t % kPnB) * NW + warp;
+        const uint32_t i = sidx(e)[k * 32 + lane];
+        const int32_t b = sbase(e)[k];
+        iv = i;
+        if (i != kPnDummy) {
+            const double* xp = b < A.x_split ? A.x_lo + b : A.x_hi + (b - A.x_split);
+            xv = ld_x(xp + (i & kDeltaMask), polx);
+        }
+    };
+    for (int e = 0; e < G / kPnB && e < ne; ++e) wait_epoch(e);
+#pragma unroll
+    for (int u = 0; u < G; ++u)
+        if (u < T) issue(u, rx[u], ri[u]);
+
+    for (int t0 = 0; t0 < T; t0 += U) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int t = t0 + u;
+            if (t >= T) break;
+            const int e = t / kPnB, k = (u % kPnB) * NW + warp;
+            const uint32_t i = ri[u];
+            if (i != kPnDummy) {
+                const int r = (int)(i >> kPnDeltaBits);
+                ys[r] = fma(sval(e)[k * 32 + lane], rx[u], ys[r]);
+            }
+            const int tn = t + G;
+            if (tn < T) {
+                if (u % kPnB == 0) wait_epoch(tn / kPnB);
+                issue(tn, rx[u], ri[u]);
+            }
+            if (u % kPnB == kPnB - 1) {   // end of epoch e: its stage is free for epoch e + NS
+                __syncthreads();
+                if (tid == 0) {
+                    load_epoch(e + NS);
+                    prefetch_epoch(e + NS + PF);
+                }
+            }
+        }
+    }
+    __syncthreads();
+
+    double mx = 0.0;
+    for (int i = tid; i < d.nrows; i += kT) {
+        const double v = ys[i];
+        A.y[d.row0 + i] = v;
+        mx = fmax(mx, fabs(v));
+    }
+    if (A.maxabs_slots) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+        if (lane == 0 && mx > 0.0)
+            atomicMax(A.maxabs_slots + ((p * NW + warp) & (kMaxSlots - 1)) * kSlotStride,
+                      (unsigned long long)__double_as_longlong(mx));
+    }
+}
+
 }  // namespace
 
 cudaError_t launch_panel(const PnArgs& a, cudaStream_t s) {
@@ -314,9 +454,14 @@ cudaError_t launch_panel(const PnArgs& a, cudaStream_t s) {
         if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
         if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel2_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel2_kernel<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel3_kernel<4, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel3_kernel<3, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel3_kernel<4, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel3_kernel<5, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         if (r != cudaSuccess) return r;
     }
     PnArgs b = a;
+    auto smem3 = [&](int NS) { return (size_t)(((a.max_rows * 8 + 127) / 128) * 128) + (size_t)NS * kStage3 + 64; };
     auto smem2 = [&](int G) { return (size_t)((a.max_rows + 1) & ~1) * 8 + (size_t)NW * G * 256; };
     if (pf_env > 0) b.pf_epochs = pf_env;
     switch (mode) {
@@ -326,6 +471,10 @@ cudaError_t launch_panel(const PnArgs& a, cudaStream_t s) {
     case 4: spmv_panel_kernel<4><<<b.n_panels, kT, smem, s>>>(b); break;
     case 6: spmv_panel_kernel<6><<<b.n_panels, kT, smem, s>>>(b); break;
     case 5: spmv_panel_kernel<5><<<b.n_panels, kT, smem, s>>>(b); break;
+    case 9: spmv_panel3_kernel<4, 8><<<b.n_panels, kT, smem3(4), s>>>(b); break;
+    case 10: spmv_panel3_kernel<3, 8><<<b.n_panels, kT, smem3(3), s>>>(b); break;
+    case 11: spmv_panel3_kernel<4, 12><<<b.n_panels, kT, smem3(4), s>>>(b); break;
+    case 12: spmv_panel3_kernel<5, 16><<<b.n_panels, kT, smem3(5), s>>>(b); break;
     case 7: spmv_panel2_kernel<8><<<b.n_panels, kT, smem2(8), s>>>(b); break;
     case 8: spmv_panel2_kernel<12><<<b.n_panels, kT, smem2(12), s>>>(b); break;
     default: spmv_panel_kernel<0><<<b.n_panels, kT, smem, s>>>(b);

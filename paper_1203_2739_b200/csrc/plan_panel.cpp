@@ -28,6 +28,7 @@
 #include "plan_panel.h"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <omp.h>
 
@@ -86,7 +87,9 @@ void build_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col
         for (int64_t e = rp[r0 + r]; e < rp[r0 + r + 1]; ++e) {
             const int64_t i = e - a;
             ents[i] = {(int32_t)r, col[e], val[e]};
-            keys[i] = ((uint64_t)(uint32_t)col[e] << 32) | (uint64_t)i;
+            // rotated sweep: panels of one block start at different columns, so
+            // concurrently running CTAs do not all hit the same x lines (L2 slices)
+            keys[i] = ((uint64_t)((uint32_t)col[e] - (uint32_t)P.rot) << 32) | (uint64_t)i;
         }
     std::sort(keys.begin(), keys.end());
     P.entries = n;
@@ -104,8 +107,8 @@ void build_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col
         // returns false when the epoch is full (entry not taken)
         auto take = [&](int64_t i) -> bool {
             const Ent& e = ents[i];
-            if (em.size() > 0 && (em.size() == 32 || (int64_t)e.col - em.base() >= kMaxDelta ||
-                                  side(e.col) != side(em.base()))) {
+            const int64_t delta = (int64_t)e.col - em.base();
+            if (em.size() > 0 && (em.size() == 32 || delta < 0 || delta >= kMaxDelta || side(e.col) != side(em.base()))) {
                 em.close();
                 if (++ng == kPnEpoch) return false;
             }
@@ -154,7 +157,7 @@ void build_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col
 bool plan_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col, const std::vector<double>& val,
                 const std::vector<std::pair<int64_t, int64_t>>& ranges, int64_t x_split, int64_t rows_target,
                 std::vector<PnPanelData>& out, PnPlanStats& st, std::string& why,
-                const std::vector<std::pair<int64_t, int64_t>>* xcols) {
+                const std::vector<std::pair<int64_t, int64_t>>* xcols, int64_t pf_sms) {
     out.clear();
     st = PnPlanStats{};
     const int64_t R = std::min<int64_t>(std::max<int64_t>(rows_target, 1), kPnRowsMax);
@@ -164,11 +167,13 @@ bool plan_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col,
         if (L <= 0) continue;
         int64_t np = (L + R - 1) / R;
         while ((L + np - 1) / np > kPnRowsMax) ++np;
-        // L2 prefetch slice: the next range's interior columns, cut in np pieces
+        // L2 prefetch slice: the interior columns of the range that starts about
+        // one wave after this one (its panels then find x in L2), cut in np pieces
         int64_t pf0 = 0, pf1 = 0;
-        if (xcols && k + 1 < xcols->size()) {
-            pf0 = (*xcols)[k + 1].first;
-            pf1 = (*xcols)[k + 1].second;
+        const size_t ahead = (size_t)std::max<int64_t>(1, (pf_sms + np - 1) / np + 1);
+        if (xcols && k + ahead < xcols->size()) {
+            pf0 = (*xcols)[k + ahead].first;
+            pf1 = (*xcols)[k + ahead].second;
         }
         for (int64_t p = 0; p < np; ++p) {
             const int64_t a = rg.first + L * p / np, e = rg.first + L * (p + 1) / np;
@@ -183,6 +188,10 @@ bool plan_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col,
             PnPanelData d;
             d.desc.row0 = (int32_t)a;
             d.desc.nrows = (int32_t)(e - a);
+            if (xcols && k < xcols->size() && getenv("SPMV_PN_NOROT") == nullptr) {
+                const int64_t c0 = (*xcols)[k].first, c1 = (*xcols)[k].second;
+                d.rot = (int32_t)(c0 + (c1 - c0) * p / np);
+            }
             if (pf1 > pf0) {
                 // 16-byte aligned slice boundaries (the bulk prefetch works in 16-byte units)
                 int64_t s0 = pf0 + (pf1 - pf0) * p / np, s1 = pf0 + (pf1 - pf0) * (p + 1) / np;

@@ -14,6 +14,7 @@ struct PnPanelData {
     std::vector<uint32_t> gidx;    // [groups*32]
     std::vector<int32_t> gbase;    // [groups]
     int64_t entries = 0, pads = 0, deferred = 0;
+    int32_t rot = 0;               // the column sweep starts at this column (wraps around)
 };
 
 struct PnPlanStats {
@@ -29,7 +30,7 @@ struct PnPlanStats {
 bool plan_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col, const std::vector<double>& val,
                 const std::vector<std::pair<int64_t, int64_t>>& ranges, int64_t x_split, int64_t rows_target,
                 std::vector<PnPanelData>& out, PnPlanStats& st, std::string& why,
-                const std::vector<std::pair<int64_t, int64_t>>* xcols = nullptr);
+                const std::vector<std::pair<int64_t, int64_t>>* xcols = nullptr, int64_t pf_sms = 148);
 
 // Test hook: decode the groups back into (row, column, value) and compare with
 // the CSR bit for bit; checks the epoch invariant (distinct rows per epoch).

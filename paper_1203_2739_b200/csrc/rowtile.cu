@@ -59,10 +59,24 @@ __device__ __forceinline__ double2 ld_v2d(const double* ptr, uint64_t pol) {
     return r;
 }
 
+__device__ __forceinline__ double gx(const double* p, int gmode, uint64_t pl) {
+    double v;
+    if (gmode == 1) {
+        asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pl));
+    } else if (gmode == 2) {
+        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pl));
+    } else {
+        v = __ldg(p);
+    }
+    return v;
+}
+
 template <bool XSPLIT>
 __device__ __forceinline__ double ldx(const RowTileArgs& A, int c) {
-    if (XSPLIT) return c < A.x_split ? __ldg(A.x_lo + c) : __ldg(A.x_hi + (c - A.x_split));
-    return __ldg(A.x_lo + c);
+    uint64_t pl = 0;
+    if (A.gmode) asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pl));
+    if (XSPLIT) return c < A.x_split ? gx(A.x_lo + c, A.gmode, pl) : gx(A.x_hi + (c - A.x_split), A.gmode, pl);
+    return gx(A.x_lo + c, A.gmode, pl);
 }
 
 
