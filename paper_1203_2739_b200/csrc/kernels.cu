@@ -272,8 +272,29 @@ __global__ void maxabs_finish_kernel(const unsigned long long* __restrict__ slot
     if (threadIdx.x == 0) *out = __longlong_as_double((long long)m);
 }
 
-__global__ void normalize_kernel(const double* __restrict__ y, const int32_t* __restrict__ owner,
-                                 const double* __restrict__ m, double* __restrict__ x, int64_t n) {
+// x_next[c] = y[owner[c]] / m, four columns per thread step: one 128-bit load
+// of owner, two 128-bit stores of x (IEEE division: bit-exact with the oracle).
+__global__ void __launch_bounds__(256) normalize_kernel(const double* __restrict__ y, const int32_t* __restrict__ owner,
+                                                        const double* __restrict__ m, double* __restrict__ x, int64_t n) {
+    const double mt = *m;
+    const int64_t n4 = n >> 2;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int4* o4 = reinterpret_cast<const int4*>(owner);
+    double2* x2 = reinterpret_cast<double2*>(x);
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n4; q += stride) {
+        int4 o;
+        asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(o.x), "=r"(o.y), "=r"(o.z), "=r"(o.w) : "l"(o4 + q));
+        const double a = __ldg(y + o.x), b = __ldg(y + o.y), c = __ldg(y + o.z), d = __ldg(y + o.w);
+        x2[2 * q] = make_double2(a / mt, b / mt);
+        x2[2 * q + 1] = make_double2(c / mt, d / mt);
+    }
+    for (int64_t c = 4 * n4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n; c += stride)
+        x[c] = __ldg(y + owner[c]) / mt;
+}
+
+__global__ void normalize_scalar_kernel(const double* __restrict__ y, const int32_t* __restrict__ owner,
+                                        const double* __restrict__ m, double* __restrict__ x, int64_t n) {
     const double mt = *m;
     for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x)
         x[c] = __ldg(y + owner[c]) / mt;
@@ -324,7 +345,11 @@ cudaError_t launch_maxabs_finish(const unsigned long long* slots, double* out, c
 cudaError_t launch_normalize(const double* y, const int32_t* owner, const double* m, double* x_next,
                              int64_t n, cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
-    normalize_kernel<<<grid_for(n, 256), 256, 0, s>>>(y, owner, m, x_next, n);
+    if (((uintptr_t)x_next & 15) || ((uintptr_t)owner & 15)) {   // vector path needs 16-byte alignment
+        normalize_scalar_kernel<<<grid_for(n, 256), 256, 0, s>>>(y, owner, m, x_next, n);
+    } else {
+        normalize_kernel<<<grid_for((n + 3) / 4, 256), 256, 0, s>>>(y, owner, m, x_next, n);
+    }
     return cudaGetLastError();
 }
 
