@@ -738,6 +738,7 @@ static spmv_status_t create_impl(int64_t m, int64_t n, int64_t nnz, const int64_
         if (kenv && strcmp(kenv, "rowtile512") == 0) h->kernel = 3;
         if (kenv && strcmp(kenv, "rowseg") == 0) h->kernel = 4;
         if (kenv && strcmp(kenv, "rowtile128") == 0) h->kernel = 5;
+        if (kenv && strcmp(kenv, "rowlin") == 0) h->kernel = 8;
     }
     h->bytes_stream = 12 * nnz_loc + 4 * (m_loc + 1) + 8 * m_loc;
 
@@ -1011,6 +1012,7 @@ static spmv_status_t run(spmv_handle_t h, const double* x, double* y, uint32_t f
         else if (h->kernel == 3) CUDA_TRY(spmvb::launch_rowtile(P, xsplit, 512, st));
         else if (h->kernel == 4) CUDA_TRY(spmvb::launch_rowseg(P, xsplit, st));
         else if (h->kernel == 5) CUDA_TRY(spmvb::launch_rowtile(P, xsplit, 128, st));
+        else if (h->kernel == 8) CUDA_TRY(spmvb::launch_rowtile(P, xsplit, 256, st, true));
         else CUDA_TRY(spmvb::launch_rowtile(P, xsplit, 256, st));
     } else if (!split) {
         A.tile_seg = h->d_tile_row;

@@ -64,7 +64,7 @@ struct PipeArgs {
 cudaError_t launch_pipe(const PipeArgs& a, bool xsplit, cudaStream_t s);
 // Default single-SpMxV kernel (rowtile.cu): one 512-thread CTA per row tile.
 using RowTileArgs = PipeArgs;
-cudaError_t launch_rowtile(const RowTileArgs& a, bool xsplit, int threads, cudaStream_t s);
+cudaError_t launch_rowtile(const RowTileArgs& a, bool xsplit, int threads, cudaStream_t s, bool lin = false);
 cudaError_t launch_rowseg(const RowTileArgs& a, bool xsplit, cudaStream_t s);
 // Fused / literal multiple-SpMxV kernel (split.cu), K <= 64 parts.
 constexpr int kMaxParts = 64;

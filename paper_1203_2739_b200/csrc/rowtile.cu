@@ -90,8 +90,23 @@ struct RTSmemT {
     double red[NT / 32];
 };
 
+__device__ __forceinline__ int32_t ld_s32(const int32_t* ptr, uint64_t pol) {
+    int32_t r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(r) : "l"(ptr), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ double ld_f64(const double* ptr, uint64_t pol) {
+    double r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(ptr), "l"(pol));
+    return r;
+}
+
 // NT threads per tile CTA; each thread streams QPT = 512/NT quads.
-template <bool XSPLIT, int NT>
+// LIN: lane-consecutive positions instead of quads (thread t takes positions
+// t, t+NT, ...): the same coalesced stream, but the 32 gathers of one warp
+// instruction are for 32 consecutive nonzeros, so sorted columns of a long
+// row share 128-byte lines (C4's banded rows).
+template <bool XSPLIT, int NT, bool LIN>
 __global__ void __launch_bounds__(NT, (NT == 512 ? 3 : NT == 256 ? 6 : 8)) spmv_rowtile_kernel(const RowTileArgs A) {
     constexpr int QPT = 512 / NT;
     __shared__ __align__(16) RTSmemT<NT> sm;
@@ -109,7 +124,24 @@ __global__ void __launch_bounds__(NT, (NT == 512 ? 3 : NT == 256 ? 6 : 8)) spmv_
         // ------------------------------------------- one long row (> a tile)
         const int64_t qa = a >> 2, qb = ((int64_t)b + 3) >> 2;
         double acc = 0.0;
-        for (int64_t q = qa + tid; q < qb; q += NT) {
+        if (LIN) {
+            for (int64_t e = a + tid; e < b; e += 4 * NT) {
+                double v[4], xv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int64_t f = e + u * NT;
+                    v[u] = 0.0;
+                    if (f < b) {
+                        v[u] = ld_f64(A.val + f, pol);
+                        xv[u] = ldx<XSPLIT>(A, ld_s32(A.col + f, pol));
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (e + u * NT < b) acc += v[u] * xv[u];
+            }
+        }
+        for (int64_t q = qa + tid; !LIN && q < qb; q += NT) {
             const int4 c = ld_v4(A.col + 4 * q, pol);
             const double2 v0 = ld_v2d(A.val + 4 * q, pol);
             const double2 v1 = ld_v2d(A.val + 4 * q + 2, pol);
@@ -137,7 +169,31 @@ __global__ void __launch_bounds__(NT, (NT == 512 ? 3 : NT == 256 ? 6 : 8)) spmv_
     // ------------------------------------------------ stage products, so[]
     for (int j = tid; j <= nr; j += NT) sm.so[j] = A.rowptr[r0 + j] - a4;
     if (tid == 0) sm.nlong = 0;
-    {
+    if (LIN) {
+        const int lo = a - a4, hi = b - a4;
+        constexpr int PPT = kTileNnz / NT;   // positions per thread
+        int32_t c[PPT];
+        double v[PPT];
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+            const int p = tid + k * NT;
+            if (p >= lo && p < hi) {
+                c[k] = ld_s32(A.col + a4 + p, pol);
+                v[k] = ld_f64(A.val + a4 + p, pol);
+            }
+        }
+        double xv[PPT];
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+            const int p = tid + k * NT;
+            if (p >= lo && p < hi) xv[k] = ldx<XSPLIT>(A, c[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+            const int p = tid + k * NT;
+            if (p >= lo && p < hi) sm.prod[p] = v[k] * xv[k];
+        }
+    } else {
         const int lo = a - a4, hi = b - a4;
         int4 c[QPT];
         double2 v0[QPT], v1[QPT];
@@ -404,17 +460,20 @@ __global__ void __launch_bounds__(kRT, 3) spmv_rowseg_kernel(const RowTileArgs A
 
 }  // namespace
 
-cudaError_t launch_rowtile(const RowTileArgs& a, bool xsplit, int nt, cudaStream_t s) {
+cudaError_t launch_rowtile(const RowTileArgs& a, bool xsplit, int nt, cudaStream_t s, bool lin) {
     if (a.n_tiles <= 0) return cudaSuccess;
-    if (nt == 256) {
-        if (xsplit) spmv_rowtile_kernel<true, 256><<<a.n_tiles, 256, 0, s>>>(a);
-        else spmv_rowtile_kernel<false, 256><<<a.n_tiles, 256, 0, s>>>(a);
+    if (lin) {
+        if (xsplit) spmv_rowtile_kernel<true, 256, true><<<a.n_tiles, 256, 0, s>>>(a);
+        else spmv_rowtile_kernel<false, 256, true><<<a.n_tiles, 256, 0, s>>>(a);
+    } else if (nt == 256) {
+        if (xsplit) spmv_rowtile_kernel<true, 256, false><<<a.n_tiles, 256, 0, s>>>(a);
+        else spmv_rowtile_kernel<false, 256, false><<<a.n_tiles, 256, 0, s>>>(a);
     } else if (nt == 128) {
-        if (xsplit) spmv_rowtile_kernel<true, 128><<<a.n_tiles, 128, 0, s>>>(a);
-        else spmv_rowtile_kernel<false, 128><<<a.n_tiles, 128, 0, s>>>(a);
+        if (xsplit) spmv_rowtile_kernel<true, 128, false><<<a.n_tiles, 128, 0, s>>>(a);
+        else spmv_rowtile_kernel<false, 128, false><<<a.n_tiles, 128, 0, s>>>(a);
     } else {
-        if (xsplit) spmv_rowtile_kernel<true, 512><<<a.n_tiles, 512, 0, s>>>(a);
-        else spmv_rowtile_kernel<false, 512><<<a.n_tiles, 512, 0, s>>>(a);
+        if (xsplit) spmv_rowtile_kernel<true, 512, false><<<a.n_tiles, 512, 0, s>>>(a);
+        else spmv_rowtile_kernel<false, 512, false><<<a.n_tiles, 512, 0, s>>>(a);
     }
     return cudaGetLastError();
 }
