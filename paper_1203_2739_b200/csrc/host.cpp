@@ -126,6 +126,12 @@ struct spmv_plan_s {
     int32_t* d_seg_row = nullptr;     // [S]
     int32_t* d_scol = nullptr;        // [nnz_loc + pad] split stream
     double* d_sval = nullptr;
+    // fused split, row-major: each row's part segments in part order (P:L109 per row)
+    int32_t* d_fcol = nullptr;        // [nnz_loc + pad]
+    double* d_fval = nullptr;
+    int32_t* d_frowseg = nullptr;     // [m_loc+1] first segment of each row
+    int32_t* d_fsegptr = nullptr;     // [S+1] segment start positions (same positions as the CSR rows)
+    bool split_rowmajor = true;
     int32_t* d_colinv = nullptr;      // ORIGINAL mode: x^[c] = x[colinv[c]]
     int32_t* d_rowperm = nullptr;     // ORIGINAL mode: y[i] = y^[row_perm[i]]
     double* d_xhat = nullptr;
@@ -798,6 +804,45 @@ static spmv_status_t create_impl(int64_t m, int64_t n, int64_t nnz, const int64_
             }
         }
         h->bytes_alg_split += 8 * S + 4 * (T * KP + 1);
+        // row-major fused layout: row r's entries regrouped by part (stable in
+        // column order inside a part); segments in part order per row
+        {
+            std::vector<int32_t> fcol(nnz_loc), frowseg(m_loc + 1), fsegptr(S + 1);
+            std::vector<double> fval(nnz_loc);
+            std::vector<int32_t> rcnt(m_loc);
+#pragma omp parallel for schedule(dynamic, 4096)
+            for (int64_t r = 0; r < m_loc; ++r) {
+                // distinct parts of the row = its segments
+                std::vector<int32_t> cnt(KP, 0);
+                for (int64_t e = rp[r]; e < rp[r + 1]; ++e) cnt[ppart[e]]++;
+                int32_t c = 0;
+                for (int k = 0; k < KP; ++k) c += cnt[k] > 0;
+                rcnt[r] = c;
+            }
+            frowseg[0] = 0;
+            for (int64_t r = 0; r < m_loc; ++r) frowseg[r + 1] = frowseg[r] + rcnt[r];
+            if (frowseg[m_loc] != S) return fail(SPMV_ERR_INTERNAL, "split layout: segment count mismatch");
+#pragma omp parallel for schedule(dynamic, 4096)
+            for (int64_t r = 0; r < m_loc; ++r) {
+                std::vector<int32_t> cnt(KP, 0), off(KP + 1, 0);
+                for (int64_t e = rp[r]; e < rp[r + 1]; ++e) cnt[ppart[e]]++;
+                for (int k = 0; k < KP; ++k) off[k + 1] = off[k] + cnt[k];
+                int32_t sg = frowseg[r];
+                for (int k = 0; k < KP; ++k)
+                    if (cnt[k]) fsegptr[sg++] = (int32_t)(rp[r] + off[k]);
+                std::vector<int32_t> pos(off.begin(), off.end() - 1);
+                for (int64_t e = rp[r]; e < rp[r + 1]; ++e) {
+                    const int64_t q = rp[r] + pos[ppart[e]]++;
+                    fcol[q] = pcol[e];
+                    fval[q] = pval[e];
+                }
+            }
+            fsegptr[S] = (int32_t)nnz_loc;
+            if ((s = upload(h, &h->d_fcol, fcol.data(), nnz_loc, nnz_loc + kPad))) return s;
+            if ((s = upload(h, &h->d_fval, fval.data(), nnz_loc, nnz_loc + kPad))) return s;
+            if ((s = upload(h, &h->d_frowseg, frowseg.data(), m_loc + 1))) return s;
+            if ((s = upload(h, &h->d_fsegptr, fsegptr.data(), S + 1))) return s;
+        }
         if ((s = upload(h, &h->d_tile_seg, tile_seg.data(), T * KP + 1))) return s;
         if ((s = upload(h, &h->d_seg_ptr, seg_ptr.data(), S + 1))) return s;
         if ((s = upload(h, &h->d_seg_row, seg_row.data(), S))) return s;
@@ -1039,6 +1084,23 @@ static spmv_status_t run(spmv_handle_t h, const double* x, double* y, uint32_t f
                 if (h->kernel == 2) CUDA_TRY(spmvb::launch_tiles(B, true, xsplit, st));
                 else CUDA_TRY(spmvb::launch_split(B, xsplit, st));
             }
+        } else if (h->split_rowmajor && h->kernel != 2 && !getenv("SPMV_SPLIT_PARTMAJOR")) {
+            // fused multiple-SpMxV, row-major segments (split.cu spmv_split_rows_kernel)
+            spmvb::RowTileArgs R{};
+            R.tile_row = h->d_tile_row;
+            R.tile_nnz = h->d_tile_nnz;
+            R.tile_cls = h->d_tile_cls;
+            R.rowptr = h->d_rowptr;
+            R.col = h->d_fcol;
+            R.val = h->d_fval;
+            R.x_lo = A.x_lo;
+            R.x_hi = A.x_hi;
+            R.x_split = A.x_split;
+            R.n_tiles = A.n_tiles;
+            R.y = yk;
+            R.maxabs_slots = A.maxabs_slots;
+            R.gmode = 2;
+            CUDA_TRY(spmvb::launch_split_rows(R, h->d_frowseg, h->d_fsegptr, xsplit, st));
         } else {
             A.k_begin = 0; A.k_end = h->n_parts;
             if (h->kernel == 2) CUDA_TRY(spmvb::launch_tiles(A, true, xsplit, st));

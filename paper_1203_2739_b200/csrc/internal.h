@@ -69,6 +69,10 @@ cudaError_t launch_rowseg(const RowTileArgs& a, bool xsplit, cudaStream_t s);
 // Fused / literal multiple-SpMxV kernel (split.cu), K <= 64 parts.
 constexpr int kMaxParts = 64;
 cudaError_t launch_split(const TileArgs& a, bool xsplit, cudaStream_t s);
+// Fused multiple-SpMxV over the row-major segment layout: per row, the part
+// segments in part order, each summed into its own temporary (split.cu).
+cudaError_t launch_split_rows(const RowTileArgs& a, const int32_t* row_seg, const int32_t* seg_ptr, bool xsplit,
+                              cudaStream_t s);
 size_t pipe_smem_bytes();
 // x^[c] = x[colinv[c]]   (ORIGINAL-mode x preparation, a3)
 cudaError_t launch_gather(const double* src, const int32_t* idx, double* dst, int64_t n, cudaStream_t s);

@@ -204,3 +204,178 @@ cudaError_t launch_split(const TileArgs& a, bool xsplit, cudaStream_t s) {
 }
 
 }  // namespace spmvb
+
+// ---------------------------------------------------------------------------
+// spmv_split_rows_kernel: fused multiple-SpMxV over the row-major segment
+// layout (host.cpp): row r's nonzeros are grouped by part, its segments are
+// [row_seg[r], row_seg[r+1]) in part order, segment s covers stream
+// positions [seg_ptr[s], seg_ptr[s+1]).  Same tiles and streaming as the
+// row-tile kernel (rowtile.cu); the reduction walks each row's segments in
+// part order, each into its own temporary, y_r += tmp (reading
+// A7) -- so no per-part CTA barriers are needed: the per-row order is the
+// whole ordering constraint.  Segments of <= 32 nonzeros are summed serially
+// (the oracle's order); rows with a longer segment go to a warp (fixed tree).
+namespace spmvb {
+namespace {
+
+constexpr int kSR = 256;                      // threads per tile CTA
+constexpr int kSRQ = kTileNnz / (4 * kSR);    // quads per thread
+
+__device__ __forceinline__ double ldx_r(const RowTileArgs& A, int c, uint64_t pl) {
+    const double* p = c < A.x_split ? A.x_lo + c : A.x_hi + (c - A.x_split);
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pl));
+    return v;
+}
+
+struct SplitRowsSmem {
+    double prod[kTileNnz];
+    int32_t rs[kTileRows + 1];      // row_seg[r0 + j] (absolute)
+    int32_t longrows[kTileRows];
+    int32_t nlong;
+    double red[kSR / 32];
+};
+
+template <bool XSPLIT>
+__global__ void __launch_bounds__(kSR, 4) spmv_split_rows_kernel(const RowTileArgs A, const int32_t* __restrict__ row_seg,
+                                                               const int32_t* __restrict__ seg_ptr) {
+    __shared__ __align__(16) SplitRowsSmem sm;
+    const int t = blockIdx.x;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int r0 = A.tile_row[t], r1 = A.tile_row[t + 1];
+    const int a = A.tile_nnz[t], b = A.tile_nnz[t + 1];
+    const int nr = r1 - r0;
+    const int a4 = a & ~3;
+    const uint64_t pol = pol_evict_first();
+    uint64_t pl;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pl));
+    double mx = 0.0;
+
+    if (b - a4 > kTileNnz) {
+        // one long row: per segment (part order), fixed-assignment partials +
+        // fixed block tree, accumulated in part order
+        double yr = 0.0;
+        const int s0 = row_seg[r0], s1 = row_seg[r0 + 1];
+        for (int sg = s0; sg < s1; ++sg) {
+            const int pa = seg_ptr[sg], pb = seg_ptr[sg + 1];
+            double acc = 0.0;
+            for (int e = pa + tid; e < pb; e += kSR) {
+                int32_t c;
+                double v;
+                asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(c) : "l"(A.col + e), "l"(pol));
+                asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(A.val + e), "l"(pol));
+                acc += v * (XSPLIT ? ldx_r(A, c, pl) : ldx_r(A, c, pl));
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+            if (lane == 0) sm.red[warp] = acc;
+            __syncthreads();
+            if (tid == 0) {
+                double tot = 0.0;
+                for (int w = 0; w < kSR / 32; ++w) tot += sm.red[w];
+                yr += tot;
+            }
+            __syncthreads();
+        }
+        if (tid == 0) {
+            A.y[r0] = yr;
+            if (A.maxabs_slots && yr != 0.0)
+                atomicMax(A.maxabs_slots + (t & (kMaxSlots - 1)) * kSlotStride,
+                          (unsigned long long)__double_as_longlong(fabs(yr)));
+        }
+        return;
+    }
+
+    // ------------------------------------------------ stage products
+    for (int j = tid; j <= nr; j += kSR) sm.rs[j] = row_seg[r0 + j];
+    if (tid == 0) sm.nlong = 0;
+    {
+        const int lo = a - a4, hi = b - a4;
+        int4 c[kSRQ];
+        double2 v0[kSRQ], v1[kSRQ];
+#pragma unroll
+        for (int k = 0; k < kSRQ; ++k) {
+            const int p = 4 * (tid + k * kSR);
+            if (a4 + p < b) {
+                c[k] = ld_v4(A.col + a4 + p, pol);
+                v0[k] = ld_v2d(A.val + a4 + p, pol);
+                v1[k] = ld_v2d(A.val + a4 + p + 2, pol);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kSRQ; ++k) {
+            const int p = 4 * (tid + k * kSR);
+            if (a4 + p < b) {
+                double2 w0, w1;
+                w0.x = (p + 0 >= lo && p + 0 < hi) ? v0[k].x * ldx_r(A, c[k].x, pl) : 0.0;
+                w0.y = (p + 1 >= lo && p + 1 < hi) ? v0[k].y * ldx_r(A, c[k].y, pl) : 0.0;
+                w1.x = (p + 2 >= lo && p + 2 < hi) ? v1[k].x * ldx_r(A, c[k].z, pl) : 0.0;
+                w1.y = (p + 3 >= lo && p + 3 < hi) ? v1[k].y * ldx_r(A, c[k].w, pl) : 0.0;
+                *reinterpret_cast<double2*>(&sm.prod[p]) = w0;
+                *reinterpret_cast<double2*>(&sm.prod[p + 2]) = w1;
+            }
+        }
+    }
+    __syncthreads();
+
+    // ------------------------------------------------ rows: segments in part order
+    for (int r = tid; r < nr; r += kSR) {
+        const int s0 = sm.rs[r], s1 = sm.rs[r + 1];
+        bool lng = false;
+        for (int sg = s0; sg < s1; ++sg) lng |= seg_ptr[sg + 1] - seg_ptr[sg] > kShortRow;
+        if (lng) {
+            sm.longrows[atomicAdd(&sm.nlong, 1)] = r;   // summed by one warp below (order irrelevant)
+            continue;
+        }
+        double yr = 0.0;
+        for (int sg = s0; sg < s1; ++sg) {
+            const int p1 = seg_ptr[sg + 1] - a4;
+            double tmp = 0.0;
+            for (int p = seg_ptr[sg] - a4; p < p1; ++p) tmp += sm.prod[p];
+            yr += tmp;
+        }
+        A.y[r0 + r] = yr;
+        mx = fmax(mx, fabs(yr));
+    }
+    __syncthreads();
+    for (int k = warp; k < sm.nlong; k += kSR / 32) {
+        const int r = sm.longrows[k];
+        double yr = 0.0;
+        for (int sg = sm.rs[r]; sg < sm.rs[r + 1]; ++sg) {
+            const int p0 = seg_ptr[sg] - a4, p1 = seg_ptr[sg + 1] - a4;
+            double tmp = 0.0;
+            if (p1 - p0 <= kShortRow) {
+                if (lane == 0)
+                    for (int p = p0; p < p1; ++p) tmp += sm.prod[p];
+            } else {
+                for (int p = p0 + lane; p < p1; p += 32) tmp += sm.prod[p];
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) tmp += __shfl_xor_sync(0xffffffffu, tmp, off);
+            }
+            yr += tmp;   // lane 0's copy is the row's value
+        }
+        if (lane == 0) {
+            A.y[r0 + r] = yr;
+            mx = fmax(mx, fabs(yr));
+        }
+    }
+    if (A.maxabs_slots) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+        if (lane == 0 && mx > 0.0)
+            atomicMax(A.maxabs_slots + ((t * (kSR / 32) + warp) & (kMaxSlots - 1)) * kSlotStride,
+                      (unsigned long long)__double_as_longlong(mx));
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_split_rows(const RowTileArgs& a, const int32_t* row_seg, const int32_t* seg_ptr, bool xsplit,
+                              cudaStream_t s) {
+    if (a.n_tiles <= 0) return cudaSuccess;
+    if (xsplit) spmv_split_rows_kernel<true><<<a.n_tiles, kSR, 0, s>>>(a, row_seg, seg_ptr);
+    else spmv_split_rows_kernel<false><<<a.n_tiles, kSR, 0, s>>>(a, row_seg, seg_ptr);
+    return cudaGetLastError();
+}
+
+}  // namespace spmvb
