@@ -100,6 +100,7 @@ struct spmv_plan_s {
     int32_t* d_tile_nnz = nullptr;    // [T+1] row_ptr[tile_row[t]]
     int* d_counter = nullptr;         // tile-claim counter of the pipe kernel
     int32_t* d_tile_cls = nullptr;    // [T] tile class (internal.h)
+    int32_t* d_long_tiles = nullptr;  // [n_long] tiles holding one long row
     int kernel = 0;                   // 0 rowtile/256, 1 pipe, 2 tile, 3 rowtile/512, 4 rowseg, 5 rowtile/128,
                                       // 6 x-staged, 7 column-sorted panels (SPMV_KERNEL=xstage/panel)
     // x-staged kernel (xstage.cu)
@@ -737,6 +738,13 @@ static spmv_status_t create_impl(int64_t m, int64_t n, int64_t nnz, const int64_
             tile_cls[t] = cls;
         }
         if ((s = upload(h, &h->d_tile_cls, tile_cls.data(), T))) return s;
+        {
+            std::vector<int32_t> lt;
+            for (int64_t t = 0; t < T; ++t)
+                if (rp[tile_row[t + 1]] - (rp[tile_row[t]] & ~int64_t(3)) > kTileNnz) lt.push_back((int32_t)t);
+            if (!lt.empty() && (s = upload(h, &h->d_long_tiles, lt.data(), lt.size()))) return s;
+            h->n_long = (int64_t)lt.size();
+        }
         const char* kenv = getenv("SPMV_KERNEL");   // A/B switch for measurements only
         h->kernel = 0;
         if (kenv && strcmp(kenv, "pipe") == 0) h->kernel = 1;
@@ -1053,12 +1061,15 @@ static spmv_status_t run(spmv_handle_t h, const double* x, double* y, uint32_t f
         // L2 evict-last (x is the reused operand; the matrix streams evict-first)
         P.gmode = 2;
         if (const char* g = getenv("SPMV_RT_GMODE")) P.gmode = atoi(g);   // measurements only
+        const bool rowtile_family = h->kernel == 0 || h->kernel == 3 || h->kernel == 5 || h->kernel == 8;
+        if (rowtile_family && h->d_long_tiles && !getenv("SPMV_LONG_INLINE")) P.long_tiles = h->d_long_tiles;
         if (h->kernel == 1) CUDA_TRY(spmvb::launch_pipe(P, xsplit, st));
         else if (h->kernel == 3) CUDA_TRY(spmvb::launch_rowtile(P, xsplit, 512, st));
         else if (h->kernel == 4) CUDA_TRY(spmvb::launch_rowseg(P, xsplit, st));
         else if (h->kernel == 5) CUDA_TRY(spmvb::launch_rowtile(P, xsplit, 128, st));
         else if (h->kernel == 8) CUDA_TRY(spmvb::launch_rowtile(P, xsplit, 256, st, true));
         else CUDA_TRY(spmvb::launch_rowtile(P, xsplit, 256, st));
+        if (P.long_tiles) CUDA_TRY(spmvb::launch_longrows(P, (int32_t)h->n_long, xsplit, st));
     } else if (!split) {
         A.tile_seg = h->d_tile_row;
         A.seg_ptr = h->d_rowptr;

@@ -60,7 +60,10 @@ struct PipeArgs {
     int* tile_counter;         // zeroed by launch_pipe before every launch
     int32_t gmode;             // x gather flavour (measurements): 0 ld.global.nc, 1 + L2 evict_last,
                                // 2 + L1 no_allocate and L2 evict_last
+    const int32_t* long_tiles; // tiles holding one row longer than a tile (run by launch_longrows), or
+                               // nullptr: the tile kernel runs them itself
 };
+cudaError_t launch_longrows(const PipeArgs& a, int32_t n_long, bool xsplit, cudaStream_t s);
 cudaError_t launch_pipe(const PipeArgs& a, bool xsplit, cudaStream_t s);
 // Default single-SpMxV kernel (rowtile.cu): one 512-thread CTA per row tile.
 using RowTileArgs = PipeArgs;

@@ -122,6 +122,7 @@ __global__ void __launch_bounds__(NT, (NT == 512 ? 3 : NT == 256 ? 6 : 8)) spmv_
 
     if (b - a4 > kTileNnz) {
         // ------------------------------------------- one long row (> a tile)
+        if (A.long_tiles) return;                   // done by spmv_longrow_kernel
         const int64_t qa = a >> 2, qb = ((int64_t)b + 3) >> 2;
         double acc = 0.0;
         if (LIN) {
@@ -458,7 +459,79 @@ __global__ void __launch_bounds__(kRT, 3) spmv_rowseg_kernel(const RowTileArgs A
     }
 }
 
+// ---------------------------------------------------------------------------
+// spmv_longrow_kernel: rows longer than a tile (CTA-per-row class), one CTA
+// each, launched over the list of long tiles.  Each thread keeps LQ quads of
+// the row in flight (all stream loads, then all gathers), which the tile
+// kernel's register budget (6 CTAs/SM) cannot afford; fixed assignment and
+// fixed block tree (deterministic).
+template <bool XSPLIT>
+__global__ void __launch_bounds__(256, 2) spmv_longrow_kernel(const RowTileArgs A) {
+    constexpr int NT = 256, LQ = 4;
+    __shared__ double red[NT / 32];
+    const int t = A.long_tiles[blockIdx.x];
+    const int tid = threadIdx.x;
+    const int r0 = A.tile_row[t];
+    const int a = A.tile_nnz[t], b = A.tile_nnz[t + 1];
+    const uint64_t pol = pol_evict_first();
+    const int64_t qa = a >> 2, qb = ((int64_t)b + 3) >> 2;
+    double acc = 0.0;
+    for (int64_t q0 = qa + tid; q0 < qb; q0 += (int64_t)LQ * NT) {
+        int4 c[LQ];
+        double2 v0[LQ], v1[LQ];
+#pragma unroll
+        for (int u = 0; u < LQ; ++u) {
+            const int64_t q = q0 + (int64_t)u * NT;
+            if (q < qb) {
+                c[u] = ld_v4(A.col + 4 * q, pol);
+                v0[u] = ld_v2d(A.val + 4 * q, pol);
+                v1[u] = ld_v2d(A.val + 4 * q + 2, pol);
+            }
+        }
+        double xv[LQ][4];
+#pragma unroll
+        for (int u = 0; u < LQ; ++u) {
+            const int64_t g = 4 * (q0 + (int64_t)u * NT);
+            if (q0 + (int64_t)u * NT < qb) {
+                xv[u][0] = (g + 0 >= a && g + 0 < b) ? ldx<XSPLIT>(A, c[u].x) : 0.0;
+                xv[u][1] = (g + 1 >= a && g + 1 < b) ? ldx<XSPLIT>(A, c[u].y) : 0.0;
+                xv[u][2] = (g + 2 >= a && g + 2 < b) ? ldx<XSPLIT>(A, c[u].z) : 0.0;
+                xv[u][3] = (g + 3 >= a && g + 3 < b) ? ldx<XSPLIT>(A, c[u].w) : 0.0;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < LQ; ++u) {
+            const int64_t g = 4 * (q0 + (int64_t)u * NT);
+            if (q0 + (int64_t)u * NT < qb) {
+                if (g + 0 >= a && g + 0 < b) acc += v0[u].x * xv[u][0];
+                if (g + 1 >= a && g + 1 < b) acc += v0[u].y * xv[u][1];
+                if (g + 2 >= a && g + 2 < b) acc += v1[u].x * xv[u][2];
+                if (g + 3 >= a && g + 3 < b) acc += v1[u].y * xv[u][3];
+            }
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if ((tid & 31) == 0) red[tid >> 5] = acc;
+    __syncthreads();
+    if (tid == 0) {
+        double tot = 0.0;
+        for (int w = 0; w < NT / 32; ++w) tot += red[w];
+        A.y[r0] = tot;
+        if (A.maxabs_slots && tot != 0.0)
+            atomicMax(A.maxabs_slots + (t & (kMaxSlots - 1)) * kSlotStride,
+                      (unsigned long long)__double_as_longlong(fabs(tot)));
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_longrows(const RowTileArgs& a, int32_t n_long, bool xsplit, cudaStream_t s) {
+    if (n_long <= 0 || !a.long_tiles) return cudaSuccess;
+    if (xsplit) spmv_longrow_kernel<true><<<n_long, 256, 0, s>>>(a);
+    else spmv_longrow_kernel<false><<<n_long, 256, 0, s>>>(a);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_rowtile(const RowTileArgs& a, bool xsplit, int nt, cudaStream_t s, bool lin) {
     if (a.n_tiles <= 0) return cudaSuccess;

@@ -230,7 +230,8 @@ __device__ __forceinline__ double ldx_r(const RowTileArgs& A, int c, uint64_t pl
 
 struct SplitRowsSmem {
     double prod[kTileNnz];
-    int32_t rs[kTileRows + 1];      // row_seg[r0 + j] (absolute)
+    int32_t sp[kTileNnz + 1];       // seg_ptr[s] - a4 for the tile's segments (each has >= 1 nonzero)
+    int32_t rs[kTileRows + 1];      // row_seg[r0 + j] - row_seg[r0]
     int32_t longrows[kTileRows];
     int32_t nlong;
     double red[kSR / 32];
@@ -287,7 +288,12 @@ __global__ void __launch_bounds__(kSR, 4) spmv_split_rows_kernel(const RowTileAr
     }
 
     // ------------------------------------------------ stage products
-    for (int j = tid; j <= nr; j += kSR) sm.rs[j] = row_seg[r0 + j];
+    const int sbase = row_seg[r0];
+    for (int j = tid; j <= nr; j += kSR) sm.rs[j] = row_seg[r0 + j] - sbase;
+    {
+        const int ns = row_seg[r1] - sbase;
+        for (int j = tid; j <= ns; j += kSR) sm.sp[j] = seg_ptr[sbase + j] - a4;
+    }
     if (tid == 0) sm.nlong = 0;
     {
         const int lo = a - a4, hi = b - a4;
@@ -322,16 +328,16 @@ __global__ void __launch_bounds__(kSR, 4) spmv_split_rows_kernel(const RowTileAr
     for (int r = tid; r < nr; r += kSR) {
         const int s0 = sm.rs[r], s1 = sm.rs[r + 1];
         bool lng = false;
-        for (int sg = s0; sg < s1; ++sg) lng |= seg_ptr[sg + 1] - seg_ptr[sg] > kShortRow;
+        for (int sg = s0; sg < s1; ++sg) lng |= sm.sp[sg + 1] - sm.sp[sg] > kShortRow;
         if (lng) {
             sm.longrows[atomicAdd(&sm.nlong, 1)] = r;   // summed by one warp below (order irrelevant)
             continue;
         }
         double yr = 0.0;
         for (int sg = s0; sg < s1; ++sg) {
-            const int p1 = seg_ptr[sg + 1] - a4;
+            const int p1 = sm.sp[sg + 1];
             double tmp = 0.0;
-            for (int p = seg_ptr[sg] - a4; p < p1; ++p) tmp += sm.prod[p];
+            for (int p = sm.sp[sg]; p < p1; ++p) tmp += sm.prod[p];
             yr += tmp;
         }
         A.y[r0 + r] = yr;
@@ -342,7 +348,7 @@ __global__ void __launch_bounds__(kSR, 4) spmv_split_rows_kernel(const RowTileAr
         const int r = sm.longrows[k];
         double yr = 0.0;
         for (int sg = sm.rs[r]; sg < sm.rs[r + 1]; ++sg) {
-            const int p0 = seg_ptr[sg] - a4, p1 = seg_ptr[sg + 1] - a4;
+            const int p0 = sm.sp[sg], p1 = sm.sp[sg + 1];
             double tmp = 0.0;
             if (p1 - p0 <= kShortRow) {
                 if (lane == 0)
