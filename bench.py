@@ -314,7 +314,8 @@ def run_ours(args, rank, world, local_rank):
     # our kernels per step: the SpMxV tile kernel, the long-row kernel when the
     # matrix has rows longer than a tile (row-tile family), max-abs finish and
     # x-update for the power iterations
-    long_launch = 1 if (info["n_long_rows"] > 0 and not split and info["kernel"] in (0, 3, 5, 8)) else 0
+    long_launch = 1 if (info["n_long_rows"] > 0 and not split and info["kernel"] in (0, 3, 5, 8)
+                        and os.environ.get("SPMV_LONG")) else 0
     launches_per_step = 1 + long_launch + (2 if power else 0)
     cur = 0
     for _ in range(args.warmup):

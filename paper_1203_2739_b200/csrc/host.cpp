@@ -101,6 +101,8 @@ struct spmv_plan_s {
     int* d_counter = nullptr;         // tile-claim counter of the pipe kernel
     int32_t* d_tile_cls = nullptr;    // [T] tile class (internal.h)
     int32_t* d_long_tiles = nullptr;  // [n_long] tiles holding one long row
+    cudaStream_t side = nullptr;      // long-row kernel stream (forked from / joined to the caller's)
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int kernel = 0;                   // 0 rowtile/256, 1 pipe, 2 tile, 3 rowtile/512, 4 rowseg, 5 rowtile/128,
                                       // 6 x-staged, 7 column-sorted panels (SPMV_KERNEL=xstage/panel)
     // x-staged kernel (xstage.cu)
@@ -179,6 +181,9 @@ void free_plan(spmv_plan_s* h) {
     for (void* p : h->allocs) cudaFree(p);
     h->allocs.clear();
     if (h->comm) ncclCommDestroy(h->comm);
+    if (h->side) cudaStreamDestroy(h->side);
+    if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+    if (h->ev_join) cudaEventDestroy(h->ev_join);
     h->comm = nullptr;
     h->magic = 0;
     delete h;
@@ -1062,14 +1067,28 @@ static spmv_status_t run(spmv_handle_t h, const double* x, double* y, uint32_t f
         P.gmode = 2;
         if (const char* g = getenv("SPMV_RT_GMODE")) P.gmode = atoi(g);   // measurements only
         const bool rowtile_family = h->kernel == 0 || h->kernel == 3 || h->kernel == 5 || h->kernel == 8;
-        if (rowtile_family && h->d_long_tiles && !getenv("SPMV_LONG_INLINE")) P.long_tiles = h->d_long_tiles;
+        const char* lenv = getenv("SPMV_LONG");   // measurements: "separate" / "side" stream; default inline
+        if (rowtile_family && h->d_long_tiles && lenv) P.long_tiles = h->d_long_tiles;
+        const bool side = P.long_tiles && strcmp(lenv, "side") == 0;
+        if (side) {
+            if (!h->side) {
+                CUDA_TRY(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+                CUDA_TRY(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+                CUDA_TRY(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
+            }
+            CUDA_TRY(cudaEventRecord(h->ev_fork, st));
+            CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev_fork, 0));
+            CUDA_TRY(spmvb::launch_longrows(P, (int32_t)h->n_long, xsplit, h->side));
+            CUDA_TRY(cudaEventRecord(h->ev_join, h->side));
+        }
         if (h->kernel == 1) CUDA_TRY(spmvb::launch_pipe(P, xsplit, st));
         else if (h->kernel == 3) CUDA_TRY(spmvb::launch_rowtile(P, xsplit, 512, st));
         else if (h->kernel == 4) CUDA_TRY(spmvb::launch_rowseg(P, xsplit, st));
         else if (h->kernel == 5) CUDA_TRY(spmvb::launch_rowtile(P, xsplit, 128, st));
         else if (h->kernel == 8) CUDA_TRY(spmvb::launch_rowtile(P, xsplit, 256, st, true));
         else CUDA_TRY(spmvb::launch_rowtile(P, xsplit, 256, st));
-        if (P.long_tiles) CUDA_TRY(spmvb::launch_longrows(P, (int32_t)h->n_long, xsplit, st));
+        if (side) CUDA_TRY(cudaStreamWaitEvent(st, h->ev_join, 0));
+        else if (P.long_tiles) CUDA_TRY(spmvb::launch_longrows(P, (int32_t)h->n_long, xsplit, st));
     } else if (!split) {
         A.tile_seg = h->d_tile_row;
         A.seg_ptr = h->d_rowptr;

@@ -146,7 +146,8 @@ constexpr int kPnEpoch = kPnWarps * kPnB;    // groups per epoch
 constexpr int kPnRowsMax = 28672;            // y rows per panel (224 KB of shared memory)
 constexpr int kPnRowBits = 15;               // idx = (row_in_panel << 17) | (col - group base)
 constexpr int kPnDeltaBits = 17;
-constexpr uint32_t kPnDummy = 0xFFFFFFFFu;
+constexpr uint32_t kPnDummy = 0xFFFE0000u;   // row field 0x7FFF (-> scratch y slot), delta 0 (a valid x
+                                             // address): padding lanes run the same code branch-free
 
 struct PnPanel {
     int32_t row0;      // first local row

@@ -85,6 +85,7 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
     const uint64_t polx = pol_evict_last();   // x is the reused operand
     const int PF = A.pf_epochs > 0 ? A.pf_epochs : kPF;
     const int T = d.ne * kPnB;                       // steps per warp
+    const int scratch = A.max_rows;                  // y slot of the padding lanes
     const int64_t gw = (int64_t)d.g0 + warp;         // group of step t: gw + 16 t
 
     double rv[kD];
@@ -101,7 +102,17 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
     auto gather = [&](uint32_t i, int32_t b) -> double {
         if (MODE == 1) return 1.0;
         if (MODE == 6) return __ldg(A.x_lo + ((b + (int)(i & 0xFFF)) & 0x3FFFF));
-        if (i == kPnDummy) return 0.0;
+        if (MODE == 15) {
+            if (i == kPnDummy) return 0.0;
+            const double* xp = b < A.x_split ? A.x_lo + b : A.x_hi + (b - A.x_split);
+            return __ldg(xp + (i & kDeltaMask));
+        }
+        if (MODE == 16) return ld_x(A.x_lo + ((b + (int)(i & 0xFFF)) & 0x3FFFF), polx);
+        if (MODE == 13) return i == kPnDummy ? 0.0 : ld_x(A.x_lo + ((b + (int)(i & kDeltaMask)) & 0x3FFFF), polx);
+        if (MODE == 14) return i == kPnDummy ? 0.0 : ld_x(A.x_lo + ((b & 0x3FFFF) + (int)(i & kDeltaMask)), polx);
+        // unconditional: a padding lane reads x[base] (valid) and adds 0 * x into
+        // the scratch y slot -- a predicated-off load behind a branch made the
+        // warp wait for the gather at the branch (measured 1.6x slower)
         const double* xp = b < A.x_split ? A.x_lo + b : A.x_hi + (b - A.x_split);
         return ld_x(xp + (i & kDeltaMask), polx);
     };
@@ -151,8 +162,9 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
             const uint32_t i = ri[u];
             if (MODE == 2) {
                 racc = fma(rv[u], rx[u % kGD], racc);
-            } else if (i != kPnDummy) {
-                const int r = (int)(i >> kPnDeltaBits);
+            } else {
+                int r = (int)(i >> kPnDeltaBits);
+                r = r == (int)(kPnDummy >> kPnDeltaBits) ? scratch : r;
                 ys[r] = fma(rv[u], rx[u % kGD], ys[r]);
             }
             if (t + kD < T) load(t + kD, rv[u], ri[u], rb[u]);
@@ -193,7 +205,7 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel2_kernel(const PnArgs A) {
     const int p = blockIdx.x;
     const PnPanel d = A.panel[p];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    double* gr = sm2 + ((A.max_rows + 1) & ~1) + warp * G * 32;
+    double* gr = sm2 + ((A.max_rows + 2) & ~1) + warp * G * 32;
     const uint32_t gr_s = (uint32_t)__cvta_generic_to_shared(gr) + lane * 8;
     for (int i = tid; i < d.nrows; i += kT) ys[i] = 0.0;
     __syncthreads();
@@ -306,7 +318,7 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel3_kernel(const PnArgs A) {
     const int p = blockIdx.x;
     const PnPanel d = A.panel[p];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int yb = ((A.max_rows * 8 + 127) / 128) * 128;
+    const int yb = (((A.max_rows + 1) * 8 + 127) / 128) * 128;
     double* ys = reinterpret_cast<double*>(sm3);
     unsigned char* st = sm3 + yb;
     uint64_t* full = reinterpret_cast<uint64_t*>(st + NS * kStage3);
@@ -378,10 +390,8 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel3_kernel(const PnArgs A) {
         const uint32_t i = sidx(e)[k * 32 + lane];
         const int32_t b = sbase(e)[k];
         iv = i;
-        if (i != kPnDummy) {
-            const double* xp = b < A.x_split ? A.x_lo + b : A.x_hi + (b - A.x_split);
-            xv = ld_x(xp + (i & kDeltaMask), polx);
-        }
+        const double* xp = b < A.x_split ? A.x_lo + b : A.x_hi + (b - A.x_split);
+        xv = ld_x(xp + (i & kDeltaMask), polx);   // padding lanes: x[base], added 0 * x into the scratch slot
     };
     for (int e = 0; e < G / kPnB && e < ne; ++e) wait_epoch(e);
 #pragma unroll
@@ -395,8 +405,9 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel3_kernel(const PnArgs A) {
             if (t >= T) break;
             const int e = t / kPnB, k = (u % kPnB) * NW + warp;
             const uint32_t i = ri[u];
-            if (i != kPnDummy) {
-                const int r = (int)(i >> kPnDeltaBits);
+            {
+                int r = (int)(i >> kPnDeltaBits);
+                r = r == (int)(kPnDummy >> kPnDeltaBits) ? A.max_rows : r;
                 ys[r] = fma(sval(e)[k * 32 + lane], rx[u], ys[r]);
             }
             const int tn = t + G;
@@ -437,19 +448,23 @@ cudaError_t launch_panel(const PnArgs& a, cudaStream_t s) {
     static int mode = -1, pf_env = 0;
     // only the panel's y in shared memory: the rest of the 256 KB L1/shared
     // array stays L1, which holds the global loads in flight
-    const size_t smem = (size_t)std::max(a.max_rows, 1) * sizeof(double);
+    const size_t smem = (size_t)(a.max_rows + 1) * sizeof(double);   // + the padding lanes' scratch slot
     if (mode < 0) {
         const char* e = getenv("SPMV_PN_MODE");   // ablations for measurements only
         mode = e ? atoi(e) : 0;
         const char* f = getenv("SPMV_PN_PF");
         pf_env = f ? atoi(f) : 0;
         cudaError_t r = cudaSuccess;
-        const int smax = kPnRowsMax * (int)sizeof(double);
+        const int smax = 227 * 1024;
         r = cudaFuncSetAttribute(spmv_panel_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
         if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
         if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
         if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
         if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
+        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<15>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
+        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
+        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<13>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
+        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<14>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
         if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
         if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
         if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel2_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -461,14 +476,18 @@ cudaError_t launch_panel(const PnArgs& a, cudaStream_t s) {
         if (r != cudaSuccess) return r;
     }
     PnArgs b = a;
-    auto smem3 = [&](int NS) { return (size_t)(((a.max_rows * 8 + 127) / 128) * 128) + (size_t)NS * kStage3 + 64; };
-    auto smem2 = [&](int G) { return (size_t)((a.max_rows + 1) & ~1) * 8 + (size_t)NW * G * 256; };
+    auto smem3 = [&](int NS) { return (size_t)((((a.max_rows + 1) * 8 + 127) / 128) * 128) + (size_t)NS * kStage3 + 64; };
+    auto smem2 = [&](int G) { return (size_t)((a.max_rows + 2) & ~1) * 8 + (size_t)NW * G * 256; };
     if (pf_env > 0) b.pf_epochs = pf_env;
     switch (mode) {
     case 1: spmv_panel_kernel<1><<<b.n_panels, kT, smem, s>>>(b); break;
     case 2: spmv_panel_kernel<2><<<b.n_panels, kT, smem, s>>>(b); break;
     case 3: spmv_panel_kernel<3><<<b.n_panels, kT, smem, s>>>(b); break;
     case 4: spmv_panel_kernel<4><<<b.n_panels, kT, smem, s>>>(b); break;
+    case 15: spmv_panel_kernel<15><<<b.n_panels, kT, smem, s>>>(b); break;
+    case 16: spmv_panel_kernel<16><<<b.n_panels, kT, smem, s>>>(b); break;
+    case 13: spmv_panel_kernel<13><<<b.n_panels, kT, smem, s>>>(b); break;
+    case 14: spmv_panel_kernel<14><<<b.n_panels, kT, smem, s>>>(b); break;
     case 6: spmv_panel_kernel<6><<<b.n_panels, kT, smem, s>>>(b); break;
     case 5: spmv_panel_kernel<5><<<b.n_panels, kT, smem, s>>>(b); break;
     case 9: spmv_panel3_kernel<4, 8><<<b.n_panels, kT, smem3(4), s>>>(b); break;
