@@ -81,6 +81,20 @@ __device__ __forceinline__ double ldx(const RowTileArgs& A, int c) {
 
 
 
+// fixed gather flavour of the default path (no run-time switch, no branch):
+// L1 no-allocate (a gathered line is not reused inside a tile) and L2
+// evict-last (x is the reused operand)
+template <bool XSPLIT>
+__device__ __forceinline__ double ldx2(const RowTileArgs& A, int c) {
+    uint64_t pl;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pl));
+    const double* p = A.x_lo + c;
+    if (XSPLIT) p = c < A.x_split ? A.x_lo + c : A.x_hi + (c - A.x_split);
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pl));
+    return v;
+}
+
 template <int NT>
 struct RTSmemT {
     double prod[kTileNnz];          // product of position p (nonzero a4 + p)
@@ -143,14 +157,17 @@ __global__ void __launch_bounds__(NT, (NT == 512 ? 3 : NT == 256 ? 6 : 8)) spmv_
             }
         }
         for (int64_t q = qa + tid; !LIN && q < qb; q += NT) {
+            // all four gathers unconditional (the quad's columns are valid), products masked
             const int4 c = ld_v4(A.col + 4 * q, pol);
             const double2 v0 = ld_v2d(A.val + 4 * q, pol);
             const double2 v1 = ld_v2d(A.val + 4 * q + 2, pol);
+            const double x0 = ldx2<XSPLIT>(A, c.x), x1 = ldx2<XSPLIT>(A, c.y);
+            const double x2 = ldx2<XSPLIT>(A, c.z), x3 = ldx2<XSPLIT>(A, c.w);
             const int64_t g = 4 * q;
-            if (g + 0 >= a && g + 0 < b) acc += v0.x * ldx<XSPLIT>(A, c.x);
-            if (g + 1 >= a && g + 1 < b) acc += v0.y * ldx<XSPLIT>(A, c.y);
-            if (g + 2 >= a && g + 2 < b) acc += v1.x * ldx<XSPLIT>(A, c.z);
-            if (g + 3 >= a && g + 3 < b) acc += v1.y * ldx<XSPLIT>(A, c.w);
+            acc += (g + 0 >= a && g + 0 < b) ? v0.x * x0 : 0.0;
+            acc += (g + 1 >= a && g + 1 < b) ? v0.y * x1 : 0.0;
+            acc += (g + 2 >= a && g + 2 < b) ? v1.x * x2 : 0.0;
+            acc += (g + 3 >= a && g + 3 < b) ? v1.y * x3 : 0.0;
         }
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
@@ -195,36 +212,40 @@ __global__ void __launch_bounds__(NT, (NT == 512 ? 3 : NT == 256 ? 6 : 8)) spmv_
             if (p >= lo && p < hi) sm.prod[p] = v[k] * xv[k];
         }
     } else {
+        // Branch-free staging: every thread loads its QPT quads and gathers all
+        // 4 x values unconditionally -- quads past the tile end are clamped to
+        // the tile's first quad (a valid address), positions outside
+        // [lo, hi) have their product masked to 0 afterwards.  (A gather
+        // behind a per-lane branch made the warp wait for it at the
+        // reconvergence point: measured on the panel kernel.)
         const int lo = a - a4, hi = b - a4;
         int4 c[QPT];
         double2 v0[QPT], v1[QPT];
 #pragma unroll
         for (int k = 0; k < QPT; ++k) {
             const int p = 4 * (tid + k * NT);
-            if (a4 + p < b) {
-                c[k] = ld_v4(A.col + a4 + p, pol);
-                v0[k] = ld_v2d(A.val + a4 + p, pol);
-                v1[k] = ld_v2d(A.val + a4 + p + 2, pol);
-            }
+            const int pq = (a4 + p < b) ? p : 0;
+            c[k] = ld_v4(A.col + a4 + pq, pol);
+            v0[k] = ld_v2d(A.val + a4 + pq, pol);
+            v1[k] = ld_v2d(A.val + a4 + pq + 2, pol);
         }
         double xv[QPT][4];
 #pragma unroll
         for (int k = 0; k < QPT; ++k) {
-            const int p = 4 * (tid + k * NT);
-            if (a4 + p < b) {
-                xv[k][0] = (p + 0 >= lo && p + 0 < hi) ? ldx<XSPLIT>(A, c[k].x) : 0.0;
-                xv[k][1] = (p + 1 >= lo && p + 1 < hi) ? ldx<XSPLIT>(A, c[k].y) : 0.0;
-                xv[k][2] = (p + 2 >= lo && p + 2 < hi) ? ldx<XSPLIT>(A, c[k].z) : 0.0;
-                xv[k][3] = (p + 3 >= lo && p + 3 < hi) ? ldx<XSPLIT>(A, c[k].w) : 0.0;
-            }
+            xv[k][0] = ldx2<XSPLIT>(A, c[k].x);
+            xv[k][1] = ldx2<XSPLIT>(A, c[k].y);
+            xv[k][2] = ldx2<XSPLIT>(A, c[k].z);
+            xv[k][3] = ldx2<XSPLIT>(A, c[k].w);
         }
 #pragma unroll
         for (int k = 0; k < QPT; ++k) {
             const int p = 4 * (tid + k * NT);
+            double2 w0, w1;
+            w0.x = (p + 0 >= lo && p + 0 < hi) ? v0[k].x * xv[k][0] : 0.0;
+            w0.y = (p + 1 >= lo && p + 1 < hi) ? v0[k].y * xv[k][1] : 0.0;
+            w1.x = (p + 2 >= lo && p + 2 < hi) ? v1[k].x * xv[k][2] : 0.0;
+            w1.y = (p + 3 >= lo && p + 3 < hi) ? v1[k].y * xv[k][3] : 0.0;
             if (a4 + p < b) {
-                double2 w0, w1;
-                w0.x = v0[k].x * xv[k][0]; w0.y = v0[k].y * xv[k][1];
-                w1.x = v1[k].x * xv[k][2]; w1.y = v1[k].y * xv[k][3];
                 *reinterpret_cast<double2*>(&sm.prod[p]) = w0;
                 *reinterpret_cast<double2*>(&sm.prod[p + 2]) = w1;
             }
@@ -493,10 +514,11 @@ __global__ void __launch_bounds__(256, 2) spmv_longrow_kernel(const RowTileArgs 
         for (int u = 0; u < LQ; ++u) {
             const int64_t g = 4 * (q0 + (int64_t)u * NT);
             if (q0 + (int64_t)u * NT < qb) {
-                xv[u][0] = (g + 0 >= a && g + 0 < b) ? ldx<XSPLIT>(A, c[u].x) : 0.0;
-                xv[u][1] = (g + 1 >= a && g + 1 < b) ? ldx<XSPLIT>(A, c[u].y) : 0.0;
-                xv[u][2] = (g + 2 >= a && g + 2 < b) ? ldx<XSPLIT>(A, c[u].z) : 0.0;
-                xv[u][3] = (g + 3 >= a && g + 3 < b) ? ldx<XSPLIT>(A, c[u].w) : 0.0;
+                (void)g;
+                xv[u][0] = ldx2<XSPLIT>(A, c[u].x);
+                xv[u][1] = ldx2<XSPLIT>(A, c[u].y);
+                xv[u][2] = ldx2<XSPLIT>(A, c[u].z);
+                xv[u][3] = ldx2<XSPLIT>(A, c[u].w);
             }
         }
 #pragma unroll

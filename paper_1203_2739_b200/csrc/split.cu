@@ -130,19 +130,21 @@ __global__ void __launch_bounds__(kST, 2) spmv_split_kernel(const TileArgs A) {
         for (int k = kb + tid; k <= ke; k += kST) sm.kseg[k - kb] = A.tile_seg[t * K + k] - s_lo;
         if (tid == 0) sm.nlong = 0;
         {
+            // branch-free: loads clamped to a valid quad, products masked
             const int p = 4 * tid;
+            const int pq = (a4 + p < b) ? p : 0;
+            const int4 c = ld_v4(A.col + a4 + pq, pol);
+            const double2 v0 = ld_v2d(A.val + a4 + pq, pol);
+            const double2 v1 = ld_v2d(A.val + a4 + pq + 2, pol);
+            const int lo = a - a4, hi = b - a4;
+            const double x0 = ldx<XSPLIT>(A, c.x), x1 = ldx<XSPLIT>(A, c.y);
+            const double x2 = ldx<XSPLIT>(A, c.z), x3 = ldx<XSPLIT>(A, c.w);
+            double2 w0, w1;
+            w0.x = (p + 0 >= lo && p + 0 < hi) ? v0.x * x0 : 0.0;
+            w0.y = (p + 1 >= lo && p + 1 < hi) ? v0.y * x1 : 0.0;
+            w1.x = (p + 2 >= lo && p + 2 < hi) ? v1.x * x2 : 0.0;
+            w1.y = (p + 3 >= lo && p + 3 < hi) ? v1.y * x3 : 0.0;
             if (a4 + p < b) {
-                const int4 c = ld_v4(A.col + a4 + p, pol);
-                const double2 v0 = ld_v2d(A.val + a4 + p, pol);
-                const double2 v1 = ld_v2d(A.val + a4 + p + 2, pol);
-                const int lo = a - a4, hi = b - a4;
-                const double x0 = (p + 0 >= lo && p + 0 < hi) ? ldx<XSPLIT>(A, c.x) : 0.0;
-                const double x1 = (p + 1 >= lo && p + 1 < hi) ? ldx<XSPLIT>(A, c.y) : 0.0;
-                const double x2 = (p + 2 >= lo && p + 2 < hi) ? ldx<XSPLIT>(A, c.z) : 0.0;
-                const double x3 = (p + 3 >= lo && p + 3 < hi) ? ldx<XSPLIT>(A, c.w) : 0.0;
-                double2 w0, w1;
-                w0.x = v0.x * x0; w0.y = v0.y * x1;
-                w1.x = v1.x * x2; w1.y = v1.y * x3;
                 *reinterpret_cast<double2*>(&sm.prod[p]) = w0;
                 *reinterpret_cast<double2*>(&sm.prod[p + 2]) = w1;
             }
@@ -300,23 +302,30 @@ __global__ void __launch_bounds__(kSR, 4) spmv_split_rows_kernel(const RowTileAr
         int4 c[kSRQ];
         double2 v0[kSRQ], v1[kSRQ];
 #pragma unroll
-        for (int k = 0; k < kSRQ; ++k) {
+        for (int k = 0; k < kSRQ; ++k) {   // branch-free: clamped loads, unconditional gathers
             const int p = 4 * (tid + k * kSR);
-            if (a4 + p < b) {
-                c[k] = ld_v4(A.col + a4 + p, pol);
-                v0[k] = ld_v2d(A.val + a4 + p, pol);
-                v1[k] = ld_v2d(A.val + a4 + p + 2, pol);
-            }
+            const int pq = (a4 + p < b) ? p : 0;
+            c[k] = ld_v4(A.col + a4 + pq, pol);
+            v0[k] = ld_v2d(A.val + a4 + pq, pol);
+            v1[k] = ld_v2d(A.val + a4 + pq + 2, pol);
+        }
+        double xv[kSRQ][4];
+#pragma unroll
+        for (int k = 0; k < kSRQ; ++k) {
+            xv[k][0] = ldx_r(A, c[k].x, pl);
+            xv[k][1] = ldx_r(A, c[k].y, pl);
+            xv[k][2] = ldx_r(A, c[k].z, pl);
+            xv[k][3] = ldx_r(A, c[k].w, pl);
         }
 #pragma unroll
         for (int k = 0; k < kSRQ; ++k) {
             const int p = 4 * (tid + k * kSR);
+            double2 w0, w1;
+            w0.x = (p + 0 >= lo && p + 0 < hi) ? v0[k].x * xv[k][0] : 0.0;
+            w0.y = (p + 1 >= lo && p + 1 < hi) ? v0[k].y * xv[k][1] : 0.0;
+            w1.x = (p + 2 >= lo && p + 2 < hi) ? v1[k].x * xv[k][2] : 0.0;
+            w1.y = (p + 3 >= lo && p + 3 < hi) ? v1[k].y * xv[k][3] : 0.0;
             if (a4 + p < b) {
-                double2 w0, w1;
-                w0.x = (p + 0 >= lo && p + 0 < hi) ? v0[k].x * ldx_r(A, c[k].x, pl) : 0.0;
-                w0.y = (p + 1 >= lo && p + 1 < hi) ? v0[k].y * ldx_r(A, c[k].y, pl) : 0.0;
-                w1.x = (p + 2 >= lo && p + 2 < hi) ? v1[k].x * ldx_r(A, c[k].z, pl) : 0.0;
-                w1.y = (p + 3 >= lo && p + 3 < hi) ? v1[k].y * ldx_r(A, c[k].w, pl) : 0.0;
                 *reinterpret_cast<double2*>(&sm.prod[p]) = w0;
                 *reinterpret_cast<double2*>(&sm.prod[p + 2]) = w1;
             }
