@@ -412,7 +412,7 @@ def run_ours(args, rank, world, local_rank):
 
     # ---------------- second roofline: the LSU x-gather rate, measured live
     gather = None
-    if not args.no_gather_peak:
+    if not args.no_gather_peak and info["kernel"] != 7:   # the panel kernel does not gather once per nonzero
         gx = torch.rand(4 << 20, dtype=torch.float64, device=dev)      # 32 MB, L2-resident
         sink = torch.zeros(1, dtype=torch.float64, device=dev)
         cnt = 1 << 29
@@ -466,7 +466,9 @@ def run_ours(args, rank, world, local_rank):
                                 "fused multiple-SpMxV" if split else "SpMxV"),
                        "l2": ("flushed (512 MB write) before every SpMxV; step time = SpMxV time" if l2_flush
                               else f"inputs larger than L2 ({bytes_tot / 1e9:.1f} GB vs 126 MB)"),
-                       "parallelism": f"sb-rowblock{world}" if world > 1 else "1gpu"},
+                       "parallelism": f"sb-rowblock{world}" if world > 1 else "1gpu",
+                       "kernel": {7: "panel (column-sorted, y in shared memory)", 0: "row-tile"}.get(info["kernel"],
+                                                                                                      str(info["kernel"]))},
             "hbm_gbs": bytes_tot / (avg_spmv_max * 1e-3) / 1e9,
             "spmv_ms": avg_spmv_max,
             "roofline": roofline,

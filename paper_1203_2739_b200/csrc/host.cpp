@@ -104,7 +104,7 @@ struct spmv_plan_s {
     cudaStream_t side = nullptr;      // long-row kernel stream (forked from / joined to the caller's)
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int kernel = 0;                   // 0 rowtile/256, 1 pipe, 2 tile, 3 rowtile/512, 4 rowseg, 5 rowtile/128,
-                                      // 6 x-staged, 7 column-sorted panels (SPMV_KERNEL=xstage/panel)
+                                      // 6 x-staged, 7 column-sorted panels (default for SB handles)
     // x-staged kernel (xstage.cu)
     spmvb::XsPanel* d_xs_panel = nullptr;
     int32_t* d_xs_wg = nullptr;
@@ -391,10 +391,10 @@ static spmv_status_t plan_pn(spmv_plan_s* h, const std::vector<int64_t>& rp, con
     // panels: about kPnRowsMax rows, their count a multiple of the SM count
     // when possible (whole waves of one CTA per SM)
     const int64_t sms = spmvb::kernel_num_sms();
-    int64_t target = spmvb::kPnRowsMax;
-    for (int64_t k = 1; k <= 64; ++k) {
+    int64_t target = spmvb::kPnRowsTarget;
+    for (int64_t k = 1; k <= 4096; ++k) {
         const int64_t r = (h->m_loc + sms * k - 1) / (sms * k);
-        if (r <= spmvb::kPnRowsMax) {
+        if (r <= spmvb::kPnRowsTarget) {
             target = r;
             break;
         }
@@ -869,7 +869,7 @@ static spmv_status_t create_impl(int64_t m, int64_t n, int64_t nnz, const int64_
         const bool sb = blocks && h->kind == SPMV_SB && nnz_loc > 0;
         if (sb && kenv && strcmp(kenv, "xstage") == 0) {
             if ((s = plan_xs(h, rp, pcol, pval, rbp, cbp))) return s;
-        } else if (sb && kenv && strcmp(kenv, "panel") == 0) {
+        } else if (sb && (!kenv || strcmp(kenv, "panel") == 0)) {
             if ((s = plan_pn(h, rp, pcol, pval, rbp, cbp))) return s;
         }
     }

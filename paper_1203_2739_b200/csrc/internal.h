@@ -144,6 +144,8 @@ constexpr int kPnWarps = 16;                 // warps per panel CTA
 constexpr int kPnB = 4;                      // groups per warp per epoch
 constexpr int kPnEpoch = kPnWarps * kPnB;    // groups per epoch
 constexpr int kPnRowsMax = 28672;            // y rows per panel (224 KB of shared memory)
+constexpr int kPnRowsTarget = 16384;         // default panel size: 128 KB of y, the rest of the
+                                             // 256 KB L1/shared array stays L1 (measured best, §5.3)
 constexpr int kPnRowBits = 15;               // idx = (row_in_panel << 17) | (col - group base)
 constexpr int kPnDeltaBits = 17;
 constexpr uint32_t kPnDummy = 0xFFFE0000u;   // row field 0x7FFF (-> scratch y slot), delta 0 (a valid x

@@ -30,7 +30,7 @@ namespace {
 
 constexpr int NW = kPnWarps;
 constexpr int kT = NW * 32;
-constexpr int kD = 16;    // groups in flight per warp
+constexpr int kD = 16;    // groups in flight per warp (template default; the launch default is 12)
 constexpr int kPF = 8;    // default: epochs of the group stream prefetched into L2 ahead
 static_assert(kD % kPnB == 0, "ring geometry");
 constexpr uint32_t kDeltaMask = (1u << kPnDeltaBits) - 1u;
@@ -70,10 +70,11 @@ __device__ __forceinline__ int32_t ld_base(const int32_t* p) {
 // 2 no shared-memory y update (register sum), 3 no epoch barriers (racy),
 // 4 no L2 prefetch of the group stream, 5 gathers 4 steps ahead (not 8),
 // 6 gathers of a fixed 2 MB window (no dependence on the loaded indices' values)
-template <int MODE>
+template <int MODE, int KD_ = kD, int KGD_ = 8>
 __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
-    constexpr int kGD = MODE == 5 ? 4 : 8;   // gathers issued this many steps ahead
-    static_assert(kD % kGD == 0, "ring geometry");
+    constexpr int kD = KD_;                              // groups in flight per warp
+    constexpr int kGD = MODE == 5 ? 4 : KGD_;            // gathers issued this many steps ahead
+    static_assert(kD % kGD == 0 && kD % kPnB == 0, "ring geometry");
     extern __shared__ __align__(16) double ys[];
     const int p = blockIdx.x;
     const PnPanel d = A.panel[p];
@@ -461,6 +462,10 @@ cudaError_t launch_panel(const PnArgs& a, cudaStream_t s) {
         if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
         if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
         if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
+        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<0, 24, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
+        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<0, 16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
+        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<0, 12, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
+        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<0, 20, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
         if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<15>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
         if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
         if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<13>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
@@ -484,6 +489,10 @@ cudaError_t launch_panel(const PnArgs& a, cudaStream_t s) {
     case 2: spmv_panel_kernel<2><<<b.n_panels, kT, smem, s>>>(b); break;
     case 3: spmv_panel_kernel<3><<<b.n_panels, kT, smem, s>>>(b); break;
     case 4: spmv_panel_kernel<4><<<b.n_panels, kT, smem, s>>>(b); break;
+    case 17: spmv_panel_kernel<0, 24, 8><<<b.n_panels, kT, smem, s>>>(b); break;
+    case 18: spmv_panel_kernel<0, 16, 4><<<b.n_panels, kT, smem, s>>>(b); break;
+    case 19: spmv_panel_kernel<0, 12, 4><<<b.n_panels, kT, smem, s>>>(b); break;
+    case 20: spmv_panel_kernel<0, 20, 4><<<b.n_panels, kT, smem, s>>>(b); break;
     case 15: spmv_panel_kernel<15><<<b.n_panels, kT, smem, s>>>(b); break;
     case 16: spmv_panel_kernel<16><<<b.n_panels, kT, smem, s>>>(b); break;
     case 13: spmv_panel_kernel<13><<<b.n_panels, kT, smem, s>>>(b); break;
@@ -496,7 +505,8 @@ cudaError_t launch_panel(const PnArgs& a, cudaStream_t s) {
     case 12: spmv_panel3_kernel<5, 16><<<b.n_panels, kT, smem3(5), s>>>(b); break;
     case 7: spmv_panel2_kernel<8><<<b.n_panels, kT, smem2(8), s>>>(b); break;
     case 8: spmv_panel2_kernel<12><<<b.n_panels, kT, smem2(12), s>>>(b); break;
-    default: spmv_panel_kernel<0><<<b.n_panels, kT, smem, s>>>(b);
+    case 21: spmv_panel_kernel<0><<<b.n_panels, kT, smem, s>>>(b); break;   // previous default (16, 8)
+    default: spmv_panel_kernel<0, 12, 4><<<b.n_panels, kT, smem, s>>>(b);
     }
     return cudaGetLastError();
 }

@@ -1,6 +1,6 @@
 """GPU parity of the SB panel kernels against the CPU oracle (oracle/):
-  panel  (panel.cu, kernel 7): column-sorted panels, y in shared memory,
-         epoch barriers;
+  panel  (panel.cu, kernel 7, the SB default): column-sorted panels, y in
+         shared memory, epoch barriers;
   xstage (xstage.cu, kernel 6): x chunks streamed through shared memory.
 Odd block widths and chunk-straddling blocks, blocks without a border, empty
 and dense rows, bit-exact integer data, alignment errors, determinism."""
@@ -78,9 +78,9 @@ def test_presets(kernel, name, variant):
 
 @pytest.mark.parametrize("variant", ["int", "real"])
 def test_c5_like_default_geometry(monkeypatch, variant):
-    """The panel kernel at its own panel size on a C5-shaped block pair."""
-    monkeypatch.setenv("SPMV_KERNEL", "panel")
-    monkeypatch.setenv("SPMV_PN_ROWS", "30000")
+    """The SB default (panel kernel) at its default panel size on a C5-shaped block pair."""
+    monkeypatch.delenv("SPMV_KERNEL", raising=False)
+    monkeypatch.delenv("SPMV_PN_ROWS", raising=False)
     p = _c5_like(seed=3)
     if variant == "int":
         rng = np.random.default_rng(1)
