@@ -78,9 +78,11 @@ def test_presets(kernel, name, variant):
 
 @pytest.mark.parametrize("variant", ["int", "real"])
 def test_c5_like_default_geometry(monkeypatch, variant):
-    """The SB default (panel kernel) at its default panel size on a C5-shaped block pair."""
+    """The SB default (panel kernel) on a C5-shaped block pair, at the panel size
+    the default plan picks for full C5 (16,384 rows; this small matrix would
+    otherwise get 1,024-row panels)."""
     monkeypatch.delenv("SPMV_KERNEL", raising=False)
-    monkeypatch.delenv("SPMV_PN_ROWS", raising=False)
+    monkeypatch.setenv("SPMV_PN_ROWS", "16384")
     p = _c5_like(seed=3)
     if variant == "int":
         rng = np.random.default_rng(1)
