@@ -122,6 +122,7 @@ struct spmv_plan_s {
     double* d_pn_gval = nullptr;
     uint32_t* d_pn_gidx = nullptr;
     int32_t* d_pn_gbase = nullptr;
+    int32_t* d_pn_gbase4 = nullptr;
     int64_t pn_panels = 0, pn_groups = 0, pn_pad = 0;
     int32_t pn_max_rows = 0;
     int32_t* d_tile_seg = nullptr;    // [T*K+1]
@@ -423,6 +424,7 @@ static spmv_status_t plan_pn(spmv_plan_s* h, const std::vector<int64_t>& rp, con
     if ((s = dalloc(h, &h->d_pn_gval, G * 32))) return s;
     if ((s = dalloc(h, &h->d_pn_gidx, G * 32))) return s;
     if ((s = dalloc(h, &h->d_pn_gbase, G))) return s;
+    if ((s = dalloc(h, &h->d_pn_gbase4, G))) return s;
     for (int64_t p = 0; p < P; ++p) {
         spmvb::PnPanelData& D = pd[p];
         const int64_t g0 = D.desc.g0, ng = (int64_t)D.gbase.size();
@@ -430,10 +432,12 @@ static spmv_status_t plan_pn(spmv_plan_s* h, const std::vector<int64_t>& rp, con
             CUDA_TRY(cudaMemcpy(h->d_pn_gval + g0 * 32, D.gval.data(), ng * 32 * 8, cudaMemcpyHostToDevice));
             CUDA_TRY(cudaMemcpy(h->d_pn_gidx + g0 * 32, D.gidx.data(), ng * 32 * 4, cudaMemcpyHostToDevice));
             CUDA_TRY(cudaMemcpy(h->d_pn_gbase + g0, D.gbase.data(), ng * 4, cudaMemcpyHostToDevice));
+            CUDA_TRY(cudaMemcpy(h->d_pn_gbase4 + g0, D.gbase4.data(), ng * 4, cudaMemcpyHostToDevice));
         }
         std::vector<double>().swap(D.gval);
         std::vector<uint32_t>().swap(D.gidx);
         std::vector<int32_t>().swap(D.gbase);
+        std::vector<int32_t>().swap(D.gbase4);
     }
     h->pn_panels = P;
     h->pn_max_rows = 0;
@@ -1024,6 +1028,7 @@ static spmv_status_t run(spmv_handle_t h, const double* x, double* y, uint32_t f
         X.gval = h->d_pn_gval;
         X.gidx = h->d_pn_gidx;
         X.gbase = h->d_pn_gbase;
+        X.gbase4 = h->d_pn_gbase4;
         X.x_lo = A.x_lo;
         X.x_hi = A.x_hi;
         X.y = yk;

@@ -168,6 +168,7 @@ struct PnArgs {
     const double* gval;       // [groups*32]
     const uint32_t* gidx;     // [groups*32]
     const int32_t* gbase;     // [groups] first column of the group (local id)
+    const int32_t* gbase4;    // [groups] same, (epoch, warp, step) order (16-byte loads)
     const double* x_lo;
     const double* x_hi;
     double* y;

@@ -93,11 +93,22 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
     uint32_t ri[kD];
     int32_t rb[kD];
     double rx[kGD];
+    // one 16-byte load per epoch gives the warp the bases of its kPnB groups
+    // (slots u..u+3 of the ring; the bases of u+1..u+3 it replaces were last
+    // used by gathers issued >= 1 step earlier, since kGD >= kPnB)
+    static_assert(MODE != 0 || kGD >= kPnB, "base quad overwrites bases still needed");
+    const int4* gb4 = reinterpret_cast<const int4*>(A.gbase4) + (int64_t)d.g0 / kPnB + warp;
     auto load = [&](int t, double& v, uint32_t& i, int32_t& b) {
         const int64_t g = gw + 16 * (int64_t)t;
         v = ld_val(A.gval + g * 32 + lane, pol);
         i = ld_u32(A.gidx + g * 32 + lane, pol);
-        b = ld_base(A.gbase + g);
+        if (MODE != 0) b = ld_base(A.gbase + g);
+    };
+    auto load_b4 = [&](int t, int32_t& b0, int32_t& b1, int32_t& b2, int32_t& b3) {   // t % kPnB == 0
+        int4 q;
+        asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(q.x), "=r"(q.y), "=r"(q.z), "=r"(q.w) : "l"(gb4 + (int64_t)(t / kPnB) * kPnWarps));
+        b0 = q.x; b1 = q.y; b2 = q.z; b3 = q.w;
     };
     double racc = 0.0;
     auto gather = [&](uint32_t i, int32_t b) -> double {
@@ -129,8 +140,8 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
                          : "memory");
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.gidx + g * 32), "r"(kPnEpoch * 32 * 4)
                          : "memory");
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.gbase + g), "r"(kPnEpoch * 4)
-                         : "memory");
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"((MODE == 0 ? A.gbase4 : A.gbase) + g),
+                         "r"(kPnEpoch * 4) : "memory");
         }
     };
     if (MODE != 4) {
@@ -149,8 +160,10 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
         }
     }
 #pragma unroll
-    for (int u = 0; u < kD; ++u)
+    for (int u = 0; u < kD; ++u) {
         if (u < T) load(u, rv[u], ri[u], rb[u]);
+        if (MODE == 0 && u % kPnB == 0 && u < T) load_b4(u, rb[u], rb[u + 1], rb[u + 2], rb[u + 3]);
+    }
 #pragma unroll
     for (int u = 0; u < kGD; ++u)
         if (u < T) rx[u] = gather(ri[u], rb[u]);
@@ -168,7 +181,11 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
                 r = r == (int)(kPnDummy >> kPnDeltaBits) ? scratch : r;
                 ys[r] = fma(rv[u], rx[u % kGD], ys[r]);
             }
-            if (t + kD < T) load(t + kD, rv[u], ri[u], rb[u]);
+            if (t + kD < T) {
+                load(t + kD, rv[u], ri[u], rb[u]);
+                if (MODE == 0 && u % kPnB == 0)
+                    load_b4(t + kD, rb[u], rb[(u + 1) % kD], rb[(u + 2) % kD], rb[(u + 3) % kD]);
+            }
             if (t + kGD < T) rx[u % kGD] = gather(ri[(u + kGD) % kD], rb[(u + kGD) % kD]);
             if (u % kPnB == kPnB - 1) {                  // epoch boundary (T is a multiple of kPnB)
                 if (MODE != 3) __syncthreads();

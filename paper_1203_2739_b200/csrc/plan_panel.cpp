@@ -150,6 +150,11 @@ void build_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col
         ++epoch;
     }
     P.desc.ne = epoch;
+    P.gbase4.resize(P.gbase.size());
+    for (int32_t e = 0; e < epoch; ++e)
+        for (int w = 0; w < kPnWarps; ++w)
+            for (int b = 0; b < kPnB; ++b)
+                P.gbase4[((int64_t)e * kPnWarps + w) * kPnB + b] = P.gbase[(int64_t)e * kPnEpoch + b * kPnWarps + w];
 }
 
 }  // namespace
@@ -235,6 +240,10 @@ bool verify_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& co
         const PnPanel& d = P.desc;
         std::string e;
         if ((int64_t)P.gbase.size() != (int64_t)d.ne * kPnEpoch) e = "group count != epochs * kPnEpoch";
+        for (int64_t g = 0; g < (int64_t)P.gbase.size() && e.empty(); ++g) {
+            const int64_t ep = g / kPnEpoch, k = g % kPnEpoch, b = k / kPnWarps, w = k % kPnWarps;
+            if (P.gbase4[(ep * kPnWarps + w) * kPnB + b] != P.gbase[g]) e = "gbase4 is not the (epoch, warp, step) order of gbase";
+        }
         std::vector<std::vector<std::pair<int32_t, double>>> got(d.nrows);
         std::vector<int32_t> stamp(d.nrows, -1);
         for (int64_t ep = 0; ep < d.ne && e.empty(); ++ep)

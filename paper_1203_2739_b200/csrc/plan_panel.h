@@ -13,6 +13,8 @@ struct PnPanelData {
     std::vector<double> gval;      // [groups*32]
     std::vector<uint32_t> gidx;    // [groups*32]
     std::vector<int32_t> gbase;    // [groups]
+    std::vector<int32_t> gbase4;   // [groups] the same bases in (epoch, warp, step) order: one 16-byte
+                                   // load gives a warp the bases of its kPnB groups of an epoch
     int64_t entries = 0, pads = 0, deferred = 0;
     int32_t rot = 0;               // the column sweep starts at this column (wraps around)
 };
