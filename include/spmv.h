@@ -239,8 +239,10 @@ spmv_status_t spmv_xs_plan_check(int64_t m, int64_t n, const int64_t* row_ptr, c
  * (the row ranges of `blocks`, or the whole matrix when blocks is NULL) of
  * about rows_target rows, decodes the groups again and compares them with the
  * CSR bit for bit, checking that no row repeats within an epoch.
- * stats[6] = panels, groups, padding slots, deferred nonzeros, epochs,
- * nonzeros packed.  OK on an exact round trip; INTERNAL otherwise. */
+ * stats[8] = panels, groups, padding slots, deferred nonzeros, epochs,
+ * nonzeros packed, and 1000 x the mean predicted shared-memory wavefronts of
+ * a group's y access with natural / bank-coloured y slots.  OK on an exact
+ * round trip; INTERNAL otherwise. */
 spmv_status_t spmv_pn_plan_check(int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
                                  const spmv_blocks_t* blocks, int64_t rows_target, int64_t* stats);
 

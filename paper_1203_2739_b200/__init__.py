@@ -243,10 +243,13 @@ def spmv_pn_plan_check(m: int, n: int, row_ptr, col, val, blocks, rows_target: i
         b = _Blocks(int(blocks["kind"]), int(blocks["K"]), rbp.ctypes.data, cbp.ctypes.data, None)
         keep += [rbp, cbp, b]
         bptr = ctypes.byref(b)
-    stats = np.zeros(6, dtype=np.int64)
+    stats = np.zeros(8, dtype=np.int64)
     _check(lib().spmv_pn_plan_check(m, n, _addr(rp), _addr(ci), _addr(va), bptr, rows_target, stats.ctypes.data),
            "spmv_pn_plan_check")
-    return dict(zip(("panels", "groups", "pads", "deferred", "epochs", "entries"), (int(v) for v in stats)))
+    d = dict(zip(("panels", "groups", "pads", "deferred", "epochs", "entries"), (int(v) for v in stats[:6])))
+    d["y_wavefronts_natural"] = stats[6] / 1000.0
+    d["y_wavefronts_coloured"] = stats[7] / 1000.0
+    return d
 
 
 def spmv_apply(h, x, y, flags: int = 0, stream=None, x_len: int | None = None, y_len: int | None = None):

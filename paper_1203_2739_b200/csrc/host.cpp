@@ -123,6 +123,7 @@ struct spmv_plan_s {
     uint32_t* d_pn_gidx = nullptr;
     int32_t* d_pn_gbase = nullptr;
     int32_t* d_pn_gbase4 = nullptr;
+    uint16_t* d_pn_r2s = nullptr;     // [m_loc] y slot of each row in its panel
     int64_t pn_panels = 0, pn_groups = 0, pn_pad = 0;
     int32_t pn_max_rows = 0;
     int32_t* d_tile_seg = nullptr;    // [T*K+1]
@@ -425,6 +426,12 @@ static spmv_status_t plan_pn(spmv_plan_s* h, const std::vector<int64_t>& rp, con
     if ((s = dalloc(h, &h->d_pn_gidx, G * 32))) return s;
     if ((s = dalloc(h, &h->d_pn_gbase, G))) return s;
     if ((s = dalloc(h, &h->d_pn_gbase4, G))) return s;
+    {
+        std::vector<uint16_t> r2s(std::max<int64_t>(h->m_loc, 1), 0);
+        for (int64_t p = 0; p < P; ++p)
+            std::copy(pd[p].row2slot.begin(), pd[p].row2slot.end(), r2s.begin() + pd[p].desc.row0);
+        if ((s = upload(h, &h->d_pn_r2s, r2s.data(), r2s.size()))) return s;
+    }
     for (int64_t p = 0; p < P; ++p) {
         spmvb::PnPanelData& D = pd[p];
         const int64_t g0 = D.desc.g0, ng = (int64_t)D.gbase.size();
@@ -441,7 +448,7 @@ static spmv_status_t plan_pn(spmv_plan_s* h, const std::vector<int64_t>& rp, con
     }
     h->pn_panels = P;
     h->pn_max_rows = 0;
-    for (int64_t p = 0; p < P; ++p) h->pn_max_rows = std::max(h->pn_max_rows, desc[p].nrows);
+    for (int64_t p = 0; p < P; ++p) h->pn_max_rows = std::max(h->pn_max_rows, (desc[p].nrows + 15) & ~15);
     h->pn_groups = G;
     h->pn_pad = st.pads;
     h->bytes_stream = (12 * 32 + 4) * G + 8 * h->m_loc;
@@ -1034,6 +1041,7 @@ static spmv_status_t run(spmv_handle_t h, const double* x, double* y, uint32_t f
         X.y = yk;
         X.maxabs_slots = A.maxabs_slots;
         X.max_rows = h->pn_max_rows;
+        X.row2slot = h->d_pn_r2s;
         CUDA_TRY(spmvb::launch_panel(X, st));
     } else if (!split && h->kernel == 6) {
         spmvb::XsArgs X{};
@@ -1310,6 +1318,7 @@ spmv_status_t spmv_pn_plan_check(int64_t m, int64_t n, const int64_t* row_ptr, c
             return fail(SPMV_ERR_UNSUPPORTED, "pn_plan_check: %s", why.c_str());
         stats[0] = st.panels; stats[1] = st.groups; stats[2] = st.pads;
         stats[3] = st.deferred; stats[4] = st.epochs; stats[5] = st.entries;
+        stats[6] = (int64_t)(st.ywf0 * 1000.0); stats[7] = (int64_t)(st.ywf1 * 1000.0);
         if (st.entries != nnz) return fail(SPMV_ERR_INTERNAL, "pn_plan_check: plan holds %lld of %lld nonzeros",
                                            (long long)st.entries, (long long)nnz);
         if (!spmvb::verify_panel(rp, c, v, INT32_MAX, pd, why))

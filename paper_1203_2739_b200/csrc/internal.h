@@ -173,7 +173,9 @@ struct PnArgs {
     const double* x_hi;
     double* y;
     unsigned long long* maxabs_slots;
-    int32_t max_rows;         // largest panel: shared memory = 8 * max_rows bytes (the rest stays L1)
+    int32_t max_rows;         // largest panel's y slots (a multiple of 16); slot max_rows is the padding
+                              // lanes' scratch; shared memory = 8 * (max_rows + 1) bytes (the rest stays L1)
+    const uint16_t* row2slot; // [local rows] y slot of each row within its panel (bank colouring)
     int32_t pf_epochs;        // epochs of the group stream prefetched into L2 ahead (0 = default)
 };
 cudaError_t launch_panel(const PnArgs& a, cudaStream_t s);

@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
     const int p = blockIdx.x;
     const PnPanel d = A.panel[p];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    for (int i = tid; i < d.nrows; i += kT) ys[i] = 0.0;
+    for (int i = tid; i < ((d.nrows + 15) & ~15); i += kT) ys[i] = 0.0;   // the panel's slots
     __syncthreads();
 
     const uint64_t pol = pol_evict_first();
@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
 
     double mx = 0.0;
     for (int i = tid; i < d.nrows; i += kT) {
-        const double v = ys[i];
+        const double v = ys[A.row2slot[d.row0 + i]];
         A.y[d.row0 + i] = v;
         mx = fmax(mx, fabs(v));
     }
@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel2_kernel(const PnArgs A) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     double* gr = sm2 + ((A.max_rows + 2) & ~1) + warp * G * 32;
     const uint32_t gr_s = (uint32_t)__cvta_generic_to_shared(gr) + lane * 8;
-    for (int i = tid; i < d.nrows; i += kT) ys[i] = 0.0;
+    for (int i = tid; i < ((d.nrows + 15) & ~15); i += kT) ys[i] = 0.0;   // the panel's slots
     __syncthreads();
 
     const uint64_t pol = pol_evict_first();
@@ -307,7 +307,7 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel2_kernel(const PnArgs A) {
 
     double mx = 0.0;
     for (int i = tid; i < d.nrows; i += kT) {
-        const double v = ys[i];
+        const double v = ys[A.row2slot[d.row0 + i]];
         A.y[d.row0 + i] = v;
         mx = fmax(mx, fabs(v));
     }
@@ -384,7 +384,7 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel3_kernel(const PnArgs A) {
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
-    for (int i = tid; i < d.nrows; i += kT) ys[i] = 0.0;
+    for (int i = tid; i < ((d.nrows + 15) & ~15); i += kT) ys[i] = 0.0;   // the panel's slots
     __syncthreads();
     if (tid == 0) {
         for (int e = 0; e < NS; ++e) load_epoch(e);
@@ -446,7 +446,7 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel3_kernel(const PnArgs A) {
 
     double mx = 0.0;
     for (int i = tid; i < d.nrows; i += kT) {
-        const double v = ys[i];
+        const double v = ys[A.row2slot[d.row0 + i]];
         A.y[d.row0 + i] = v;
         mx = fmax(mx, fabs(v));
     }

@@ -43,39 +43,156 @@ struct Ent {
 
 class Emitter {
   public:
-    explicit Emitter(PnPanelData& P) : P_(P) {}
+    explicit Emitter(std::vector<Ent>& ents, std::vector<int32_t>& bases) : E_(ents), B_(bases) {}
     void add(const Ent& e) { cur_[n_++] = e; }
     int size() const { return n_; }
     int32_t base() const { return cur_[0].col; }
-    void close() {
-        // lanes: entries sorted by y bank alternate between the half-warps
-        Ent s[32];
-        std::copy(cur_, cur_ + n_, s);
-        std::stable_sort(s, s + n_, [](const Ent& a, const Ent& b) { return (a.row & 15) < (b.row & 15); });
-        uint32_t idx[32];
-        double val[32];
-        for (int l = 0; l < 32; ++l) {
-            idx[l] = kPnDummy;
-            val[l] = 0.0;
-        }
-        const int32_t base = n_ ? cur_[0].col : 0;
-        for (int k = 0; k < n_; ++k) {
-            const int lane = (k & 1) * 16 + (k >> 1);
-            idx[lane] = ((uint32_t)s[k].row << kPnDeltaBits) | (uint32_t)(s[k].col - base);
-            val[lane] = s[k].v;
-        }
-        P_.gval.insert(P_.gval.end(), val, val + 32);
-        P_.gidx.insert(P_.gidx.end(), idx, idx + 32);
-        P_.gbase.push_back(base);
-        P_.pads += 32 - n_;
+    void close() {   // the group's entries (row -1 = padding), emitted after the y-slot colouring
+        for (int k = 0; k < 32; ++k) E_.push_back(k < n_ ? cur_[k] : Ent{-1, 0, 0.0});
+        B_.push_back(n_ ? cur_[0].col : 0);
         n_ = 0;
     }
 
   private:
-    PnPanelData& P_;
+    std::vector<Ent>& E_;
+    std::vector<int32_t>& B_;
     Ent cur_[32];
     int n_ = 0;
 };
+
+// Shared-memory y slots: 8-byte bank = slot mod 16.  A warp-wide 64-bit access
+// costs (per half-warp) as many wavefronts as the most repeated bank, so the
+// rows of each group should spread over the 16 banks.  Start from slot = row
+// (bank = row mod 16, all banks the same size) and improve by swapping the
+// banks of two rows when that lowers sum over groups of sum_b count_b^2 (a
+// local search, deterministic: fixed pseudo-random order).  Then rows of bank
+// b take slots b, b+16, ... in row order.
+void colour_slots(int32_t nr, const std::vector<Ent>& ents, int64_t G, std::vector<uint16_t>& row2slot,
+                  std::vector<int32_t>& slot_of_row) {
+    std::vector<int32_t> bank(nr);
+    for (int32_t r = 0; r < nr; ++r) bank[r] = r & 15;
+    // row -> groups
+    std::vector<int32_t> rg_ptr(nr + 1, 0);
+    for (int64_t i = 0; i < G * 32; ++i)
+        if (ents[i].row >= 0) rg_ptr[ents[i].row + 1]++;
+    for (int32_t r = 0; r < nr; ++r) rg_ptr[r + 1] += rg_ptr[r];
+    std::vector<int32_t> rg(rg_ptr[nr]), fill(rg_ptr.begin(), rg_ptr.end() - 1);
+    for (int64_t g = 0; g < G; ++g)
+        for (int k = 0; k < 32; ++k) {
+            const int32_t r = ents[g * 32 + k].row;
+            if (r >= 0) rg[fill[r]++] = (int32_t)g;
+        }
+    std::vector<uint8_t> cnt(G * 16, 0);
+    for (int64_t g = 0; g < G; ++g)
+        for (int k = 0; k < 32; ++k) {
+            const int32_t r = ents[g * 32 + k].row;
+            if (r >= 0) cnt[g * 16 + bank[r]]++;
+        }
+    // rows of each bank (for picking swap partners)
+    std::vector<std::vector<int32_t>> of_bank(16);
+    std::vector<int32_t> pos(nr);
+    for (int32_t r = 0; r < nr; ++r) {
+        pos[r] = (int32_t)of_bank[bank[r]].size();
+        of_bank[bank[r]].push_back(r);
+    }
+    uint64_t rs = 0x9E3779B97F4A7C15ull ^ (uint64_t)nr;
+    auto rnd = [&]() {
+        rs ^= rs << 13; rs ^= rs >> 7; rs ^= rs << 17;
+        return rs;
+    };
+    auto gain_move = [&](int32_t r, int b1, int b2, int32_t other) {
+        // cost change of moving r from b1 to b2 (groups also holding `other` are skipped: swapped pair cancels)
+        int64_t d = 0;
+        for (int32_t q = rg_ptr[r]; q < rg_ptr[r + 1]; ++q) {
+            const int64_t g = rg[q];
+            bool both = false;
+            for (int32_t u = rg_ptr[other]; u < rg_ptr[other + 1]; ++u)
+                if (rg[u] == g) { both = true; break; }
+            if (both) continue;
+            d += 2 * ((int)cnt[g * 16 + b2] - (int)cnt[g * 16 + b1] + 1);
+        }
+        return d;
+    };
+    auto apply_move = [&](int32_t r, int b1, int b2) {
+        for (int32_t q = rg_ptr[r]; q < rg_ptr[r + 1]; ++q) {
+            const int64_t g = rg[q];
+            cnt[g * 16 + b1]--;
+            cnt[g * 16 + b2]++;
+        }
+    };
+    static const int kSweeps = getenv("SPMV_PN_SWEEPS") ? atoi(getenv("SPMV_PN_SWEEPS")) : 2;
+    static const int kTries = getenv("SPMV_PN_TRIES") ? atoi(getenv("SPMV_PN_TRIES")) : 3;
+    for (int sw = 0; sw < kSweeps; ++sw)
+        for (int32_t i = 0; i < nr; ++i) {
+            const int32_t r = (int32_t)((i * 40503ull + sw * 7919ull) % (uint64_t)nr);   // fixed visiting order
+            if (rg_ptr[r + 1] == rg_ptr[r]) continue;
+            const int b1 = bank[r];
+            int64_t best = 0;
+            int32_t bs = -1;
+            for (int k = 0; k < kTries; ++k) {
+                const int b2 = (b1 + 1 + (int)(rnd() % 15)) & 15;
+                if (of_bank[b2].empty()) continue;
+                const int32_t s2 = of_bank[b2][rnd() % of_bank[b2].size()];
+                const int64_t d = gain_move(r, b1, b2, s2) + gain_move(s2, b2, b1, r);
+                if (d < best) { best = d; bs = s2; }
+            }
+            if (bs >= 0) {
+                const int b2 = bank[bs];
+                apply_move(r, b1, b2);
+                apply_move(bs, b2, b1);
+                std::swap(of_bank[b1][pos[r]], of_bank[b2][pos[bs]]);
+                std::swap(pos[r], pos[bs]);
+                bank[r] = b2;
+                bank[bs] = b1;
+            }
+        }
+    row2slot.assign(nr, 0);
+    slot_of_row.assign(nr, 0);
+    std::vector<int32_t> next(16, 0);
+    for (int32_t r = 0; r < nr; ++r) {
+        const int32_t sl = bank[r] + 16 * next[bank[r]]++;
+        row2slot[r] = (uint16_t)sl;
+        slot_of_row[r] = sl;
+    }
+}
+
+// Predicted wavefronts of one warp-wide 64-bit y access for a group whose
+// lanes were assigned by emit_group (sum over the half-warps of the largest
+// bank multiplicity).
+double y_wavefronts(const uint32_t* idx) {
+    double w = 0;
+    for (int h = 0; h < 2; ++h) {
+        int c[16] = {0}, m = 0;
+        for (int l = h * 16; l < h * 16 + 16; ++l)
+            if (idx[l] != kPnDummy) m = std::max(m, ++c[(idx[l] >> kPnDeltaBits) & 15]);
+        w += std::max(m, 1);
+    }
+    return w;
+}
+
+// lanes: entries sorted by slot bank alternate between the half-warps
+void emit_group(const Ent* e, int32_t base, const std::vector<int32_t>& slot, PnPanelData& P) {
+    Ent s[32];
+    int n = 0;
+    for (int k = 0; k < 32; ++k)
+        if (e[k].row >= 0) s[n++] = e[k];
+    std::stable_sort(s, s + n, [&](const Ent& a, const Ent& b) { return (slot[a.row] & 15) < (slot[b.row] & 15); });
+    uint32_t idx[32];
+    double val[32];
+    for (int l = 0; l < 32; ++l) {
+        idx[l] = kPnDummy;
+        val[l] = 0.0;
+    }
+    for (int k = 0; k < n; ++k) {
+        const int lane = (k & 1) * 16 + (k >> 1);
+        idx[lane] = ((uint32_t)slot[s[k].row] << kPnDeltaBits) | (uint32_t)(s[k].col - base);
+        val[lane] = s[k].v;
+    }
+    P.gval.insert(P.gval.end(), val, val + 32);
+    P.gidx.insert(P.gidx.end(), idx, idx + 32);
+    P.gbase.push_back(base);
+    P.pads += 32 - n;
+}
 
 void build_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col, const std::vector<double>& val,
                  int64_t x_split, PnPanelData& P) {
@@ -98,7 +215,9 @@ void build_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col
     auto side = [&](int32_t c) { return (int64_t)c >= x_split; };
     std::vector<int32_t> stamp(nr, -1);
     std::vector<int64_t> deferred, nd;
-    Emitter em(P);
+    std::vector<Ent> gents;
+    std::vector<int32_t> gbases;
+    Emitter em(gents, gbases);
     int64_t pos = 0;
     int32_t epoch = 0;
     while (pos < n || !deferred.empty()) {
@@ -150,6 +269,33 @@ void build_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col
         ++epoch;
     }
     P.desc.ne = epoch;
+    // y-slot colouring, then the groups' lanes and packed indices
+    const int64_t G = (int64_t)gbases.size();
+    std::vector<int32_t> slot;
+    std::vector<int32_t> ident(nr);
+    for (int32_t r = 0; r < (int32_t)nr; ++r) ident[r] = r;
+    {   // statistics: natural slots
+        PnPanelData tmp;
+        double w = 0;
+        for (int64_t g = 0; g < G; ++g) {
+            emit_group(&gents[g * 32], gbases[g], ident, tmp);
+            w += y_wavefronts(&tmp.gidx[g * 32]);
+        }
+        P.ywf0 = G ? w / G : 0;
+    }
+    if (getenv("SPMV_PN_NOCOLOUR")) {
+        P.row2slot.resize(nr);
+        for (int32_t r = 0; r < (int32_t)nr; ++r) P.row2slot[r] = (uint16_t)r;
+        slot = ident;
+    } else {
+        colour_slots((int32_t)nr, gents, G, P.row2slot, slot);
+    }
+    double w = 0;
+    for (int64_t g = 0; g < G; ++g) {
+        emit_group(&gents[g * 32], gbases[g], slot, P);
+        w += y_wavefronts(&P.gidx[g * 32]);
+    }
+    P.ywf1 = G ? w / G : 0;
     P.gbase4.resize(P.gbase.size());
     for (int32_t e = 0; e < epoch; ++e)
         for (int w = 0; w < kPnWarps; ++w)
@@ -225,8 +371,14 @@ bool plan_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col,
         st.pads += P.pads;
         st.deferred += P.deferred;
         st.epochs += P.desc.ne;
+        st.ywf0 += P.ywf0 * (double)P.gbase.size();
+        st.ywf1 += P.ywf1 * (double)P.gbase.size();
     }
     st.groups = g;
+    if (g) {
+        st.ywf0 /= (double)g;
+        st.ywf1 /= (double)g;
+    }
     return true;
 }
 
@@ -246,6 +398,14 @@ bool verify_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& co
         }
         std::vector<std::vector<std::pair<int32_t, double>>> got(d.nrows);
         std::vector<int32_t> stamp(d.nrows, -1);
+        const int32_t nsl = ((d.nrows + 15) / 16) * 16;
+        std::vector<int32_t> row_of_slot(nsl, -1);
+        if ((int32_t)P.row2slot.size() != d.nrows) e = "row2slot size";
+        for (int32_t r = 0; r < d.nrows && e.empty(); ++r) {
+            const int32_t sl = P.row2slot[r];
+            if (sl >= nsl || row_of_slot[sl] != -1) e = "row2slot is not injective into the panel's slots";
+            else row_of_slot[sl] = r;
+        }
         for (int64_t ep = 0; ep < d.ne && e.empty(); ++ep)
             for (int k = 0; k < kPnEpoch && e.empty(); ++k) {
                 const int64_t g = ep * kPnEpoch + k;
@@ -258,9 +418,10 @@ bool verify_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& co
                         if (v != 0.0) e = "dummy slot with a value";
                         continue;
                     }
-                    const int32_t r = (int32_t)(i >> kPnDeltaBits);
+                    const int32_t sl = (int32_t)(i >> kPnDeltaBits);
                     const int64_t c = (int64_t)base + (i & ((1u << kPnDeltaBits) - 1));
-                    if (r >= d.nrows) { e = "row outside the panel"; break; }
+                    if (sl >= nsl || row_of_slot[sl] < 0) { e = "slot outside the panel"; break; }
+                    const int32_t r = row_of_slot[sl];
                     if (stamp[r] == ep) { e = "row repeated within an epoch"; break; }
                     stamp[r] = (int32_t)ep;
                     const int sd = c >= x_split;

@@ -15,12 +15,15 @@ struct PnPanelData {
     std::vector<int32_t> gbase;    // [groups]
     std::vector<int32_t> gbase4;   // [groups] the same bases in (epoch, warp, step) order: one 16-byte
                                    // load gives a warp the bases of its kPnB groups of an epoch
+    std::vector<uint16_t> row2slot; // [nrows] shared-memory y slot of each panel row (bank colouring)
     int64_t entries = 0, pads = 0, deferred = 0;
     int32_t rot = 0;               // the column sweep starts at this column (wraps around)
+    double ywf0 = 0, ywf1 = 0;     // predicted y wavefronts per group access: natural slots / coloured
 };
 
 struct PnPlanStats {
     int64_t panels = 0, groups = 0, entries = 0, pads = 0, deferred = 0, epochs = 0;
+    double ywf0 = 0, ywf1 = 0;     // mean predicted y wavefronts per group access, before / after colouring
 };
 
 // Row ranges [r0, r1) (local rows; e.g. the SB blocks of this rank) are cut
