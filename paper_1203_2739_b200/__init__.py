@@ -22,7 +22,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libspmv_b200.so")
+LIB_PATH = os.environ.get("SPMV_LIB") or os.path.join(_HERE, "libspmv_b200.so")   # SPMV_LIB: A/B builds
 
 SPMV_OK, SPMV_ERR_USAGE, SPMV_ERR_DATA, SPMV_ERR_INTERNAL, SPMV_ERR_UNSUPPORTED = range(5)
 SPMV_SB, SPMV_DB = 1, 2

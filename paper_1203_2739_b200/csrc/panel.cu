@@ -194,13 +194,32 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
         }
     }
     if (MODE == 2 && racc == 1.2345) ys[0] = racc;
+    // epilogue: y[row] = ys[slot(row)].  The slot loads are batched 16 per
+    // thread (clamped addresses, no branch) and the first batch is issued
+    // before the barrier, so their latency is not paid once per row.
+    constexpr int EB = 16;
+    uint16_t sl[EB];
+    const uint16_t* r2s = A.row2slot + d.row0;
+    const int nrl = d.nrows;
+    auto load_slots = [&](int i0) {
+#pragma unroll
+        for (int k = 0; k < EB; ++k) sl[k] = r2s[min(i0 + k * kT, nrl - 1)];
+    };
+    load_slots(tid);
     __syncthreads();
 
     double mx = 0.0;
-    for (int i = tid; i < d.nrows; i += kT) {
-        const double v = ys[A.row2slot[d.row0 + i]];
-        A.y[d.row0 + i] = v;
-        mx = fmax(mx, fabs(v));
+    for (int i0 = tid; i0 < nrl; i0 += EB * kT) {
+        if (i0 != tid) load_slots(i0);
+#pragma unroll
+        for (int k = 0; k < EB; ++k) {
+            const int i = i0 + k * kT;
+            if (i < nrl) {
+                const double v = ys[sl[k]];
+                A.y[d.row0 + i] = v;
+                mx = fmax(mx, fabs(v));
+            }
+        }
     }
     if (A.maxabs_slots) {
 #pragma unroll
