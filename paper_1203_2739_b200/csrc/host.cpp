@@ -1314,14 +1314,18 @@ spmv_status_t spmv_pn_plan_check(int64_t m, int64_t n, const int64_t* row_ptr, c
         std::vector<spmvb::PnPanelData> pd;
         spmvb::PnPlanStats st;
         std::string why;
-        if (!spmvb::plan_panel(rp, c, v, ranges, INT32_MAX, rows_target, pd, st, why))
+        // SB: columns >= C_B's start come from the second x pointer (the border
+        // exchange buffer at world > 1); groups must not mix the two sides
+        const int64_t xs = (blocks && blocks->K > 0 && blocks->col_block_ptr) ? blocks->col_block_ptr[blocks->K]
+                                                                            : (int64_t)INT32_MAX;
+        if (!spmvb::plan_panel(rp, c, v, ranges, xs, rows_target, pd, st, why))
             return fail(SPMV_ERR_UNSUPPORTED, "pn_plan_check: %s", why.c_str());
         stats[0] = st.panels; stats[1] = st.groups; stats[2] = st.pads;
         stats[3] = st.deferred; stats[4] = st.epochs; stats[5] = st.entries;
         stats[6] = (int64_t)(st.ywf0 * 1000.0); stats[7] = (int64_t)(st.ywf1 * 1000.0);
         if (st.entries != nnz) return fail(SPMV_ERR_INTERNAL, "pn_plan_check: plan holds %lld of %lld nonzeros",
                                            (long long)st.entries, (long long)nnz);
-        if (!spmvb::verify_panel(rp, c, v, INT32_MAX, pd, why))
+        if (!spmvb::verify_panel(rp, c, v, xs, pd, why))
             return fail(SPMV_ERR_INTERNAL, "pn_plan_check: %s", why.c_str());
     } catch (const std::bad_alloc&) {
         return fail(SPMV_ERR_INTERNAL, "out of host memory");
