@@ -57,7 +57,8 @@ def _newer(target: str, deps) -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     nccl = _nccl_dir()
-    inc = ["-I" + CSRC, "-I" + os.path.join(ROOT, "include"), "-I" + os.path.join(nccl, "include"),
+    defs = os.environ.get("SPMV_BUILD_DEFS", "").split()   # A/B builds only (e.g. -DSPMV_PN_B=8)
+    inc = defs + ["-I" + CSRC, "-I" + os.path.join(ROOT, "include"), "-I" + os.path.join(nccl, "include"),
            "-I" + os.path.join(CUDA, "include")]
     hdrs = [os.path.join(CSRC, h) for h in HEADERS]
     objs = []

@@ -141,7 +141,10 @@ size_t xstage_smem_bytes();
 // shared-memory y updates of one epoch never race, and a CTA barrier
 // separates epochs.
 constexpr int kPnWarps = 16;                 // warps per panel CTA
-constexpr int kPnB = 4;                      // groups per warp per epoch
+#ifndef SPMV_PN_B
+#define SPMV_PN_B 4
+#endif
+constexpr int kPnB = SPMV_PN_B;              // groups per warp per epoch
 constexpr int kPnEpoch = kPnWarps * kPnB;    // groups per epoch
 constexpr int kPnRowsMax = 28672;            // y rows per panel (224 KB of shared memory)
 constexpr int kPnRowsTarget = 16384;         // default panel size: 128 KB of y, the rest of the

@@ -30,7 +30,8 @@ namespace {
 
 constexpr int NW = kPnWarps;
 constexpr int kT = NW * 32;
-constexpr int kD = 16;    // groups in flight per warp (template default; the launch default is 12)
+constexpr int kD = 16;    // groups in flight per warp (template default)
+constexpr int kDefD = kPnB == 8 ? 16 : 12;   // the launch default
 constexpr int kPF = 8;    // default: epochs of the group stream prefetched into L2 ahead
 static_assert(kD % kPnB == 0, "ring geometry");
 constexpr uint32_t kDeltaMask = (1u << kPnDeltaBits) - 1u;
@@ -96,18 +97,20 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
     // one 16-byte load per epoch gives the warp the bases of its kPnB groups
     // (slots u..u+3 of the ring; the bases of u+1..u+3 it replaces were last
     // used by gathers issued >= 1 step earlier, since kGD >= kPnB)
-    static_assert(MODE != 0 || kGD >= kPnB, "base quad overwrites bases still needed");
-    const int4* gb4 = reinterpret_cast<const int4*>(A.gbase4) + (int64_t)d.g0 / kPnB + warp;
+    static_assert(MODE != 0 || kGD >= 4, "base quad overwrites bases still needed");
+    static_assert(kPnB % 4 == 0, "bases are loaded four at a time");
+    const int4* gb4 = reinterpret_cast<const int4*>(A.gbase4 + d.g0);
     auto load = [&](int t, double& v, uint32_t& i, int32_t& b) {
         const int64_t g = gw + 16 * (int64_t)t;
         v = ld_val(A.gval + g * 32 + lane, pol);
         i = ld_u32(A.gidx + g * 32 + lane, pol);
         if (MODE != 0) b = ld_base(A.gbase + g);
     };
-    auto load_b4 = [&](int t, int32_t& b0, int32_t& b1, int32_t& b2, int32_t& b3) {   // t % kPnB == 0
+    auto load_b4 = [&](int t, int32_t& b0, int32_t& b1, int32_t& b2, int32_t& b3) {   // t % 4 == 0
         int4 q;
+        const int64_t o = ((int64_t)(t / kPnB) * kPnWarps + warp) * (kPnB / 4) + (t % kPnB) / 4;
         asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(q.x), "=r"(q.y), "=r"(q.z), "=r"(q.w) : "l"(gb4 + (int64_t)(t / kPnB) * kPnWarps));
+                     : "=r"(q.x), "=r"(q.y), "=r"(q.z), "=r"(q.w) : "l"(gb4 + o));
         b0 = q.x; b1 = q.y; b2 = q.z; b3 = q.w;
     };
     double racc = 0.0;
@@ -162,7 +165,7 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
 #pragma unroll
     for (int u = 0; u < kD; ++u) {
         if (u < T) load(u, rv[u], ri[u], rb[u]);
-        if (MODE == 0 && u % kPnB == 0 && u < T) load_b4(u, rb[u], rb[u + 1], rb[u + 2], rb[u + 3]);
+        if (MODE == 0 && u % 4 == 0 && u < T) load_b4(u, rb[u], rb[u + 1], rb[u + 2], rb[u + 3]);
     }
 #pragma unroll
     for (int u = 0; u < kGD; ++u)
@@ -183,7 +186,7 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
             }
             if (t + kD < T) {
                 load(t + kD, rv[u], ri[u], rb[u]);
-                if (MODE == 0 && u % kPnB == 0)
+                if (MODE == 0 && u % 4 == 0)
                     load_b4(t + kD, rb[u], rb[(u + 1) % kD], rb[(u + 2) % kD], rb[(u + 3) % kD]);
             }
             if (t + kGD < T) rx[u % kGD] = gather(ri[(u + kGD) % kD], rb[(u + kGD) % kD]);
@@ -498,10 +501,14 @@ cudaError_t launch_panel(const PnArgs& a, cudaStream_t s) {
         if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
         if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
         if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
+#if SPMV_PN_B == 4
         if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<0, 24, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
+#endif
         if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<0, 16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
-        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<0, 12, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
+        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<0, kDefD, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
+#if SPMV_PN_B == 4
         if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<0, 20, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
+#endif
         if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<15>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
         if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
         if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<13>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
@@ -512,8 +519,12 @@ cudaError_t launch_panel(const PnArgs& a, cudaStream_t s) {
         if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel2_kernel<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel3_kernel<4, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel3_kernel<3, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+#if SPMV_PN_B == 4
         if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel3_kernel<4, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+#endif
+#if SPMV_PN_B == 4
         if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel3_kernel<5, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+#endif
         if (r != cudaSuccess) return r;
     }
     PnArgs b = a;
@@ -525,10 +536,16 @@ cudaError_t launch_panel(const PnArgs& a, cudaStream_t s) {
     case 2: spmv_panel_kernel<2><<<b.n_panels, kT, smem, s>>>(b); break;
     case 3: spmv_panel_kernel<3><<<b.n_panels, kT, smem, s>>>(b); break;
     case 4: spmv_panel_kernel<4><<<b.n_panels, kT, smem, s>>>(b); break;
+#if SPMV_PN_B == 4
     case 17: spmv_panel_kernel<0, 24, 8><<<b.n_panels, kT, smem, s>>>(b); break;
+#endif
     case 18: spmv_panel_kernel<0, 16, 4><<<b.n_panels, kT, smem, s>>>(b); break;
+#if SPMV_PN_B == 4
     case 19: spmv_panel_kernel<0, 12, 4><<<b.n_panels, kT, smem, s>>>(b); break;
+#endif
+#if SPMV_PN_B == 4
     case 20: spmv_panel_kernel<0, 20, 4><<<b.n_panels, kT, smem, s>>>(b); break;
+#endif
     case 15: spmv_panel_kernel<15><<<b.n_panels, kT, smem, s>>>(b); break;
     case 16: spmv_panel_kernel<16><<<b.n_panels, kT, smem, s>>>(b); break;
     case 13: spmv_panel_kernel<13><<<b.n_panels, kT, smem, s>>>(b); break;
@@ -537,12 +554,16 @@ cudaError_t launch_panel(const PnArgs& a, cudaStream_t s) {
     case 5: spmv_panel_kernel<5><<<b.n_panels, kT, smem, s>>>(b); break;
     case 9: spmv_panel3_kernel<4, 8><<<b.n_panels, kT, smem3(4), s>>>(b); break;
     case 10: spmv_panel3_kernel<3, 8><<<b.n_panels, kT, smem3(3), s>>>(b); break;
+#if SPMV_PN_B == 4
     case 11: spmv_panel3_kernel<4, 12><<<b.n_panels, kT, smem3(4), s>>>(b); break;
+#endif
+#if SPMV_PN_B == 4
     case 12: spmv_panel3_kernel<5, 16><<<b.n_panels, kT, smem3(5), s>>>(b); break;
+#endif
     case 7: spmv_panel2_kernel<8><<<b.n_panels, kT, smem2(8), s>>>(b); break;
     case 8: spmv_panel2_kernel<12><<<b.n_panels, kT, smem2(12), s>>>(b); break;
     case 21: spmv_panel_kernel<0><<<b.n_panels, kT, smem, s>>>(b); break;   // previous default (16, 8)
-    default: spmv_panel_kernel<0, 12, 4><<<b.n_panels, kT, smem, s>>>(b);
+    default: spmv_panel_kernel<0, kDefD, 4><<<b.n_panels, kT, smem, s>>>(b);
     }
     return cudaGetLastError();
 }
