@@ -123,7 +123,10 @@ struct spmv_plan_s {
     uint32_t* d_pn_gidx = nullptr;
     int32_t* d_pn_gbase = nullptr;
     int32_t* d_pn_gbase4 = nullptr;
-    uint16_t* d_pn_r2s = nullptr;     // [m_loc] y slot of each row in its panel
+    uint16_t* d_pn_r2s = nullptr;     // [m_loc] y slot of each row in its panel (or split entry)
+    int32_t* d_pn_split_first = nullptr;
+    int32_t* d_pn_split_cnt = nullptr;
+    uint16_t* d_pn_split_slots = nullptr;
     int64_t pn_panels = 0, pn_groups = 0, pn_pad = 0;
     int32_t pn_max_rows = 0;
     int32_t* d_tile_seg = nullptr;    // [T*K+1]
@@ -383,19 +386,28 @@ static spmv_status_t plan_pn(spmv_plan_s* h, const std::vector<int64_t>& rp, con
     const int64_t R0 = h->row_begin, R1 = h->row_begin + h->m_loc;
     std::vector<std::pair<int64_t, int64_t>> ranges, xcols;
     const int64_t q0 = h->world > 1 ? h->x_int_begin : 0;
-    for (int k = 0; k < K; ++k) {
-        const int64_t a = std::max(rbp[k], R0), b = std::min(rbp[k + 1], R1);
-        if (b > a) {
-            ranges.push_back({a - R0, b - R0});
-            xcols.push_back({cbp[k] - q0, cbp[k + 1] - q0});
+    if (h->kind == SPMV_SB) {
+        for (int k = 0; k < K; ++k) {
+            const int64_t a = std::max(rbp[k], R0), b = std::min(rbp[k + 1], R1);
+            if (b > a) {
+                ranges.push_back({a - R0, b - R0});
+                xcols.push_back({cbp[k] - q0, cbp[k + 1] - q0});
+            }
         }
+    } else {   // no SB structure: panels of consecutive rows, no x prefetch / rotation
+        ranges.push_back({0, h->m_loc});
+    }
+    int64_t total_slots = 0;
+    for (int64_t r = 0; r < h->m_loc; ++r) {
+        const int64_t L = rp[r + 1] - rp[r];
+        total_slots += L > spmvb::kPnSplitAt ? (L + spmvb::kPnVMax - 1) / spmvb::kPnVMax : 1;
     }
     // panels: about kPnRowsMax rows, their count a multiple of the SM count
     // when possible (whole waves of one CTA per SM)
     const int64_t sms = spmvb::kernel_num_sms();
     int64_t target = spmvb::kPnRowsTarget;
     for (int64_t k = 1; k <= 4096; ++k) {
-        const int64_t r = (h->m_loc + sms * k - 1) / (sms * k);
+        const int64_t r = (total_slots + sms * k - 1) / (sms * k);
         if (r <= spmvb::kPnRowsTarget) {
             target = r;
             break;
@@ -410,7 +422,8 @@ static spmv_status_t plan_pn(spmv_plan_s* h, const std::vector<int64_t>& rp, con
     std::vector<spmvb::PnPanelData> pd;
     spmvb::PnPlanStats st;
     std::string why;
-    if (!spmvb::plan_panel(rp, pcol, pval, ranges, xs, target, pd, st, why, &xcols, sms)) return SPMV_OK;
+    if (!spmvb::plan_panel(rp, pcol, pval, ranges, xs, target, pd, st, why, xcols.empty() ? nullptr : &xcols, sms))
+        return SPMV_OK;
     if (st.entries != h->nnz_loc)
         return fail(SPMV_ERR_INTERNAL, "panel plan lost nonzeros (%lld of %lld)", (long long)st.entries,
                     (long long)h->nnz_loc);
@@ -428,9 +441,29 @@ static spmv_status_t plan_pn(spmv_plan_s* h, const std::vector<int64_t>& rp, con
     if ((s = dalloc(h, &h->d_pn_gbase4, G))) return s;
     {
         std::vector<uint16_t> r2s(std::max<int64_t>(h->m_loc, 1), 0);
-        for (int64_t p = 0; p < P; ++p)
+        std::vector<int32_t> sf, sc;
+        std::vector<uint16_t> ss;
+        for (int64_t p = 0; p < P; ++p) {
             std::copy(pd[p].row2slot.begin(), pd[p].row2slot.end(), r2s.begin() + pd[p].desc.row0);
+            desc[p].split_off = (int32_t)sf.size();
+            desc[p].nslots = pd[p].nslots;
+            const int32_t base = (int32_t)ss.size();
+            for (size_t k = 0; k < pd[p].split_first.size(); ++k) {
+                sf.push_back(base + pd[p].split_first[k]);   // absolute index into split_slots
+                sc.push_back(pd[p].split_cnt[k]);
+            }
+            ss.insert(ss.end(), pd[p].split_slots.begin(), pd[p].split_slots.end());
+        }
         if ((s = upload(h, &h->d_pn_r2s, r2s.data(), r2s.size()))) return s;
+        if (sf.empty()) {
+            sf.push_back(0);
+            sc.push_back(0);
+            ss.push_back(0);
+        }
+        if ((s = upload(h, &h->d_pn_split_first, sf.data(), sf.size()))) return s;
+        if ((s = upload(h, &h->d_pn_split_cnt, sc.data(), sc.size()))) return s;
+        if ((s = upload(h, &h->d_pn_split_slots, ss.data(), ss.size()))) return s;
+        CUDA_TRY(cudaMemcpy(h->d_pn_panel, desc.data(), P * sizeof(spmvb::PnPanel), cudaMemcpyHostToDevice));
     }
     for (int64_t p = 0; p < P; ++p) {
         spmvb::PnPanelData& D = pd[p];
@@ -448,7 +481,7 @@ static spmv_status_t plan_pn(spmv_plan_s* h, const std::vector<int64_t>& rp, con
     }
     h->pn_panels = P;
     h->pn_max_rows = 0;
-    for (int64_t p = 0; p < P; ++p) h->pn_max_rows = std::max(h->pn_max_rows, (desc[p].nrows + 15) & ~15);
+    for (int64_t p = 0; p < P; ++p) h->pn_max_rows = std::max(h->pn_max_rows, (pd[p].nslots + 15) & ~15);
     h->pn_groups = G;
     h->pn_pad = st.pads;
     h->bytes_stream = (12 * 32 + 4) * G + 8 * h->m_loc;
@@ -878,9 +911,10 @@ static spmv_status_t create_impl(int64_t m, int64_t n, int64_t nnz, const int64_
     {
         const char* kenv = getenv("SPMV_KERNEL");
         const bool sb = blocks && h->kind == SPMV_SB && nnz_loc > 0;
+        const bool generic = nnz_loc > 0 && world == 1;   // any matrix: panels of consecutive rows
         if (sb && kenv && strcmp(kenv, "xstage") == 0) {
             if ((s = plan_xs(h, rp, pcol, pval, rbp, cbp))) return s;
-        } else if (sb && (!kenv || strcmp(kenv, "panel") == 0)) {
+        } else if ((sb || generic) && (!kenv || strcmp(kenv, "panel") == 0)) {
             if ((s = plan_pn(h, rp, pcol, pval, rbp, cbp))) return s;
         }
     }
@@ -1042,6 +1076,9 @@ static spmv_status_t run(spmv_handle_t h, const double* x, double* y, uint32_t f
         X.maxabs_slots = A.maxabs_slots;
         X.max_rows = h->pn_max_rows;
         X.row2slot = h->d_pn_r2s;
+        X.split_first = h->d_pn_split_first;
+        X.split_cnt = h->d_pn_split_cnt;
+        X.split_slots = h->d_pn_split_slots;
         CUDA_TRY(spmvb::launch_panel(X, st));
     } else if (!split && h->kernel == 6) {
         spmvb::XsArgs X{};

@@ -161,8 +161,15 @@ struct PnPanel {
     int32_t ne;        // epochs
     int32_t pf_col;    // x_lo[pf_col, pf_col + pf_len) is prefetched into L2 at panel start
     int32_t pf_len;    //   (a slice of the next block's interior columns, SB Eq.(1))
-    int32_t pad0, pad1;
+    int32_t split_off; // first entry of this panel in PnArgs::split_first / split_cnt
+    int32_t nslots;    // y slots (virtual rows) of the panel
 };
+#ifndef SPMV_PN_VMAX
+#define SPMV_PN_VMAX 16
+#endif
+constexpr int kPnSplitAt = 32;               // a row with more nonzeros is split into interleaved
+constexpr int kPnVMax = SPMV_PN_VMAX;        // virtual rows of <= kPnVMax nonzeros (own y slots,
+                                             // folded in order in the epilogue)
 
 struct PnArgs {
     const PnPanel* panel;
@@ -178,7 +185,11 @@ struct PnArgs {
     unsigned long long* maxabs_slots;
     int32_t max_rows;         // largest panel's y slots (a multiple of 16); slot max_rows is the padding
                               // lanes' scratch; shared memory = 8 * (max_rows + 1) bytes (the rest stays L1)
-    const uint16_t* row2slot; // [local rows] y slot of each row within its panel (bank colouring)
+    const uint16_t* row2slot; // [local rows] y slot of each row within its panel (bank colouring), or
+                              // 0x8000 | k: row split into virtual rows, see split_*
+    const int32_t* split_first;   // [split rows] first entry in split_slots (absolute)
+    const int32_t* split_cnt;     // [split rows] virtual rows of the row
+    const uint16_t* split_slots;  // slots of the virtual rows, in fold order
     int32_t pf_epochs;        // epochs of the group stream prefetched into L2 ahead (0 = default)
 };
 cudaError_t launch_panel(const PnArgs& a, cudaStream_t s);

@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
     const int p = blockIdx.x;
     const PnPanel d = A.panel[p];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    for (int i = tid; i < ((d.nrows + 15) & ~15); i += kT) ys[i] = 0.0;   // the panel's slots
+    for (int i = tid; i < ((d.nslots + 15) & ~15); i += kT) ys[i] = 0.0;   // the panel's y slots
     __syncthreads();
 
     const uint64_t pol = pol_evict_first();
@@ -209,6 +209,15 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
         for (int k = 0; k < EB; ++k) sl[k] = r2s[min(i0 + k * kT, nrl - 1)];
     };
     load_slots(tid);
+    // y of a row: its slot, or the in-order sum of its virtual rows' slots
+    auto fold = [&](uint16_t q) -> double {
+        if (q < 0x8000) return ys[q];
+        const int k = d.split_off + (q & 0x7FFF);
+        const int f = A.split_first[k], c = A.split_cnt[k];
+        double v = 0.0;
+        for (int j = 0; j < c; ++j) v += ys[A.split_slots[f + j]];
+        return v;
+    };
     __syncthreads();
 
     double mx = 0.0;
@@ -218,7 +227,7 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
         for (int k = 0; k < EB; ++k) {
             const int i = i0 + k * kT;
             if (i < nrl) {
-                const double v = ys[sl[k]];
+                const double v = fold(sl[k]);
                 A.y[d.row0 + i] = v;
                 mx = fmax(mx, fabs(v));
             }
@@ -247,7 +256,7 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel2_kernel(const PnArgs A) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     double* gr = sm2 + ((A.max_rows + 2) & ~1) + warp * G * 32;
     const uint32_t gr_s = (uint32_t)__cvta_generic_to_shared(gr) + lane * 8;
-    for (int i = tid; i < ((d.nrows + 15) & ~15); i += kT) ys[i] = 0.0;   // the panel's slots
+    for (int i = tid; i < ((d.nslots + 15) & ~15); i += kT) ys[i] = 0.0;   // the panel's y slots
     __syncthreads();
 
     const uint64_t pol = pol_evict_first();
@@ -329,7 +338,14 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel2_kernel(const PnArgs A) {
 
     double mx = 0.0;
     for (int i = tid; i < d.nrows; i += kT) {
-        const double v = ys[A.row2slot[d.row0 + i]];
+        const uint16_t q = A.row2slot[d.row0 + i];
+        double v = 0.0;
+        if (q < 0x8000) {
+            v = ys[q];
+        } else {
+            const int k = d.split_off + (q & 0x7FFF);
+            for (int j = 0; j < A.split_cnt[k]; ++j) v += ys[A.split_slots[A.split_first[k] + j]];
+        }
         A.y[d.row0 + i] = v;
         mx = fmax(mx, fabs(v));
     }
@@ -406,7 +422,7 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel3_kernel(const PnArgs A) {
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
-    for (int i = tid; i < ((d.nrows + 15) & ~15); i += kT) ys[i] = 0.0;   // the panel's slots
+    for (int i = tid; i < ((d.nslots + 15) & ~15); i += kT) ys[i] = 0.0;   // the panel's y slots
     __syncthreads();
     if (tid == 0) {
         for (int e = 0; e < NS; ++e) load_epoch(e);
@@ -468,7 +484,14 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel3_kernel(const PnArgs A) {
 
     double mx = 0.0;
     for (int i = tid; i < d.nrows; i += kT) {
-        const double v = ys[A.row2slot[d.row0 + i]];
+        const uint16_t q = A.row2slot[d.row0 + i];
+        double v = 0.0;
+        if (q < 0x8000) {
+            v = ys[q];
+        } else {
+            const int k = d.split_off + (q & 0x7FFF);
+            for (int j = 0; j < A.split_cnt[k]; ++j) v += ys[A.split_slots[A.split_first[k] + j]];
+        }
         A.y[d.row0 + i] = v;
         mx = fmax(mx, fabs(v));
     }

@@ -28,6 +28,7 @@
 #include "plan_panel.h"
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <omp.h>
@@ -196,14 +197,28 @@ void emit_group(const Ent* e, int32_t base, const std::vector<int32_t>& slot, Pn
 
 void build_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col, const std::vector<double>& val,
                  int64_t x_split, PnPanelData& P) {
-    const int64_t r0 = P.desc.row0, nr = P.desc.nrows;
-    const int64_t a = rp[r0], n = rp[r0 + nr] - a;
+    const int64_t r0 = P.desc.row0, nrr = P.desc.nrows;
+    const int64_t a = rp[r0], n = rp[r0 + nrr] - a;
+    // virtual rows: a row with L > kPnVMax nonzeros gets ceil(L / kPnVMax)
+    // interleaved virtual rows (its j-th nonzero in column order goes to
+    // virtual row j mod nv), so no epoch needs more than one nonzero of it
+    // per virtual row; the epilogue folds them in order.
+    std::vector<int32_t> vbase(nrr + 1), vcount(nrr);
+    vbase[0] = 0;
+    for (int64_t r = 0; r < nrr; ++r) {
+        const int64_t L = rp[r0 + r + 1] - rp[r0 + r];
+        vcount[r] = L > kPnSplitAt ? (int32_t)((L + kPnVMax - 1) / kPnVMax) : 1;
+        vbase[r + 1] = vbase[r] + vcount[r];
+    }
+    const int64_t nr = vbase[nrr];   // virtual rows = y slots
+    P.nslots = (int32_t)nr;
     std::vector<Ent> ents(n);
     std::vector<uint64_t> keys(n);
-    for (int64_t r = 0; r < nr; ++r)
+    for (int64_t r = 0; r < nrr; ++r)
         for (int64_t e = rp[r0 + r]; e < rp[r0 + r + 1]; ++e) {
             const int64_t i = e - a;
-            ents[i] = {(int32_t)r, col[e], val[e]};
+            const int32_t vr = vbase[r] + (int32_t)((e - rp[r0 + r]) % vcount[r]);
+            ents[i] = {vr, col[e], val[e]};
             // rotated sweep: panels of one block start at different columns, so
             // concurrently running CTAs do not all hit the same x lines (L2 slices)
             keys[i] = ((uint64_t)((uint32_t)col[e] - (uint32_t)P.rot) << 32) | (uint64_t)i;
@@ -262,6 +277,12 @@ void build_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col
             em.close();
             ++ng;
         }
+        if (getenv("SPMV_PN_DEBUG") && P.desc.row0 == 0) {
+            int64_t filled = 0;
+            for (int64_t q = (int64_t)gents.size() - 32 * ng; q < (int64_t)gents.size(); ++q) filled += gents[q].row >= 0;
+            fprintf(stderr, "epoch %d: groups %d entries %lld deferred-queue %zu pos %lld/%lld\n", epoch, ng,
+                    (long long)filled, deferred.size(), (long long)pos, (long long)n);
+        }
         while (ng < kPnEpoch) {   // all-dummy groups complete the epoch
             em.close();
             ++ng;
@@ -274,6 +295,7 @@ void build_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col
     std::vector<int32_t> slot;
     std::vector<int32_t> ident(nr);
     for (int32_t r = 0; r < (int32_t)nr; ++r) ident[r] = r;
+    if (nr > 0x7FFF) return;   // caller rejects the plan (slot field)
     {   // statistics: natural slots
         PnPanelData tmp;
         double w = 0;
@@ -283,12 +305,25 @@ void build_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col
         }
         P.ywf0 = G ? w / G : 0;
     }
+    std::vector<uint16_t> v2s;
     if (getenv("SPMV_PN_NOCOLOUR")) {
-        P.row2slot.resize(nr);
-        for (int32_t r = 0; r < (int32_t)nr; ++r) P.row2slot[r] = (uint16_t)r;
+        v2s.resize(nr);
+        for (int32_t r = 0; r < (int32_t)nr; ++r) v2s[r] = (uint16_t)r;
         slot = ident;
     } else {
-        colour_slots((int32_t)nr, gents, G, P.row2slot, slot);
+        colour_slots((int32_t)nr, gents, G, v2s, slot);
+    }
+    // real rows -> slot, or -> split entry (virtual rows' slots in fold order)
+    P.row2slot.resize(nrr);
+    for (int64_t r = 0; r < nrr; ++r) {
+        if (vcount[r] == 1) {
+            P.row2slot[r] = v2s[vbase[r]];
+        } else {
+            P.row2slot[r] = (uint16_t)(0x8000 | P.split_first.size());
+            P.split_first.push_back((int32_t)P.split_slots.size());
+            P.split_cnt.push_back(vcount[r]);
+            for (int32_t j = 0; j < vcount[r]; ++j) P.split_slots.push_back(v2s[vbase[r] + j]);
+        }
     }
     double w = 0;
     for (int64_t g = 0; g < G; ++g) {
@@ -312,12 +347,31 @@ bool plan_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col,
     out.clear();
     st = PnPlanStats{};
     const int64_t R = std::min<int64_t>(std::max<int64_t>(rows_target, 1), kPnRowsMax);
+    auto slots_of = [&](int64_t r) -> int64_t {
+        const int64_t L = rp[r + 1] - rp[r];
+        return L > kPnSplitAt ? (L + kPnVMax - 1) / kPnVMax : 1;
+    };
     for (size_t k = 0; k < ranges.size(); ++k) {
         const auto& rg = ranges[k];
         const int64_t L = rg.second - rg.first;
         if (L <= 0) continue;
-        int64_t np = (L + R - 1) / R;
-        while ((L + np - 1) / np > kPnRowsMax) ++np;
+        // panel boundaries: about R y slots (virtual rows) per panel
+        int64_t S = 0;
+        for (int64_t r = rg.first; r < rg.second; ++r) S += slots_of(r);
+        int64_t np = (S + R - 1) / R;
+        std::vector<int64_t> cut(1, rg.first);
+        {
+            int64_t acc = 0, pi = 1;
+            for (int64_t r = rg.first; r < rg.second && pi < np; ++r) {
+                acc += slots_of(r);
+                if (acc >= S * pi / np) {
+                    cut.push_back(r + 1);
+                    ++pi;
+                }
+            }
+            cut.push_back(rg.second);
+            np = (int64_t)cut.size() - 1;
+        }
         // L2 prefetch slice: the interior columns of the range that starts about
         // one wave after this one (its panels then find x in L2), cut in np pieces
         int64_t pf0 = 0, pf1 = 0;
@@ -327,9 +381,11 @@ bool plan_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col,
             pf1 = (*xcols)[k + ahead].second;
         }
         for (int64_t p = 0; p < np; ++p) {
-            const int64_t a = rg.first + L * p / np, e = rg.first + L * (p + 1) / np;
-            if (e - a > (int64_t(1) << kPnRowBits) - 1) {
-                why = "panel rows beyond the packed row field";
+            const int64_t a = cut[p], e = cut[p + 1];
+            int64_t ps = 0;
+            for (int64_t r = a; r < e; ++r) ps += slots_of(r);
+            if (ps > kPnRowsMax || ps > (int64_t(1) << kPnRowBits) - 1) {
+                why = "panel y slots beyond shared memory / the packed slot field (a very long row)";
                 return false;
             }
             if (rp[e] - rp[a] >= (int64_t(1) << 32)) {
@@ -397,14 +453,23 @@ bool verify_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& co
             if (P.gbase4[(ep * kPnWarps + w) * kPnB + b] != P.gbase[g]) e = "gbase4 is not the (epoch, warp, step) order of gbase";
         }
         std::vector<std::vector<std::pair<int32_t, double>>> got(d.nrows);
-        std::vector<int32_t> stamp(d.nrows, -1);
-        const int32_t nsl = ((d.nrows + 15) / 16) * 16;
+        const int32_t nsl = ((P.nslots + 15) / 16) * 16;
+        std::vector<int32_t> stamp(nsl, -1);
         std::vector<int32_t> row_of_slot(nsl, -1);
         if ((int32_t)P.row2slot.size() != d.nrows) e = "row2slot size";
+        auto own = [&](int32_t sl, int32_t r) {
+            if (sl >= nsl || row_of_slot[sl] != -1) e = "slot map is not injective into the panel's slots";
+            else row_of_slot[sl] = r;
+        };
         for (int32_t r = 0; r < d.nrows && e.empty(); ++r) {
             const int32_t sl = P.row2slot[r];
-            if (sl >= nsl || row_of_slot[sl] != -1) e = "row2slot is not injective into the panel's slots";
-            else row_of_slot[sl] = r;
+            if (sl < 0x8000) {
+                own(sl, r);
+            } else {
+                const int32_t k = sl & 0x7FFF;
+                if (k >= (int32_t)P.split_first.size()) { e = "split index out of range"; break; }
+                for (int32_t j = 0; j < P.split_cnt[k] && e.empty(); ++j) own(P.split_slots[P.split_first[k] + j], r);
+            }
         }
         for (int64_t ep = 0; ep < d.ne && e.empty(); ++ep)
             for (int k = 0; k < kPnEpoch && e.empty(); ++k) {
@@ -422,8 +487,8 @@ bool verify_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& co
                     const int64_t c = (int64_t)base + (i & ((1u << kPnDeltaBits) - 1));
                     if (sl >= nsl || row_of_slot[sl] < 0) { e = "slot outside the panel"; break; }
                     const int32_t r = row_of_slot[sl];
-                    if (stamp[r] == ep) { e = "row repeated within an epoch"; break; }
-                    stamp[r] = (int32_t)ep;
+                    if (stamp[sl] == ep) { e = "y slot repeated within an epoch"; break; }
+                    stamp[sl] = (int32_t)ep;
                     const int sd = c >= x_split;
                     if (s >= 0 && sd != s) { e = "group mixes both sides of x_split"; break; }
                     s = sd;

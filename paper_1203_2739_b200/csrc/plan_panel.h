@@ -15,7 +15,11 @@ struct PnPanelData {
     std::vector<int32_t> gbase;    // [groups]
     std::vector<int32_t> gbase4;   // [groups] the same bases in (epoch, warp, step) order: one 16-byte
                                    // load gives a warp the bases of its kPnB groups of an epoch
-    std::vector<uint16_t> row2slot; // [nrows] shared-memory y slot of each panel row (bank colouring)
+    std::vector<uint16_t> row2slot; // [nrows] y slot of each panel row (bank colouring), or 0x8000 | k for a
+                                    // row split into virtual rows: split_* entry k of this panel
+    std::vector<int32_t> split_first, split_cnt;   // per split row: its virtual rows' slots in split_slots
+    std::vector<uint16_t> split_slots;
+    int32_t nslots = 0;             // y slots used (virtual rows), before rounding to 16
     int64_t entries = 0, pads = 0, deferred = 0;
     int32_t rot = 0;               // the column sweep starts at this column (wraps around)
     double ywf0 = 0, ywf1 = 0;     // predicted y wavefronts per group access: natural slots / coloured
