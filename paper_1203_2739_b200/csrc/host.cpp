@@ -911,7 +911,9 @@ static spmv_status_t create_impl(int64_t m, int64_t n, int64_t nnz, const int64_
     {
         const char* kenv = getenv("SPMV_KERNEL");
         const bool sb = blocks && h->kind == SPMV_SB && nnz_loc > 0;
-        const bool generic = nnz_loc > 0 && world == 1;   // any matrix: panels of consecutive rows
+        // any matrix at world 1: panels of consecutive rows -- measured slower than the
+        // row-tile kernel on C4 (0.274 vs 0.259 ms), so opt-in only (SPMV_KERNEL=panel)
+        const bool generic = nnz_loc > 0 && world == 1 && kenv && strcmp(kenv, "panel") == 0;
         if (sb && kenv && strcmp(kenv, "xstage") == 0) {
             if ((s = plan_xs(h, rp, pcol, pval, rbp, cbp))) return s;
         } else if ((sb || generic) && (!kenv || strcmp(kenv, "panel") == 0)) {
