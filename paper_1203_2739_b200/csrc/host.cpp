@@ -127,6 +127,8 @@ struct spmv_plan_s {
     int32_t* d_pn_split_first = nullptr;
     int32_t* d_pn_split_cnt = nullptr;
     uint16_t* d_pn_split_slots = nullptr;
+    int32_t* d_pn_split_row = nullptr;
+    int32_t pn_max_sslots = 0;
     int64_t pn_panels = 0, pn_groups = 0, pn_pad = 0;
     int32_t pn_max_rows = 0;
     int32_t* d_tile_seg = nullptr;    // [T*K+1]
@@ -441,16 +443,22 @@ static spmv_status_t plan_pn(spmv_plan_s* h, const std::vector<int64_t>& rp, con
     if ((s = dalloc(h, &h->d_pn_gbase4, G))) return s;
     {
         std::vector<uint16_t> r2s(std::max<int64_t>(h->m_loc, 1), 0);
-        std::vector<int32_t> sf, sc;
+        std::vector<int32_t> sf, sc, sr;
         std::vector<uint16_t> ss;
+        h->pn_max_sslots = 0;
         for (int64_t p = 0; p < P; ++p) {
             std::copy(pd[p].row2slot.begin(), pd[p].row2slot.end(), r2s.begin() + pd[p].desc.row0);
             desc[p].split_off = (int32_t)sf.size();
             desc[p].nslots = pd[p].nslots;
             const int32_t base = (int32_t)ss.size();
+            desc[p].split_n = (int32_t)pd[p].split_first.size();
+            desc[p].sslot0 = base;
+            desc[p].sslot_n = (int32_t)pd[p].split_slots.size();
+            h->pn_max_sslots = std::max(h->pn_max_sslots, desc[p].sslot_n);
             for (size_t k = 0; k < pd[p].split_first.size(); ++k) {
                 sf.push_back(base + pd[p].split_first[k]);   // absolute index into split_slots
                 sc.push_back(pd[p].split_cnt[k]);
+                sr.push_back(pd[p].split_row[k]);
             }
             ss.insert(ss.end(), pd[p].split_slots.begin(), pd[p].split_slots.end());
         }
@@ -458,8 +466,10 @@ static spmv_status_t plan_pn(spmv_plan_s* h, const std::vector<int64_t>& rp, con
         if (sf.empty()) {
             sf.push_back(0);
             sc.push_back(0);
+            sr.push_back(0);
             ss.push_back(0);
         }
+        if ((s = upload(h, &h->d_pn_split_row, sr.data(), sr.size()))) return s;
         if ((s = upload(h, &h->d_pn_split_first, sf.data(), sf.size()))) return s;
         if ((s = upload(h, &h->d_pn_split_cnt, sc.data(), sc.size()))) return s;
         if ((s = upload(h, &h->d_pn_split_slots, ss.data(), ss.size()))) return s;
@@ -1081,6 +1091,8 @@ static spmv_status_t run(spmv_handle_t h, const double* x, double* y, uint32_t f
         X.split_first = h->d_pn_split_first;
         X.split_cnt = h->d_pn_split_cnt;
         X.split_slots = h->d_pn_split_slots;
+        X.split_row = h->d_pn_split_row;
+        X.max_sslots = h->pn_max_sslots;
         CUDA_TRY(spmvb::launch_panel(X, st));
     } else if (!split && h->kernel == 6) {
         spmvb::XsArgs X{};

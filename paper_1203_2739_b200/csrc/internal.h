@@ -161,8 +161,12 @@ struct PnPanel {
     int32_t ne;        // epochs
     int32_t pf_col;    // x_lo[pf_col, pf_col + pf_len) is prefetched into L2 at panel start
     int32_t pf_len;    //   (a slice of the next block's interior columns, SB Eq.(1))
-    int32_t split_off; // first entry of this panel in PnArgs::split_first / split_cnt
+    int32_t split_off; // first entry of this panel in PnArgs::split_first / split_cnt / split_row
     int32_t nslots;    // y slots (virtual rows) of the panel
+    int32_t split_n;   // rows of the panel split into virtual rows
+    int32_t sslot0;    // their virtual rows' slots: split_slots[sslot0, sslot0 + sslot_n)
+    int32_t sslot_n;
+    int32_t pad0;
 };
 #ifndef SPMV_PN_VMAX
 #define SPMV_PN_VMAX 16
@@ -190,6 +194,8 @@ struct PnArgs {
     const int32_t* split_first;   // [split rows] first entry in split_slots (absolute)
     const int32_t* split_cnt;     // [split rows] virtual rows of the row
     const uint16_t* split_slots;  // slots of the virtual rows, in fold order
+    const int32_t* split_row;     // [split rows] panel-local row
+    int32_t max_sslots;           // largest sslot_n over the panels (shared-memory copy)
     int32_t pf_epochs;        // epochs of the group stream prefetched into L2 ahead (0 = default)
 };
 cudaError_t launch_panel(const PnArgs& a, cudaStream_t s);

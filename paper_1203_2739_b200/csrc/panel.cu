@@ -81,6 +81,11 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
     const PnPanel d = A.panel[p];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     for (int i = tid; i < ((d.nslots + 15) & ~15); i += kT) ys[i] = 0.0;   // the panel's y slots
+    // virtual-row slot lists of the panel's split rows, copied to shared memory
+    // once (the epilogue folds them by warps)
+    uint16_t* ssl = reinterpret_cast<uint16_t*>(ys + A.max_rows + 1);
+    if (MODE == 0)
+        for (int i = tid; i < d.sslot_n; i += kT) ssl[i] = A.split_slots[d.sslot0 + i];
     __syncthreads();
 
     const uint64_t pol = pol_evict_first();
@@ -209,15 +214,6 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
         for (int k = 0; k < EB; ++k) sl[k] = r2s[min(i0 + k * kT, nrl - 1)];
     };
     load_slots(tid);
-    // y of a row: its slot, or the in-order sum of its virtual rows' slots
-    auto fold = [&](uint16_t q) -> double {
-        if (q < 0x8000) return ys[q];
-        const int k = d.split_off + (q & 0x7FFF);
-        const int f = A.split_first[k], c = A.split_cnt[k];
-        double v = 0.0;
-        for (int j = 0; j < c; ++j) v += ys[A.split_slots[f + j]];
-        return v;
-    };
     __syncthreads();
 
     double mx = 0.0;
@@ -226,11 +222,25 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
 #pragma unroll
         for (int k = 0; k < EB; ++k) {
             const int i = i0 + k * kT;
-            if (i < nrl) {
-                const double v = fold(sl[k]);
+            if (i < nrl && sl[k] < 0x8000) {        // split rows: below
+                const double v = ys[sl[k]];
                 A.y[d.row0 + i] = v;
                 mx = fmax(mx, fabs(v));
             }
+        }
+    }
+    // rows split into virtual rows: one warp each, lanes sum strided slots,
+    // fixed xor tree (deterministic order)
+    for (int k = warp; k < d.split_n; k += NW) {
+        const int e = d.split_off + k;
+        const int f = A.split_first[e] - d.sslot0, c = A.split_cnt[e];
+        double v = 0.0;
+        for (int j = lane; j < c; j += 32) v += ys[ssl[f + j]];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        if (lane == 0) {
+            A.y[d.row0 + A.split_row[e]] = v;
+            mx = fmax(mx, fabs(v));
         }
     }
     if (A.maxabs_slots) {
@@ -511,7 +521,8 @@ cudaError_t launch_panel(const PnArgs& a, cudaStream_t s) {
     static int mode = -1, pf_env = 0;
     // only the panel's y in shared memory: the rest of the 256 KB L1/shared
     // array stays L1, which holds the global loads in flight
-    const size_t smem = (size_t)(a.max_rows + 1) * sizeof(double);   // + the padding lanes' scratch slot
+    const size_t smem = (size_t)(a.max_rows + 1) * sizeof(double)     // + the padding lanes' scratch slot
+                        + (((size_t)a.max_sslots * 2 + 15) & ~size_t(15));   // split rows' slot lists
     if (mode < 0) {
         const char* e = getenv("SPMV_PN_MODE");   // ablations for measurements only
         mode = e ? atoi(e) : 0;

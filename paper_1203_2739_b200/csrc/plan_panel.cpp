@@ -322,6 +322,7 @@ void build_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col
             P.row2slot[r] = (uint16_t)(0x8000 | P.split_first.size());
             P.split_first.push_back((int32_t)P.split_slots.size());
             P.split_cnt.push_back(vcount[r]);
+            P.split_row.push_back((int32_t)r);
             for (int32_t j = 0; j < vcount[r]; ++j) P.split_slots.push_back(v2s[vbase[r] + j]);
         }
     }

@@ -18,6 +18,7 @@ struct PnPanelData {
     std::vector<uint16_t> row2slot; // [nrows] y slot of each panel row (bank colouring), or 0x8000 | k for a
                                     // row split into virtual rows: split_* entry k of this panel
     std::vector<int32_t> split_first, split_cnt;   // per split row: its virtual rows' slots in split_slots
+    std::vector<int32_t> split_row;                // per split row: its panel-local row
     std::vector<uint16_t> split_slots;
     int32_t nslots = 0;             // y slots used (virtual rows), before rounding to 16
     int64_t entries = 0, pads = 0, deferred = 0;
