@@ -230,6 +230,24 @@ def spmv_xs_plan_check(m: int, n: int, row_ptr, col, val, blocks, rows_target: i
     return dict(zip(("panels", "groups_i", "groups_b", "pad_i", "pad_b", "entries"), (int(v) for v in stats)))
 
 
+class _Shard(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_int64) for k in (
+        "block_begin", "block_end", "row_begin", "row_end", "x_interior_begin", "x_interior_len",
+        "x_border_begin", "x_border_len", "x_local_len", "border_begin", "border_total")]
+
+
+def spmv_shard_plan(blocks, m: int, n: int, rank: int, world: int) -> dict:
+    """Host-side SB shard plan of rank `rank` of `world` (see spmv.h)."""
+    rbp = _np(blocks["row_block_ptr"], np.int64)
+    cbp = _np(blocks["col_block_ptr"], np.int64)
+    bop = _np(blocks.get("border_owner_ptr"), np.int64)
+    b = _Blocks(int(blocks["kind"]), int(blocks["K"]), rbp.ctypes.data, cbp.ctypes.data,
+                None if bop is None else bop.ctypes.data)
+    out = _Shard()
+    _check(lib().spmv_shard_plan(ctypes.byref(b), m, n, rank, world, ctypes.byref(out)), "spmv_shard_plan")
+    return {k: int(getattr(out, k)) for k, _ in _Shard._fields_}
+
+
 def spmv_pn_plan_check(m: int, n: int, row_ptr, col, val, blocks, rows_target: int) -> dict:
     """Host-only round trip of the column-sorted panel planner (see spmv.h); raises on mismatch."""
     rp = _np(row_ptr, np.int64)

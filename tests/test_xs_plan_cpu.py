@@ -88,3 +88,36 @@ def test_panel_plan_random_sb_odd_blocks():
     m, n, rp, col, val, blocks = _random_sb(7, 4, [37, 600, 1201, 90], [1, 2047, 2049, 5001], 333, 0.01, 0.01)
     st = sp.spmv_pn_plan_check(m, n, rp, col, val, blocks, 400)
     assert st["entries"] == len(col)
+
+
+@pytest.mark.parametrize("world,rank", [(2, 0), (2, 1), (4, 3)])
+def test_panel_plan_rank_local_layout(world, rank):
+    """A rank's shard at world > 1: rows of its SB blocks, columns in the local
+    layout [interior columns | full C_B] (host.cpp), border columns read from
+    the exchange buffer -- so no group may mix the two sides (x_split = C_B's
+    local start).  Built from the scrambled C5 stand-in through the shard plan."""
+    p = synth.make("c5s")
+    sh = sp.spmv_shard_plan(p.blocks, p.m, p.n, rank, world)
+    rp_g, col_g, val_g = synth_permuted(p)
+    r0, r1 = sh["row_begin"], sh["row_end"]
+    q0, nint, b0 = sh["x_interior_begin"], sh["x_interior_len"], sh["border_begin"]
+    a, b = int(rp_g[r0]), int(rp_g[r1])
+    rp = rp_g[r0:r1 + 1] - a
+    c = col_g[a:b].astype(np.int64)
+    loc = np.where(c >= b0, nint + (c - b0), c - q0).astype(np.int32)
+    assert loc.min() >= 0 and loc.max() < nint + sh["border_total"]
+    k0, k1 = sh["block_begin"], sh["block_end"]
+    rbp, cbp = p.blocks["row_block_ptr"], p.blocks["col_block_ptr"]
+    K = k1 - k0
+    blocks = {"kind": 1, "K": K,
+              "row_block_ptr": np.array([rbp[k] - r0 for k in range(k0, k1 + 1)] + [r1 - r0], dtype=np.int64),
+              "col_block_ptr": np.array([cbp[k] - q0 for k in range(k0, k1 + 1)] + [nint + sh["border_total"]],
+                                        dtype=np.int64)}
+    st = sp.spmv_pn_plan_check(r1 - r0, nint + sh["border_total"], rp, loc, val_g[a:b], blocks, 1500)
+    assert st["entries"] == b - a
+
+
+def synth_permuted(p):
+    import oracle
+    rp, col, val, _ = oracle.permute(p.m, p.n, p.row_ptr, p.col, p.val, p.row_perm, p.col_perm)
+    return rp, col, val
