@@ -1,33 +1,34 @@
-// rowtile.cu -- the default single-SpMxV kernel y^ = A^ x^: one CTA
-// of 512 threads per row tile of <= 2048 nonzeros, launched in tile order.
+// rowtile.cu -- the row-tile single-SpMxV kernel y^ = A^ x^: the
+// default for matrices without an SB descriptor (C1, C4) and the fallback
+// when the panel plan pads too much (panel.cu is the SB default).  One CTA
+// of 256 threads per row tile of <= 2048 nonzeros, launched in tile order.
 //
-// Why this shape (measured on B200): the x gathers are the
-// binding limit (~1 lane-request per clock per SM through the LSU,
-// scripts/gather_modes.py), so the kernel maximises independent gathers in
-// flight: 3 CTAs x 512 threads per SM, one 128-bit quad of (col, val) per
-// thread, no per-tile pipeline barriers beyond one __syncthreads.  The
-// hardware block scheduler issues tiles in order, so all SMs sweep the rows
-// together and the live x footprint is one SB block's x(C_k) + x(C_B)
-// (Eq.(1)) -- L2-resident, the paper's "fits into the cache"
-// condition with the 126 MB L2 as the cache.  (A persistent schedule
-// with static tile strides let CTAs drift and overflowed L2: 4.7x the
-// algorithmic DRAM bytes on C5.)
+// Why this shape (measured on B200): row-ordered x gathers
+// cost one L1TEX wavefront per nonzero (~1 line per SM clock), so the kernel
+// keeps as many independent gathers in flight as it can: 6 CTAs x 256
+// threads per SM, 2 quads of (col, val) per thread, all loads and gathers
+// issued without branches, one __syncthreads per tile.  The hardware block
+// scheduler issues tiles in order, so all SMs sweep the rows together and the
+// live x footprint is one SB block's x(C_k) + x(C_B) (Eq.(1)) --
+// L2-resident, the paper's "fits into the cache" condition with the
+// 126 MB L2 as the cache.
 //
 // Per tile:
-//   1. thread q loads quad q of the tile's col/val (positions 4q..4q+3 from
-//      the 16-byte aligned a & ~3), L1 no-allocate + L2 evict-first (the
-//      matrix is read once), gathers x[col] through the read-only path
-//      (x is the reused operand) and stages the products in shared
-//      memory; the tile's row pointers are staged alongside;
+//   1. each thread loads 128-bit quads of the tile's col/val (positions from
+//      the 16-byte aligned a & ~3; quads past the tile end clamped to a valid
+//      one), L1 no-allocate + L2 evict-first (the matrix is read once,
+//      P:L47); gathers x[col] with L1 no-allocate + L2 evict-last (x is the
+//      reused operand); masks the products outside the tile and
+//      stages them in shared memory; the tile's row pointers alongside;
 //   2. tiles whose rows all have <= 32 nonzeros: vector-per-row, V lanes per
-//      row (V = 1..32 chosen per tile at plan time so that rows x V fills the
-//      CTA; V = 1 is the paper's serial per-row temporary); lane j
-//      sums positions j, j+V, ... of its row, then a fixed xor-shuffle tree;
-//      other tiles: thread-per-row for rows <= 32, warp-per-row (fixed lane
-//      assignment and tree) for longer rows;
-//   3. y is stored coalesced; max |y| is folded per CTA (one atomicMax).
-// Rows longer than a tile get a tile of their own: all 512 threads stream
-// the row with a fixed assignment and a fixed tree.
+//      row (V = 1..32 chosen per tile at plan time; V = 1 is the paper's
+//      serial per-row temporary); lane j sums positions j, j+V, ...
+//      of its row, then a fixed xor-shuffle tree; other tiles: thread-per-row
+//      for rows <= 32, warp-per-row (fixed lane assignment and tree) for
+//      longer rows;
+//   3. y is stored coalesced; max |y| is folded per warp (one atomicMax).
+// Rows longer than a tile get a tile of their own (CTA-per-row class): all
+// threads stream the row with a fixed assignment and a fixed tree.
 #include <cstdint>
 #include <cuda_runtime.h>
 
