@@ -467,8 +467,9 @@ def run_ours(args, rank, world, local_rank):
                        "l2": ("flushed (512 MB write) before every SpMxV; step time = SpMxV time" if l2_flush
                               else f"inputs larger than L2 ({bytes_tot / 1e9:.1f} GB vs 126 MB)"),
                        "parallelism": f"sb-rowblock{world}" if world > 1 else "1gpu",
-                       "kernel": {7: "panel (column-sorted, y in shared memory)", 0: "row-tile"}.get(info["kernel"],
-                                                                                                      str(info["kernel"]))},
+                       "kernel": ("fused multiple-SpMxV (row-major part segments)" if split else
+                                  {7: "panel (column-sorted, y in shared memory)", 0: "row-tile"}.get(
+                                      info["kernel"], str(info["kernel"])))},
             "hbm_gbs": bytes_tot / (avg_spmv_max * 1e-3) / 1e9,
             "spmv_ms": avg_spmv_max,
             "roofline": roofline,

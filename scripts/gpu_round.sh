@@ -1,8 +1,5 @@
 set -x
+mkdir -p gpurun_out
 python -m paper_1203_2739_b200.build > /dev/null
-timeout 600 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
-python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
-SPMV_KERNEL=panel timeout 300 python -m pytest tests/test_gpu_parity.py -q -x -k "spmv_parity or edge" 2>&1 | tail -2
-cd scripts
-timeout 300 python ab.py c4 panel,rowtile
-K=16 KERNELS=panel timeout 300 python xs_probe.py 2>&1 | grep -E '"panel_ms"'
+for w in c4 c3 c2 c1; do timeout 300 python bench.py --workload $w --no-e2e > gpurun_out/r53_bench_$w.json 2> gpurun_out/r53_bench_$w.err; python -c "import json;d=json.load(open('gpurun_out/r53_bench_$w.json'));print('$w', d['value'], d['spmv_ms'], d['roofline']['frac'], d['config'].get('kernel'), d['parity']['failures'])"; done
+cd scripts && timeout 300 python c3_split.py > ../gpurun_out/r53_c3_split.json 2>&1; cat ../gpurun_out/r53_c3_split.json
