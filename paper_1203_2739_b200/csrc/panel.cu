@@ -540,6 +540,7 @@ cudaError_t launch_panel(const PnArgs& a, cudaStream_t s) {
 #endif
         if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<0, 16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
         if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<0, kDefD, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
+        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<0, 8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
 #if SPMV_PN_B == 4
         if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<0, 20, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
 #endif
@@ -597,6 +598,7 @@ cudaError_t launch_panel(const PnArgs& a, cudaStream_t s) {
     case 7: spmv_panel2_kernel<8><<<b.n_panels, kT, smem2(8), s>>>(b); break;
     case 8: spmv_panel2_kernel<12><<<b.n_panels, kT, smem2(12), s>>>(b); break;
     case 21: spmv_panel_kernel<0><<<b.n_panels, kT, smem, s>>>(b); break;   // previous default (16, 8)
+    case 22: spmv_panel_kernel<0, 8, 4><<<b.n_panels, kT, smem, s>>>(b); break;
     default: spmv_panel_kernel<0, kDefD, 4><<<b.n_panels, kT, smem, s>>>(b);
     }
     return cudaGetLastError();
