@@ -128,7 +128,7 @@ struct spmv_plan_s {
     int32_t* d_pn_split_cnt = nullptr;
     uint16_t* d_pn_split_slots = nullptr;
     int32_t* d_pn_split_row = nullptr;
-    int32_t pn_max_sslots = 0;
+    int32_t pn_max_sslots = 0, pn_max_split_n = 0;
     int64_t pn_panels = 0, pn_groups = 0, pn_pad = 0;
     int32_t pn_max_rows = 0;
     int32_t* d_tile_seg = nullptr;    // [T*K+1]
@@ -446,6 +446,7 @@ static spmv_status_t plan_pn(spmv_plan_s* h, const std::vector<int64_t>& rp, con
         std::vector<int32_t> sf, sc, sr;
         std::vector<uint16_t> ss;
         h->pn_max_sslots = 0;
+        h->pn_max_split_n = 0;
         for (int64_t p = 0; p < P; ++p) {
             std::copy(pd[p].row2slot.begin(), pd[p].row2slot.end(), r2s.begin() + pd[p].desc.row0);
             desc[p].split_off = (int32_t)sf.size();
@@ -455,6 +456,7 @@ static spmv_status_t plan_pn(spmv_plan_s* h, const std::vector<int64_t>& rp, con
             desc[p].sslot0 = base;
             desc[p].sslot_n = (int32_t)pd[p].split_slots.size();
             h->pn_max_sslots = std::max(h->pn_max_sslots, desc[p].sslot_n);
+            h->pn_max_split_n = std::max(h->pn_max_split_n, desc[p].split_n);
             for (size_t k = 0; k < pd[p].split_first.size(); ++k) {
                 sf.push_back(base + pd[p].split_first[k]);   // absolute index into split_slots
                 sc.push_back(pd[p].split_cnt[k]);
@@ -921,9 +923,9 @@ static spmv_status_t create_impl(int64_t m, int64_t n, int64_t nnz, const int64_
     {
         const char* kenv = getenv("SPMV_KERNEL");
         const bool sb = blocks && h->kind == SPMV_SB && nnz_loc > 0;
-        // any matrix at world 1: panels of consecutive rows -- measured slower than the
-        // row-tile kernel on C4 (0.274 vs 0.259 ms), so opt-in only (SPMV_KERNEL=panel)
-        const bool generic = nnz_loc > 0 && world == 1 && kenv && strcmp(kenv, "panel") == 0;
+        // any matrix at world 1: panels of consecutive rows (C4: 0.231 vs 0.259 ms for the
+        // row-tile kernel); small matrices fall back to row tiles through the padding test
+        const bool generic = nnz_loc > 0 && world == 1;
         if (sb && kenv && strcmp(kenv, "xstage") == 0) {
             if ((s = plan_xs(h, rp, pcol, pval, rbp, cbp))) return s;
         } else if ((sb || generic) && (!kenv || strcmp(kenv, "panel") == 0)) {
@@ -1093,6 +1095,7 @@ static spmv_status_t run(spmv_handle_t h, const double* x, double* y, uint32_t f
         X.split_slots = h->d_pn_split_slots;
         X.split_row = h->d_pn_split_row;
         X.max_sslots = h->pn_max_sslots;
+        X.max_split_n = h->pn_max_split_n;
         CUDA_TRY(spmvb::launch_panel(X, st));
     } else if (!split && h->kernel == 6) {
         spmvb::XsArgs X{};

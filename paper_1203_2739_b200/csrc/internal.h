@@ -196,6 +196,7 @@ struct PnArgs {
     const uint16_t* split_slots;  // slots of the virtual rows, in fold order
     const int32_t* split_row;     // [split rows] panel-local row
     int32_t max_sslots;           // largest sslot_n over the panels (shared-memory copy)
+    int32_t max_split_n;          // largest split_n over the panels (shared-memory copy of the descriptors)
     int32_t pf_epochs;        // epochs of the group stream prefetched into L2 ahead (0 = default)
 };
 cudaError_t launch_panel(const PnArgs& a, cudaStream_t s);

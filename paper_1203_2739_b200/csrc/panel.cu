@@ -84,8 +84,16 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
     // virtual-row slot lists of the panel's split rows, copied to shared memory
     // once (the epilogue folds them by warps)
     uint16_t* ssl = reinterpret_cast<uint16_t*>(ys + A.max_rows + 1);
-    if (MODE == 0)
+    int32_t* sdesc = reinterpret_cast<int32_t*>(ssl + ((A.max_sslots + 7) & ~7));   // (first, count, row) per split row
+    if (MODE == 0) {
         for (int i = tid; i < d.sslot_n; i += kT) ssl[i] = A.split_slots[d.sslot0 + i];
+        for (int i = tid; i < d.split_n; i += kT) {
+            const int e = d.split_off + i;
+            sdesc[3 * i] = A.split_first[e] - d.sslot0;
+            sdesc[3 * i + 1] = A.split_cnt[e];
+            sdesc[3 * i + 2] = A.split_row[e];
+        }
+    }
     __syncthreads();
 
     const uint64_t pol = pol_evict_first();
@@ -232,14 +240,13 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
     // rows split into virtual rows: one warp each, lanes sum strided slots,
     // fixed xor tree (deterministic order)
     for (int k = warp; k < d.split_n; k += NW) {
-        const int e = d.split_off + k;
-        const int f = A.split_first[e] - d.sslot0, c = A.split_cnt[e];
+        const int f = sdesc[3 * k], c = sdesc[3 * k + 1];
         double v = 0.0;
         for (int j = lane; j < c; j += 32) v += ys[ssl[f + j]];
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
         if (lane == 0) {
-            A.y[d.row0 + A.split_row[e]] = v;
+            A.y[d.row0 + sdesc[3 * k + 2]] = v;
             mx = fmax(mx, fabs(v));
         }
     }
@@ -522,7 +529,8 @@ cudaError_t launch_panel(const PnArgs& a, cudaStream_t s) {
     // only the panel's y in shared memory: the rest of the 256 KB L1/shared
     // array stays L1, which holds the global loads in flight
     const size_t smem = (size_t)(a.max_rows + 1) * sizeof(double)     // + the padding lanes' scratch slot
-                        + (((size_t)a.max_sslots * 2 + 15) & ~size_t(15));   // split rows' slot lists
+                        + (size_t)((a.max_sslots + 7) & ~7) * 2           // split rows' slot lists
+                        + (size_t)a.max_split_n * 12;                     // and their (first, count, row)
     if (mode < 0) {
         const char* e = getenv("SPMV_PN_MODE");   // ablations for measurements only
         mode = e ? atoi(e) : 0;

@@ -1,7 +1,12 @@
 set -x
-mkdir -p gpurun_out
 python -m paper_1203_2739_b200.build > /dev/null
-timeout 600 python -m pytest tests -m gpu -q > gpurun_out/r60_pytest.log 2>&1; tail -2 gpurun_out/r60_pytest.log
-python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
-timeout 900 python bench.py > gpurun_out/r60_bench.json 2> gpurun_out/r60_bench.err; tail -1 gpurun_out/r60_bench.err; cat gpurun_out/r60_bench.json
-for w in c4 c3 c2 c1; do timeout 300 python bench.py --workload $w > gpurun_out/r60_bench_$w.json 2> gpurun_out/r60_bench_$w.err; python -c "import json;d=json.load(open('gpurun_out/r60_bench_$w.json'));print('$w', d['value'], d['spmv_ms'], d['roofline']['frac'], d['parity']['failures'], d['e2e']['value'], d.get('reordering',{}).get('speedup'), d.get('warm_l2_spmv_ms'))"; done
+timeout 600 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
+cd scripts
+timeout 300 python ab.py c4 panel
+SPMV_LIB=/root/repo/ablib/vmax8.so timeout 300 python ab.py c4 panel | sed "s/^/vmax8 /"
+SPMV_LIB=/root/repo/ablib/vmax32.so timeout 300 python ab.py c4 panel | sed "s/^/vmax32 /"
+for w in c1 c2 c4; do python -c "
+import os,sys; sys.path.insert(0,'..')
+import synth, paper_1203_2739_b200 as sp
+p=synth.make('$w'); h=sp.spmv_create(p.m,p.n,p.row_ptr,p.col,p.val,row_perm=p.row_perm,col_perm=p.col_perm,blocks=p.blocks)
+i=sp.spmv_get_info(h); print('$w kernel', i['kernel'], 'panels', i['xs_panels'], 'pad', i['xs_pad_slots'], 'groups', i['xs_groups'])"; done
