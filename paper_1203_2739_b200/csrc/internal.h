@@ -169,7 +169,7 @@ struct PnPanel {
     int32_t pad0;
 };
 #ifndef SPMV_PN_VMAX
-#define SPMV_PN_VMAX 16
+#define SPMV_PN_VMAX 32
 #endif
 constexpr int kPnSplitAt = 32;               // a row with more nonzeros is split into interleaved
 constexpr int kPnVMax = SPMV_PN_VMAX;        // virtual rows of <= kPnVMax nonzeros (own y slots,
