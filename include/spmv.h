@@ -165,9 +165,10 @@ typedef struct {
     int64_t bytes_stream;         /* device bytes the apply kernel actually reads + writes (no x reuse) */
     int32_t n_parts, rank, world, kind;
     int32_t has_owner_map;        /* spmv_normalize is available */
-    int32_t kernel;               /* single-SpMxV kernel: 7 column-sorted panels (default for SB handles
-                                     whose plan pads < 25 %), 0 row-tile (default otherwise); the others
-                                     are measurement variants (SPMV_KERNEL environment variable) */
+    int32_t kernel;               /* single-SpMxV kernel: 7 column-sorted panels (default: SB handles at
+                                     any world size, any matrix at world 1, when the plan pads < 25 %),
+                                     0 row-tile (otherwise); the others are measurement variants
+                                     (SPMV_KERNEL environment variable at create) */
     int32_t reserved[2];
 } spmv_info_t;
 
