@@ -1,7 +1,8 @@
-"""GPU parity of the single-SpMxV kernel variants selectable with SPMV_KERNEL
-(measurement A/B switches) against the CPU oracle: the row-tile family
-(rowtile.cu: quad and lane-consecutive streaming, 128/256/512-thread CTAs),
-rowseg, pipe and the first tile kernel.  Integer data: bit-exact; real data:
+"""GPU parity of the single-SpMxV kernels selectable with SPMV_KERNEL against
+the CPU oracle: the panel kernel forced onto small matrices (panel.cu; c4s
+has rows of up to 3,000 nonzeros -> virtual rows and warp folds), the
+row-tile family (rowtile.cu: quad and lane-consecutive streaming,
+128/256/512-thread CTAs), rowseg, pipe and the first tile kernel.  Integer data: bit-exact; real data:
 the north_star tolerance."""
 import pytest
 
@@ -12,7 +13,8 @@ from gpu_util import assert_parity, create, gpu_apply, oracle_permuted
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
-VARIANTS = {"rowtile": 0, "pipe": 1, "tile": 2, "rowtile512": 3, "rowseg": 4, "rowtile128": 5, "rowlin": 8}
+VARIANTS = {"rowtile": 0, "pipe": 1, "tile": 2, "rowtile512": 3, "rowseg": 4, "rowtile128": 5, "rowlin": 8,
+            "panel": 7}
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -26,6 +28,7 @@ def cuda():
 @pytest.mark.parametrize("name,variant", [("c4s", "int"), ("c5s", "int"), ("c4s", "real"), ("c1", "dyadic")])
 def test_variant_parity(monkeypatch, kernel, name, variant):
     monkeypatch.setenv("SPMV_KERNEL", kernel)
+    monkeypatch.setenv("SPMV_PN_ROWS", "2000")   # panel: several panels, c4s's long rows become virtual rows
     p = synth.make(name, variant=variant)
     x = p.x()
     xh, yh_ref, S = oracle_permuted(p, x)
