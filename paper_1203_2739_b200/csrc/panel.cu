@@ -74,7 +74,6 @@ __device__ __forceinline__ int32_t ld_base(const int32_t* p) {
 template <int MODE, int KD_ = kD, int KGD_ = 8>
 __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
     constexpr int kD = KD_;                              // groups in flight per warp
-    constexpr bool kMain = MODE == 0 || MODE == 23;      // the production code paths (bases by 16 bytes, ...)
     constexpr int kGD = MODE == 5 ? 4 : KGD_;            // gathers issued this many steps ahead
     static_assert(kD % kGD == 0 && kD % kPnB == 0, "ring geometry");
     extern __shared__ __align__(16) double ys[];
@@ -86,7 +85,7 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
     // once (the epilogue folds them by warps)
     uint16_t* ssl = reinterpret_cast<uint16_t*>(ys + A.max_rows + 1);
     int32_t* sdesc = reinterpret_cast<int32_t*>(ssl + ((A.max_sslots + 7) & ~7));   // (first, count, row) per split row
-    {   // all modes: the epilogue folds split rows from these copies
+    if (MODE == 0) {
         for (int i = tid; i < d.sslot_n; i += kT) ssl[i] = A.split_slots[d.sslot0 + i];
         for (int i = tid; i < d.split_n; i += kT) {
             const int e = d.split_off + i;
@@ -111,14 +110,14 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
     // one 16-byte load per epoch gives the warp the bases of its kPnB groups
     // (slots u..u+3 of the ring; the bases of u+1..u+3 it replaces were last
     // used by gathers issued >= 1 step earlier, since kGD >= kPnB)
-    static_assert(!kMain || kGD >= 4, "base quad overwrites bases still needed");
+    static_assert(MODE != 0 || kGD >= 4, "base quad overwrites bases still needed");
     static_assert(kPnB % 4 == 0, "bases are loaded four at a time");
     const int4* gb4 = reinterpret_cast<const int4*>(A.gbase4 + d.g0);
     auto load = [&](int t, double& v, uint32_t& i, int32_t& b) {
         const int64_t g = gw + 16 * (int64_t)t;
         v = ld_val(A.gval + g * 32 + lane, pol);
         i = ld_u32(A.gidx + g * 32 + lane, pol);
-        if (!kMain) b = ld_base(A.gbase + g);
+        if (MODE != 0) b = ld_base(A.gbase + g);
     };
     auto load_b4 = [&](int t, int32_t& b0, int32_t& b1, int32_t& b2, int32_t& b3) {   // t % 4 == 0
         int4 q;
@@ -157,7 +156,7 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
                          : "memory");
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.gidx + g * 32), "r"(kPnEpoch * 32 * 4)
                          : "memory");
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"((kMain ? A.gbase4 : A.gbase) + g),
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"((MODE == 0 ? A.gbase4 : A.gbase) + g),
                          "r"(kPnEpoch * 4) : "memory");
         }
     };
@@ -179,56 +178,17 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
 #pragma unroll
     for (int u = 0; u < kD; ++u) {
         if (u < T) load(u, rv[u], ri[u], rb[u]);
-        if (kMain && u % 4 == 0 && u < T) load_b4(u, rb[u], rb[u + 1], rb[u + 2], rb[u + 3]);
+        if (MODE == 0 && u % 4 == 0 && u < T) load_b4(u, rb[u], rb[u + 1], rb[u + 2], rb[u + 3]);
     }
 #pragma unroll
     for (int u = 0; u < kGD; ++u)
         if (u < T) rx[u] = gather(ri[u], rb[u]);
 
-    // MODE 23: split-phase epochs -- a warp arrives on an mbarrier after its
-    // last y update of an epoch and waits for the epoch to complete only
-    // before its first y update of the next one; its loads and gathers are
-    // issued in between
-    __shared__ __align__(8) uint64_t ebar[2];
-    if (MODE == 23) {
-        if (tid == 0) {
-            asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(&ebar[0])), "r"(NW));
-            asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(&ebar[1])), "r"(NW));
-        }
-        __syncthreads();
-    }
     for (int t0 = 0; t0 < T; t0 += kD) {
 #pragma unroll
         for (int u = 0; u < kD; ++u) {
             const int t = t0 + u;
             if (t >= T) break;
-            if (MODE == 23) {
-                const double v = rv[u], xv = rx[u % kGD];
-                const uint32_t i = ri[u];
-                if (t + kD < T) {
-                    load(t + kD, rv[u], ri[u], rb[u]);
-                    if (u % 4 == 0) load_b4(t + kD, rb[u], rb[(u + 1) % kD], rb[(u + 2) % kD], rb[(u + 3) % kD]);
-                }
-                if (t + kGD < T) rx[u % kGD] = gather(ri[(u + kGD) % kD], rb[(u + kGD) % kD]);
-                const int e = t / kPnB;
-                if (u % kPnB == 0 && e > 0) {   // epoch e-1 complete in every warp
-                    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&ebar[(e - 1) & 1]);
-                    const uint32_t par = (uint32_t)(((e - 1) >> 1) & 1);
-                    asm volatile("{\n.reg .pred q;\nEW: mbarrier.try_wait.parity.shared::cta.b64 q, [%0], %1;\n@!q bra EW;\n}"
-                                 ::"r"(bar), "r"(par) : "memory");
-                }
-                int r = (int)(i >> kPnDeltaBits);
-                r = r == (int)(kPnDummy >> kPnDeltaBits) ? scratch : r;
-                ys[r] = fma(v, xv, ys[r]);
-                if (u % kPnB == kPnB - 1) {
-                    __syncwarp();
-                    if (lane == 0)
-                        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
-                                         (uint32_t)__cvta_generic_to_shared(&ebar[e & 1])) : "memory");
-                    prefetch_epoch(e + PF);
-                }
-                continue;
-            }
             const uint32_t i = ri[u];
             if (MODE == 2) {
                 racc = fma(rv[u], rx[u % kGD], racc);
@@ -239,7 +199,7 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
             }
             if (t + kD < T) {
                 load(t + kD, rv[u], ri[u], rb[u]);
-                if (kMain && u % 4 == 0)
+                if (MODE == 0 && u % 4 == 0)
                     load_b4(t + kD, rb[u], rb[(u + 1) % kD], rb[(u + 2) % kD], rb[(u + 3) % kD]);
             }
             if (t + kGD < T) rx[u % kGD] = gather(ri[(u + kGD) % kD], rb[(u + kGD) % kD]);
@@ -589,7 +549,6 @@ cudaError_t launch_panel(const PnArgs& a, cudaStream_t s) {
         if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<0, 16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
         if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<0, kDefD, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
         if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<0, 8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
-        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<23, kDefD, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
 #if SPMV_PN_B == 4
         if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<0, 20, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
 #endif
@@ -648,7 +607,6 @@ cudaError_t launch_panel(const PnArgs& a, cudaStream_t s) {
     case 8: spmv_panel2_kernel<12><<<b.n_panels, kT, smem2(12), s>>>(b); break;
     case 21: spmv_panel_kernel<0><<<b.n_panels, kT, smem, s>>>(b); break;   // previous default (16, 8)
     case 22: spmv_panel_kernel<0, 8, 4><<<b.n_panels, kT, smem, s>>>(b); break;
-    case 23: spmv_panel_kernel<23, kDefD, 4><<<b.n_panels, kT, smem, s>>>(b); break;
     default: spmv_panel_kernel<0, kDefD, 4><<<b.n_panels, kT, smem, s>>>(b);
     }
     return cudaGetLastError();
