@@ -74,6 +74,23 @@ struct DevBuf {
 
 }  // namespace
 
+struct PanelPlan {
+    spmvb::PnPanel* d_panel = nullptr;
+    double* d_gval = nullptr;
+    uint32_t* d_gidx = nullptr;
+    int32_t* d_gbase = nullptr;
+    int32_t* d_gbase4 = nullptr;
+    uint16_t* d_r2s = nullptr;        // [m_loc] y slot of each row in its panel (or split entry)
+    int32_t* d_split_first = nullptr;
+    int32_t* d_split_cnt = nullptr;
+    uint16_t* d_split_slots = nullptr;
+    int32_t* d_split_row = nullptr;
+    int32_t max_sslots = 0, max_split_n = 0;
+    int64_t panels = 0, groups = 0, pad = 0;
+    int32_t max_rows = 0;
+    bool ok() const { return panels > 0; }
+};
+
 struct spmv_plan_s {
     uint32_t magic = kMagic;
     int device = 0;
@@ -117,20 +134,9 @@ struct spmv_plan_s {
     int32_t xs_cbits = 0;
     int64_t xs_panels = 0, xs_groups = 0, xs_pad = 0, xs_gb = 0;
     int64_t bytes_stream = 0;
-    // column-sorted panel kernel (panel.cu)
-    spmvb::PnPanel* d_pn_panel = nullptr;
-    double* d_pn_gval = nullptr;
-    uint32_t* d_pn_gidx = nullptr;
-    int32_t* d_pn_gbase = nullptr;
-    int32_t* d_pn_gbase4 = nullptr;
-    uint16_t* d_pn_r2s = nullptr;     // [m_loc] y slot of each row in its panel (or split entry)
-    int32_t* d_pn_split_first = nullptr;
-    int32_t* d_pn_split_cnt = nullptr;
-    uint16_t* d_pn_split_slots = nullptr;
-    int32_t* d_pn_split_row = nullptr;
-    int32_t pn_max_sslots = 0, pn_max_split_n = 0;
-    int64_t pn_panels = 0, pn_groups = 0, pn_pad = 0;
-    int32_t pn_max_rows = 0;
+    // column-sorted panel kernel (panel.cu): single SpMxV, and the fused
+    // multiple-SpMxV over (row, part) virtual rows
+    PanelPlan pn, pns;
     int32_t* d_tile_seg = nullptr;    // [T*K+1]
     int32_t* d_seg_ptr = nullptr;     // [S+1]
     int32_t* d_seg_row = nullptr;     // [S]
@@ -381,9 +387,10 @@ static spmv_status_t plan_xs(spmv_plan_s* h, const std::vector<int64_t>& rp, con
 
 // Builds and uploads the column-sorted panel kernel's plan (plan_panel.cpp).
 // Leaves the handle on the row-tile kernel when the plan would be poor.
-static spmv_status_t plan_pn(spmv_plan_s* h, const std::vector<int64_t>& rp, const std::vector<int32_t>& pcol,
-                             const std::vector<double>& pval, const std::vector<int64_t>& rbp,
-                             const std::vector<int64_t>& cbp) {
+static spmv_status_t plan_pn(spmv_plan_s* h, PanelPlan& pl, const std::vector<int64_t>& rp,
+                             const std::vector<int32_t>& pcol, const std::vector<double>& pval,
+                             const std::vector<int64_t>& rbp, const std::vector<int64_t>& cbp,
+                             const std::vector<int32_t>* part) {
     const int K = (int)rbp.size() - 2;
     const int64_t R0 = h->row_begin, R1 = h->row_begin + h->m_loc;
     std::vector<std::pair<int64_t, int64_t>> ranges, xcols;
@@ -399,11 +406,7 @@ static spmv_status_t plan_pn(spmv_plan_s* h, const std::vector<int64_t>& rp, con
     } else {   // no SB structure: panels of consecutive rows, no x prefetch / rotation
         ranges.push_back({0, h->m_loc});
     }
-    int64_t total_slots = 0;
-    for (int64_t r = 0; r < h->m_loc; ++r) {
-        const int64_t L = rp[r + 1] - rp[r];
-        total_slots += L > spmvb::kPnSplitAt ? (L + spmvb::kPnVMax - 1) / spmvb::kPnVMax : 1;
-    }
+    const int64_t total_slots = spmvb::panel_total_slots(rp, h->m_loc, part);
     // panels: about kPnRowsMax rows, their count a multiple of the SM count
     // when possible (whole waves of one CTA per SM)
     const int64_t sms = spmvb::kernel_num_sms();
@@ -424,7 +427,7 @@ static spmv_status_t plan_pn(spmv_plan_s* h, const std::vector<int64_t>& rp, con
     std::vector<spmvb::PnPanelData> pd;
     spmvb::PnPlanStats st;
     std::string why;
-    if (!spmvb::plan_panel(rp, pcol, pval, ranges, xs, target, pd, st, why, xcols.empty() ? nullptr : &xcols, sms))
+    if (!spmvb::plan_panel(rp, pcol, pval, ranges, xs, target, pd, st, why, xcols.empty() ? nullptr : &xcols, sms, part))
         return SPMV_OK;
     if (st.entries != h->nnz_loc)
         return fail(SPMV_ERR_INTERNAL, "panel plan lost nonzeros (%lld of %lld)", (long long)st.entries,
@@ -436,17 +439,17 @@ static spmv_status_t plan_pn(spmv_plan_s* h, const std::vector<int64_t>& rp, con
     std::vector<spmvb::PnPanel> desc(P);
     for (int64_t p = 0; p < P; ++p) desc[p] = pd[p].desc;
     spmv_status_t s;
-    if ((s = upload(h, &h->d_pn_panel, desc.data(), P))) return s;
-    if ((s = dalloc(h, &h->d_pn_gval, G * 32))) return s;
-    if ((s = dalloc(h, &h->d_pn_gidx, G * 32))) return s;
-    if ((s = dalloc(h, &h->d_pn_gbase, G))) return s;
-    if ((s = dalloc(h, &h->d_pn_gbase4, G))) return s;
+    if ((s = upload(h, &pl.d_panel, desc.data(), P))) return s;
+    if ((s = dalloc(h, &pl.d_gval, G * 32))) return s;
+    if ((s = dalloc(h, &pl.d_gidx, G * 32))) return s;
+    if ((s = dalloc(h, &pl.d_gbase, G))) return s;
+    if ((s = dalloc(h, &pl.d_gbase4, G))) return s;
     {
         std::vector<uint16_t> r2s(std::max<int64_t>(h->m_loc, 1), 0);
         std::vector<int32_t> sf, sc, sr;
         std::vector<uint16_t> ss;
-        h->pn_max_sslots = 0;
-        h->pn_max_split_n = 0;
+        pl.max_sslots = 0;
+        pl.max_split_n = 0;
         for (int64_t p = 0; p < P; ++p) {
             std::copy(pd[p].row2slot.begin(), pd[p].row2slot.end(), r2s.begin() + pd[p].desc.row0);
             desc[p].split_off = (int32_t)sf.size();
@@ -455,8 +458,8 @@ static spmv_status_t plan_pn(spmv_plan_s* h, const std::vector<int64_t>& rp, con
             desc[p].split_n = (int32_t)pd[p].split_first.size();
             desc[p].sslot0 = base;
             desc[p].sslot_n = (int32_t)pd[p].split_slots.size();
-            h->pn_max_sslots = std::max(h->pn_max_sslots, desc[p].sslot_n);
-            h->pn_max_split_n = std::max(h->pn_max_split_n, desc[p].split_n);
+            pl.max_sslots = std::max(pl.max_sslots, desc[p].sslot_n);
+            pl.max_split_n = std::max(pl.max_split_n, desc[p].split_n);
             for (size_t k = 0; k < pd[p].split_first.size(); ++k) {
                 sf.push_back(base + pd[p].split_first[k]);   // absolute index into split_slots
                 sc.push_back(pd[p].split_cnt[k]);
@@ -464,40 +467,42 @@ static spmv_status_t plan_pn(spmv_plan_s* h, const std::vector<int64_t>& rp, con
             }
             ss.insert(ss.end(), pd[p].split_slots.begin(), pd[p].split_slots.end());
         }
-        if ((s = upload(h, &h->d_pn_r2s, r2s.data(), r2s.size()))) return s;
+        if ((s = upload(h, &pl.d_r2s, r2s.data(), r2s.size()))) return s;
         if (sf.empty()) {
             sf.push_back(0);
             sc.push_back(0);
             sr.push_back(0);
             ss.push_back(0);
         }
-        if ((s = upload(h, &h->d_pn_split_row, sr.data(), sr.size()))) return s;
-        if ((s = upload(h, &h->d_pn_split_first, sf.data(), sf.size()))) return s;
-        if ((s = upload(h, &h->d_pn_split_cnt, sc.data(), sc.size()))) return s;
-        if ((s = upload(h, &h->d_pn_split_slots, ss.data(), ss.size()))) return s;
-        CUDA_TRY(cudaMemcpy(h->d_pn_panel, desc.data(), P * sizeof(spmvb::PnPanel), cudaMemcpyHostToDevice));
+        if ((s = upload(h, &pl.d_split_row, sr.data(), sr.size()))) return s;
+        if ((s = upload(h, &pl.d_split_first, sf.data(), sf.size()))) return s;
+        if ((s = upload(h, &pl.d_split_cnt, sc.data(), sc.size()))) return s;
+        if ((s = upload(h, &pl.d_split_slots, ss.data(), ss.size()))) return s;
+        CUDA_TRY(cudaMemcpy(pl.d_panel, desc.data(), P * sizeof(spmvb::PnPanel), cudaMemcpyHostToDevice));
     }
     for (int64_t p = 0; p < P; ++p) {
         spmvb::PnPanelData& D = pd[p];
         const int64_t g0 = D.desc.g0, ng = (int64_t)D.gbase.size();
         if (ng) {
-            CUDA_TRY(cudaMemcpy(h->d_pn_gval + g0 * 32, D.gval.data(), ng * 32 * 8, cudaMemcpyHostToDevice));
-            CUDA_TRY(cudaMemcpy(h->d_pn_gidx + g0 * 32, D.gidx.data(), ng * 32 * 4, cudaMemcpyHostToDevice));
-            CUDA_TRY(cudaMemcpy(h->d_pn_gbase + g0, D.gbase.data(), ng * 4, cudaMemcpyHostToDevice));
-            CUDA_TRY(cudaMemcpy(h->d_pn_gbase4 + g0, D.gbase4.data(), ng * 4, cudaMemcpyHostToDevice));
+            CUDA_TRY(cudaMemcpy(pl.d_gval + g0 * 32, D.gval.data(), ng * 32 * 8, cudaMemcpyHostToDevice));
+            CUDA_TRY(cudaMemcpy(pl.d_gidx + g0 * 32, D.gidx.data(), ng * 32 * 4, cudaMemcpyHostToDevice));
+            CUDA_TRY(cudaMemcpy(pl.d_gbase + g0, D.gbase.data(), ng * 4, cudaMemcpyHostToDevice));
+            CUDA_TRY(cudaMemcpy(pl.d_gbase4 + g0, D.gbase4.data(), ng * 4, cudaMemcpyHostToDevice));
         }
         std::vector<double>().swap(D.gval);
         std::vector<uint32_t>().swap(D.gidx);
         std::vector<int32_t>().swap(D.gbase);
         std::vector<int32_t>().swap(D.gbase4);
     }
-    h->pn_panels = P;
-    h->pn_max_rows = 0;
-    for (int64_t p = 0; p < P; ++p) h->pn_max_rows = std::max(h->pn_max_rows, (pd[p].nslots + 15) & ~15);
-    h->pn_groups = G;
-    h->pn_pad = st.pads;
-    h->bytes_stream = (12 * 32 + 4) * G + 8 * h->m_loc;
-    h->kernel = 7;
+    pl.panels = P;
+    pl.max_rows = 0;
+    for (int64_t p = 0; p < P; ++p) pl.max_rows = std::max(pl.max_rows, (pd[p].nslots + 15) & ~15);
+    pl.groups = G;
+    pl.pad = st.pads;
+    if (!part) {
+        h->bytes_stream = (12 * 32 + 4) * G + 8 * h->m_loc;
+        h->kernel = 7;
+    }
     return SPMV_OK;
 }
 
@@ -919,6 +924,11 @@ static spmv_status_t create_impl(int64_t m, int64_t n, int64_t nnz, const int64_
         if ((s = upload(h, &h->d_sval, sval.data(), nnz_loc, nnz_loc + kPad))) return s;
     }
 
+    // ---------------- fused multiple-SpMxV on panels (a8): (row, part) virtual rows
+    if (n_parts && world == 1 && nnz_loc > 0 && !getenv("SPMV_SPLIT_ROWTILE")) {
+        if ((s = plan_pn(h, h->pns, rp, pcol, pval, rbp, cbp, &ppart))) return s;
+    }
+
     // ------------------------------------ x-staged plan (SB handles, a5/a6)
     {
         const char* kenv = getenv("SPMV_KERNEL");
@@ -929,7 +939,7 @@ static spmv_status_t create_impl(int64_t m, int64_t n, int64_t nnz, const int64_
         if (sb && kenv && strcmp(kenv, "xstage") == 0) {
             if ((s = plan_xs(h, rp, pcol, pval, rbp, cbp))) return s;
         } else if ((sb || generic) && (!kenv || strcmp(kenv, "panel") == 0)) {
-            if ((s = plan_pn(h, rp, pcol, pval, rbp, cbp))) return s;
+            if ((s = plan_pn(h, h->pn, rp, pcol, pval, rbp, cbp, nullptr))) return s;
         }
     }
 
@@ -1032,6 +1042,23 @@ static spmv_status_t check_vectors(spmv_handle_t h, const double* x, int64_t x_l
     return SPMV_OK;
 }
 
+static void fill_pn_args(const PanelPlan& pl, spmvb::PnArgs& X) {
+    X.panel = pl.d_panel;
+    X.n_panels = (int32_t)pl.panels;
+    X.gval = pl.d_gval;
+    X.gidx = pl.d_gidx;
+    X.gbase = pl.d_gbase;
+    X.gbase4 = pl.d_gbase4;
+    X.max_rows = pl.max_rows;
+    X.row2slot = pl.d_r2s;
+    X.split_first = pl.d_split_first;
+    X.split_cnt = pl.d_split_cnt;
+    X.split_slots = pl.d_split_slots;
+    X.split_row = pl.d_split_row;
+    X.max_sslots = pl.max_sslots;
+    X.max_split_n = pl.max_split_n;
+}
+
 static spmv_status_t run(spmv_handle_t h, const double* x, double* y, uint32_t flags, cudaStream_t st,
                          bool split) {
     CUDA_TRY(cudaSetDevice(h->device));
@@ -1077,25 +1104,12 @@ static spmv_status_t run(spmv_handle_t h, const double* x, double* y, uint32_t f
     }
     if (!split && h->kernel == 7) {
         spmvb::PnArgs X{};
-        X.panel = h->d_pn_panel;
-        X.n_panels = (int32_t)h->pn_panels;
+        fill_pn_args(h->pn, X);
         X.x_split = A.x_split;
-        X.gval = h->d_pn_gval;
-        X.gidx = h->d_pn_gidx;
-        X.gbase = h->d_pn_gbase;
-        X.gbase4 = h->d_pn_gbase4;
         X.x_lo = A.x_lo;
         X.x_hi = A.x_hi;
         X.y = yk;
         X.maxabs_slots = A.maxabs_slots;
-        X.max_rows = h->pn_max_rows;
-        X.row2slot = h->d_pn_r2s;
-        X.split_first = h->d_pn_split_first;
-        X.split_cnt = h->d_pn_split_cnt;
-        X.split_slots = h->d_pn_split_slots;
-        X.split_row = h->d_pn_split_row;
-        X.max_sslots = h->pn_max_sslots;
-        X.max_split_n = h->pn_max_split_n;
         CUDA_TRY(spmvb::launch_panel(X, st));
     } else if (!split && h->kernel == 6) {
         spmvb::XsArgs X{};
@@ -1181,6 +1195,17 @@ static spmv_status_t run(spmv_handle_t h, const double* x, double* y, uint32_t f
                 if (h->kernel == 2) CUDA_TRY(spmvb::launch_tiles(B, true, xsplit, st));
                 else CUDA_TRY(spmvb::launch_split(B, xsplit, st));
             }
+        } else if (h->pns.ok() && h->kernel != 2) {
+            // fused multiple-SpMxV on column-sorted panels: each (row, part)
+            // segment accumulates in its own y slot, folded per row
+            spmvb::PnArgs X{};
+            fill_pn_args(h->pns, X);
+            X.x_split = A.x_split;
+            X.x_lo = A.x_lo;
+            X.x_hi = A.x_hi;
+            X.y = yk;
+            X.maxabs_slots = A.maxabs_slots;
+            CUDA_TRY(spmvb::launch_panel(X, st));
         } else if (h->split_rowmajor && h->kernel != 2 && !getenv("SPMV_SPLIT_PARTMAJOR")) {
             // fused multiple-SpMxV, row-major segments (split.cu spmv_split_rows_kernel)
             spmvb::RowTileArgs R{};
@@ -1239,9 +1264,9 @@ spmv_status_t spmv_get_info(spmv_handle_t h, spmv_info_t* info) {
     info->split_segments = h->n_seg;
     info->n_parts = h->n_parts; info->rank = h->rank; info->world = h->world; info->kind = h->kind;
     info->has_owner_map = h->has_owner ? 1 : 0;
-    info->xs_panels = h->kernel == 7 ? h->pn_panels : h->xs_panels;
-    info->xs_groups = h->kernel == 7 ? h->pn_groups : h->xs_groups;
-    info->xs_pad_slots = h->kernel == 7 ? h->pn_pad : h->xs_pad;
+    info->xs_panels = h->kernel == 7 ? h->pn.panels : h->xs_panels;
+    info->xs_groups = h->kernel == 7 ? h->pn.groups : h->xs_groups;
+    info->xs_pad_slots = h->kernel == 7 ? h->pn.pad : h->xs_pad;
     info->bytes_stream = h->bytes_stream;
     info->kernel = h->kernel;
     return SPMV_OK;

@@ -195,19 +195,58 @@ void emit_group(const Ent* e, int32_t base, const std::vector<int32_t>& slot, Pn
     P.pads += 32 - n;
 }
 
+// Virtual rows of row r.  Without a split: ceil(L / kPnVMax) interleaved
+// virtual rows when L > kPnSplitAt, else 1.  With a split (multiple-SpMxV,
+// P:L107-109): each part segment of the row (its nonzeros of part k, in
+// part order) gets its own virtual rows, split the same way by the segment's
+// length -- the per-(row, part) temporaries of reading A7, folded in part
+// order by the epilogue.  vr[j] (optional) receives the virtual row (relative
+// to the row's first) of the row's j-th nonzero.
+int32_t row_vrows(const int64_t* rp, const int32_t* part, int64_t r, int32_t* vr) {
+    const int64_t a = rp[r], L = rp[r + 1] - a;
+    auto nv_of = [](int64_t len) -> int32_t { return len > kPnSplitAt ? (int32_t)((len + kPnVMax - 1) / kPnVMax) : 1; };
+    if (!part) {
+        const int32_t nv = nv_of(L);
+        if (vr)
+            for (int64_t j = 0; j < L; ++j) vr[j] = (int32_t)(j % nv);
+        return std::max(nv, (int32_t)1);
+    }
+    if (L == 0) return 1;
+    // segments in part order: stable sort of the row's positions by part
+    int64_t idx_small[64];
+    std::vector<int64_t> idx_big;
+    int64_t* idx = idx_small;
+    if (L > 64) {
+        idx_big.resize(L);
+        idx = idx_big.data();
+    }
+    for (int64_t j = 0; j < L; ++j) idx[j] = j;
+    std::stable_sort(idx, idx + L, [&](int64_t u, int64_t v) { return part[a + u] < part[a + v]; });
+    int32_t total = 0;
+    for (int64_t s0 = 0; s0 < L;) {
+        int64_t s1 = s0;
+        while (s1 < L && part[a + idx[s1]] == part[a + idx[s0]]) ++s1;
+        const int32_t nv = nv_of(s1 - s0);
+        if (vr)
+            for (int64_t q = s0; q < s1; ++q) vr[idx[q]] = total + (int32_t)((q - s0) % nv);
+        total += nv;
+        s0 = s1;
+    }
+    return total;
+}
+
 void build_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col, const std::vector<double>& val,
-                 int64_t x_split, PnPanelData& P) {
+                 int64_t x_split, PnPanelData& P, const int32_t* part) {
     const int64_t r0 = P.desc.row0, nrr = P.desc.nrows;
     const int64_t a = rp[r0], n = rp[r0 + nrr] - a;
     // virtual rows: a row with L > kPnVMax nonzeros gets ceil(L / kPnVMax)
     // interleaved virtual rows (its j-th nonzero in column order goes to
     // virtual row j mod nv), so no epoch needs more than one nonzero of it
     // per virtual row; the epilogue folds them in order.
-    std::vector<int32_t> vbase(nrr + 1), vcount(nrr);
+    std::vector<int32_t> vbase(nrr + 1), vcount(nrr), evr(n);
     vbase[0] = 0;
     for (int64_t r = 0; r < nrr; ++r) {
-        const int64_t L = rp[r0 + r + 1] - rp[r0 + r];
-        vcount[r] = L > kPnSplitAt ? (int32_t)((L + kPnVMax - 1) / kPnVMax) : 1;
+        vcount[r] = row_vrows(rp.data(), part, r0 + r, evr.data() + (rp[r0 + r] - a));
         vbase[r + 1] = vbase[r] + vcount[r];
     }
     const int64_t nr = vbase[nrr];   // virtual rows = y slots
@@ -217,7 +256,7 @@ void build_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col
     for (int64_t r = 0; r < nrr; ++r)
         for (int64_t e = rp[r0 + r]; e < rp[r0 + r + 1]; ++e) {
             const int64_t i = e - a;
-            const int32_t vr = vbase[r] + (int32_t)((e - rp[r0 + r]) % vcount[r]);
+            const int32_t vr = vbase[r] + evr[i];
             ents[i] = {vr, col[e], val[e]};
             // rotated sweep: panels of one block start at different columns, so
             // concurrently running CTAs do not all hit the same x lines (L2 slices)
@@ -344,14 +383,13 @@ void build_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col
 bool plan_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col, const std::vector<double>& val,
                 const std::vector<std::pair<int64_t, int64_t>>& ranges, int64_t x_split, int64_t rows_target,
                 std::vector<PnPanelData>& out, PnPlanStats& st, std::string& why,
-                const std::vector<std::pair<int64_t, int64_t>>* xcols, int64_t pf_sms) {
+                const std::vector<std::pair<int64_t, int64_t>>* xcols, int64_t pf_sms,
+                const std::vector<int32_t>* part) {
     out.clear();
     st = PnPlanStats{};
     const int64_t R = std::min<int64_t>(std::max<int64_t>(rows_target, 1), kPnRowsMax);
-    auto slots_of = [&](int64_t r) -> int64_t {
-        const int64_t L = rp[r + 1] - rp[r];
-        return L > kPnSplitAt ? (L + kPnVMax - 1) / kPnVMax : 1;
-    };
+    const int32_t* pp = part ? part->data() : nullptr;
+    auto slots_of = [&](int64_t r) -> int64_t { return row_vrows(rp.data(), pp, r, nullptr); };
     for (size_t k = 0; k < ranges.size(); ++k) {
         const auto& rg = ranges[k];
         const int64_t L = rg.second - rg.first;
@@ -414,7 +452,7 @@ bool plan_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col,
         }
     }
 #pragma omp parallel for schedule(dynamic, 1)
-    for (int64_t p = 0; p < (int64_t)out.size(); ++p) build_panel(rp, col, val, x_split, out[p]);
+    for (int64_t p = 0; p < (int64_t)out.size(); ++p) build_panel(rp, col, val, x_split, out[p], pp);
     int64_t g = 0;
     for (PnPanelData& P : out) {
         P.desc.g0 = (int32_t)g;
@@ -437,6 +475,14 @@ bool plan_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col,
         st.ywf1 /= (double)g;
     }
     return true;
+}
+
+int64_t panel_total_slots(const std::vector<int64_t>& rp, int64_t m, const std::vector<int32_t>* part) {
+    int64_t t = 0;
+    const int32_t* pp = part ? part->data() : nullptr;
+#pragma omp parallel for reduction(+ : t) schedule(dynamic, 4096)
+    for (int64_t r = 0; r < m; ++r) t += row_vrows(rp.data(), pp, r, nullptr);
+    return t;
 }
 
 bool verify_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col, const std::vector<double>& val,

@@ -37,10 +37,16 @@ struct PnPlanStats {
 // why) when the plan would be poor (caller falls back to the row-tile kernel).
 // xcols (optional, one per range): the range's interior columns [c0, c1) --
 // each panel of range k then prefetches a slice of range k+1's columns.
+// part (optional, per CSR nonzero): plan the multiple-SpMxV -- each (row,
+// part) segment gets its own virtual rows, folded in part order.
 bool plan_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col, const std::vector<double>& val,
                 const std::vector<std::pair<int64_t, int64_t>>& ranges, int64_t x_split, int64_t rows_target,
                 std::vector<PnPanelData>& out, PnPlanStats& st, std::string& why,
-                const std::vector<std::pair<int64_t, int64_t>>* xcols = nullptr, int64_t pf_sms = 148);
+                const std::vector<std::pair<int64_t, int64_t>>* xcols = nullptr, int64_t pf_sms = 148,
+                const std::vector<int32_t>* part = nullptr);
+
+// y slots (virtual rows) the plan needs for local rows [0, m) (panel sizing).
+int64_t panel_total_slots(const std::vector<int64_t>& rp, int64_t m, const std::vector<int32_t>* part = nullptr);
 
 // Test hook: decode the groups back into (row, column, value) and compare with
 // the CSR bit for bit; checks the epoch invariant (distinct rows per epoch).

@@ -1,8 +1,10 @@
 set -x
 python -m paper_1203_2739_b200.build > /dev/null
-SPMV_PN_MODE=23 timeout 300 python -m pytest tests/test_gpu_xstage.py tests/test_gpu_variants.py -q -x -k "panel" 2>&1 | tail -1
+timeout 600 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
+SPMV_KERNEL=panel SPMV_PN_ROWS=700 timeout 300 python -m pytest tests/test_gpu_parity.py -q -x -k split 2>&1 | tail -1
 cd scripts
-run() { SPMV_PN_MODE=$1 K=16 KERNELS=panel timeout 300 python xs_probe.py 2>&1 | grep -E '"panel_ms"|rror' | sed "s/^/K16 mode $1 /"; }
-run 0; run 23; run 0; run 23
-SPMV_PN_MODE=23 timeout 300 python ab.py c4 panel | sed "s/^/mode23 /"
-timeout 300 python ab.py c4 panel | sed "s/^/mode0 /"
+timeout 300 python c3_split.py 2>&1 | tail -9
+python -c "
+import sys; sys.path.insert(0,'..')
+import synth, paper_1203_2739_b200 as sp
+p=synth.make('c3'); h=sp.spmv_create(p.m,p.n,p.row_ptr,p.col,p.val,blocks=p.blocks,parts=p.parts,n_parts=p.n_parts); print(sp.spmv_get_info(h))"
