@@ -169,7 +169,10 @@ typedef struct {
                                      any world size, any matrix at world 1, when the plan pads < 25 %),
                                      0 row-tile (otherwise); the others are measurement variants
                                      (SPMV_KERNEL environment variable at create) */
-    int32_t reserved[2];
+    int32_t split_kernel;         /* fused multiple-SpMxV kernel: 7 column-sorted panels with one y slot
+                                     per (row, part) segment (default), 3 row-major part segments,
+                                     1 part-major tiles; 0 without a split */
+    int32_t reserved;
 } spmv_info_t;
 
 spmv_status_t spmv_get_info(spmv_handle_t h, spmv_info_t* info);

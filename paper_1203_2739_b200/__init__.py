@@ -61,8 +61,9 @@ class spmv_info_t(ctypes.Structure):
         "x_interior_len", "x_border_begin", "x_border_len", "border_total", "n_tiles", "n_long_rows",
         "bytes_alg", "bytes_alg_split", "split_segments", "xs_panels", "xs_groups", "xs_pad_slots",
         "bytes_stream")] + [
-        (k, ctypes.c_int32) for k in ("n_parts", "rank", "world", "kind", "has_owner_map", "kernel")] + [
-        ("reserved", ctypes.c_int32 * 2)]
+        (k, ctypes.c_int32) for k in ("n_parts", "rank", "world", "kind", "has_owner_map", "kernel",
+                                      "split_kernel")] + [
+        ("reserved", ctypes.c_int32)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}

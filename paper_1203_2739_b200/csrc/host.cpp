@@ -456,6 +456,7 @@ static spmv_status_t plan_pn(spmv_plan_s* h, PanelPlan& pl, const std::vector<in
             desc[p].nslots = pd[p].nslots;
             const int32_t base = (int32_t)ss.size();
             desc[p].split_n = (int32_t)pd[p].split_first.size();
+            desc[p].split_short = pd[p].split_short;
             desc[p].sslot0 = base;
             desc[p].sslot_n = (int32_t)pd[p].split_slots.size();
             pl.max_sslots = std::max(pl.max_sslots, desc[p].sslot_n);
@@ -1269,6 +1270,9 @@ spmv_status_t spmv_get_info(spmv_handle_t h, spmv_info_t* info) {
     info->xs_pad_slots = h->kernel == 7 ? h->pn.pad : h->xs_pad;
     info->bytes_stream = h->bytes_stream;
     info->kernel = h->kernel;
+    info->split_kernel = h->n_parts == 0 ? 0
+                         : (h->pns.ok() && h->kernel != 2) ? 7
+                         : (h->split_rowmajor && h->kernel != 2 && !getenv("SPMV_SPLIT_PARTMAJOR")) ? 3 : 1;
     return SPMV_OK;
 }
 

@@ -166,8 +166,12 @@ struct PnPanel {
     int32_t split_n;   // rows of the panel split into virtual rows
     int32_t sslot0;    // their virtual rows' slots: split_slots[sslot0, sslot0 + sslot_n)
     int32_t sslot_n;
-    int32_t pad0;
+    int32_t split_short; // split rows [0, split_short) have <= kPnFoldSeq virtual rows (folded by one thread)
 };
+#ifndef SPMV_PN_FOLDSEQ
+#define SPMV_PN_FOLDSEQ 32
+#endif
+constexpr int kPnFoldSeq = SPMV_PN_FOLDSEQ;   // virtual rows a thread folds sequentially
 #ifndef SPMV_PN_VMAX
 #define SPMV_PN_VMAX 32
 #endif

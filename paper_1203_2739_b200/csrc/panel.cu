@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
     // once (the epilogue folds them by warps)
     uint16_t* ssl = reinterpret_cast<uint16_t*>(ys + A.max_rows + 1);
     int32_t* sdesc = reinterpret_cast<int32_t*>(ssl + ((A.max_sslots + 7) & ~7));   // (first, count, row) per split row
-    if (MODE == 0) {
+    {
         for (int i = tid; i < d.sslot_n; i += kT) ssl[i] = A.split_slots[d.sslot0 + i];
         for (int i = tid; i < d.split_n; i += kT) {
             const int e = d.split_off + i;
@@ -237,9 +237,18 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
             }
         }
     }
-    // rows split into virtual rows: one warp each, lanes sum strided slots,
-    // fixed xor tree (deterministic order)
-    for (int k = warp; k < d.split_n; k += NW) {
+    // rows split into virtual rows (long rows; a split handle's (row, part)
+    // segments): up to kPnFoldSeq slots, one thread per row adds them in fold
+    // order (part order); longer rows one warp each, lanes sum strided
+    // slots, fixed xor tree.  Both orders are fixed by the plan (deterministic).
+    for (int k = tid; k < d.split_short; k += kT) {
+        const int f = sdesc[3 * k], c = sdesc[3 * k + 1];
+        double v = ys[ssl[f]];
+        for (int j = 1; j < c; ++j) v += ys[ssl[f + j]];
+        A.y[d.row0 + sdesc[3 * k + 2]] = v;
+        mx = fmax(mx, fabs(v));
+    }
+    for (int k = d.split_short + warp; k < d.split_n; k += NW) {
         const int f = sdesc[3 * k], c = sdesc[3 * k + 1];
         double v = 0.0;
         for (int j = lane; j < c; j += 32) v += ys[ssl[f + j]];

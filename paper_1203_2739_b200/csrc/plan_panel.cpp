@@ -353,17 +353,22 @@ void build_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col
         colour_slots((int32_t)nr, gents, G, v2s, slot);
     }
     // real rows -> slot, or -> split entry (virtual rows' slots in fold order)
+    // split rows with <= kPnFoldSeq virtual rows first (the epilogue folds
+    // those one thread per row, sequentially), then the longer ones (a warp each)
     P.row2slot.resize(nrr);
-    for (int64_t r = 0; r < nrr; ++r) {
-        if (vcount[r] == 1) {
-            P.row2slot[r] = v2s[vbase[r]];
-        } else {
-            P.row2slot[r] = (uint16_t)(0x8000 | P.split_first.size());
-            P.split_first.push_back((int32_t)P.split_slots.size());
-            P.split_cnt.push_back(vcount[r]);
-            P.split_row.push_back((int32_t)r);
-            for (int32_t j = 0; j < vcount[r]; ++j) P.split_slots.push_back(v2s[vbase[r] + j]);
+    for (int pass = 0; pass < 2; ++pass) {
+        for (int64_t r = 0; r < nrr; ++r) {
+            if (vcount[r] == 1) {
+                if (pass == 0) P.row2slot[r] = v2s[vbase[r]];
+            } else if ((vcount[r] <= kPnFoldSeq) == (pass == 0)) {
+                P.row2slot[r] = (uint16_t)(0x8000 | P.split_first.size());
+                P.split_first.push_back((int32_t)P.split_slots.size());
+                P.split_cnt.push_back(vcount[r]);
+                P.split_row.push_back((int32_t)r);
+                for (int32_t j = 0; j < vcount[r]; ++j) P.split_slots.push_back(v2s[vbase[r] + j]);
+            }
         }
+        if (pass == 0) P.split_short = (int32_t)P.split_first.size();
     }
     double w = 0;
     for (int64_t g = 0; g < G; ++g) {
@@ -394,23 +399,46 @@ bool plan_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col,
         const auto& rg = ranges[k];
         const int64_t L = rg.second - rg.first;
         if (L <= 0) continue;
-        // panel boundaries: about R y slots (virtual rows) per panel
-        int64_t S = 0;
-        for (int64_t r = rg.first; r < rg.second; ++r) S += slots_of(r);
-        int64_t np = (S + R - 1) / R;
-        std::vector<int64_t> cut(1, rg.first);
-        {
-            int64_t acc = 0, pi = 1;
-            for (int64_t r = rg.first; r < rg.second && pi < np; ++r) {
-                acc += slots_of(r);
-                if (acc >= S * pi / np) {
+        // panel boundaries: np = ceil(slots / R) panels, cut at equal shares of
+        // the bytes they move (12 per nonzero, 8 + 2 per y slot: the y write
+        // and its slot map), so panels of rows with few and many nonzeros take
+        // about the same time (C4's Zipf rows: balancing by slots left a 13 %
+        // tail); a panel never exceeds 1.25 R slots (its y lives in shared
+        // memory, and the rest of the L1 holds the loads in flight) -- when that
+        // cap would add panels (a second wave), the cuts balance slots instead
+        int64_t S = 0, C = 0;
+        for (int64_t r = rg.first; r < rg.second; ++r) {
+            const int64_t s = slots_of(r);
+            S += s;
+            C += 12 * (rp[r + 1] - rp[r]) + 10 * s;
+        }
+        const int64_t np0 = (S + R - 1) / R;
+        const int64_t cap = std::min<int64_t>(R + R / 4, kPnRowsMax);
+        auto make_cuts = [&](bool by_bytes) {
+            std::vector<int64_t> cut(1, rg.first);
+            const int64_t tot = by_bytes ? C : S;
+            int64_t acc = 0, ps = 0, pi = 1;
+            for (int64_t r = rg.first; r < rg.second; ++r) {
+                const int64_t s = slots_of(r);
+                if (by_bytes && ps > 0 && ps + s > cap) {   // slot cap: cut before r
+                    cut.push_back(r);
+                    ps = 0;
+                    while (pi < np0 && acc >= tot * pi / np0) ++pi;
+                }
+                acc += by_bytes ? 12 * (rp[r + 1] - rp[r]) + 10 * s : s;
+                ps += s;
+                if (pi < np0 && acc >= tot * pi / np0 && r + 1 < rg.second) {
                     cut.push_back(r + 1);
-                    ++pi;
+                    ps = 0;
+                    while (pi < np0 && acc >= tot * pi / np0) ++pi;
                 }
             }
             cut.push_back(rg.second);
-            np = (int64_t)cut.size() - 1;
-        }
+            return cut;
+        };
+        std::vector<int64_t> cut = make_cuts(true);
+        if ((int64_t)cut.size() - 1 > np0) cut = make_cuts(false);   // the cap added panels: cut by slots
+        int64_t np = (int64_t)cut.size() - 1;
         // L2 prefetch slice: the interior columns of the range that starts about
         // one wave after this one (its panels then find x in L2), cut in np pieces
         int64_t pf0 = 0, pf1 = 0;
@@ -515,6 +543,8 @@ bool verify_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& co
             } else {
                 const int32_t k = sl & 0x7FFF;
                 if (k >= (int32_t)P.split_first.size()) { e = "split index out of range"; break; }
+                if ((k < P.split_short) != (P.split_cnt[k] <= kPnFoldSeq)) { e = "split rows not ordered short first"; break; }
+                if (P.split_row[k] != r) { e = "split_row does not name the row"; break; }
                 for (int32_t j = 0; j < P.split_cnt[k] && e.empty(); ++j) own(P.split_slots[P.split_first[k] + j], r);
             }
         }

@@ -20,6 +20,7 @@ struct PnPanelData {
     std::vector<int32_t> split_first, split_cnt;   // per split row: its virtual rows' slots in split_slots
     std::vector<int32_t> split_row;                // per split row: its panel-local row
     std::vector<uint16_t> split_slots;
+    int32_t split_short = 0;        // split rows [0, split_short) have <= kPnFoldSeq virtual rows
     int32_t nslots = 0;             // y slots used (virtual rows), before rounding to 16
     int64_t entries = 0, pads = 0, deferred = 0;
     int32_t rot = 0;               // the column sweep starts at this column (wraps around)

@@ -123,6 +123,7 @@ def test_split_on_panels(monkeypatch, variant):
     p = synth.make("c3s", variant=variant)
     x = p.x()
     h = create(p)
+    assert sp.spmv_get_info(h)["split_kernel"] == 7
     y = gpu_apply(h, x, p.m, split=True)
     yref = oracle.split(p.row_ptr, p.col, p.val, p.parts, p.n_parts, x)
     S = oracle.spmv(p.row_ptr, p.col, p.val, x)[1]
@@ -143,3 +144,15 @@ def test_split_on_panels_random_parts(monkeypatch):
     y = gpu_apply(h, x, p.m, split=True)
     yref = oracle.split(p.row_ptr, p.col, p.val, parts, 5, x)
     assert_parity(y, yref, None, exact=True, what="split-on-panels/random parts")
+
+
+def test_split_rowmajor_kernel(monkeypatch):
+    """The row-major segment kernel (used when the panel plan is rejected)."""
+    monkeypatch.setenv("SPMV_SPLIT_ROWTILE", "1")
+    p = synth.make("c3s", variant="int")
+    x = p.x()
+    h = create(p)
+    assert sp.spmv_get_info(h)["split_kernel"] == 3
+    y = gpu_apply(h, x, p.m, split=True)
+    yref = oracle.split(p.row_ptr, p.col, p.val, p.parts, p.n_parts, x)
+    assert_parity(y, yref, None, exact=True, what="split row-major")
