@@ -73,6 +73,7 @@ __device__ __forceinline__ int32_t ld_base(const int32_t* p) {
 // 6 gathers of a fixed 2 MB window (no dependence on the loaded indices' values)
 template <int MODE, int KD_ = kD, int KGD_ = 8>
 __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
+    constexpr bool kMain = MODE == 0 || MODE == 24;      // the kernel (24: without the next-panel prefetch)
     constexpr int kD = KD_;                              // groups in flight per warp
     constexpr int kGD = MODE == 5 ? 4 : KGD_;            // gathers issued this many steps ahead
     static_assert(kD % kGD == 0 && kD % kPnB == 0, "ring geometry");
@@ -110,14 +111,14 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
     // one 16-byte load per epoch gives the warp the bases of its kPnB groups
     // (slots u..u+3 of the ring; the bases of u+1..u+3 it replaces were last
     // used by gathers issued >= 1 step earlier, since kGD >= kPnB)
-    static_assert(MODE != 0 || kGD >= 4, "base quad overwrites bases still needed");
+    static_assert(!kMain || kGD >= 4, "base quad overwrites bases still needed");
     static_assert(kPnB % 4 == 0, "bases are loaded four at a time");
     const int4* gb4 = reinterpret_cast<const int4*>(A.gbase4 + d.g0);
     auto load = [&](int t, double& v, uint32_t& i, int32_t& b) {
         const int64_t g = gw + 16 * (int64_t)t;
         v = ld_val(A.gval + g * 32 + lane, pol);
         i = ld_u32(A.gidx + g * 32 + lane, pol);
-        if (MODE != 0) b = ld_base(A.gbase + g);
+        if (!kMain) b = ld_base(A.gbase + g);
     };
     auto load_b4 = [&](int t, int32_t& b0, int32_t& b1, int32_t& b2, int32_t& b3) {   // t % 4 == 0
         int4 q;
@@ -148,15 +149,31 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
     // prefetch per array per epoch, issued by thread 0): the register ring
     // then waits for L2, not HBM, latency -- the x gathers depend on the
     // loaded indices, so their distance is what bounds the pipeline.
+    // Past the panel's last epoch it prefetches the first epochs of panel
+    // p + gridDim.x -- about the panel the block scheduler starts next, on
+    // whichever SM frees first -- so a new CTA's ring does not fill from HBM.
+    int nx_g0 = 0, nx_ne = 0;
+    if (tid == 0 && MODE != 24 && p + (int)gridDim.x < A.n_panels) {
+        nx_g0 = A.panel[p + gridDim.x].g0;
+        nx_ne = A.panel[p + gridDim.x].ne;
+    }
     auto prefetch_epoch = [&](int e) {
-        if (tid == 0 && e < d.ne) {
+        if (tid == 0 && e >= d.ne && e - d.ne < nx_ne) {
+            const int64_t g = (int64_t)nx_g0 + (int64_t)(e - d.ne) * kPnEpoch;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.gval + g * 32), "r"(kPnEpoch * 32 * 8)
+                         : "memory");
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.gidx + g * 32), "r"(kPnEpoch * 32 * 4)
+                         : "memory");
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"((kMain ? A.gbase4 : A.gbase) + g),
+                         "r"(kPnEpoch * 4) : "memory");
+        } else if (tid == 0 && e < d.ne) {
             const int64_t g = (int64_t)d.g0 + (int64_t)e * kPnEpoch;
             // normal priority: an evict_first prefetch is the first victim of the next one
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.gval + g * 32), "r"(kPnEpoch * 32 * 8)
                          : "memory");
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.gidx + g * 32), "r"(kPnEpoch * 32 * 4)
                          : "memory");
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"((MODE == 0 ? A.gbase4 : A.gbase) + g),
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"((kMain ? A.gbase4 : A.gbase) + g),
                          "r"(kPnEpoch * 4) : "memory");
         }
     };
@@ -178,7 +195,7 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
 #pragma unroll
     for (int u = 0; u < kD; ++u) {
         if (u < T) load(u, rv[u], ri[u], rb[u]);
-        if (MODE == 0 && u % 4 == 0 && u < T) load_b4(u, rb[u], rb[u + 1], rb[u + 2], rb[u + 3]);
+        if (kMain && u % 4 == 0 && u < T) load_b4(u, rb[u], rb[u + 1], rb[u + 2], rb[u + 3]);
     }
 #pragma unroll
     for (int u = 0; u < kGD; ++u)
@@ -199,7 +216,7 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
             }
             if (t + kD < T) {
                 load(t + kD, rv[u], ri[u], rb[u]);
-                if (MODE == 0 && u % 4 == 0)
+                if (kMain && u % 4 == 0)
                     load_b4(t + kD, rb[u], rb[(u + 1) % kD], rb[(u + 2) % kD], rb[(u + 3) % kD]);
             }
             if (t + kGD < T) rx[u % kGD] = gather(ri[(u + kGD) % kD], rb[(u + kGD) % kD]);
@@ -558,6 +575,7 @@ cudaError_t launch_panel(const PnArgs& a, cudaStream_t s) {
         if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<0, 16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
         if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<0, kDefD, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
         if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<0, 8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
+        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<24, kDefD, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
 #if SPMV_PN_B == 4
         if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<0, 20, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
 #endif
@@ -616,6 +634,7 @@ cudaError_t launch_panel(const PnArgs& a, cudaStream_t s) {
     case 8: spmv_panel2_kernel<12><<<b.n_panels, kT, smem2(12), s>>>(b); break;
     case 21: spmv_panel_kernel<0><<<b.n_panels, kT, smem, s>>>(b); break;   // previous default (16, 8)
     case 22: spmv_panel_kernel<0, 8, 4><<<b.n_panels, kT, smem, s>>>(b); break;
+    case 24: spmv_panel_kernel<24, kDefD, 4><<<b.n_panels, kT, smem, s>>>(b); break;   // no next-panel prefetch
     default: spmv_panel_kernel<0, kDefD, 4><<<b.n_panels, kT, smem, s>>>(b);
     }
     return cudaGetLastError();
