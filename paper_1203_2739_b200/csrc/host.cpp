@@ -78,7 +78,6 @@ struct PanelPlan {
     spmvb::PnPanel* d_panel = nullptr;
     double* d_gval = nullptr;
     uint32_t* d_gidx = nullptr;
-    int32_t* d_gbase = nullptr;
     int32_t* d_gbase4 = nullptr;
     uint16_t* d_r2s = nullptr;        // [m_loc] y slot of each row in its panel (or split entry)
     int32_t* d_split_first = nullptr;
@@ -442,7 +441,6 @@ static spmv_status_t plan_pn(spmv_plan_s* h, PanelPlan& pl, const std::vector<in
     if ((s = upload(h, &pl.d_panel, desc.data(), P))) return s;
     if ((s = dalloc(h, &pl.d_gval, G * 32))) return s;
     if ((s = dalloc(h, &pl.d_gidx, G * 32))) return s;
-    if ((s = dalloc(h, &pl.d_gbase, G))) return s;
     if ((s = dalloc(h, &pl.d_gbase4, G))) return s;
     {
         std::vector<uint16_t> r2s(std::max<int64_t>(h->m_loc, 1), 0);
@@ -481,13 +479,28 @@ static spmv_status_t plan_pn(spmv_plan_s* h, PanelPlan& pl, const std::vector<in
         if ((s = upload(h, &pl.d_split_slots, ss.data(), ss.size()))) return s;
         CUDA_TRY(cudaMemcpy(pl.d_panel, desc.data(), P * sizeof(spmvb::PnPanel), cudaMemcpyHostToDevice));
     }
+    std::vector<double> tv;
+    std::vector<uint32_t> ti;
     for (int64_t p = 0; p < P; ++p) {
         spmvb::PnPanelData& D = pd[p];
         const int64_t g0 = D.desc.g0, ng = (int64_t)D.gbase.size();
         if (ng) {
-            CUDA_TRY(cudaMemcpy(pl.d_gval + g0 * 32, D.gval.data(), ng * 32 * 8, cudaMemcpyHostToDevice));
-            CUDA_TRY(cudaMemcpy(pl.d_gidx + g0 * 32, D.gidx.data(), ng * 32 * 4, cudaMemcpyHostToDevice));
-            CUDA_TRY(cudaMemcpy(pl.d_gbase + g0, D.gbase.data(), ng * 4, cudaMemcpyHostToDevice));
+            // device layout of the group stream (panel.cu): per (epoch, warp) a
+            // 128-entry block; values as (step pair, lane, step & 1), indices as
+            // (lane, step), so 16-byte loads cover 2 / 4 of a warp's steps
+            tv.resize(ng * 32);
+            ti.resize(ng * 32);
+            for (int64_t g = 0; g < ng; ++g) {
+                const int64_t q = g / spmvb::kPnWarps, w = g % spmvb::kPnWarps;   // g = (e * 4 + b) * 16 + w
+                const int64_t e = q / spmvb::kPnB, b = q % spmvb::kPnB;
+                const int64_t blk = (e * spmvb::kPnWarps + w) * 128;
+                for (int l = 0; l < 32; ++l) {
+                    tv[blk + (b / 2) * 64 + l * 2 + (b & 1)] = D.gval[g * 32 + l];
+                    ti[blk + l * 4 + b] = D.gidx[g * 32 + l];
+                }
+            }
+            CUDA_TRY(cudaMemcpy(pl.d_gval + g0 * 32, tv.data(), ng * 32 * 8, cudaMemcpyHostToDevice));
+            CUDA_TRY(cudaMemcpy(pl.d_gidx + g0 * 32, ti.data(), ng * 32 * 4, cudaMemcpyHostToDevice));
             CUDA_TRY(cudaMemcpy(pl.d_gbase4 + g0, D.gbase4.data(), ng * 4, cudaMemcpyHostToDevice));
         }
         std::vector<double>().swap(D.gval);
@@ -1048,7 +1061,6 @@ static void fill_pn_args(const PanelPlan& pl, spmvb::PnArgs& X) {
     X.n_panels = (int32_t)pl.panels;
     X.gval = pl.d_gval;
     X.gidx = pl.d_gidx;
-    X.gbase = pl.d_gbase;
     X.gbase4 = pl.d_gbase4;
     X.max_rows = pl.max_rows;
     X.row2slot = pl.d_r2s;

@@ -183,9 +183,8 @@ struct PnArgs {
     const PnPanel* panel;
     int32_t n_panels;
     int32_t x_split;          // columns >= x_split read x_hi[c - x_split]
-    const double* gval;       // [groups*32]
-    const uint32_t* gidx;     // [groups*32]
-    const int32_t* gbase;     // [groups] first column of the group (local id)
+    const double* gval;       // [groups*32] per (epoch, warp) blocks of 128: (step pair, lane, step & 1)
+    const uint32_t* gidx;     // [groups*32] per (epoch, warp) blocks of 128: (lane, step)
     const int32_t* gbase4;    // [groups] same, (epoch, warp, step) order (16-byte loads)
     const double* x_lo;
     const double* x_hi;

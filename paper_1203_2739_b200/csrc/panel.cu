@@ -30,10 +30,8 @@ namespace {
 
 constexpr int NW = kPnWarps;
 constexpr int kT = NW * 32;
-constexpr int kD = 16;    // groups in flight per warp (template default)
-constexpr int kDefD = kPnB == 8 ? 16 : 12;   // the launch default
+constexpr int kDefD = 12;   // steps (groups) in flight per warp, the launch default
 constexpr int kPF = 8;    // default: epochs of the group stream prefetched into L2 ahead
-static_assert(kD % kPnB == 0, "ring geometry");
 constexpr uint32_t kDeltaMask = (1u << kPnDeltaBits) - 1u;
 
 __device__ __forceinline__ uint64_t pol_evict_first() {
@@ -51,49 +49,41 @@ __device__ __forceinline__ double ld_x(const double* p, uint64_t pol) {
     asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
     return v;
 }
-__device__ __forceinline__ double ld_val(const double* p, uint64_t pol) {
-    double v;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
-    return v;
-}
-__device__ __forceinline__ uint32_t ld_u32(const uint32_t* p, uint64_t pol) {
-    uint32_t v;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
-    return v;
-}
-__device__ __forceinline__ int32_t ld_base(const int32_t* p) {
-    int32_t v;
-    asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
-    return v;
-}
-
+// Group stream layout (host.cpp upload_panel_stream): the kPnB = 4 groups a
+// warp runs in one epoch form a 128-entry block, (epoch e, warp w) at
+// g0 * 32 + (e * 16 + w) * 128: values as two (step, lane, step & 1) pairs
+// -- one 16-byte load per lane covers two steps -- and indices as (lane,
+// step) quads -- one 16-byte load per lane covers the four steps.  A warp
+// issues 4 stream loads per epoch (2 value, 1 index, 1 base quad) instead of
+// 9, so fewer L1 requests carry the same bytes.
+//
 // MODE (ablation, measurements only; 0 = the kernel): 1 no x gathers (x = 1),
 // 2 no shared-memory y update (register sum), 3 no epoch barriers (racy),
-// 4 no L2 prefetch of the group stream, 5 gathers 4 steps ahead (not 8),
-// 6 gathers of a fixed 2 MB window (no dependence on the loaded indices' values)
-template <int MODE, int KD_ = kD, int KGD_ = 8>
+// 4 no L2 prefetch of the group stream, 6 gathers of a fixed 2 MB window (no
+// dependence on the loaded indices' values), 24 no next-panel prefetch
+template <int MODE, int KD_ = kDefD, int KGD_ = 4>
 __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
-    constexpr bool kMain = MODE == 0 || MODE == 24;      // the kernel (24: without the next-panel prefetch)
-    constexpr int kD = KD_;                              // groups in flight per warp
-    constexpr int kGD = MODE == 5 ? 4 : KGD_;            // gathers issued this many steps ahead
-    static_assert(kD % kGD == 0 && kD % kPnB == 0, "ring geometry");
+    constexpr int kD = KD_;                              // steps (groups) in flight per warp
+    constexpr int kGD = KGD_;                            // gathers issued this many steps ahead
+    // the ring is refilled four slots at a time after the last step of a warp's
+    // epoch, so 9..12 (kD - 3..kD) steps are loaded ahead; a gather needs its
+    // step's index loaded: kGD <= kD - 4
+    static_assert(kPnB == 4 && kD % 4 == 0 && kGD >= 1 && kGD <= kD - 4, "ring geometry");
     extern __shared__ __align__(16) double ys[];
     const int p = blockIdx.x;
     const PnPanel d = A.panel[p];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     for (int i = tid; i < ((d.nslots + 15) & ~15); i += kT) ys[i] = 0.0;   // the panel's y slots
     // virtual-row slot lists of the panel's split rows, copied to shared memory
-    // once (the epilogue folds them by warps)
+    // once (the epilogue folds them)
     uint16_t* ssl = reinterpret_cast<uint16_t*>(ys + A.max_rows + 1);
     int32_t* sdesc = reinterpret_cast<int32_t*>(ssl + ((A.max_sslots + 7) & ~7));   // (first, count, row) per split row
-    {
-        for (int i = tid; i < d.sslot_n; i += kT) ssl[i] = A.split_slots[d.sslot0 + i];
-        for (int i = tid; i < d.split_n; i += kT) {
-            const int e = d.split_off + i;
-            sdesc[3 * i] = A.split_first[e] - d.sslot0;
-            sdesc[3 * i + 1] = A.split_cnt[e];
-            sdesc[3 * i + 2] = A.split_row[e];
-        }
+    for (int i = tid; i < d.sslot_n; i += kT) ssl[i] = A.split_slots[d.sslot0 + i];
+    for (int i = tid; i < d.split_n; i += kT) {
+        const int e = d.split_off + i;
+        sdesc[3 * i] = A.split_first[e] - d.sslot0;
+        sdesc[3 * i + 1] = A.split_cnt[e];
+        sdesc[3 * i + 2] = A.split_row[e];
     }
     __syncthreads();
 
@@ -102,43 +92,30 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
     const int PF = A.pf_epochs > 0 ? A.pf_epochs : kPF;
     const int T = d.ne * kPnB;                       // steps per warp
     const int scratch = A.max_rows;                  // y slot of the padding lanes
-    const int64_t gw = (int64_t)d.g0 + warp;         // group of step t: gw + 16 t
 
     double rv[kD];
     uint32_t ri[kD];
     int32_t rb[kD];
     double rx[kGD];
-    // one 16-byte load per epoch gives the warp the bases of its kPnB groups
-    // (slots u..u+3 of the ring; the bases of u+1..u+3 it replaces were last
-    // used by gathers issued >= 1 step earlier, since kGD >= kPnB)
-    static_assert(!kMain || kGD >= 4, "base quad overwrites bases still needed");
-    static_assert(kPnB % 4 == 0, "bases are loaded four at a time");
-    const int4* gb4 = reinterpret_cast<const int4*>(A.gbase4 + d.g0);
-    auto load = [&](int t, double& v, uint32_t& i, int32_t& b) {
-        const int64_t g = gw + 16 * (int64_t)t;
-        v = ld_val(A.gval + g * 32 + lane, pol);
-        i = ld_u32(A.gidx + g * 32 + lane, pol);
-        if (!kMain) b = ld_base(A.gbase + g);
-    };
-    auto load_b4 = [&](int t, int32_t& b0, int32_t& b1, int32_t& b2, int32_t& b3) {   // t % 4 == 0
-        int4 q;
-        const int64_t o = ((int64_t)(t / kPnB) * kPnWarps + warp) * (kPnB / 4) + (t % kPnB) / 4;
+    // the warp's four steps s..s+3 (s % 4 == 0) of epoch s / 4 into ring slots u..u+3
+    auto load4 = [&](int s, int u) {
+        const int64_t blk = (int64_t)d.g0 * 32 + ((int64_t)(s >> 2) * kPnWarps + warp) * 128;
+        const double* vp = A.gval + blk + lane * 2;
+        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+                     : "=d"(rv[u]), "=d"(rv[u + 1]) : "l"(vp), "l"(pol));
+        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+                     : "=d"(rv[u + 2]), "=d"(rv[u + 3]) : "l"(vp + 64), "l"(pol));
+        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                     : "=r"(ri[u]), "=r"(ri[u + 1]), "=r"(ri[u + 2]), "=r"(ri[u + 3])
+                     : "l"(A.gidx + blk + lane * 4), "l"(pol));
         asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(q.x), "=r"(q.y), "=r"(q.z), "=r"(q.w) : "l"(gb4 + o));
-        b0 = q.x; b1 = q.y; b2 = q.z; b3 = q.w;
+                     : "=r"(rb[u]), "=r"(rb[u + 1]), "=r"(rb[u + 2]), "=r"(rb[u + 3])
+                     : "l"(A.gbase4 + d.g0 + ((int64_t)(s >> 2) * kPnWarps + warp) * 4));
     };
     double racc = 0.0;
     auto gather = [&](uint32_t i, int32_t b) -> double {
         if (MODE == 1) return 1.0;
         if (MODE == 6) return __ldg(A.x_lo + ((b + (int)(i & 0xFFF)) & 0x3FFFF));
-        if (MODE == 15) {
-            if (i == kPnDummy) return 0.0;
-            const double* xp = b < A.x_split ? A.x_lo + b : A.x_hi + (b - A.x_split);
-            return __ldg(xp + (i & kDeltaMask));
-        }
-        if (MODE == 16) return ld_x(A.x_lo + ((b + (int)(i & 0xFFF)) & 0x3FFFF), polx);
-        if (MODE == 13) return i == kPnDummy ? 0.0 : ld_x(A.x_lo + ((b + (int)(i & kDeltaMask)) & 0x3FFFF), polx);
-        if (MODE == 14) return i == kPnDummy ? 0.0 : ld_x(A.x_lo + ((b & 0x3FFFF) + (int)(i & kDeltaMask)), polx);
         // unconditional: a padding lane reads x[base] (valid) and adds 0 * x into
         // the scratch y slot -- a predicated-off load behind a branch made the
         // warp wait for the gather at the branch (measured 1.6x slower)
@@ -158,24 +135,17 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
         nx_ne = A.panel[p + gridDim.x].ne;
     }
     auto prefetch_epoch = [&](int e) {
-        if (tid == 0 && e >= d.ne && e - d.ne < nx_ne) {
-            const int64_t g = (int64_t)nx_g0 + (int64_t)(e - d.ne) * kPnEpoch;
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.gval + g * 32), "r"(kPnEpoch * 32 * 8)
-                         : "memory");
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.gidx + g * 32), "r"(kPnEpoch * 32 * 4)
-                         : "memory");
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"((kMain ? A.gbase4 : A.gbase) + g),
-                         "r"(kPnEpoch * 4) : "memory");
-        } else if (tid == 0 && e < d.ne) {
-            const int64_t g = (int64_t)d.g0 + (int64_t)e * kPnEpoch;
-            // normal priority: an evict_first prefetch is the first victim of the next one
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.gval + g * 32), "r"(kPnEpoch * 32 * 8)
-                         : "memory");
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.gidx + g * 32), "r"(kPnEpoch * 32 * 4)
-                         : "memory");
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"((kMain ? A.gbase4 : A.gbase) + g),
-                         "r"(kPnEpoch * 4) : "memory");
-        }
+        if (tid != 0) return;
+        int64_t g;
+        if (e < d.ne) g = (int64_t)d.g0 + (int64_t)e * kPnEpoch;
+        else if (e - d.ne < nx_ne) g = (int64_t)nx_g0 + (int64_t)(e - d.ne) * kPnEpoch;
+        else return;
+        // normal priority: an evict_first prefetch is the first victim of the next one
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.gval + g * 32), "r"(kPnEpoch * 32 * 8)
+                     : "memory");
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.gidx + g * 32), "r"(kPnEpoch * 32 * 4)
+                     : "memory");
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.gbase4 + g), "r"(kPnEpoch * 4) : "memory");
     };
     if (MODE != 4) {
         for (int e = 0; e < PF; ++e) prefetch_epoch(e);
@@ -193,10 +163,8 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
         }
     }
 #pragma unroll
-    for (int u = 0; u < kD; ++u) {
-        if (u < T) load(u, rv[u], ri[u], rb[u]);
-        if (kMain && u % 4 == 0 && u < T) load_b4(u, rb[u], rb[u + 1], rb[u + 2], rb[u + 3]);
-    }
+    for (int u = 0; u < kD; u += 4)
+        if (u < T) load4(u, u);
 #pragma unroll
     for (int u = 0; u < kGD; ++u)
         if (u < T) rx[u] = gather(ri[u], rb[u]);
@@ -214,11 +182,9 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
                 r = r == (int)(kPnDummy >> kPnDeltaBits) ? scratch : r;
                 ys[r] = fma(rv[u], rx[u % kGD], ys[r]);
             }
-            if (t + kD < T) {
-                load(t + kD, rv[u], ri[u], rb[u]);
-                if (kMain && u % 4 == 0)
-                    load_b4(t + kD, rb[u], rb[(u + 1) % kD], rb[(u + 2) % kD], rb[(u + 3) % kD]);
-            }
+            // after the warp's last step of an epoch: refill its four slots with
+            // the steps kD later (T is a multiple of 4, so all four exist or none)
+            if (u % 4 == 3 && t + kD - 3 < T) load4(t + kD - 3, u - 3);
             if (t + kGD < T) rx[u % kGD] = gather(ri[(u + kGD) % kD], rb[(u + kGD) % kD]);
             if (u % kPnB == kPnB - 1) {                  // epoch boundary (T is a multiple of kPnB)
                 if (MODE != 3) __syncthreads();
@@ -285,268 +251,6 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
     }
 }
 
-// ---------------------------------------------------------------------------
-// Variant with the x gathers going to shared memory (cp.async, no register
-// cost per gather in flight): G steps of gathers in flight per warp.
-template <int G>
-__global__ void __launch_bounds__(kT, 1) spmv_panel2_kernel(const PnArgs A) {
-    constexpr int kD2 = 24;   // groups of (value, index, base) in flight per warp (registers)
-    static_assert(kD2 % kPnB == 0 && kD2 % G == 0 && G >= 2 && G < kD2, "ring geometry");
-    extern __shared__ __align__(16) double sm2[];
-    double* ys = sm2;
-    const int p = blockIdx.x;
-    const PnPanel d = A.panel[p];
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    double* gr = sm2 + ((A.max_rows + 2) & ~1) + warp * G * 32;
-    const uint32_t gr_s = (uint32_t)__cvta_generic_to_shared(gr) + lane * 8;
-    for (int i = tid; i < ((d.nslots + 15) & ~15); i += kT) ys[i] = 0.0;   // the panel's y slots
-    __syncthreads();
-
-    const uint64_t pol = pol_evict_first();
-    const uint64_t polx = pol_evict_last();
-    const int PF = A.pf_epochs > 0 ? A.pf_epochs : kPF;
-    const int T = d.ne * kPnB;
-    const int64_t gw = (int64_t)d.g0 + warp;
-
-    double rv[kD2];
-    uint32_t ri[kD2];
-    int32_t rb[kD2];
-    auto load = [&](int t, double& v, uint32_t& i, int32_t& b) {
-        const int64_t g = gw + 16 * (int64_t)t;
-        v = ld_val(A.gval + g * 32 + lane, pol);
-        i = ld_u32(A.gidx + g * 32 + lane, pol);
-        b = ld_base(A.gbase + g);
-    };
-    auto issue = [&](int slot, uint32_t i, int32_t b) {
-        if (i != kPnDummy) {
-            const double* xp = (b < A.x_split ? A.x_lo + b : A.x_hi + (b - A.x_split)) + (i & kDeltaMask);
-            asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;" ::"r"(gr_s + slot * 256),
-                         "l"(xp), "l"(polx) : "memory");
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-    };
-    auto prefetch_epoch = [&](int e) {
-        if (tid == 0 && e < d.ne) {
-            const int64_t g = (int64_t)d.g0 + (int64_t)e * kPnEpoch;
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.gval + g * 32), "r"(kPnEpoch * 32 * 8)
-                         : "memory");
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.gidx + g * 32), "r"(kPnEpoch * 32 * 4)
-                         : "memory");
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.gbase + g), "r"(kPnEpoch * 4)
-                         : "memory");
-        }
-    };
-    for (int e = 0; e < PF; ++e) prefetch_epoch(e);
-    if (tid == 32 && d.pf_len > 0) {
-        const uintptr_t a0 = reinterpret_cast<uintptr_t>(A.x_lo + d.pf_col) & ~uintptr_t(15);
-        const uintptr_t a1 = reinterpret_cast<uintptr_t>(A.x_lo + d.pf_col + d.pf_len) & ~uintptr_t(15);
-        for (uintptr_t a = a0; a < a1; a += 32768) {
-            const uint32_t n = (uint32_t)(a1 - a < 32768 ? a1 - a : 32768);
-            asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(a), "r"(n), "l"(polx)
-                         : "memory");
-        }
-    }
-#pragma unroll
-    for (int u = 0; u < kD2; ++u)
-        if (u < T) load(u, rv[u], ri[u], rb[u]);
-#pragma unroll
-    for (int u = 0; u < G - 1; ++u) {
-        if (u < T) issue(u, ri[u], rb[u]);
-        else asm volatile("cp.async.commit_group;" ::: "memory");
-    }
-
-    for (int t0 = 0; t0 < T; t0 += kD2) {
-#pragma unroll
-        for (int u = 0; u < kD2; ++u) {
-            const int t = t0 + u;
-            if (t >= T) break;
-            // gathers of step t + G - 1 into ring slot (t + G - 1) % G (consumed at step t - 1)
-            if (t + G - 1 < T) issue((u + G - 1) % G, ri[(u + G - 1) % kD2], rb[(u + G - 1) % kD2]);
-            else asm volatile("cp.async.commit_group;" ::: "memory");
-            asm volatile("cp.async.wait_group %0;" ::"n"(G - 1) : "memory");
-            const uint32_t i = ri[u];
-            if (i != kPnDummy) {
-                const int r = (int)(i >> kPnDeltaBits);
-                ys[r] = fma(rv[u], gr[(u % G) * 32 + lane], ys[r]);
-            }
-            if (t + kD2 < T) load(t + kD2, rv[u], ri[u], rb[u]);
-            if (u % kPnB == kPnB - 1) {
-                __syncthreads();
-                prefetch_epoch(t / kPnB + PF);
-            }
-        }
-    }
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    __syncthreads();
-
-    double mx = 0.0;
-    for (int i = tid; i < d.nrows; i += kT) {
-        const uint16_t q = A.row2slot[d.row0 + i];
-        double v = 0.0;
-        if (q < 0x8000) {
-            v = ys[q];
-        } else {
-            const int k = d.split_off + (q & 0x7FFF);
-            for (int j = 0; j < A.split_cnt[k]; ++j) v += ys[A.split_slots[A.split_first[k] + j]];
-        }
-        A.y[d.row0 + i] = v;
-        mx = fmax(mx, fabs(v));
-    }
-    if (A.maxabs_slots) {
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-        if (lane == 0 && mx > 0.0)
-            atomicMax(A.maxabs_slots + ((p * NW + warp) & (kMaxSlots - 1)) * kSlotStride,
-                      (unsigned long long)__double_as_longlong(mx));
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Variant 3: the group stream goes HBM -> L2 (bulk prefetch) -> shared memory
-// (bulk copies, one per array per epoch, mbarrier-tracked) instead of
-// through registers, so the LSU queue carries only the x gathers (L2 hits)
-// and the shared-memory traffic.  NS epochs of stream staged, G steps of
-// gathers in flight per warp.
-constexpr int kStage3 = kPnEpoch * 32 * 8 + kPnEpoch * 32 * 4 + kPnEpoch * 4;   // 24,832 B per epoch
-
-template <int NS, int G>
-__global__ void __launch_bounds__(kT, 1) spmv_panel3_kernel(const PnArgs A) {
-    static_assert(G % kPnB == 0 && G / kPnB <= NS - 1, "gathers read stages loaded ahead");
-    constexpr int U = G;   // unroll (multiple of kPnB)
-    extern __shared__ __align__(128) unsigned char sm3[];
-    const int p = blockIdx.x;
-    const PnPanel d = A.panel[p];
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int yb = (((A.max_rows + 1) * 8 + 127) / 128) * 128;
-    double* ys = reinterpret_cast<double*>(sm3);
-    unsigned char* st = sm3 + yb;
-    uint64_t* full = reinterpret_cast<uint64_t*>(st + NS * kStage3);
-    auto sval = [&](int e) { return reinterpret_cast<const double*>(st + (e % NS) * kStage3); };
-    auto sidx = [&](int e) { return reinterpret_cast<const uint32_t*>(st + (e % NS) * kStage3 + kPnEpoch * 32 * 8); };
-    auto sbase = [&](int e) { return reinterpret_cast<const int32_t*>(st + (e % NS) * kStage3 + kPnEpoch * 32 * 12); };
-
-    const uint64_t polx = pol_evict_last();
-    const uint64_t pol = pol_evict_first();
-    const int PF = A.pf_epochs > 0 ? A.pf_epochs : kPF;
-    const int ne = d.ne, T = ne * kPnB;
-    auto bulk = [&](void* dst, const void* src, int bytes, uint64_t* bar) {
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
-                     ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src), "r"(bytes),
-                     "r"((uint32_t)__cvta_generic_to_shared(bar)), "l"(pol) : "memory");
-    };
-    auto load_epoch = [&](int e) {   // thread 0 only
-        if (e >= ne) return;
-        uint64_t* bar = &full[e % NS];
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)),
-                     "r"(kStage3) : "memory");
-        const int64_t g = (int64_t)d.g0 + (int64_t)e * kPnEpoch;
-        unsigned char* dst = st + (e % NS) * kStage3;
-        bulk(dst, A.gval + g * 32, kPnEpoch * 32 * 8, bar);
-        bulk(dst + kPnEpoch * 32 * 8, A.gidx + g * 32, kPnEpoch * 32 * 4, bar);
-        bulk(dst + kPnEpoch * 32 * 12, A.gbase + g, kPnEpoch * 4, bar);
-    };
-    auto prefetch_epoch = [&](int e) {   // thread 0 only
-        if (e >= ne) return;
-        const int64_t g = (int64_t)d.g0 + (int64_t)e * kPnEpoch;
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.gval + g * 32), "r"(kPnEpoch * 32 * 8) : "memory");
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.gidx + g * 32), "r"(kPnEpoch * 32 * 4) : "memory");
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.gbase + g), "r"(kPnEpoch * 4) : "memory");
-    };
-    auto wait_epoch = [&](int e) {
-        const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&full[e % NS]);
-        const uint32_t par = (uint32_t)((e / NS) & 1);
-        asm volatile("{\n.reg .pred q;\nW3: mbarrier.try_wait.parity.shared::cta.b64 q, [%0], %1;\n@!q bra W3;\n}"
-                     ::"r"(bar), "r"(par) : "memory");
-    };
-
-    if (tid == 0) {
-        for (int s = 0; s < NS; ++s)
-            asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&full[s])));
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    }
-    for (int i = tid; i < ((d.nslots + 15) & ~15); i += kT) ys[i] = 0.0;   // the panel's y slots
-    __syncthreads();
-    if (tid == 0) {
-        for (int e = 0; e < NS; ++e) load_epoch(e);
-        for (int e = NS; e < NS + PF; ++e) prefetch_epoch(e);
-    }
-    if (tid == 32 && d.pf_len > 0) {
-        const uintptr_t a0 = reinterpret_cast<uintptr_t>(A.x_lo + d.pf_col) & ~uintptr_t(15);
-        const uintptr_t a1 = reinterpret_cast<uintptr_t>(A.x_lo + d.pf_col + d.pf_len) & ~uintptr_t(15);
-        for (uintptr_t a = a0; a < a1; a += 32768) {
-            const uint32_t n = (uint32_t)(a1 - a < 32768 ? a1 - a : 32768);
-            asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(a), "r"(n), "l"(polx)
-                         : "memory");
-        }
-    }
-
-    double rx[G];
-    uint32_t ri[G];
-    // gather of step t: group k = (t % kPnB) * 16 + warp of epoch t / kPnB
-    auto issue = [&](int t, double& xv, uint32_t& iv) {
-        const int e = t / kPnB, k = (t % kPnB) * NW + warp;
-        const uint32_t i = sidx(e)[k * 32 + lane];
-        const int32_t b = sbase(e)[k];
-        iv = i;
-        const double* xp = b < A.x_split ? A.x_lo + b : A.x_hi + (b - A.x_split);
-        xv = ld_x(xp + (i & kDeltaMask), polx);   // padding lanes: x[base], added 0 * x into the scratch slot
-    };
-    for (int e = 0; e < G / kPnB && e < ne; ++e) wait_epoch(e);
-#pragma unroll
-    for (int u = 0; u < G; ++u)
-        if (u < T) issue(u, rx[u], ri[u]);
-
-    for (int t0 = 0; t0 < T; t0 += U) {
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int t = t0 + u;
-            if (t >= T) break;
-            const int e = t / kPnB, k = (u % kPnB) * NW + warp;
-            const uint32_t i = ri[u];
-            {
-                int r = (int)(i >> kPnDeltaBits);
-                r = r == (int)(kPnDummy >> kPnDeltaBits) ? A.max_rows : r;
-                ys[r] = fma(sval(e)[k * 32 + lane], rx[u], ys[r]);
-            }
-            const int tn = t + G;
-            if (tn < T) {
-                if (u % kPnB == 0) wait_epoch(tn / kPnB);
-                issue(tn, rx[u], ri[u]);
-            }
-            if (u % kPnB == kPnB - 1) {   // end of epoch e: its stage is free for epoch e + NS
-                __syncthreads();
-                if (tid == 0) {
-                    load_epoch(e + NS);
-                    prefetch_epoch(e + NS + PF);
-                }
-            }
-        }
-    }
-    __syncthreads();
-
-    double mx = 0.0;
-    for (int i = tid; i < d.nrows; i += kT) {
-        const uint16_t q = A.row2slot[d.row0 + i];
-        double v = 0.0;
-        if (q < 0x8000) {
-            v = ys[q];
-        } else {
-            const int k = d.split_off + (q & 0x7FFF);
-            for (int j = 0; j < A.split_cnt[k]; ++j) v += ys[A.split_slots[A.split_first[k] + j]];
-        }
-        A.y[d.row0 + i] = v;
-        mx = fmax(mx, fabs(v));
-    }
-    if (A.maxabs_slots) {
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-        if (lane == 0 && mx > 0.0)
-            atomicMax(A.maxabs_slots + ((p * NW + warp) & (kMaxSlots - 1)) * kSlotStride,
-                      (unsigned long long)__double_as_longlong(mx));
-    }
-}
-
 }  // namespace
 
 cudaError_t launch_panel(const PnArgs& a, cudaStream_t s) {
@@ -562,80 +266,36 @@ cudaError_t launch_panel(const PnArgs& a, cudaStream_t s) {
         mode = e ? atoi(e) : 0;
         const char* f = getenv("SPMV_PN_PF");
         pf_env = f ? atoi(f) : 0;
-        cudaError_t r = cudaSuccess;
         const int smax = 227 * 1024;
-        r = cudaFuncSetAttribute(spmv_panel_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
-        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
-        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
-        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
-        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
-#if SPMV_PN_B == 4
-        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<0, 24, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
-#endif
-        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<0, 16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
-        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<0, kDefD, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
-        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<0, 8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
-        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<24, kDefD, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
-#if SPMV_PN_B == 4
-        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<0, 20, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
-#endif
-        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<15>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
-        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
-        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<13>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
-        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<14>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
-        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
-        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
-        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel2_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel2_kernel<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel3_kernel<4, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel3_kernel<3, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-#if SPMV_PN_B == 4
-        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel3_kernel<4, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-#endif
-#if SPMV_PN_B == 4
-        if (r == cudaSuccess) r = cudaFuncSetAttribute(spmv_panel3_kernel<5, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-#endif
+        cudaError_t r = cudaSuccess;
+        auto attr = [&](const void* k) {
+            if (r == cudaSuccess) r = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
+        };
+        attr((const void*)spmv_panel_kernel<0>);
+        attr((const void*)spmv_panel_kernel<1>);
+        attr((const void*)spmv_panel_kernel<2>);
+        attr((const void*)spmv_panel_kernel<3>);
+        attr((const void*)spmv_panel_kernel<4>);
+        attr((const void*)spmv_panel_kernel<6>);
+        attr((const void*)spmv_panel_kernel<24>);
+        attr((const void*)spmv_panel_kernel<0, 8, 4>);
+        attr((const void*)spmv_panel_kernel<0, 16, 4>);
+        attr((const void*)spmv_panel_kernel<0, 16, 8>);
         if (r != cudaSuccess) return r;
     }
     PnArgs b = a;
-    auto smem3 = [&](int NS) { return (size_t)((((a.max_rows + 1) * 8 + 127) / 128) * 128) + (size_t)NS * kStage3 + 64; };
-    auto smem2 = [&](int G) { return (size_t)((a.max_rows + 2) & ~1) * 8 + (size_t)NW * G * 256; };
     if (pf_env > 0) b.pf_epochs = pf_env;
     switch (mode) {
     case 1: spmv_panel_kernel<1><<<b.n_panels, kT, smem, s>>>(b); break;
     case 2: spmv_panel_kernel<2><<<b.n_panels, kT, smem, s>>>(b); break;
     case 3: spmv_panel_kernel<3><<<b.n_panels, kT, smem, s>>>(b); break;
     case 4: spmv_panel_kernel<4><<<b.n_panels, kT, smem, s>>>(b); break;
-#if SPMV_PN_B == 4
-    case 17: spmv_panel_kernel<0, 24, 8><<<b.n_panels, kT, smem, s>>>(b); break;
-#endif
-    case 18: spmv_panel_kernel<0, 16, 4><<<b.n_panels, kT, smem, s>>>(b); break;
-#if SPMV_PN_B == 4
-    case 19: spmv_panel_kernel<0, 12, 4><<<b.n_panels, kT, smem, s>>>(b); break;
-#endif
-#if SPMV_PN_B == 4
-    case 20: spmv_panel_kernel<0, 20, 4><<<b.n_panels, kT, smem, s>>>(b); break;
-#endif
-    case 15: spmv_panel_kernel<15><<<b.n_panels, kT, smem, s>>>(b); break;
-    case 16: spmv_panel_kernel<16><<<b.n_panels, kT, smem, s>>>(b); break;
-    case 13: spmv_panel_kernel<13><<<b.n_panels, kT, smem, s>>>(b); break;
-    case 14: spmv_panel_kernel<14><<<b.n_panels, kT, smem, s>>>(b); break;
     case 6: spmv_panel_kernel<6><<<b.n_panels, kT, smem, s>>>(b); break;
-    case 5: spmv_panel_kernel<5><<<b.n_panels, kT, smem, s>>>(b); break;
-    case 9: spmv_panel3_kernel<4, 8><<<b.n_panels, kT, smem3(4), s>>>(b); break;
-    case 10: spmv_panel3_kernel<3, 8><<<b.n_panels, kT, smem3(3), s>>>(b); break;
-#if SPMV_PN_B == 4
-    case 11: spmv_panel3_kernel<4, 12><<<b.n_panels, kT, smem3(4), s>>>(b); break;
-#endif
-#if SPMV_PN_B == 4
-    case 12: spmv_panel3_kernel<5, 16><<<b.n_panels, kT, smem3(5), s>>>(b); break;
-#endif
-    case 7: spmv_panel2_kernel<8><<<b.n_panels, kT, smem2(8), s>>>(b); break;
-    case 8: spmv_panel2_kernel<12><<<b.n_panels, kT, smem2(12), s>>>(b); break;
-    case 21: spmv_panel_kernel<0><<<b.n_panels, kT, smem, s>>>(b); break;   // previous default (16, 8)
-    case 22: spmv_panel_kernel<0, 8, 4><<<b.n_panels, kT, smem, s>>>(b); break;
-    case 24: spmv_panel_kernel<24, kDefD, 4><<<b.n_panels, kT, smem, s>>>(b); break;   // no next-panel prefetch
-    default: spmv_panel_kernel<0, kDefD, 4><<<b.n_panels, kT, smem, s>>>(b);
+    case 24: spmv_panel_kernel<24><<<b.n_panels, kT, smem, s>>>(b); break;
+    case 22: spmv_panel_kernel<0, 8, 4><<<b.n_panels, kT, smem, s>>>(b); break;     // ring depth variants
+    case 18: spmv_panel_kernel<0, 16, 4><<<b.n_panels, kT, smem, s>>>(b); break;
+    case 21: spmv_panel_kernel<0, 16, 8><<<b.n_panels, kT, smem, s>>>(b); break;
+    default: spmv_panel_kernel<0><<<b.n_panels, kT, smem, s>>>(b);
     }
     return cudaGetLastError();
 }
