@@ -402,8 +402,9 @@ static spmv_status_t plan_pn(spmv_plan_s* h, PanelPlan& pl, const std::vector<in
                 xcols.push_back({cbp[k] - q0, cbp[k + 1] - q0});
             }
         }
-    } else {   // no SB structure: panels of consecutive rows, no x prefetch / rotation
+    } else {   // no SB structure: panels of consecutive rows, no x prefetch
         ranges.push_back({0, h->m_loc});
+        if (getenv("SPMV_PN_ROT_GENERIC")) xcols.push_back({0, h->n});   // measurement: rotated sweeps
     }
     const int64_t total_slots = spmvb::panel_total_slots(rp, h->m_loc, part);
     // panels: about kPnRowsMax rows, their count a multiple of the SM count

@@ -44,6 +44,11 @@ __device__ __forceinline__ uint64_t pol_evict_last() {
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
+__device__ __forceinline__ double ld_x_na(const double* p, uint64_t pol) {
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
 __device__ __forceinline__ double ld_x(const double* p, uint64_t pol) {
     double v;
     asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
@@ -60,7 +65,8 @@ __device__ __forceinline__ double ld_x(const double* p, uint64_t pol) {
 // MODE (ablation, measurements only; 0 = the kernel): 1 no x gathers (x = 1),
 // 2 no shared-memory y update (register sum), 3 no epoch barriers (racy),
 // 4 no L2 prefetch of the group stream, 6 gathers of a fixed 2 MB window (no
-// dependence on the loaded indices' values), 24 no next-panel prefetch
+// dependence on the loaded indices' values), 24 no next-panel prefetch,
+// 25 x gathers L1::no_allocate
 template <int MODE, int KD_ = kDefD, int KGD_ = 4>
 __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
     constexpr int kD = KD_;                              // steps (groups) in flight per warp
@@ -120,6 +126,7 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
         // the scratch y slot -- a predicated-off load behind a branch made the
         // warp wait for the gather at the branch (measured 1.6x slower)
         const double* xp = b < A.x_split ? A.x_lo + b : A.x_hi + (b - A.x_split);
+        if (MODE == 25) return ld_x_na(xp + (i & kDeltaMask), polx);
         return ld_x(xp + (i & kDeltaMask), polx);
     };
     // L2 prefetch of the panel's group stream kPF epochs ahead (one bulk
@@ -278,6 +285,7 @@ cudaError_t launch_panel(const PnArgs& a, cudaStream_t s) {
         attr((const void*)spmv_panel_kernel<4>);
         attr((const void*)spmv_panel_kernel<6>);
         attr((const void*)spmv_panel_kernel<24>);
+        attr((const void*)spmv_panel_kernel<25>);
         attr((const void*)spmv_panel_kernel<0, 8, 4>);
         attr((const void*)spmv_panel_kernel<0, 16, 4>);
         attr((const void*)spmv_panel_kernel<0, 16, 8>);
@@ -292,6 +300,7 @@ cudaError_t launch_panel(const PnArgs& a, cudaStream_t s) {
     case 4: spmv_panel_kernel<4><<<b.n_panels, kT, smem, s>>>(b); break;
     case 6: spmv_panel_kernel<6><<<b.n_panels, kT, smem, s>>>(b); break;
     case 24: spmv_panel_kernel<24><<<b.n_panels, kT, smem, s>>>(b); break;
+    case 25: spmv_panel_kernel<25><<<b.n_panels, kT, smem, s>>>(b); break;
     case 22: spmv_panel_kernel<0, 8, 4><<<b.n_panels, kT, smem, s>>>(b); break;     // ring depth variants
     case 18: spmv_panel_kernel<0, 16, 4><<<b.n_panels, kT, smem, s>>>(b); break;
     case 21: spmv_panel_kernel<0, 16, 8><<<b.n_panels, kT, smem, s>>>(b); break;
