@@ -56,6 +56,7 @@ class ClockSampler:
     def __init__(self, device_index: int, period_s: float = 0.02):
         self.idx, self.period = device_index, period_s
         self.samples, self.reasons = [], set()
+        self.mem, self.temp, self.power = [], [], []
         self.max_mhz = None
         self._stop = threading.Event()
         self._t = None
@@ -73,6 +74,9 @@ class ClockSampler:
         while not self._stop.is_set():
             try:
                 self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.mem.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_MEM))
+                self.temp.append(self.nv.nvmlDeviceGetTemperature(self.h, self.nv.NVML_TEMPERATURE_GPU))
+                self.power.append(self.nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0)
                 r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
                 for bit, name in self.REASONS.items():
                     if r & bit and bit != 0x1:
@@ -95,8 +99,15 @@ class ClockSampler:
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
-        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        out = {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+               "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        if self.mem:
+            out["mem_mhz"] = statistics.median(self.mem)
+        if self.temp:
+            out["gpu_temp_c_max"] = max(self.temp)
+        if self.power:
+            out["power_w_max"] = max(self.power)
+        return out
 
 
 # --------------------------------------------------------------------------
@@ -496,13 +507,15 @@ def run_ours(args, rank, world, local_rank):
         wm = []
         for _ in range(3):
             apply(xbuf[cur])
-        for _ in range(10):
-            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        # queued back to back (one sync at the end), as in the timed loop: a
+        # per-call sync would put the host's launch latency inside the events
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(10)]
+        for a_, b_ in evs:
             a_.record(stream)
             apply(xbuf[cur])
             b_.record(stream)
-            torch.cuda.synchronize()
-            wm.append(a_.elapsed_time(b_))
+        torch.cuda.synchronize()
+        wm = [a_.elapsed_time(b_) for a_, b_ in evs]
         extra["warm_l2_spmv_ms"] = statistics.median(wm)
 
     # ---------------- reordering effect (the paper's Table 2 analog)
@@ -533,16 +546,15 @@ def run_ours(args, rank, world, local_rank):
             kern = sp.spmv_get_info(hs)["kernel"]
             for _ in range(3):
                 sp.spmv_apply(hs, xs_, ys_, stream=stream)
-            tms = []
-            for _ in range(10):
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(10)]
+            for a_, b_ in evs:   # queued back to back, one sync (no host launch latency inside the events)
                 if l2_flush:
                     flush_buf.fill_(1.0)
-                a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a_.record(stream)
                 sp.spmv_apply(hs, xs_, ys_, stream=stream)
                 b_.record(stream)
-                torch.cuda.synchronize()
-                tms.append(a_.elapsed_time(b_))
+            torch.cuda.synchronize()
+            tms = [a_.elapsed_time(b_) for a_, b_ in evs]
             sp.spmv_destroy(hs)
             return statistics.median(tms), KERNEL_NAMES.get(kern, str(kern))
 
@@ -556,6 +568,45 @@ def run_ours(args, rank, world, local_rank):
                                                            "(the panel's own column sort recovers part of the locality)",
                                "note": "same matrix and x: input order vs SB-reordered (Table 2 analog, P:L51-55)"}
         del xs_, ys_
+
+    # ---------------- cuSPARSE comparator (informational): the
+    # vendor CSR SpMV (torch.mv on a CSR tensor -> cusparseSpMV, fp64, int32
+    # indices) on the same reordered matrix, same L2 protocol; not the product
+    # path and not a baseline arm
+    if world == 1 and not args.no_cusparse:
+        try:
+            if h is not None:
+                sp.spmv_destroy(h)
+                h = None
+            torch.cuda.empty_cache()
+            import synth
+            q = synth.make(args.workload, scramble=0) if p.row_perm is not None else p
+            idt = np.int32 if q.nnz < 2**31 else np.int64
+            crow = torch.from_numpy(np.asarray(q.row_ptr).astype(idt)).to(dev)
+            colq = torch.from_numpy(np.asarray(q.col).astype(idt)).to(dev)
+            valq = torch.from_numpy(np.asarray(q.val)).to(dev)
+            Acs = torch.sparse_csr_tensor(crow, colq, valq, size=(q.m, q.n))
+            xq = torch.rand(q.n, dtype=torch.float64, device=dev)
+            with torch.cuda.stream(stream):
+                for _ in range(3):
+                    yq = torch.mv(Acs, xq)
+                evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(10)]
+                for a_, b_ in evs:   # queued back to back, as for our kernel
+                    if l2_flush:
+                        flush_buf.fill_(1.0)
+                    a_.record(stream)
+                    yq = torch.mv(Acs, xq)
+                    b_.record(stream)
+                torch.cuda.synchronize()
+                tcs = [a_.elapsed_time(b_) for a_, b_ in evs]
+            cms = statistics.median(tcs)
+            extra["cusparse"] = {"spmv_ms": cms, "ours_spmv_ms": avg_spmv_ms, "speedup_ours": cms / avg_spmv_ms,
+                                 "gflops": 2.0 * q.nnz / (cms * 1e-3) / 1e9,
+                                 "what": "torch.mv(CSR fp64, int32 indices) -> cusparseSpMV on the reordered matrix"}
+            del Acs, crow, colq, valq, xq, yq, q
+            torch.cuda.empty_cache()
+        except Exception as e:   # informational only
+            extra["cusparse"] = {"error": f"{type(e).__name__}: {str(e)[:200]}"}
 
     if rank == 0:
         line = {
@@ -607,6 +658,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-gather-peak", action="store_true")
     ap.add_argument("--no-reorder-ref", action="store_true", help="skip the scrambled-order reference timing")
+    ap.add_argument("--no-cusparse", action="store_true", help="skip the cuSPARSE comparator timing")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--parity-rows", type=int, default=200000)
     ap.add_argument("--e2e-steps", type=int, default=10)
