@@ -87,6 +87,7 @@ struct PanelPlan {
     int32_t max_sslots = 0, max_split_n = 0;
     int64_t panels = 0, groups = 0, pad = 0;
     int32_t max_rows = 0;
+    int32_t gather_na = 0;            // x gathers bypass L1 allocation (SPMV_PN_GATHER_NA at create)
     bool ok() const { return panels > 0; }
 };
 
@@ -514,6 +515,12 @@ static spmv_status_t plan_pn(spmv_plan_s* h, PanelPlan& pl, const std::vector<in
     for (int64_t p = 0; p < P; ++p) pl.max_rows = std::max(pl.max_rows, (pd[p].nslots + 15) & ~15);
     pl.groups = G;
     pl.pad = st.pads;
+    // SB blocks: a panel's gathers rarely revisit an x line across groups, and
+    // skipping the L1 allocation leaves the L1 to the loads in flight
+    // (interleaved A/B on C5: -0.9 %, 5 of 6 rounds); matrices without blocks
+    // (C4: band columns revisited) keep allocating (+8 % without)
+    pl.gather_na = h->kind == SPMV_SB ? 1 : 0;
+    if (const char* e = getenv("SPMV_PN_GATHER_NA")) pl.gather_na = atoi(e);
     if (!part) {
         h->bytes_stream = (12 * 32 + 4) * G + 8 * h->m_loc;
         h->kernel = 7;
@@ -1071,6 +1078,7 @@ static void fill_pn_args(const PanelPlan& pl, spmvb::PnArgs& X) {
     X.split_row = pl.d_split_row;
     X.max_sslots = pl.max_sslots;
     X.max_split_n = pl.max_split_n;
+    X.gather_na = pl.gather_na;
 }
 
 static spmv_status_t run(spmv_handle_t h, const double* x, double* y, uint32_t flags, cudaStream_t st,

@@ -201,6 +201,7 @@ struct PnArgs {
     int32_t max_sslots;           // largest sslot_n over the panels (shared-memory copy)
     int32_t max_split_n;          // largest split_n over the panels (shared-memory copy of the descriptors)
     int32_t pf_epochs;        // epochs of the group stream prefetched into L2 ahead (0 = default)
+    int32_t gather_na;        // x gathers L1::no_allocate (plan choice; 0 = allocate)
 };
 cudaError_t launch_panel(const PnArgs& a, cudaStream_t s);
 

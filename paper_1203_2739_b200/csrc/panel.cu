@@ -304,7 +304,9 @@ cudaError_t launch_panel(const PnArgs& a, cudaStream_t s) {
     case 22: spmv_panel_kernel<0, 8, 4><<<b.n_panels, kT, smem, s>>>(b); break;     // ring depth variants
     case 18: spmv_panel_kernel<0, 16, 4><<<b.n_panels, kT, smem, s>>>(b); break;
     case 21: spmv_panel_kernel<0, 16, 8><<<b.n_panels, kT, smem, s>>>(b); break;
-    default: spmv_panel_kernel<0><<<b.n_panels, kT, smem, s>>>(b);
+    default:
+        if (b.gather_na) spmv_panel_kernel<25><<<b.n_panels, kT, smem, s>>>(b);
+        else spmv_panel_kernel<0><<<b.n_panels, kT, smem, s>>>(b);
     }
     return cudaGetLastError();
 }
