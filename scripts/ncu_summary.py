@@ -86,3 +86,32 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def sass_table(path: str, min_exec: int = 1000000) -> str:
+    """Per-SASS-opcode memory counters of the report's first kernel (source page),
+    per executed warp instruction: L1 tag requests (global lines), shared
+    wavefronts, L2 sectors."""
+    out = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    h = rows[1]
+    i_src, i_ex = h.index("Source"), h.index("Instructions Executed")
+    cols = ["L1 Tag Requests Global", "L1 Wavefronts Shared", "L2 Theoretical Sectors Global"]
+    ic = [h.index(c) for c in cols]
+    agg = {}
+    for r in rows[2:]:
+        src = r[i_src].strip()
+        op = src.split()[1] if src.startswith("@") else (src.split() or [""])[0]
+        if not (op.startswith("LDG") or op.startswith("LDS") or op.startswith("STS") or op.startswith("STG")):
+            continue
+        ex = int(r[i_ex] or 0)
+        a = agg.setdefault(op, [0, 0.0, 0.0, 0.0])
+        a[0] += ex
+        for j, i in enumerate(ic):
+            a[j + 1] += float(r[i] or 0)
+    lines = ["| SASS | executed | L1 tag requests (global lines) | shared wavefronts | L2 sectors |", "|---|---|---|---|---|"]
+    for op, a in agg.items():
+        if a[0] >= min_exec:
+            lines.append(f"| {op} | {a[0]} | {a[1] / a[0]:.2f} | {a[2] / a[0]:.2f} | {a[3] / a[0]:.2f} |")
+    return "\n".join(lines)
