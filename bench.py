@@ -450,10 +450,29 @@ def run_ours(args, rank, world, local_rank):
             t = torch.tensor([ems], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = t.item()
+        # the e2e step's own bound: the same H2D and D2H copies, concurrent on
+        # their two streams, with no compute (the host link, full duplex)
+        l0, l1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        l0.record(stream)
+        s_in.wait_stream(stream)
+        s_out.wait_stream(stream)
+        for i in range(Ke):
+            with torch.cuda.stream(s_in):
+                xin[i % 2].copy_(hx, non_blocking=True)
+            with torch.cuda.stream(s_out):
+                hy[i % 2].copy_(yb[i % 2], non_blocking=True)
+        stream.wait_stream(s_in)
+        stream.wait_stream(s_out)
+        l1.record(stream)
+        torch.cuda.synchronize()
+        lms = l0.elapsed_time(l1) / Ke
         e2e = {"value": 2.0 * p.nnz / (ems * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": ems,
                "h2d_bytes_per_step": int(hx.numel() * 8),
                "d2h_bytes_per_step": int(hy[0].numel() * 8 + (8 if power else 0)),
-               "steps": Ke, "pipelined": "3 streams: H2D(i+1) and D2H(i-1) overlap compute(i), double-buffered"}
+               "steps": Ke, "pipelined": "3 streams: H2D(i+1) and D2H(i-1) overlap compute(i), double-buffered",
+               "link_bound_ms_per_step": lms, "frac_of_link_bound": lms / ems,
+               "link_note": "the same H2D + D2H copies concurrently, no compute, measured in this run"}
         del xin, yb, hy
 
     # ---------------- second roofline: the LSU x-gather rate, measured live

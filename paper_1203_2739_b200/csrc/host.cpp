@@ -481,6 +481,11 @@ static spmv_status_t plan_pn(spmv_plan_s* h, PanelPlan& pl, const std::vector<in
         if ((s = upload(h, &pl.d_split_slots, ss.data(), ss.size()))) return s;
         CUDA_TRY(cudaMemcpy(pl.d_panel, desc.data(), P * sizeof(spmvb::PnPanel), cudaMemcpyHostToDevice));
     }
+    pl.max_rows = 0;
+    for (int64_t p = 0; p < P; ++p) pl.max_rows = std::max(pl.max_rows, (pd[p].nslots + 15) & ~15);
+    // padding lanes: the planner's dummy index becomes the scratch y slot
+    // max_rows (delta 0: a valid x read, times the value 0)
+    const uint32_t dummy_dev = (uint32_t)pl.max_rows << spmvb::kPnDeltaBits;
     std::vector<double> tv;
     std::vector<uint32_t> ti;
     for (int64_t p = 0; p < P; ++p) {
@@ -498,7 +503,8 @@ static spmv_status_t plan_pn(spmv_plan_s* h, PanelPlan& pl, const std::vector<in
                 const int64_t blk = (e * spmvb::kPnWarps + w) * 128;
                 for (int l = 0; l < 32; ++l) {
                     tv[blk + (b / 2) * 64 + l * 2 + (b & 1)] = D.gval[g * 32 + l];
-                    ti[blk + l * 4 + b] = D.gidx[g * 32 + l];
+                    const uint32_t i = D.gidx[g * 32 + l];
+                    ti[blk + l * 4 + b] = i == spmvb::kPnDummy ? dummy_dev : i;
                 }
             }
             CUDA_TRY(cudaMemcpy(pl.d_gval + g0 * 32, tv.data(), ng * 32 * 8, cudaMemcpyHostToDevice));
@@ -511,8 +517,6 @@ static spmv_status_t plan_pn(spmv_plan_s* h, PanelPlan& pl, const std::vector<in
         std::vector<int32_t>().swap(D.gbase4);
     }
     pl.panels = P;
-    pl.max_rows = 0;
-    for (int64_t p = 0; p < P; ++p) pl.max_rows = std::max(pl.max_rows, (pd[p].nslots + 15) & ~15);
     pl.groups = G;
     pl.pad = st.pads;
     // SB blocks: a panel's gathers rarely revisit an x line across groups, and

@@ -67,7 +67,7 @@ __device__ __forceinline__ double ld_x(const double* p, uint64_t pol) {
 // 4 no L2 prefetch of the group stream, 6 gathers of a fixed 2 MB window (no
 // dependence on the loaded indices' values), 24 no next-panel prefetch,
 // 25 x gathers L1::no_allocate
-template <int MODE, int KD_ = kDefD, int KGD_ = 4>
+template <int MODE, int KD_ = kDefD, int KGD_ = 4, bool XS = true>
 __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
     constexpr int kD = KD_;                              // steps (groups) in flight per warp
     constexpr int kGD = KGD_;                            // gathers issued this many steps ahead
@@ -97,7 +97,6 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
     const uint64_t polx = pol_evict_last();   // x is the reused operand
     const int PF = A.pf_epochs > 0 ? A.pf_epochs : kPF;
     const int T = d.ne * kPnB;                       // steps per warp
-    const int scratch = A.max_rows;                  // y slot of the padding lanes
 
     double rv[kD];
     uint32_t ri[kD];
@@ -125,7 +124,9 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
         // unconditional: a padding lane reads x[base] (valid) and adds 0 * x into
         // the scratch y slot -- a predicated-off load behind a branch made the
         // warp wait for the gather at the branch (measured 1.6x slower)
-        const double* xp = b < A.x_split ? A.x_lo + b : A.x_hi + (b - A.x_split);
+        // XS: x is split at x_split between two buffers (world > 1: interior |
+        // gathered border); world 1 reads one vector (no select per gather)
+        const double* xp = !XS ? A.x_lo + b : b < A.x_split ? A.x_lo + b : A.x_hi + (b - A.x_split);
         if (MODE == 25) return ld_x_na(xp + (i & kDeltaMask), polx);
         return ld_x(xp + (i & kDeltaMask), polx);
     };
@@ -185,8 +186,8 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
             if (MODE == 2) {
                 racc = fma(rv[u], rx[u % kGD], racc);
             } else {
-                int r = (int)(i >> kPnDeltaBits);
-                r = r == (int)(kPnDummy >> kPnDeltaBits) ? scratch : r;
+                // padding lanes carry the scratch slot (host upload), value 0
+                const int r = (int)(i >> kPnDeltaBits);
                 ys[r] = fma(rv[u], rx[u % kGD], ys[r]);
             }
             // after the warp's last step of an epoch: refill its four slots with
@@ -286,6 +287,8 @@ cudaError_t launch_panel(const PnArgs& a, cudaStream_t s) {
         attr((const void*)spmv_panel_kernel<6>);
         attr((const void*)spmv_panel_kernel<24>);
         attr((const void*)spmv_panel_kernel<25>);
+        attr((const void*)spmv_panel_kernel<0, kDefD, 4, false>);
+        attr((const void*)spmv_panel_kernel<25, kDefD, 4, false>);
         attr((const void*)spmv_panel_kernel<0, 8, 4>);
         attr((const void*)spmv_panel_kernel<0, 16, 4>);
         attr((const void*)spmv_panel_kernel<0, 16, 8>);
@@ -304,9 +307,16 @@ cudaError_t launch_panel(const PnArgs& a, cudaStream_t s) {
     case 22: spmv_panel_kernel<0, 8, 4><<<b.n_panels, kT, smem, s>>>(b); break;     // ring depth variants
     case 18: spmv_panel_kernel<0, 16, 4><<<b.n_panels, kT, smem, s>>>(b); break;
     case 21: spmv_panel_kernel<0, 16, 8><<<b.n_panels, kT, smem, s>>>(b); break;
-    default:
-        if (b.gather_na) spmv_panel_kernel<25><<<b.n_panels, kT, smem, s>>>(b);
-        else spmv_panel_kernel<0><<<b.n_panels, kT, smem, s>>>(b);
+    default: {
+        const bool xs = b.x_split != INT32_MAX;
+        if (b.gather_na) {
+            if (xs) spmv_panel_kernel<25, kDefD, 4, true><<<b.n_panels, kT, smem, s>>>(b);
+            else spmv_panel_kernel<25, kDefD, 4, false><<<b.n_panels, kT, smem, s>>>(b);
+        } else {
+            if (xs) spmv_panel_kernel<0, kDefD, 4, true><<<b.n_panels, kT, smem, s>>>(b);
+            else spmv_panel_kernel<0, kDefD, 4, false><<<b.n_panels, kT, smem, s>>>(b);
+        }
+    }
     }
     return cudaGetLastError();
 }

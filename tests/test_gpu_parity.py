@@ -77,10 +77,16 @@ def _edge_matrix(lengths, n, seed=0, variant="int"):
 @pytest.mark.parametrize("case", ["tile_edges", "long_rows", "empty_rows", "rect_wide", "rect_tall",
                                   "single", "all_empty", "ragged_mix"])
 @pytest.mark.parametrize("variant", ["int", "real"])
-def test_edge_shapes(case, variant):
+@pytest.mark.parametrize("kernel", ["default", "panel"])
+def test_edge_shapes(monkeypatch, case, variant, kernel):
     """Row lengths at every tile/class boundary +-1, rows longer than a tile,
     empty rows, m != n (Table 1's rectangular group), odd row
-    starts (exercise the 128-bit quad peeling)."""
+    starts (exercise the 128-bit quad peeling).  kernel=panel forces the
+    column-sorted panel kernel on small panels (virtual rows of very long
+    rows, the warp fold of rows with > 32 of them, empty panels' rows)."""
+    if kernel == "panel":
+        monkeypatch.setenv("SPMV_KERNEL", "panel")
+        monkeypatch.setenv("SPMV_PN_ROWS", "700")
     T = 2048   # kTileNnz
     rng = np.random.default_rng(5)
     if case == "tile_edges":
@@ -156,6 +162,31 @@ def test_split_k1_and_random_parts():
     h5 = sp.spmv_create(p.m, p.n, p.row_ptr, p.col, p.val, parts=parts, n_parts=5)
     assert np.array_equal(gpu_apply(h5, x, p.m, split=True), oracle.split(p.row_ptr, p.col, p.val, parts, 5, x))
     assert np.array_equal(gpu_apply(h5, x, p.m, split=True, flags=sp.SPMV_SPLIT_LITERAL), y_ref)
+
+
+def test_split_on_panels_edges(monkeypatch):
+    """Fused split on forced small panels: K = 1, parts that never occur, rows
+    whose nonzeros all sit in one part, empty rows, long segments."""
+    monkeypatch.setenv("SPMV_KERNEL", "panel")
+    monkeypatch.setenv("SPMV_PN_ROWS", "700")
+    lengths = [0, 1, 40, 3000, 0, 7, 33, 2] * 150
+    rp, col, val, x = _edge_matrix(lengths, 5000, seed=3)
+    m, nnz = len(lengths), int(rp[-1])
+    y_ref, _ = oracle.spmv(rp, col, val, x)
+    rng = np.random.default_rng(4)
+    cases = {
+        "k1": (np.zeros(nnz, np.int32), 1),
+        "sparse_ids": (rng.choice([0, 3, 6], nnz).astype(np.int32), 7),
+        "row_parts": (np.repeat(np.arange(m) % 4, np.diff(rp)).astype(np.int32), 4),
+        "random": (rng.integers(0, 9, nnz).astype(np.int32), 9),
+    }
+    for what, (parts, K) in cases.items():
+        h = sp.spmv_create(m, 5000, rp, col, val, parts=parts, n_parts=K)
+        assert sp.spmv_get_info(h)["split_kernel"] == 7, what
+        ys = gpu_apply(h, x, m, split=True)
+        assert np.array_equal(ys, oracle.split(rp, col, val, parts, K, x)), what
+        assert np.array_equal(ys, y_ref), what
+        sp.spmv_destroy(h)
 
 
 def test_split_with_permutation():
