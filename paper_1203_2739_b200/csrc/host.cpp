@@ -441,9 +441,15 @@ static spmv_status_t plan_pn(spmv_plan_s* h, PanelPlan& pl, const std::vector<in
     for (int64_t p = 0; p < P; ++p) desc[p] = pd[p].desc;
     spmv_status_t s;
     if ((s = upload(h, &pl.d_panel, desc.data(), P))) return s;
-    if ((s = dalloc(h, &pl.d_gval, G * 32))) return s;
-    if ((s = dalloc(h, &pl.d_gidx, G * 32))) return s;
-    if ((s = dalloc(h, &pl.d_gbase4, G))) return s;
+    // + kPnPadGroups zero groups: the kernel's register ring reads ahead past
+    // the last panel's last epoch without bounds checks
+    const int64_t Gp = G + spmvb::kPnPadGroups;
+    if ((s = dalloc(h, &pl.d_gval, Gp * 32))) return s;
+    if ((s = dalloc(h, &pl.d_gidx, Gp * 32))) return s;
+    if ((s = dalloc(h, &pl.d_gbase4, Gp))) return s;
+    CUDA_TRY(cudaMemset(pl.d_gval + G * 32, 0, spmvb::kPnPadGroups * 32 * sizeof(double)));
+    CUDA_TRY(cudaMemset(pl.d_gidx + G * 32, 0, spmvb::kPnPadGroups * 32 * sizeof(uint32_t)));
+    CUDA_TRY(cudaMemset(pl.d_gbase4 + G, 0, spmvb::kPnPadGroups * sizeof(int32_t)));
     {
         std::vector<uint16_t> r2s(std::max<int64_t>(h->m_loc, 1), 0);
         std::vector<int32_t> sf, sc, sr;

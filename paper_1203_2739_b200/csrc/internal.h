@@ -146,6 +146,7 @@ constexpr int kPnWarps = 16;                 // warps per panel CTA
 #endif
 constexpr int kPnB = SPMV_PN_B;              // groups per warp per epoch
 constexpr int kPnEpoch = kPnWarps * kPnB;    // groups per epoch
+constexpr int kPnPadGroups = 4 * kPnEpoch;  // zero groups after the stream (ring read-ahead, <= 16 steps)
 constexpr int kPnRowsMax = 28672;            // y rows per panel (224 KB of shared memory)
 constexpr int kPnRowsTarget = 16384;         // default panel size: 128 KB of y, the rest of the
                                              // 256 KB L1/shared array stays L1 (measured best, §5.3)

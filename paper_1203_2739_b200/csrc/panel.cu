@@ -103,19 +103,25 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
     int32_t rb[kD];
     double rx[kGD];
     // the warp's four steps s..s+3 (s % 4 == 0) of epoch s / 4 into ring slots u..u+3
-    auto load4 = [&](int s, int u) {
-        const int64_t blk = (int64_t)d.g0 * 32 + ((int64_t)(s >> 2) * kPnWarps + warp) * 128;
-        const double* vp = A.gval + blk + lane * 2;
+    // running stream pointers: the warp's block of the next epoch to load
+    // (the stream is padded by kPnPadGroups groups, so the ring may read
+    // ahead past the panel's last epoch without bounds checks)
+    const int64_t blk0 = (int64_t)d.g0 * 32 + warp * 128;
+    const double* vp = A.gval + blk0 + lane * 2;
+    const uint32_t* ip = A.gidx + blk0 + lane * 4;
+    const int4* bp = reinterpret_cast<const int4*>(A.gbase4 + d.g0) + warp;
+    auto load4 = [&](int u) {   // the next epoch's four steps into ring slots u..u+3
         asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
                      : "=d"(rv[u]), "=d"(rv[u + 1]) : "l"(vp), "l"(pol));
         asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
                      : "=d"(rv[u + 2]), "=d"(rv[u + 3]) : "l"(vp + 64), "l"(pol));
         asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
-                     : "=r"(ri[u]), "=r"(ri[u + 1]), "=r"(ri[u + 2]), "=r"(ri[u + 3])
-                     : "l"(A.gidx + blk + lane * 4), "l"(pol));
+                     : "=r"(ri[u]), "=r"(ri[u + 1]), "=r"(ri[u + 2]), "=r"(ri[u + 3]) : "l"(ip), "l"(pol));
         asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(rb[u]), "=r"(rb[u + 1]), "=r"(rb[u + 2]), "=r"(rb[u + 3])
-                     : "l"(A.gbase4 + d.g0 + ((int64_t)(s >> 2) * kPnWarps + warp) * 4));
+                     : "=r"(rb[u]), "=r"(rb[u + 1]), "=r"(rb[u + 2]), "=r"(rb[u + 3]) : "l"(bp));
+        vp += kPnWarps * 128;
+        ip += kPnWarps * 128;
+        bp += kPnWarps;
     };
     double racc = 0.0;
     auto gather = [&](uint32_t i, int32_t b) -> double {
@@ -126,9 +132,13 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
         // warp wait for the gather at the branch (measured 1.6x slower)
         // XS: x is split at x_split between two buffers (world > 1: interior |
         // gathered border); world 1 reads one vector (no select per gather)
-        const double* xp = !XS ? A.x_lo + b : b < A.x_split ? A.x_lo + b : A.x_hi + (b - A.x_split);
-        if (MODE == 25) return ld_x_na(xp + (i & kDeltaMask), polx);
-        return ld_x(xp + (i & kDeltaMask), polx);
+        // column = base + delta (non-negative, < 2^31): one unsigned 32-bit add
+        // and one wide multiply-add form the address
+        const uint32_t c = (uint32_t)b + (i & kDeltaMask);
+        const double* xa = !XS ? A.x_lo + c
+                               : (int32_t)c < A.x_split ? A.x_lo + c : A.x_hi + (c - (uint32_t)A.x_split);
+        if (MODE == 25) return ld_x_na(xa, polx);
+        return ld_x(xa, polx);
     };
     // L2 prefetch of the panel's group stream kPF epochs ahead (one bulk
     // prefetch per array per epoch, issued by thread 0): the register ring
@@ -171,34 +181,45 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
         }
     }
 #pragma unroll
-    for (int u = 0; u < kD; u += 4)
-        if (u < T) load4(u, u);
+    for (int u = 0; u < kD; u += 4) load4(u);
 #pragma unroll
-    for (int u = 0; u < kGD; ++u)
-        if (u < T) rx[u] = gather(ri[u], rb[u]);
+    for (int u = 0; u < kGD; ++u) rx[u] = gather(ri[u], rb[u]);
 
-    for (int t0 = 0; t0 < T; t0 += kD) {
+    auto step = [&](int u) {   // consume ring slot u (compile-time)
+        const uint32_t i = ri[u];
+        if (MODE == 2) {
+            racc = fma(rv[u], rx[u % kGD], racc);
+        } else {
+            // padding lanes carry the scratch slot (host upload), value 0
+            const int r = (int)(i >> kPnDeltaBits);
+            ys[r] = fma(rv[u], rx[u % kGD], ys[r]);
+        }
+    };
+    auto epoch_end = [&](int t) {
+        if (MODE != 3) __syncthreads();
+        if (MODE != 4) prefetch_epoch(t / kPnB + PF);
+    };
+    // whole ring turns without bounds checks: loads and gathers past the
+    // panel's end read the next panel's (or the pad's) valid stream
+    int t0 = 0;
+    for (; t0 + kD <= T; t0 += kD) {
 #pragma unroll
         for (int u = 0; u < kD; ++u) {
-            const int t = t0 + u;
-            if (t >= T) break;
-            const uint32_t i = ri[u];
-            if (MODE == 2) {
-                racc = fma(rv[u], rx[u % kGD], racc);
-            } else {
-                // padding lanes carry the scratch slot (host upload), value 0
-                const int r = (int)(i >> kPnDeltaBits);
-                ys[r] = fma(rv[u], rx[u % kGD], ys[r]);
-            }
+            step(u);
             // after the warp's last step of an epoch: refill its four slots with
-            // the steps kD later (T is a multiple of 4, so all four exist or none)
-            if (u % 4 == 3 && t + kD - 3 < T) load4(t + kD - 3, u - 3);
-            if (t + kGD < T) rx[u % kGD] = gather(ri[(u + kGD) % kD], rb[(u + kGD) % kD]);
-            if (u % kPnB == kPnB - 1) {                  // epoch boundary (T is a multiple of kPnB)
-                if (MODE != 3) __syncthreads();
-                if (MODE != 4) prefetch_epoch(t / kPnB + PF);
-            }
+            // the steps kD later
+            if (u % 4 == 3) load4(u - 3);
+            rx[u % kGD] = gather(ri[(u + kGD) % kD], rb[(u + kGD) % kD]);
+            if (u % kPnB == kPnB - 1) epoch_end(t0 + u);   // epoch boundary
         }
+    }
+    // the last T - t0 (0, 4 or 8) steps are already in the ring
+#pragma unroll
+    for (int u = 0; u < kD - 4; ++u) {
+        if (t0 + u >= T) break;
+        step(u);
+        if (u + kGD < kD) rx[u % kGD] = gather(ri[(u + kGD) % kD], rb[(u + kGD) % kD]);
+        if (u % kPnB == kPnB - 1) epoch_end(t0 + u);
     }
     if (MODE == 2 && racc == 1.2345) ys[0] = racc;
     // epilogue: y[row] = ys[slot(row)].  The slot loads are batched 16 per
