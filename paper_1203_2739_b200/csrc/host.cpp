@@ -411,16 +411,24 @@ static spmv_status_t plan_pn(spmv_plan_s* h, PanelPlan& pl, const std::vector<in
     // panels: about kPnRowsMax rows, their count a multiple of the SM count
     // when possible (whole waves of one CTA per SM)
     const int64_t sms = spmvb::kernel_num_sms();
-    int64_t target = spmvb::kPnRowsTarget;
+    int64_t target = spmvb::kPnRowsTarget, waves = 0;
     for (int64_t k = 1; k <= 4096; ++k) {
         const int64_t r = (total_slots + sms * k - 1) / (sms * k);
         if (r <= spmvb::kPnRowsTarget) {
             target = r;
+            waves = k;
             break;
         }
     }
-    target = std::max<int64_t>(target, 1024);
-    if (const char* e = getenv("SPMV_PN_ROWS")) target = std::max<int64_t>(1, atoll(e));   // tests / measurements
+    if (target < 1024) {
+        target = 1024;
+        waves = 0;
+    }
+    if (const char* e = getenv("SPMV_PN_ROWS")) {   // tests / measurements
+        target = std::max<int64_t>(1, atoll(e));
+        waves = 0;
+    }
+    if (getenv("SPMV_PN_NOWAVES")) waves = 0;   // measurement: per-range ceil(slots / target)
     if (const char* e = getenv("SPMV_L2_PERSIST_MB")) {   // measurements: L2 set-aside for evict_last lines
         CUDA_TRY(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)atoll(e) << 20));
     }
@@ -428,7 +436,8 @@ static spmv_status_t plan_pn(spmv_plan_s* h, PanelPlan& pl, const std::vector<in
     std::vector<spmvb::PnPanelData> pd;
     spmvb::PnPlanStats st;
     std::string why;
-    if (!spmvb::plan_panel(rp, pcol, pval, ranges, xs, target, pd, st, why, xcols.empty() ? nullptr : &xcols, sms, part))
+    if (!spmvb::plan_panel(rp, pcol, pval, ranges, xs, target, pd, st, why, xcols.empty() ? nullptr : &xcols, sms, part,
+                           waves * sms))
         return SPMV_OK;
     if (st.entries != h->nnz_loc)
         return fail(SPMV_ERR_INTERNAL, "panel plan lost nonzeros (%lld of %lld)", (long long)st.entries,

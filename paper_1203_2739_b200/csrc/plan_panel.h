@@ -40,11 +40,13 @@ struct PnPlanStats {
 // each panel of range k then prefetches a slice of range k+1's columns.
 // part (optional, per CSR nonzero): plan the multiple-SpMxV -- each (row,
 // part) segment gets its own virtual rows, folded in part order.
+// total_panels (optional): split the ranges into this many panels in all
+// (proportional to their slots), e.g. whole waves of one CTA per SM.
 bool plan_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col, const std::vector<double>& val,
                 const std::vector<std::pair<int64_t, int64_t>>& ranges, int64_t x_split, int64_t rows_target,
                 std::vector<PnPanelData>& out, PnPlanStats& st, std::string& why,
                 const std::vector<std::pair<int64_t, int64_t>>* xcols = nullptr, int64_t pf_sms = 148,
-                const std::vector<int32_t>* part = nullptr);
+                const std::vector<int32_t>* part = nullptr, int64_t total_panels = 0);
 
 // y slots (virtual rows) the plan needs for local rows [0, m) (panel sizing).
 int64_t panel_total_slots(const std::vector<int64_t>& rp, int64_t m, const std::vector<int32_t>* part = nullptr);
