@@ -89,6 +89,7 @@ struct PanelPlan {
     int32_t max_rows = 0;
     int32_t gather_na = 0;            // x gathers bypass L1 allocation (SPMV_PN_GATHER_NA at create)
     int32_t ring = 0;                 // register-ring depth (SPMV_PN_RING at create; 0 = default)
+    int32_t pf = 0;                   // L2 prefetch distance in epochs (SPMV_PN_PF at create; 0 = default)
     bool ok() const { return panels > 0; }
 };
 
@@ -542,6 +543,7 @@ static spmv_status_t plan_pn(spmv_plan_s* h, PanelPlan& pl, const std::vector<in
     pl.gather_na = h->kind == SPMV_SB ? 1 : 0;
     if (const char* e = getenv("SPMV_PN_GATHER_NA")) pl.gather_na = atoi(e);
     if (const char* e = getenv("SPMV_PN_RING")) pl.ring = atoi(e);   // measurements: 8, 12 or 16
+    if (const char* e = getenv("SPMV_PN_PF")) pl.pf = atoi(e);       // measurements: epochs ahead
     if (!part) {
         h->bytes_stream = (12 * 32 + 4) * G + 8 * h->m_loc;
         h->kernel = 7;
@@ -1101,6 +1103,7 @@ static void fill_pn_args(const PanelPlan& pl, spmvb::PnArgs& X) {
     X.max_split_n = pl.max_split_n;
     X.gather_na = pl.gather_na;
     X.ring = pl.ring;
+    X.pf_epochs = pl.pf;
 }
 
 static spmv_status_t run(spmv_handle_t h, const double* x, double* y, uint32_t flags, cudaStream_t st,

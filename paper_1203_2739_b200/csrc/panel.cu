@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
 
 cudaError_t launch_panel(const PnArgs& a, cudaStream_t s) {
     if (a.n_panels <= 0) return cudaSuccess;
-    static int mode = -1, pf_env = 0;
+    static int mode = -1;
     // only the panel's y in shared memory: the rest of the 256 KB L1/shared
     // array stays L1, which holds the global loads in flight
     const size_t smem = (size_t)(a.max_rows + 1) * sizeof(double)     // + the padding lanes' scratch slot
@@ -294,8 +294,6 @@ cudaError_t launch_panel(const PnArgs& a, cudaStream_t s) {
     if (mode < 0) {
         const char* e = getenv("SPMV_PN_MODE");   // ablations for measurements only
         mode = e ? atoi(e) : 0;
-        const char* f = getenv("SPMV_PN_PF");
-        pf_env = f ? atoi(f) : 0;
         const int smax = 227 * 1024;
         cudaError_t r = cudaSuccess;
         auto attr = [&](const void* k) {
@@ -327,7 +325,6 @@ cudaError_t launch_panel(const PnArgs& a, cudaStream_t s) {
         if (r != cudaSuccess) return r;
     }
     PnArgs b = a;
-    if (pf_env > 0) b.pf_epochs = pf_env;
     switch (mode) {
     case 1: spmv_panel_kernel<1><<<b.n_panels, kT, smem, s>>>(b); break;
     case 2: spmv_panel_kernel<2><<<b.n_panels, kT, smem, s>>>(b); break;
