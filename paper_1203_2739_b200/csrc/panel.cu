@@ -32,7 +32,8 @@ constexpr int NW = kPnWarps;
 constexpr int kT = NW * 32;
 constexpr int kDefD = 8;    // steps (groups) in flight per warp, the launch default (8 beat 12 and 16 on C5
                             // by 2.5 % / 1 %, interleaved A/B; equal on C4 and C3)
-constexpr int kPF = 8;    // default: epochs of the group stream prefetched into L2 ahead
+constexpr int kPF = 4;    // default: epochs of the group stream prefetched into L2 ahead (with the 8-deep
+                          // ring: 4 beat 2, 3, 5, 6, 8, 12 -- C5 -3.8 %, C4 -2.2 % vs 8, interleaved A/B)
 constexpr uint32_t kDeltaMask = (1u << kPnDeltaBits) - 1u;
 
 __device__ __forceinline__ uint64_t pol_evict_first() {
