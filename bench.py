@@ -114,39 +114,56 @@ class ClockSampler:
 # workload
 # --------------------------------------------------------------------------
 def make_problem(name: str, rank: int, world: int):
-    """Generate (or, for world > 1, share via /dev/shm) the synthetic problem."""
+    """Generate the synthetic problem; for world > 1 rank 0 generates it once
+    and shares it through a memory-mapped cache (/dev/shm, else /tmp, whichever
+    has room: C5 is 14 GB); if neither has room, or writing fails, every rank
+    generates it (the generator is counter-based, so all ranks get the same
+    matrix)."""
     import synth
     if world == 1:
         return synth.make(name)
     import pickle
+    import shutil
     import torch.distributed as dist
-    cache = f"/dev/shm/spmv_bench_{name}_{os.environ.get('MASTER_PORT', '0')}"
+    keys = ("row_ptr", "col", "val", "row_perm", "col_perm", "parts", "owner")
+    port = os.environ.get("MASTER_PORT", "0")
+    p, cache = None, None
     if rank == 0:
         p = synth.make(name)
-        os.makedirs(cache, exist_ok=True)
-        meta = {}
-        for k in ("row_ptr", "col", "val", "row_perm", "col_perm", "parts", "owner"):
-            a = getattr(p, k)
-            if a is not None:
-                np.save(os.path.join(cache, k + ".npy"), a)
-                meta[k] = True
-        with open(os.path.join(cache, "meta.pkl"), "wb") as f:
-            pickle.dump({"p": {k: v for k, v in p.__dict__.items() if not isinstance(v, np.ndarray)}}, f)
-        dist.barrier()
-        dist.barrier()
-        import shutil
+        need = sum(getattr(p, k).nbytes for k in keys if getattr(p, k) is not None) * 1.05 + (64 << 20)
+        for root in ("/dev/shm", "/tmp"):
+            try:
+                if shutil.disk_usage(root).free < need:
+                    continue
+                c = os.path.join(root, f"spmv_bench_{name}_{port}")
+                os.makedirs(c, exist_ok=True)
+                for k in keys:
+                    a = getattr(p, k)
+                    if a is not None:
+                        np.save(os.path.join(c, k + ".npy"), a)
+                with open(os.path.join(c, "meta.pkl"), "wb") as f:
+                    pickle.dump({"p": {k: v for k, v in p.__dict__.items() if not isinstance(v, np.ndarray)}}, f)
+                cache = c
+                break
+            except OSError as e:
+                log(f"problem cache in {root} failed ({e}); trying the next")
+                shutil.rmtree(os.path.join(root, f"spmv_bench_{name}_{port}"), ignore_errors=True)
+    obj = [cache]
+    dist.broadcast_object_list(obj, src=0)
+    cache = obj[0]
+    if rank != 0:
+        if cache is None:
+            p = synth.make(name)
+        else:
+            with open(os.path.join(cache, "meta.pkl"), "rb") as f:
+                d = pickle.load(f)["p"]
+            for k in keys:
+                fn = os.path.join(cache, k + ".npy")
+                d[k] = np.load(fn, mmap_mode="r") if os.path.exists(fn) else None
+            p = synth.Problem(**d)
+    dist.barrier()   # every rank has mapped the files (pages stay mapped after the unlink)
+    if rank == 0 and cache is not None:
         shutil.rmtree(cache, ignore_errors=True)
-        return p
-    dist.barrier()
-    with open(os.path.join(cache, "meta.pkl"), "rb") as f:
-        d = pickle.load(f)["p"]
-    for k in ("row_ptr", "col", "val", "row_perm", "col_perm", "parts", "owner"):
-        fn = os.path.join(cache, k + ".npy")
-        d[k] = np.load(fn, mmap_mode="r") if os.path.exists(fn) else None
-    import synth as S
-    p = S.Problem(**d)
-    # touch before the cache dir is removed (pages stay mapped)
-    dist.barrier()
     return p
 
 

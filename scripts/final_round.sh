@@ -11,6 +11,8 @@ for c in c1 c2 c3 c4 c5; do
   timeout 900 python bench.py --workload $c > gpurun_out/${R}_bench_$c.json 2> gpurun_out/${R}_bench_$c.err
   echo "bench $c rc=$?"
 done
+(cd scripts && timeout 600 python c3_split.py > ../gpurun_out/${R}_c3_split.json 2> ../gpurun_out/${R}_c3_split.err); echo "c3 split rc=$?"
+(cd scripts && timeout 600 python c5_drift.py c5 10 > ../gpurun_out/${R}_c5_drift.jsonl 2> ../gpurun_out/${R}_c5_drift.err); echo "drift rc=$?"
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/${R}_bench_ref.json 2> gpurun_out/${R}_bench_ref.err; echo "ref rc=$?"
 B="python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-parity --no-gather-peak --no-reorder-ref --no-cusparse"
 timeout 600 $B --workload c5 > gpurun_out/${R}_plain_c5.json 2>&1; echo "plain c5 rc=$?"

@@ -1,4 +1,3 @@
 python -m paper_1203_2739_b200.build > /dev/null
 cd scripts
-ROUNDS=6 timeout 900 python ab_inter.py c4 "SPMV_PN_PF=2" "SPMV_PN_PF=3" "SPMV_PN_PF=4" "SPMV_PN_PF=5" 2>&1 | tail -1
-ROUNDS=8 timeout 1200 python ab_inter.py c5 "SPMV_PN_PF=3" "SPMV_PN_PF=4" "SPMV_PN_PF=5" "" 2>&1 | tail -1
+ROUNDS=8 timeout 1200 python ab_inter.py c5 "" "SPMV_PN_ROWS=13000" "SPMV_PN_ROWS=18000" "SPMV_PN_GATHER_NA=0" 2>&1 | tail -1

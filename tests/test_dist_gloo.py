@@ -111,3 +111,38 @@ def test_sb_sharding_gloo(world):
     assert all(r[2] for r in res), res
     assert all(r[3] for r in res), res
     assert sum(r[4] for r in res) == synth.make("c5s").m
+
+
+def _bench_problem_worker(rank, world, port, shm_limit, result_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import shutil
+    import bench
+    if shm_limit:   # pretend neither cache root has room: every rank generates
+        real = shutil.disk_usage
+        shutil.disk_usage = lambda path: real(path)._replace(free=0)
+    p = bench.make_problem("c5s", rank, world)
+    q = synth.make("c5s")
+    same = all(np.array_equal(np.asarray(getattr(p, k)), getattr(q, k))
+               for k in ("row_ptr", "col", "val", "row_perm", "col_perm"))
+    dist.barrier()
+    dist.destroy_process_group()
+    result_q.put((rank, same))
+
+
+@pytest.mark.parametrize("shm_limit", [False, True])
+def test_bench_problem_sharing_gloo(shm_limit):
+    """bench.py's multi-rank problem setup: rank 0 generates and shares the
+    matrix through a memory-mapped cache, or (no room) every rank generates
+    it; either way each rank sees the generator's matrix bit for bit."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bench_problem_worker, args=(r, 2, port, shm_limit, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = sorted(q.get(timeout=300) for _ in range(2))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    assert all(r[1] for r in res), res
