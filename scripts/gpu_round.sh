@@ -1,3 +1,3 @@
 python -m paper_1203_2739_b200.build > /dev/null
-cd scripts
-ROUNDS=8 timeout 1200 python ab_inter.py c5 "" "SPMV_PN_ROWS=13000" "SPMV_PN_ROWS=18000" "SPMV_PN_GATHER_NA=0" 2>&1 | tail -1
+timeout 1200 /usr/local/cuda/bin/compute-sanitizer --tool memcheck --error-exitcode 9 python -m pytest tests/test_gpu_xstage.py tests/test_gpu_parity.py -q -x -k "panel or c5_like or split or edge" 2>&1 | tail -15
+echo "memcheck rc=$?"
