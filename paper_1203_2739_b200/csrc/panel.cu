@@ -1,5 +1,7 @@
-// panel.cu -- column-sorted panel SpMxV y^ = A^ x^ for SB-form
-// matrices (Eq.(1)): the default single-SpMxV kernel of SB handles.
+// panel.cu -- column-sorted panel SpMxV y^ = A^ x^: the default
+// kernel at world 1 (and of SB-form handles, Eq.(1), at any world
+// size), and of the fused multiple-SpMxV, whose (row, part)
+// segments are planned as virtual rows of their own.
 //
 // Why (measured on B200, profiles/r01_micro.json): an x gather
 // costs one L1TEX wavefront per distinct 128-byte line it touches, ~1 line per
@@ -10,7 +12,9 @@
 // -- keeps their y in shared memory, and walks the panel's nonzeros sorted by
 // column (plan_panel.cpp), so a warp's 32 gathers hit only a few lines.
 //
-// One CTA of 16 warps per panel (224 KB of shared memory, 1 CTA per SM).
+// One CTA of 16 warps per panel (y of up to 28,672 slots in shared memory,
+// about 16 K by default so the rest of the L1 holds the loads in flight; 1
+// CTA per SM; panel counts sum to whole waves).
 // Warp w processes groups g0 + 16 t + w, t = 0, 1, ...; every kPnB steps is an
 // epoch boundary (__syncthreads): within an epoch all rows are distinct, so
 // the shared-memory read-modify-writes y_s[r] += v * x[c] never race.
@@ -74,8 +78,8 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
     constexpr int kD = KD_;                              // steps (groups) in flight per warp
     constexpr int kGD = KGD_;                            // gathers issued this many steps ahead
     // the ring is refilled four slots at a time after the last step of a warp's
-    // epoch, so 9..12 (kD - 3..kD) steps are loaded ahead; a gather needs its
-    // step's index loaded: kGD <= kD - 4
+    // epoch, so kD - 3..kD steps are loaded ahead; a gather needs its step's
+    // index loaded: kGD <= kD - 4
     static_assert(kPnB == 4 && kD % 4 == 0 && kGD >= 1 && kGD <= kD - 4, "ring geometry");
     extern __shared__ __align__(16) double ys[];
     const int p = blockIdx.x;
@@ -104,7 +108,6 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
     uint32_t ri[kD];
     int32_t rb[kD];
     double rx[kGD];
-    // the warp's four steps s..s+3 (s % 4 == 0) of epoch s / 4 into ring slots u..u+3
     // running stream pointers: the warp's block of the next epoch to load
     // (the stream is padded by kPnPadGroups groups, so the ring may read
     // ahead past the panel's last epoch without bounds checks)
