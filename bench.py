@@ -494,6 +494,30 @@ def run_ours(args, rank, world, local_rank):
 
     # ---------------- second roofline: the LSU x-gather rate, measured live
     gather = None
+    if not args.no_gather_peak and info["kernel"] == 7 and not split and info["gather_sectors"] > 0:
+        # the panel kernel's second roofline: bytes crossing L2 -> SM per launch
+        # (its group stream + the distinct 32-byte x sectors its gathers request,
+        # counted at plan time) against an L2-resident LDG stream measured live
+        gb = torch.rand((16 << 20) // 8, dtype=torch.float64, device=dev)    # 16 MB, L2-resident
+        sink = torch.zeros(1, dtype=torch.float64, device=dev)
+        cnt = 8 << 30
+        for _ in range(2):
+            sp.spmv_diag_micro(1, 0, gb, gb.numel() * 8, cnt, sink, stream=stream)
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(3):
+            sp.spmv_diag_micro(1, 0, gb, gb.numel() * 8, cnt, sink, stream=stream)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        fpeak = 3 * cnt / (g0.elapsed_time(g1) * 1e-3) / 1e9
+        fbytes = info["bytes_stream"] + 32 * info["gather_sectors"]
+        fach = fbytes / (avg_spmv_ms * 1e-3) / 1e9
+        gather = {"bound": "l2_to_sm", "achieved": fach, "peak": fpeak, "unit": "GB/s", "frac": fach / fpeak,
+                  "bytes_per_launch": fbytes,
+                  "note": "group stream + distinct 32-byte x sectors of the gathers (plan-time count) per launch / "
+                          "SpMxV time; peak = 128-bit LDG stream over a 16 MB L2-resident buffer, measured in this "
+                          "run (spmv_diag_micro kind 1)"}
+        del gb
     if not args.no_gather_peak and info["kernel"] != 7:   # the panel kernel does not gather once per nonzero
         gx = torch.rand(4 << 20, dtype=torch.float64, device=dev)      # 32 MB, L2-resident
         sink = torch.zeros(1, dtype=torch.float64, device=dev)

@@ -173,6 +173,9 @@ typedef struct {
                                      per (row, part) segment (default), 3 row-major part segments,
                                      1 part-major tiles; 0 without a split */
     int32_t reserved;
+    int64_t gather_sectors;       /* panel kernel (7): distinct 32-byte x sectors its gathers request per
+                                     launch (counted at plan time); with bytes_stream, the bytes that cross
+                                     L2 -> SM per launch (the kernel's second roofline) */
 } spmv_info_t;
 
 spmv_status_t spmv_get_info(spmv_handle_t h, spmv_info_t* info);

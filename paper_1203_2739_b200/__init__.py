@@ -63,7 +63,7 @@ class spmv_info_t(ctypes.Structure):
         "bytes_stream")] + [
         (k, ctypes.c_int32) for k in ("n_parts", "rank", "world", "kind", "has_owner_map", "kernel",
                                       "split_kernel")] + [
-        ("reserved", ctypes.c_int32)]
+        ("reserved", ctypes.c_int32), ("gather_sectors", ctypes.c_int64)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}

@@ -85,7 +85,7 @@ struct PanelPlan {
     uint16_t* d_split_slots = nullptr;
     int32_t* d_split_row = nullptr;
     int32_t max_sslots = 0, max_split_n = 0;
-    int64_t panels = 0, groups = 0, pad = 0;
+    int64_t panels = 0, groups = 0, pad = 0, gsectors = 0;
     int32_t max_rows = 0;
     int32_t gather_na = 0;            // x gathers bypass L1 allocation (SPMV_PN_GATHER_NA at create)
     int32_t ring = 0;                 // register-ring depth (SPMV_PN_RING at create; 0 = default)
@@ -536,6 +536,7 @@ static spmv_status_t plan_pn(spmv_plan_s* h, PanelPlan& pl, const std::vector<in
     pl.panels = P;
     pl.groups = G;
     pl.pad = st.pads;
+    pl.gsectors = st.gsectors;
     // SB blocks: a panel's gathers rarely revisit an x line across groups, and
     // skipping the L1 allocation leaves the L1 to the loads in flight
     // (interleaved A/B on C5: -0.9 %, 5 of 6 rounds); matrices without blocks
@@ -1316,6 +1317,7 @@ spmv_status_t spmv_get_info(spmv_handle_t h, spmv_info_t* info) {
     info->xs_pad_slots = h->kernel == 7 ? h->pn.pad : h->xs_pad;
     info->bytes_stream = h->bytes_stream;
     info->kernel = h->kernel;
+    info->gather_sectors = h->kernel == 7 ? h->pn.gsectors : 0;
     info->split_kernel = h->n_parts == 0 ? 0
                          : (h->pns.ok() && h->kernel != 2) ? 7
                          : (h->split_rowmajor && h->kernel != 2 && !getenv("SPMV_SPLIT_PARTMAJOR")) ? 3 : 1;

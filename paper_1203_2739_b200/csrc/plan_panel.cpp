@@ -374,6 +374,18 @@ void build_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col
     for (int64_t g = 0; g < G; ++g) {
         emit_group(&gents[g * 32], gbases[g], slot, P);
         w += y_wavefronts(&P.gidx[g * 32]);
+        // distinct 32-byte x sectors the group's gather requests (padding
+        // lanes read x[base]): the gather bytes that cross L2 -> SM
+        int64_t sec[32];
+        int ns = 0;
+        for (int k = 0; k < 32; ++k) {
+            const int64_t c = gents[g * 32 + k].row >= 0 ? gents[g * 32 + k].col : gbases[g];
+            const int64_t s = c < x_split ? (c >> 2) : ((int64_t(1) << 40) | ((c - x_split) >> 2));
+            bool seen = false;
+            for (int j = 0; j < ns && !seen; ++j) seen = sec[j] == s;
+            if (!seen) sec[ns++] = s;
+        }
+        P.gsectors += ns;
     }
     P.ywf1 = G ? w / G : 0;
     P.gbase4.resize(P.gbase.size());
@@ -524,6 +536,7 @@ bool plan_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col,
         st.entries += P.entries;
         st.pads += P.pads;
         st.deferred += P.deferred;
+        st.gsectors += P.gsectors;
         st.epochs += P.desc.ne;
         st.ywf0 += P.ywf0 * (double)P.gbase.size();
         st.ywf1 += P.ywf1 * (double)P.gbase.size();
