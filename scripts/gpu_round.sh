@@ -1,3 +1,4 @@
 python -m paper_1203_2739_b200.build > /dev/null
-timeout 1200 /usr/local/cuda/bin/compute-sanitizer --tool memcheck --error-exitcode 9 python -m pytest tests/test_gpu_xstage.py tests/test_gpu_parity.py -q -x -k "panel or c5_like or split or edge" 2>&1 | tail -15
-echo "memcheck rc=$?"
+for c in c4 c5; do
+timeout 600 python bench.py --workload $c --no-e2e --no-cpu-baseline --no-parity --no-reorder-ref --no-cusparse 2>/dev/null | python -c "import json,sys; j=json.loads(sys.stdin.read()); print('$c', j['spmv_ms'], j['roofline']['frac'], j['roofline_gather'])"
+done
