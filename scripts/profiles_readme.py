@@ -20,6 +20,13 @@ step (pinned host memory, copies pipelined against compute).  cuSPARSE = `cuspar
 `torch.mv` on an fp64 CSR tensor) on the same reordered matrix, same protocol, informational.
 
 {table}
+Second roofline of the panel kernel (`roofline_gather` in the C4/C5 lines): bytes crossing
+L2 → SM per launch (group stream + the gathers' distinct 32-byte x sectors, counted at plan time)
+over the SpMxV time, against a 128-bit LDG stream over an L2-resident buffer measured in the same
+run: C5 {b5['roofline_gather']['bytes_per_launch'] / 1e9:.1f} GB per launch, {b5['roofline_gather']['achieved']:,.0f} of {b5['roofline_gather']['peak']:,.0f} GB/s =
+**{b5['roofline_gather']['frac']:.2f}**; C4 {b4['roofline_gather']['bytes_per_launch'] / 1e9:.2f} GB, {b4['roofline_gather']['frac']:.2f}.  This fabric, not HBM, is what the C5
+kernel runs into (DESIGN §5.1–5.2).
+
 C5 and C4 time a power iteration (SpMxV with fused max-abs, max finish, x-update); the table's
 SpMxV column is the SpMxV launch alone.  The C5 SpMxV runs under the board's power cap: a cold
 GPU does it in {min(r['median_ms'] for r in drift[:1]):.2f} ms at {drift[0]['sm']} MHz, a warm one in
