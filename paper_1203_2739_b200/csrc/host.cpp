@@ -150,6 +150,7 @@ struct spmv_plan_s {
     int32_t* d_frowseg = nullptr;     // [m_loc+1] first segment of each row
     int32_t* d_fsegptr = nullptr;     // [S+1] segment start positions (same positions as the CSR rows)
     bool split_rowmajor = true;
+    std::vector<int64_t> blk_slots;   // SB: y slots per block over the whole matrix (panel cuts)
     int32_t* d_colinv = nullptr;      // ORIGINAL mode: x^[c] = x[colinv[c]]
     int32_t* d_rowperm = nullptr;     // ORIGINAL mode: y[i] = y^[row_perm[i]]
     double* d_xhat = nullptr;
@@ -409,7 +410,13 @@ static spmv_status_t plan_pn(spmv_plan_s* h, PanelPlan& pl, const std::vector<in
         ranges.push_back({0, h->m_loc});
         if (getenv("SPMV_PN_ROT_GENERIC")) xcols.push_back({0, h->n});   // measurement: rotated sweeps
     }
-    const int64_t total_slots = spmvb::panel_total_slots(rp, h->m_loc, part);
+    // the global per-block counts (SB, no split) decide the cuts, else this rank's rows
+    const bool global = h->kind == SPMV_SB && !part && (int)h->blk_slots.size() == K;
+    int64_t total_slots = 0;
+    if (global)
+        for (int64_t v : h->blk_slots) total_slots += v;
+    else
+        total_slots = spmvb::panel_total_slots(rp, h->m_loc, part);
     // panels: about kPnRowsMax rows, their count a multiple of the SM count
     // when possible (whole waves of one CTA per SM)
     const int64_t sms = spmvb::kernel_num_sms();
@@ -438,8 +445,14 @@ static spmv_status_t plan_pn(spmv_plan_s* h, PanelPlan& pl, const std::vector<in
     std::vector<spmvb::PnPanelData> pd;
     spmvb::PnPlanStats st;
     std::string why;
+    std::vector<int64_t> range_panels;
+    if (global) {
+        const std::vector<int64_t> np_all = spmvb::panel_counts(h->blk_slots, target, waves * sms);
+        for (int k = 0; k < K; ++k)
+            if (std::min(rbp[k + 1], R1) > std::max(rbp[k], R0)) range_panels.push_back(np_all[k]);
+    }
     if (!spmvb::plan_panel(rp, pcol, pval, ranges, xs, target, pd, st, why, xcols.empty() ? nullptr : &xcols, sms, part,
-                           waves * sms))
+                           waves * sms, global ? &range_panels : nullptr))
         return SPMV_OK;
     if (st.entries != h->nnz_loc)
         return fail(SPMV_ERR_INTERNAL, "panel plan lost nonzeros (%lld of %lld)", (long long)st.entries,
@@ -973,6 +986,21 @@ static spmv_status_t create_impl(int64_t m, int64_t n, int64_t nnz, const int64_
     // ---------------- fused multiple-SpMxV on panels (a8): (row, part) virtual rows
     if (n_parts && world == 1 && nnz_loc > 0 && !getenv("SPMV_SPLIT_ROWTILE")) {
         if ((s = plan_pn(h, h->pns, rp, pcol, pval, rbp, cbp, &ppart))) return s;
+    }
+
+    // global per-block y-slot counts (SB): every rank cuts its blocks into the
+    // same panels as a single GPU would, so the summation order of a row --
+    // and y -- does not depend on the number of GPUs
+    if (blocks && h->kind == SPMV_SB && nnz_loc > 0) {
+        const int K = (int)rbp.size() - 2;
+        h->blk_slots.assign(K, 0);
+        std::vector<int64_t> loc(K, 0);
+        for (int64_t i = 0; i < m; ++i) {
+            const int64_t nr = row_perm ? row_perm[i] : i;
+            const int k = (int)(std::upper_bound(rbp.begin(), rbp.begin() + K + 1, nr) - rbp.begin()) - 1;
+            if (k >= 0 && k < K) loc[k] += spmvb::row_slots(row_ptr[i + 1] - row_ptr[i]);
+        }
+        h->blk_slots = loc;
     }
 
     // ------------------------------------ x-staged plan (SB handles, a5/a6)

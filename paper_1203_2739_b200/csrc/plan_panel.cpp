@@ -401,41 +401,22 @@ bool plan_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col,
                 const std::vector<std::pair<int64_t, int64_t>>& ranges, int64_t x_split, int64_t rows_target,
                 std::vector<PnPanelData>& out, PnPlanStats& st, std::string& why,
                 const std::vector<std::pair<int64_t, int64_t>>* xcols, int64_t pf_sms,
-                const std::vector<int32_t>* part, int64_t total_panels) {
+                const std::vector<int32_t>* part, int64_t total_panels,
+                const std::vector<int64_t>* range_panels) {
     out.clear();
     st = PnPlanStats{};
     const int64_t R = std::min<int64_t>(std::max<int64_t>(rows_target, 1), kPnRowsMax);
     const int32_t* pp = part ? part->data() : nullptr;
     auto slots_of = [&](int64_t r) -> int64_t { return row_vrows(rp.data(), pp, r, nullptr); };
-    // panels per range: ceil(slots / R), or -- given a total (whole waves of
-    // one CTA per SM) -- shares of that total proportional to the ranges'
-    // slots (largest remainder), so several SB blocks still add up to whole
-    // waves (C5: 64 blocks x 63 panels = 27.2 waves left a 0.24-wave tail)
-    std::vector<int64_t> np_of(ranges.size(), 0), Sk(ranges.size(), 0);
-    {
-        int64_t Stot = 0;
-        for (size_t k = 0; k < ranges.size(); ++k) {
+    // panels per range (panel_counts), unless the caller fixed them
+    std::vector<int64_t> np_of;
+    if (range_panels && range_panels->size() == ranges.size()) {
+        np_of = *range_panels;
+    } else {
+        std::vector<int64_t> Sk(ranges.size(), 0);
+        for (size_t k = 0; k < ranges.size(); ++k)
             for (int64_t r = ranges[k].first; r < ranges[k].second; ++r) Sk[k] += slots_of(r);
-            Stot += Sk[k];
-            np_of[k] = (Sk[k] + R - 1) / R;
-        }
-        if (total_panels > 0 && Stot > 0) {
-            std::vector<std::pair<double, size_t>> rem;
-            int64_t given = 0;
-            for (size_t k = 0; k < ranges.size(); ++k) {
-                const double q = (double)total_panels * (double)Sk[k] / (double)Stot;
-                np_of[k] = Sk[k] > 0 ? std::max<int64_t>(1, (int64_t)q) : 0;
-                given += np_of[k];
-                rem.push_back({q - (double)(int64_t)q, k});
-            }
-            std::sort(rem.begin(), rem.end(), [](const auto& a, const auto& b) {
-                return a.first != b.first ? a.first > b.first : a.second < b.second;
-            });
-            for (size_t j = 0; given < total_panels && j < rem.size(); ++j)
-                if (Sk[rem[j].second] > 0) { ++np_of[rem[j].second]; ++given; }
-            for (size_t k = 0; k < ranges.size(); ++k)   // never above the slot cap
-                np_of[k] = std::max(np_of[k], (Sk[k] + kPnRowsMax - 1) / kPnRowsMax);
-        }
+        np_of = panel_counts(Sk, R, total_panels);
     }
     for (size_t k = 0; k < ranges.size(); ++k) {
         const auto& rg = ranges[k];
@@ -547,6 +528,40 @@ bool plan_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col,
         st.ywf1 /= (double)g;
     }
     return true;
+}
+
+int64_t row_slots(int64_t L) { return L > kPnSplitAt ? (L + kPnVMax - 1) / kPnVMax : 1; }
+
+std::vector<int64_t> panel_counts(const std::vector<int64_t>& Sk, int64_t R, int64_t total) {
+    // ceil(slots / R) per range, or -- given a total (whole waves of one CTA
+    // per SM) -- shares of that total proportional to the ranges' slots
+    // (largest remainder), so several SB blocks still add up to whole waves
+    // (C5: 64 blocks x 63 panels = 27.2 waves left a 0.24-wave tail)
+    R = std::min<int64_t>(std::max<int64_t>(R, 1), kPnRowsMax);
+    std::vector<int64_t> np(Sk.size(), 0);
+    int64_t Stot = 0;
+    for (size_t k = 0; k < Sk.size(); ++k) {
+        Stot += Sk[k];
+        np[k] = (Sk[k] + R - 1) / R;
+    }
+    if (total > 0 && Stot > 0) {
+        std::vector<std::pair<double, size_t>> rem;
+        int64_t given = 0;
+        for (size_t k = 0; k < Sk.size(); ++k) {
+            const double q = (double)total * (double)Sk[k] / (double)Stot;
+            np[k] = Sk[k] > 0 ? std::max<int64_t>(1, (int64_t)q) : 0;
+            given += np[k];
+            rem.push_back({q - (double)(int64_t)q, k});
+        }
+        std::sort(rem.begin(), rem.end(), [](const auto& a, const auto& b) {
+            return a.first != b.first ? a.first > b.first : a.second < b.second;
+        });
+        for (size_t j = 0; given < total && j < rem.size(); ++j)
+            if (Sk[rem[j].second] > 0) { ++np[rem[j].second]; ++given; }
+        for (size_t k = 0; k < Sk.size(); ++k)   // never above the slot cap
+            np[k] = std::max(np[k], (Sk[k] + kPnRowsMax - 1) / kPnRowsMax);
+    }
+    return np;
 }
 
 int64_t panel_total_slots(const std::vector<int64_t>& rp, int64_t m, const std::vector<int32_t>* part) {

@@ -43,11 +43,22 @@ struct PnPlanStats {
 // part) segment gets its own virtual rows, folded in part order.
 // total_panels (optional): split the ranges into this many panels in all
 // (proportional to their slots), e.g. whole waves of one CTA per SM.
+// range_panels (optional): the panel count of each range, fixed by the caller.
 bool plan_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col, const std::vector<double>& val,
                 const std::vector<std::pair<int64_t, int64_t>>& ranges, int64_t x_split, int64_t rows_target,
                 std::vector<PnPanelData>& out, PnPlanStats& st, std::string& why,
                 const std::vector<std::pair<int64_t, int64_t>>* xcols = nullptr, int64_t pf_sms = 148,
-                const std::vector<int32_t>* part = nullptr, int64_t total_panels = 0);
+                const std::vector<int32_t>* part = nullptr, int64_t total_panels = 0,
+                const std::vector<int64_t>* range_panels = nullptr);
+
+// y slots of a row of L nonzeros without a split (its virtual rows).
+int64_t row_slots(int64_t L);
+
+// Panels per range from the ranges' slot counts: ceil(S_k / R), or shares of
+// `total` (> 0) proportional to S_k (largest remainder), never fewer than
+// the slot cap allows.  Depends only on (S, R, total), so a multi-GPU rank
+// that passes the global per-block counts gets the same cuts as world 1.
+std::vector<int64_t> panel_counts(const std::vector<int64_t>& Sk, int64_t R, int64_t total);
 
 // y slots (virtual rows) the plan needs for local rows [0, m) (panel sizing).
 int64_t panel_total_slots(const std::vector<int64_t>& rp, int64_t m, const std::vector<int32_t>* part = nullptr);
