@@ -441,7 +441,11 @@ static spmv_status_t plan_pn(spmv_plan_s* h, PanelPlan& pl, const std::vector<in
     if (const char* e = getenv("SPMV_L2_PERSIST_MB")) {   // measurements: L2 set-aside for evict_last lines
         CUDA_TRY(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)atoll(e) << 20));
     }
-    const int64_t xs = h->world > 1 ? h->x_int_len : INT32_MAX;
+    // groups never mix interior and border columns at world > 1 (two x
+    // buffers); SB plans keep the same rule at world 1 (C_B starts at
+    // cbp[K]) so the groups -- and every row's summation order -- are the
+    // same on any number of GPUs
+    const int64_t xs = h->world > 1 ? h->x_int_len : (h->kind == SPMV_SB ? cbp[K] : INT32_MAX);
     std::vector<spmvb::PnPanelData> pd;
     spmvb::PnPlanStats st;
     std::string why;
