@@ -253,6 +253,19 @@ spmv_status_t spmv_xs_plan_check(int64_t m, int64_t n, const int64_t* row_ptr, c
 spmv_status_t spmv_pn_plan_check(int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
                                  const spmv_blocks_t* blocks, int64_t rows_target, int64_t* stats);
 
+/* Host-only test hook of the multi-GPU determinism of the panel plan (SURVEY
+ * 8(e)): for each rank of `world`, builds that rank's local CSR of a PERMUTED
+ * SB matrix (its blocks' rows; columns in the rank's x layout [interior |
+ * C_B]), plans its panels exactly as spmv_create does (sms = the SM count the
+ * whole-wave rule assumes) and hashes, per block, the panels' row ranges and
+ * every group's (global row, virtual-row rank, global column, value bits) in
+ * issue order.  out[r * K + k] = rank r's hash of block k, 0 for blocks it
+ * does not own.  Equal hashes at world 1 and world G mean equal summation
+ * orders, so y is bit-identical across GPU counts.  USAGE / DATA on bad
+ * arguments (blocks must be SB). */
+spmv_status_t spmv_pn_shard_hash(int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
+                                 const spmv_blocks_t* blocks, int32_t world, int32_t sms, int64_t* out);
+
 /* Design microbenchmarks (diag2.cu): kind 1 L2->SM LDG.128 bandwidth over the
  * L2-resident `buf` (`bytes` long, `count` bytes read in total); kind 2 bulk-copy
  * L2->shared bandwidth, param = cluster size 1/2/4/8 (multicast when > 1),

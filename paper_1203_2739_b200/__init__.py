@@ -35,7 +35,7 @@ EXPORTED = ["spmv_create", "spmv_apply", "spmv_split_apply", "spmv_destroy", "sp
             "spmv_maxabs", "spmv_normalize", "spmv_debug_copy_csr", "spmv_nccl_unique_id",
             "spmv_status_string", "spmv_last_error", "spmv_version", "spmv_shard_plan",
             "spmv_diag_read", "spmv_diag_gather", "spmv_diag_csr", "spmv_diag_gather_mode", "spmv_diag_micro",
-            "spmv_xs_plan_check", "spmv_pn_plan_check"]
+            "spmv_xs_plan_check", "spmv_pn_plan_check", "spmv_pn_shard_hash"]
 
 
 class SpmvError(RuntimeError):
@@ -97,6 +97,7 @@ def lib():
         L.spmv_diag_micro.argtypes = [i32, i32, vp, i64, i64, vp, vp]
         L.spmv_xs_plan_check.argtypes = [i64, i64, vp, vp, vp, vp, i64, vp]
         L.spmv_pn_plan_check.argtypes = [i64, i64, vp, vp, vp, vp, i64, vp]
+        L.spmv_pn_shard_hash.argtypes = [i64, i64, vp, vp, vp, vp, i32, i32, vp]
         L.spmv_shard_plan.argtypes = [vp, i64, i64, i32, i32, vp]
         L.spmv_status_string.argtypes = [i32]
         L.spmv_status_string.restype = ctypes.c_char_p
@@ -269,6 +270,21 @@ def spmv_pn_plan_check(m: int, n: int, row_ptr, col, val, blocks, rows_target: i
     d["y_wavefronts_natural"] = stats[6] / 1000.0
     d["y_wavefronts_coloured"] = stats[7] / 1000.0
     return d
+
+
+def spmv_pn_shard_hash(m: int, n: int, row_ptr, col, val, blocks, world: int, sms: int = 148) -> np.ndarray:
+    """Host-only: per-rank, per-block hashes of the panel plan's summation order (see spmv.h);
+    returns an int64 array [world, K]."""
+    rp = _np(row_ptr, np.int64)
+    ci = _np(col, np.int32)
+    va = _np(val, np.float64)
+    rbp = _np(blocks["row_block_ptr"], np.int64)
+    cbp = _np(blocks["col_block_ptr"], np.int64)
+    b = _Blocks(int(blocks["kind"]), int(blocks["K"]), rbp.ctypes.data, cbp.ctypes.data, None)
+    out = np.zeros((world, int(blocks["K"])), dtype=np.int64)
+    _check(lib().spmv_pn_shard_hash(m, n, _addr(rp), _addr(ci), _addr(va), ctypes.byref(b), world, sms,
+                                    out.ctypes.data), "spmv_pn_shard_hash")
+    return out
 
 
 def spmv_apply(h, x, y, flags: int = 0, stream=None, x_len: int | None = None, y_len: int | None = None):

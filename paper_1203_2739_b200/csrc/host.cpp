@@ -388,75 +388,96 @@ static spmv_status_t plan_xs(spmv_plan_s* h, const std::vector<int64_t>& rp, con
     return SPMV_OK;
 }
 
+// The panel plan's layout decisions for one rank (pure host logic, shared by
+// plan_pn and the spmv_pn_shard_hash test hook): its row ranges (SB blocks,
+// else all rows), their interior column ranges (rotation, x prefetch), the
+// panel size target and whole-wave count, the x split, and -- for SB
+// handles without a split -- each range's panel count from the global
+// per-block slot counts, so a block's panels do not depend on the GPU count.
+struct PnSetup {
+    std::vector<std::pair<int64_t, int64_t>> ranges, xcols;
+    std::vector<int64_t> range_panels;
+    int64_t target = 0, waves = 0, xs = INT32_MAX, sms = 148;
+    bool global = false;
+};
+
+static PnSetup pn_setup(int kind, int world, int64_t row_begin, int64_t m_loc, int64_t x_int_begin, int64_t x_int_len,
+                        int64_t n, const std::vector<int64_t>& rbp, const std::vector<int64_t>& cbp,
+                        const std::vector<int64_t>& blk_slots, const std::vector<int64_t>& rp,
+                        const std::vector<int32_t>* part, int64_t sms) {
+    PnSetup S;
+    S.sms = sms;
+    const int K = (int)rbp.size() - 2;
+    const int64_t R0 = row_begin, R1 = row_begin + m_loc;
+    const int64_t q0 = world > 1 ? x_int_begin : 0;
+    if (kind == SPMV_SB) {
+        for (int k = 0; k < K; ++k) {
+            const int64_t a = std::max(rbp[k], R0), b = std::min(rbp[k + 1], R1);
+            if (b > a) {
+                S.ranges.push_back({a - R0, b - R0});
+                S.xcols.push_back({cbp[k] - q0, cbp[k + 1] - q0});
+            }
+        }
+    } else {   // no SB structure: panels of consecutive rows, no x prefetch
+        S.ranges.push_back({0, m_loc});
+        if (getenv("SPMV_PN_ROT_GENERIC")) S.xcols.push_back({0, n});   // measurement: rotated sweeps
+    }
+    // the global per-block counts (SB, no split) decide the cuts, else this rank's rows
+    S.global = kind == SPMV_SB && !part && K > 0 && (int)blk_slots.size() == K;
+    int64_t total_slots = 0;
+    if (S.global)
+        for (int64_t v : blk_slots) total_slots += v;
+    else
+        total_slots = spmvb::panel_total_slots(rp, m_loc, part);
+    // panels: about kPnRowsTarget slots, their count a multiple of the SM
+    // count when possible (whole waves of one CTA per SM)
+    S.target = spmvb::kPnRowsTarget;
+    for (int64_t k = 1; k <= 4096; ++k) {
+        const int64_t r = (total_slots + sms * k - 1) / (sms * k);
+        if (r <= spmvb::kPnRowsTarget) {
+            S.target = r;
+            S.waves = k;
+            break;
+        }
+    }
+    if (S.target < 1024) {
+        S.target = 1024;
+        S.waves = 0;
+    }
+    if (const char* e = getenv("SPMV_PN_ROWS")) {   // tests / measurements
+        S.target = std::max<int64_t>(1, atoll(e));
+        S.waves = 0;
+    }
+    if (getenv("SPMV_PN_NOWAVES")) S.waves = 0;   // measurement: per-range ceil(slots / target)
+    // groups never mix interior and border columns at world > 1 (two x
+    // buffers); SB plans keep the same rule at world 1 (C_B starts at
+    // cbp[K]) so the groups -- and every row's summation order -- are the
+    // same on any number of GPUs
+    S.xs = world > 1 ? x_int_len : (kind == SPMV_SB ? cbp[K] : INT32_MAX);
+    if (S.global) {
+        const std::vector<int64_t> np_all = spmvb::panel_counts(blk_slots, S.target, S.waves * sms);
+        for (int k = 0; k < K; ++k)
+            if (std::min(rbp[k + 1], R1) > std::max(rbp[k], R0)) S.range_panels.push_back(np_all[k]);
+    }
+    return S;
+}
+
 // Builds and uploads the column-sorted panel kernel's plan (plan_panel.cpp).
 // Leaves the handle on the row-tile kernel when the plan would be poor.
 static spmv_status_t plan_pn(spmv_plan_s* h, PanelPlan& pl, const std::vector<int64_t>& rp,
                              const std::vector<int32_t>& pcol, const std::vector<double>& pval,
                              const std::vector<int64_t>& rbp, const std::vector<int64_t>& cbp,
                              const std::vector<int32_t>* part) {
-    const int K = (int)rbp.size() - 2;
-    const int64_t R0 = h->row_begin, R1 = h->row_begin + h->m_loc;
-    std::vector<std::pair<int64_t, int64_t>> ranges, xcols;
-    const int64_t q0 = h->world > 1 ? h->x_int_begin : 0;
-    if (h->kind == SPMV_SB) {
-        for (int k = 0; k < K; ++k) {
-            const int64_t a = std::max(rbp[k], R0), b = std::min(rbp[k + 1], R1);
-            if (b > a) {
-                ranges.push_back({a - R0, b - R0});
-                xcols.push_back({cbp[k] - q0, cbp[k + 1] - q0});
-            }
-        }
-    } else {   // no SB structure: panels of consecutive rows, no x prefetch
-        ranges.push_back({0, h->m_loc});
-        if (getenv("SPMV_PN_ROT_GENERIC")) xcols.push_back({0, h->n});   // measurement: rotated sweeps
-    }
-    // the global per-block counts (SB, no split) decide the cuts, else this rank's rows
-    const bool global = h->kind == SPMV_SB && !part && (int)h->blk_slots.size() == K;
-    int64_t total_slots = 0;
-    if (global)
-        for (int64_t v : h->blk_slots) total_slots += v;
-    else
-        total_slots = spmvb::panel_total_slots(rp, h->m_loc, part);
-    // panels: about kPnRowsMax rows, their count a multiple of the SM count
-    // when possible (whole waves of one CTA per SM)
-    const int64_t sms = spmvb::kernel_num_sms();
-    int64_t target = spmvb::kPnRowsTarget, waves = 0;
-    for (int64_t k = 1; k <= 4096; ++k) {
-        const int64_t r = (total_slots + sms * k - 1) / (sms * k);
-        if (r <= spmvb::kPnRowsTarget) {
-            target = r;
-            waves = k;
-            break;
-        }
-    }
-    if (target < 1024) {
-        target = 1024;
-        waves = 0;
-    }
-    if (const char* e = getenv("SPMV_PN_ROWS")) {   // tests / measurements
-        target = std::max<int64_t>(1, atoll(e));
-        waves = 0;
-    }
-    if (getenv("SPMV_PN_NOWAVES")) waves = 0;   // measurement: per-range ceil(slots / target)
     if (const char* e = getenv("SPMV_L2_PERSIST_MB")) {   // measurements: L2 set-aside for evict_last lines
         CUDA_TRY(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)atoll(e) << 20));
     }
-    // groups never mix interior and border columns at world > 1 (two x
-    // buffers); SB plans keep the same rule at world 1 (C_B starts at
-    // cbp[K]) so the groups -- and every row's summation order -- are the
-    // same on any number of GPUs
-    const int64_t xs = h->world > 1 ? h->x_int_len : (h->kind == SPMV_SB ? cbp[K] : INT32_MAX);
+    const PnSetup S = pn_setup(h->kind, h->world, h->row_begin, h->m_loc, h->x_int_begin, h->x_int_len, h->n, rbp, cbp,
+                               h->blk_slots, rp, part, spmvb::kernel_num_sms());
     std::vector<spmvb::PnPanelData> pd;
     spmvb::PnPlanStats st;
     std::string why;
-    std::vector<int64_t> range_panels;
-    if (global) {
-        const std::vector<int64_t> np_all = spmvb::panel_counts(h->blk_slots, target, waves * sms);
-        for (int k = 0; k < K; ++k)
-            if (std::min(rbp[k + 1], R1) > std::max(rbp[k], R0)) range_panels.push_back(np_all[k]);
-    }
-    if (!spmvb::plan_panel(rp, pcol, pval, ranges, xs, target, pd, st, why, xcols.empty() ? nullptr : &xcols, sms, part,
-                           waves * sms, global ? &range_panels : nullptr))
+    if (!spmvb::plan_panel(rp, pcol, pval, S.ranges, S.xs, S.target, pd, st, why, S.xcols.empty() ? nullptr : &S.xcols,
+                           S.sms, part, S.waves * S.sms, S.global ? &S.range_panels : nullptr))
         return SPMV_OK;
     if (st.entries != h->nnz_loc)
         return fail(SPMV_ERR_INTERNAL, "panel plan lost nonzeros (%lld of %lld)", (long long)st.entries,
@@ -1490,6 +1511,99 @@ spmv_status_t spmv_pn_plan_check(int64_t m, int64_t n, const int64_t* row_ptr, c
                                            (long long)st.entries, (long long)nnz);
         if (!spmvb::verify_panel(rp, c, v, xs, pd, why))
             return fail(SPMV_ERR_INTERNAL, "pn_plan_check: %s", why.c_str());
+    } catch (const std::bad_alloc&) {
+        return fail(SPMV_ERR_INTERNAL, "out of host memory");
+    }
+    return SPMV_OK;
+}
+
+spmv_status_t spmv_pn_shard_hash(int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
+                                 const spmv_blocks_t* blocks, int32_t world, int32_t sms, int64_t* out) {
+    if (m < 0 || n < 0 || !row_ptr || !out || !blocks || world < 1 || sms < 1)
+        return fail(SPMV_ERR_USAGE, "pn_shard_hash: bad arguments");
+    if (blocks->kind != SPMV_SB || blocks->K < 1 || !blocks->row_block_ptr || !blocks->col_block_ptr)
+        return fail(SPMV_ERR_DATA, "pn_shard_hash: needs an SB block descriptor");
+    const int K = blocks->K;
+    const int64_t nnz = row_ptr[m];
+    if (nnz > 0 && (!col || !val)) return fail(SPMV_ERR_USAGE, "pn_shard_hash: NULL col/val");
+    try {
+        std::vector<int64_t> rbp(blocks->row_block_ptr, blocks->row_block_ptr + K + 2);
+        std::vector<int64_t> cbp(blocks->col_block_ptr, blocks->col_block_ptr + K + 2);
+        std::vector<int64_t> blk(K, 0);   // global per-block slots, as spmv_create counts them
+        for (int k = 0; k < K; ++k)
+            for (int64_t i = rbp[k]; i < rbp[k + 1]; ++i) blk[k] += spmvb::row_slots(row_ptr[i + 1] - row_ptr[i]);
+        for (int64_t i = 0; i < (int64_t)world * K; ++i) out[i] = 0;
+        for (int r = 0; r < world; ++r) {
+            spmv_shard_t sh;
+            spmv_status_t s = spmv_shard_plan(blocks, m, n, r, world, &sh);
+            if (s != SPMV_OK) return s;
+            const int64_t R0 = sh.row_begin, ml = sh.row_end - sh.row_begin;
+            // local CSR in the rank's x layout (create_impl's: interior columns
+            // shifted to 0, then the full C_B)
+            std::vector<int64_t> rp(ml + 1, 0);
+            std::vector<int32_t> c;
+            std::vector<double> v;
+            for (int64_t i = 0; i < ml; ++i) {
+                for (int64_t t = row_ptr[R0 + i]; t < row_ptr[R0 + i + 1]; ++t) {
+                    const int64_t g = col[t];
+                    int64_t l = g;
+                    if (world > 1)
+                        l = g >= cbp[K] ? sh.x_interior_len + (g - cbp[K]) : g - sh.x_interior_begin;
+                    c.push_back((int32_t)l);
+                    v.push_back(val[t]);
+                }
+                rp[i + 1] = (int64_t)c.size();
+            }
+            const PnSetup S = pn_setup(SPMV_SB, world, R0, ml, sh.x_interior_begin, sh.x_interior_len, n, rbp, cbp, blk,
+                                       rp, nullptr, sms);
+            std::vector<spmvb::PnPanelData> pd;
+            spmvb::PnPlanStats st;
+            std::string why;
+            if (!spmvb::plan_panel(rp, c, v, S.ranges, S.xs, S.target, pd, st, why,
+                                   S.xcols.empty() ? nullptr : &S.xcols, S.sms, nullptr, S.waves * S.sms,
+                                   S.global ? &S.range_panels : nullptr))
+                return fail(SPMV_ERR_UNSUPPORTED, "pn_shard_hash: %s", why.c_str());
+            for (const auto& P : pd) {
+                const int64_t row0 = R0 + P.desc.row0;
+                const int k = (int)(std::upper_bound(rbp.begin(), rbp.begin() + K + 1, row0) - rbp.begin()) - 1;
+                // slot -> (panel row, virtual-row rank)
+                const int32_t nsl = ((P.nslots + 15) / 16) * 16;
+                std::vector<int32_t> srow(nsl, -1), svr(nsl, 0);
+                for (int32_t i = 0; i < P.desc.nrows; ++i) {
+                    const int32_t sl = P.row2slot[i];
+                    if (sl < 0x8000) {
+                        srow[sl] = i;
+                    } else {
+                        const int32_t q = sl & 0x7FFF;
+                        for (int32_t j = 0; j < P.split_cnt[q]; ++j) {
+                            srow[P.split_slots[P.split_first[q] + j]] = i;
+                            svr[P.split_slots[P.split_first[q] + j]] = j;
+                        }
+                    }
+                }
+                uint64_t hsh = (uint64_t)out[(int64_t)r * K + k] ^ 0xcbf29ce484222325ull;
+                auto mix = [&](uint64_t x) { hsh = (hsh ^ x) * 0x100000001b3ull; };
+                mix((uint64_t)row0);
+                mix((uint64_t)P.desc.nrows);
+                const int64_t G = (int64_t)P.gbase.size();
+                for (int64_t g = 0; g < G; ++g)
+                    for (int l = 0; l < 32; ++l) {
+                        const uint32_t i = P.gidx[g * 32 + l];
+                        if (i == spmvb::kPnDummy) continue;
+                        const int32_t sl = (int32_t)(i >> spmvb::kPnDeltaBits);
+                        const int64_t lc = (int64_t)P.gbase[g] + (i & ((1u << spmvb::kPnDeltaBits) - 1));
+                        int64_t gc = lc;
+                        if (world > 1) gc = lc >= sh.x_interior_len ? cbp[K] + (lc - sh.x_interior_len) : lc + sh.x_interior_begin;
+                        uint64_t vb;
+                        memcpy(&vb, &P.gval[g * 32 + l], 8);
+                        mix((uint64_t)(R0 + P.desc.row0 + (sl < nsl ? srow[sl] : -1)));
+                        mix((uint64_t)(sl < nsl ? svr[sl] : -1));
+                        mix((uint64_t)gc);
+                        mix(vb);
+                    }
+                out[(int64_t)r * K + k] = (int64_t)hsh;
+            }
+        }
     } catch (const std::bad_alloc&) {
         return fail(SPMV_ERR_INTERNAL, "out of host memory");
     }

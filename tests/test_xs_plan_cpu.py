@@ -121,3 +121,24 @@ def synth_permuted(p):
     import oracle
     rp, col, val, _ = oracle.permute(p.m, p.n, p.row_ptr, p.col, p.val, p.row_perm, p.col_perm)
     return rp, col, val
+
+
+@pytest.mark.parametrize("name", ["c5s", "c2s"])
+def test_panel_plan_independent_of_gpu_count(name):
+    """every rank plans its SB blocks' panels from the global
+    per-block slot counts, in its own x layout, so each block's panels and
+    every row's summation order (hash of each group's rows, virtual rows,
+    global columns and values in issue order) are the same at world 1, 2, 4
+    -- y is then bit-identical across GPU counts."""
+    p = synth.make(name, scramble=0)
+    K = p.blocks["K"]
+    ref = sp.spmv_pn_shard_hash(p.m, p.n, p.row_ptr, p.col, p.val, p.blocks, 1)[0]
+    assert np.all(ref != 0)
+    for world in (2, 4):
+        h = sp.spmv_pn_shard_hash(p.m, p.n, p.row_ptr, p.col, p.val, p.blocks, world)
+        owned = (h != 0).sum(axis=0)
+        assert np.all(owned == 1), f"each block on exactly one rank (world {world})"
+        assert np.array_equal(h.sum(axis=0), ref), f"world {world} plans differ from world 1"
+    # the hash has teeth: another whole-wave count cuts other panels
+    other = sp.spmv_pn_shard_hash(p.m, p.n, p.row_ptr, p.col, p.val, p.blocks, 1, sms=1)[0]
+    assert not np.array_equal(other, ref)
