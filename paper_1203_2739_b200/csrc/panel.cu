@@ -331,6 +331,14 @@ cudaError_t launch_panel(const PnArgs& a, cudaStream_t s) {
         attr((const void*)spmv_panel_kernel<0, 16, 8, true>);
         attr((const void*)spmv_panel_kernel<25, 12, 8, true>);
         attr((const void*)spmv_panel_kernel<25, 16, 8, true>);
+        attr((const void*)spmv_panel_kernel<0, 8, 2, false>);
+        attr((const void*)spmv_panel_kernel<0, 8, 3, false>);
+        attr((const void*)spmv_panel_kernel<25, 8, 2, false>);
+        attr((const void*)spmv_panel_kernel<25, 8, 3, false>);
+        attr((const void*)spmv_panel_kernel<0, 8, 2, true>);
+        attr((const void*)spmv_panel_kernel<0, 8, 3, true>);
+        attr((const void*)spmv_panel_kernel<25, 8, 2, true>);
+        attr((const void*)spmv_panel_kernel<25, 8, 3, true>);
         attr((const void*)spmv_panel_kernel<0, 8, 4>);
         attr((const void*)spmv_panel_kernel<0, 16, 4>);
         attr((const void*)spmv_panel_kernel<0, 16, 8>);
@@ -351,8 +359,10 @@ cudaError_t launch_panel(const PnArgs& a, cudaStream_t s) {
     default: {
         const bool xs = b.x_split != INT32_MAX;
         // ring: steps in flight 8 / 12 / 16 with gathers 4 steps ahead; 1208 /
-        // 1608: 12 / 16 with gathers 8 ahead (measurements)
-        const int rd = b.ring == 8 || b.ring == 12 || b.ring == 16 || b.ring == 1208 || b.ring == 1608 ? b.ring : kDefD;
+        // 1608: 12 / 16 with gathers 8 ahead; 802 / 803: 8 with gathers 2 / 3
+        // ahead (measurements)
+        const int rd = b.ring == 8 || b.ring == 12 || b.ring == 16 || b.ring == 1208 || b.ring == 1608 ||
+                       b.ring == 802 || b.ring == 803 ? b.ring : kDefD;
 #define SPMV_PN_LAUNCH(M, D, G)                                                           \
     (xs ? (spmv_panel_kernel<M, D, G, true><<<b.n_panels, kT, smem, s>>>(b), 0)          \
         : (spmv_panel_kernel<M, D, G, false><<<b.n_panels, kT, smem, s>>>(b), 0))
@@ -361,12 +371,16 @@ cudaError_t launch_panel(const PnArgs& a, cudaStream_t s) {
             else if (rd == 16) SPMV_PN_LAUNCH(25, 16, 4);
             else if (rd == 1208) SPMV_PN_LAUNCH(25, 12, 8);
             else if (rd == 1608) SPMV_PN_LAUNCH(25, 16, 8);
+            else if (rd == 802) SPMV_PN_LAUNCH(25, 8, 2);
+            else if (rd == 803) SPMV_PN_LAUNCH(25, 8, 3);
             else SPMV_PN_LAUNCH(25, 8, 4);
         } else {
             if (rd == 12) SPMV_PN_LAUNCH(0, 12, 4);
             else if (rd == 16) SPMV_PN_LAUNCH(0, 16, 4);
             else if (rd == 1208) SPMV_PN_LAUNCH(0, 12, 8);
             else if (rd == 1608) SPMV_PN_LAUNCH(0, 16, 8);
+            else if (rd == 802) SPMV_PN_LAUNCH(0, 8, 2);
+            else if (rd == 803) SPMV_PN_LAUNCH(0, 8, 3);
             else SPMV_PN_LAUNCH(0, 8, 4);
         }
 #undef SPMV_PN_LAUNCH
