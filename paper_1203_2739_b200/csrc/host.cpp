@@ -151,6 +151,8 @@ struct spmv_plan_s {
     int32_t* d_fsegptr = nullptr;     // [S+1] segment start positions (same positions as the CSR rows)
     bool split_rowmajor = true;
     std::vector<int64_t> blk_slots;   // SB: y slots per block over the whole matrix (panel cuts)
+    int64_t xs_test = 0;              // SPMV_PN_XS_TEST at create (SB, world 1): run the kernel's x-split
+                                      // path with x_hi = x + C_B start (same values, two pointers)
     int32_t* d_colinv = nullptr;      // ORIGINAL mode: x^[c] = x[colinv[c]]
     int32_t* d_rowperm = nullptr;     // ORIGINAL mode: y[i] = y^[row_perm[i]]
     double* d_xhat = nullptr;
@@ -1013,6 +1015,8 @@ static spmv_status_t create_impl(int64_t m, int64_t n, int64_t nnz, const int64_
         if ((s = plan_pn(h, h->pns, rp, pcol, pval, rbp, cbp, &ppart))) return s;
     }
 
+    if (blocks && h->kind == SPMV_SB && world == 1 && getenv("SPMV_PN_XS_TEST") && cbp.size() >= 2)
+        h->xs_test = cbp[cbp.size() - 2];   // C_B's first column: the plan's group split (pn_setup)
     // global per-block y-slot counts (SB): every rank cuts its blocks into the
     // same panels as a single GPU would, so the summation order of a row --
     // and y -- does not depend on the number of GPUs
@@ -1209,6 +1213,10 @@ static spmv_status_t run(spmv_handle_t h, const double* x, double* y, uint32_t f
         X.x_split = A.x_split;
         X.x_lo = A.x_lo;
         X.x_hi = A.x_hi;
+        if (h->xs_test > 0 && h->world == 1) {   // test: the world > 1 two-buffer x path on one GPU
+            X.x_split = (int32_t)h->xs_test;
+            X.x_hi = A.x_lo + h->xs_test;
+        }
         X.y = yk;
         X.maxabs_slots = A.maxabs_slots;
         CUDA_TRY(spmvb::launch_panel(X, st));

@@ -1,4 +1,3 @@
 python -m paper_1203_2739_b200.build > /dev/null
-cd scripts
-ROUNDS=6 timeout 900 python ab_inter.py c4 "" "SPMV_PN_RING=802" "SPMV_PN_RING=803" 2>&1 | tail -1
-ROUNDS=8 timeout 1200 python ab_inter.py c5 "" "SPMV_PN_RING=802" "SPMV_PN_RING=803" 2>&1 | tail -1
+timeout 900 python -m pytest tests/test_gpu_xstage.py -q -x -k "x_split" 2>&1 | tail -3
+timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -2

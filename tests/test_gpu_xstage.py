@@ -156,3 +156,24 @@ def test_split_rowmajor_kernel(monkeypatch):
     y = gpu_apply(h, x, p.m, split=True)
     yref = oracle.split(p.row_ptr, p.col, p.val, p.parts, p.n_parts, x)
     assert_parity(y, yref, None, exact=True, what="split row-major")
+
+
+@pytest.mark.parametrize("name", ["c5s", "c2s"])
+def test_panel_x_split_path(monkeypatch, name):
+    """The kernel's two-buffer x path (world > 1: interior | gathered border)
+    on one GPU: SPMV_PN_XS_TEST splits the same x into x_lo = x and
+    x_hi = x + C_B start.  Same values through other pointers: y must equal
+    the one-buffer path bit for bit (and the oracle)."""
+    monkeypatch.setenv("SPMV_KERNEL", "panel")
+    monkeypatch.setenv("SPMV_PN_ROWS", "2000")
+    p = synth.make(name, variant="real")
+    x = p.x()
+    xh, yh_ref, S = oracle_permuted(p, x)
+    h1 = create(p)
+    y1 = gpu_apply(h1, xh, p.m)
+    monkeypatch.setenv("SPMV_PN_XS_TEST", "1")
+    h2 = create(p)
+    assert sp.spmv_get_info(h2)["kernel"] == 7
+    y2 = gpu_apply(h2, xh, p.m)
+    assert np.array_equal(y1.view(np.int64), y2.view(np.int64))
+    assert_parity(y2, yh_ref, S, what=f"x-split path/{name}")
