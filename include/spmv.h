@@ -266,6 +266,17 @@ spmv_status_t spmv_pn_plan_check(int64_t m, int64_t n, const int64_t* row_ptr, c
 spmv_status_t spmv_pn_shard_hash(int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
                                  const spmv_blocks_t* blocks, int32_t world, int32_t sms, int64_t* out);
 
+/* Test hook of the multi-GPU path on one GPU.  With SPMV_TEST_RANKS_NO_NCCL
+ * set in the environment, spmv_create accepts a dist descriptor whose
+ * nccl_unique_id is NULL: the handle is rank `rank` of `world` (its shard,
+ * local CSR, x layout and panel plan exactly as on a real multi-GPU run) but
+ * has no communicator; its apply skips the border all-gather, and the test
+ * supplies the full x(C_B) the all-gather would deliver through this call
+ * (`x_border`: device pointer, `len` = |C_B| doubles, copied; the apply still
+ * writes the rank's own slice into place first).  USAGE on a handle that is
+ * not such a test rank or on a length mismatch. */
+spmv_status_t spmv_test_set_border(spmv_handle_t h, const double* x_border, int64_t len);
+
 /* Design microbenchmarks (diag2.cu): kind 1 L2->SM LDG.128 bandwidth over the
  * L2-resident `buf` (`bytes` long, `count` bytes read in total); kind 2 bulk-copy
  * L2->shared bandwidth, param = cluster size 1/2/4/8 (multicast when > 1),

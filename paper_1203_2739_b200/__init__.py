@@ -35,7 +35,7 @@ EXPORTED = ["spmv_create", "spmv_apply", "spmv_split_apply", "spmv_destroy", "sp
             "spmv_maxabs", "spmv_normalize", "spmv_debug_copy_csr", "spmv_nccl_unique_id",
             "spmv_status_string", "spmv_last_error", "spmv_version", "spmv_shard_plan",
             "spmv_diag_read", "spmv_diag_gather", "spmv_diag_csr", "spmv_diag_gather_mode", "spmv_diag_micro",
-            "spmv_xs_plan_check", "spmv_pn_plan_check", "spmv_pn_shard_hash"]
+            "spmv_xs_plan_check", "spmv_pn_plan_check", "spmv_pn_shard_hash", "spmv_test_set_border"]
 
 
 class SpmvError(RuntimeError):
@@ -98,6 +98,7 @@ def lib():
         L.spmv_xs_plan_check.argtypes = [i64, i64, vp, vp, vp, vp, i64, vp]
         L.spmv_pn_plan_check.argtypes = [i64, i64, vp, vp, vp, vp, i64, vp]
         L.spmv_pn_shard_hash.argtypes = [i64, i64, vp, vp, vp, vp, i32, i32, vp]
+        L.spmv_test_set_border.argtypes = [vp, vp, i64]
         L.spmv_shard_plan.argtypes = [vp, i64, i64, i32, i32, vp]
         L.spmv_status_string.argtypes = [i32]
         L.spmv_status_string.restype = ctypes.c_char_p
@@ -206,10 +207,13 @@ def spmv_create(m: int, n: int, row_ptr, col_idx, val, row_perm=None, col_perm=N
         bptr = ctypes.byref(b)
     dptr = None
     if dist is not None:
-        uid = ctypes.create_string_buffer(bytes(dist["nccl_unique_id"]), 128)
-        d = _Dist(int(dist["rank"]), int(dist["world"]), int(dist.get("device", 0)), 0,
-                  ctypes.cast(uid, ctypes.c_void_p).value)
-        keep += [uid, d]
+        uid_ptr = None   # None: the single-process rank emulation of the tests (SPMV_TEST_RANKS_NO_NCCL)
+        if dist.get("nccl_unique_id") is not None:
+            uid = ctypes.create_string_buffer(bytes(dist["nccl_unique_id"]), 128)
+            keep.append(uid)
+            uid_ptr = ctypes.cast(uid, ctypes.c_void_p).value
+        d = _Dist(int(dist["rank"]), int(dist["world"]), int(dist.get("device", 0)), 0, uid_ptr)
+        keep.append(d)
         dptr = ctypes.byref(d)
     out = ctypes.c_void_p(0)
     st = lib().spmv_create(m, n, nnz, _addr(rp), _addr(ci), _addr(va), _addr(pr), _addr(pc), bptr,
@@ -285,6 +289,12 @@ def spmv_pn_shard_hash(m: int, n: int, row_ptr, col, val, blocks, world: int, sm
     _check(lib().spmv_pn_shard_hash(m, n, _addr(rp), _addr(ci), _addr(va), ctypes.byref(b), world, sms,
                                     out.ctypes.data), "spmv_pn_shard_hash")
     return out
+
+
+def spmv_test_set_border(h, x_border):
+    """Test hook (single-process rank emulation): the full x(C_B) the border exchange would gather."""
+    _check(lib().spmv_test_set_border(_h(h), ctypes.c_void_p(_dev(x_border)), int(x_border.numel())),
+           "spmv_test_set_border")
 
 
 def spmv_apply(h, x, y, flags: int = 0, stream=None, x_len: int | None = None, y_len: int | None = None):

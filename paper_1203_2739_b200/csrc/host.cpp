@@ -151,6 +151,7 @@ struct spmv_plan_s {
     int32_t* d_fsegptr = nullptr;     // [S+1] segment start positions (same positions as the CSR rows)
     bool split_rowmajor = true;
     std::vector<int64_t> blk_slots;   // SB: y slots per block over the whole matrix (panel cuts)
+    bool test_nocomm = false;         // a test rank without a communicator (spmv_test_set_border)
     int64_t xs_test = 0;              // SPMV_PN_XS_TEST at create (SB, world 1): run the kernel's x-split
                                       // path with x_hi = x + C_B start (same values, two pointers)
     int32_t* d_colinv = nullptr;      // ORIGINAL mode: x^[c] = x[colinv[c]]
@@ -224,14 +225,17 @@ void plan_tiles(const std::vector<int64_t>& rp, int64_t m_loc, const std::vector
         while (ci < cuts.size() && cuts[ci] <= r) ++ci;
         const int64_t lim = ci < cuts.size() ? std::min<int64_t>(cuts[ci], m_loc) : m_loc;
         // a tile's nonzeros sit at positions [(a & 3), (a & 3) + n) of a
-        // 16-byte aligned kTileNnz-slot stage buffer (pipe.cu)
-        const int64_t base = rp[r] & ~int64_t(3);
-        if (rp[r + 1] - base > kTileNnz) {
+        // 16-byte aligned kTileNnz-slot stage buffer (pipe.cu); the capacity
+        // test assumes the worst alignment (3), so the cuts do not depend on
+        // where the rank's local CSR starts -- tiles, and so every row's
+        // summation order, are the same at every world size
+        const int64_t a0 = rp[r];
+        if (rp[r + 1] - a0 + 3 > kTileNnz) {
             ++r;
             ++n_long;
         } else {
             int64_t e = r;
-            while (e < lim && e - r < kTileRows && rp[e + 1] - base <= kTileNnz) ++e;
+            while (e < lim && e - r < kTileRows && rp[e + 1] - a0 + 3 <= kTileNnz) ++e;
             r = e;
         }
         tile_row.push_back((int32_t)r);
@@ -605,8 +609,11 @@ static spmv_status_t create_impl(int64_t m, int64_t n, int64_t nnz, const int64_
     if (m > INT32_MAX - 1 || n > INT32_MAX - 1) return fail(SPMV_ERR_UNSUPPORTED, "dimension beyond int32");
     const int world = dist ? dist->world : 1;
     const int rank = dist ? dist->rank : 0;
-    if (dist && (world < 1 || rank < 0 || rank >= world || !dist->nccl_unique_id))
+    // test rank (spmv_test_set_border): a multi-GPU shard without a communicator
+    const bool test_nocomm = dist && world > 1 && !dist->nccl_unique_id && getenv("SPMV_TEST_RANKS_NO_NCCL");
+    if (dist && (world < 1 || rank < 0 || rank >= world || (!dist->nccl_unique_id && !test_nocomm)))
         return fail(SPMV_ERR_USAGE, "bad dist descriptor");
+    h->test_nocomm = test_nocomm;
     if (world > 1 && (!blocks || blocks->kind != SPMV_SB))
         return fail(SPMV_ERR_UNSUPPORTED, "world > 1 needs an SB block descriptor (DB split sharding is NEXT f1)");
     h->rank = rank;
@@ -720,9 +727,11 @@ static spmv_status_t create_impl(int64_t m, int64_t n, int64_t nnz, const int64_
     if (world > 1) {
         h->device = dist->device;
         CUDA_TRY(cudaSetDevice(h->device));
-        ncclUniqueId id;
-        memcpy(&id, dist->nccl_unique_id, sizeof id);
-        NCCL_TRY(ncclCommInitRank(&h->comm, world, id, rank));
+        if (!test_nocomm) {
+            ncclUniqueId id;
+            memcpy(&id, dist->nccl_unique_id, sizeof id);
+            NCCL_TRY(ncclCommInitRank(&h->comm, world, id, rank));
+        }
     }
 
     // --------------------------------------- permute the local rows (a1)
@@ -803,7 +812,7 @@ static spmv_status_t create_impl(int64_t m, int64_t n, int64_t nnz, const int64_
         if (dup) local_status = fail(SPMV_ERR_DATA, "duplicate (i, j) entry");
         else if (env) local_status = fail(SPMV_ERR_DATA, "nonzero outside the SB/DB envelope");
     }
-    if (world > 1) {   // every rank returns the same status
+    if (world > 1 && !test_nocomm) {   // every rank returns the same status
         int* d_st = nullptr;
         int st = (int)local_status;
         CUDA_TRY(cudaMalloc(&d_st, sizeof(int)));
@@ -893,7 +902,7 @@ static spmv_status_t create_impl(int64_t m, int64_t n, int64_t nnz, const int64_
         {
             std::vector<int32_t> lt;
             for (int64_t t = 0; t < T; ++t)
-                if (rp[tile_row[t + 1]] - (rp[tile_row[t]] & ~int64_t(3)) > kTileNnz) lt.push_back((int32_t)t);
+                if (rp[tile_row[t + 1]] - rp[tile_row[t]] + 3 > kTileNnz) lt.push_back((int32_t)t);
             if (!lt.empty() && (s = upload(h, &h->d_long_tiles, lt.data(), lt.size()))) return s;
             h->n_long = (int64_t)lt.size();
         }
@@ -1187,7 +1196,9 @@ static spmv_status_t run(spmv_handle_t h, const double* x, double* y, uint32_t f
         if (h->x_bord_len)
             CUDA_TRY(cudaMemcpyAsync(h->d_xborder + h->bord_off[h->rank], x + h->x_int_len,
                                      h->x_bord_len * sizeof(double), cudaMemcpyDeviceToDevice, st));
-        if (h->equal_slices) {
+        if (h->test_nocomm) {
+            // test rank: the other slices were supplied by spmv_test_set_border
+        } else if (h->equal_slices) {
             NCCL_TRY(ncclAllGather(h->d_xborder + h->bord_off[h->rank], h->d_xborder, h->bord_cnt[0], ncclFloat64,
                                    h->comm, st));
         } else {
@@ -1390,7 +1401,7 @@ spmv_status_t spmv_maxabs(spmv_handle_t h, double* m_dev, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
     CUDA_TRY(cudaSetDevice(h->device));
     CUDA_TRY(spmvb::launch_maxabs_finish(h->d_slots, m_dev, st));
-    if (h->world > 1) NCCL_TRY(ncclAllReduce(m_dev, m_dev, 1, ncclFloat64, ncclMax, h->comm, st));
+    if (h->world > 1 && h->comm) NCCL_TRY(ncclAllReduce(m_dev, m_dev, 1, ncclFloat64, ncclMax, h->comm, st));
     return SPMV_OK;
 }
 
@@ -1615,6 +1626,15 @@ spmv_status_t spmv_pn_shard_hash(int64_t m, int64_t n, const int64_t* row_ptr, c
     } catch (const std::bad_alloc&) {
         return fail(SPMV_ERR_INTERNAL, "out of host memory");
     }
+    return SPMV_OK;
+}
+
+spmv_status_t spmv_test_set_border(spmv_handle_t h, const double* x_border, int64_t len) {
+    if (!valid(h) || !h->test_nocomm || !x_border) return fail(SPMV_ERR_USAGE, "test_set_border: not a test rank");
+    if (len != h->border_total) return fail(SPMV_ERR_USAGE, "test_set_border: length %lld != |C_B| %lld",
+                                            (long long)len, (long long)h->border_total);
+    CUDA_TRY(cudaSetDevice(h->device));
+    if (len) CUDA_TRY(cudaMemcpy(h->d_xborder, x_border, len * sizeof(double), cudaMemcpyDeviceToDevice));
     return SPMV_OK;
 }
 

@@ -147,7 +147,7 @@ __device__ __forceinline__ void fetch(const PipeArgs& A, PipeSmem& sm, int it, S
     if (S.h.r0 < 0) return;                     // sentinel: no more tiles (stage never released)
     const int off = S.h.a & 3;
     const int n = S.h.b - S.h.a;
-    S.big = off + n > kTileNnz;
+    S.big = n + 3 > kTileNnz;   // plan_tiles' alignment-free test (off <= 3)
     int c[kE];
     if (!S.big) {
 #pragma unroll
@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(kPipeThreads, 2) spmv_pipe_kernel(const PipeAr
                     if (k > 0) mbar_wait(&sm.empty[st], (k - 1) & 1);
                     sm.hdr[st] = StageHdr{r0, r1, a, b, cls, 0, 0, 0};
                     const int a4 = a & ~3;
-                    if (b - a4 > kTileNnz) {
+                    if (b - a + 3 > kTileNnz) {   // long row (plan_tiles' alignment-free test)
                         mbar_arrive(&sm.full[st]);           // long row: consumers load directly
                     } else {
                         const int r4 = r0 & ~3;

@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(NT, (NT == 512 ? 3 : NT == 256 ? 6 : 8)) spmv_
     const uint64_t pol = pol_evict_first();
     double mx = 0.0;
 
-    if (b - a4 > kTileNnz) {
+    if (b - a + 3 > kTileNnz) {   // long row: planned as one (host plan_tiles, alignment-free test)
         // ------------------------------------------- one long row (> a tile)
         if (A.long_tiles) return;                   // done by spmv_longrow_kernel
         const int64_t qa = a >> 2, qb = ((int64_t)b + 3) >> 2;
@@ -342,7 +342,7 @@ __global__ void __launch_bounds__(kRT, 3) spmv_rowseg_kernel(const RowTileArgs A
     const uint64_t pol = pol_evict_first();
     double mx = 0.0;
 
-    if (b - a4 > kTileNnz) {
+    if (b - a + 3 > kTileNnz) {   // long row: planned as one (host plan_tiles, alignment-free test)
         // ------------------------------------------- one long row (> a tile)
         const int64_t qa = a >> 2, qb = ((int64_t)b + 3) >> 2;
         double acc = 0.0;

@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(kST, 2) spmv_split_kernel(const TileArgs A) {
 
     for (int j = tid; j < nr; j += kST) sm.ysum[j] = A.accumulate ? A.y[r0 + j] : 0.0;
 
-    if (b - a4 > kTileNnz) {
+    if (b - a + 3 > kTileNnz) {   // long row: planned as one (host plan_tiles, alignment-free test)
         // one long row (the tile is a single row): per part, fixed-assignment
         // partials + fixed block tree, accumulated in part order
         __syncthreads();
@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(kSR, 4) spmv_split_rows_kernel(const RowTileAr
     asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pl));
     double mx = 0.0;
 
-    if (b - a4 > kTileNnz) {
+    if (b - a + 3 > kTileNnz) {   // long row: planned as one (host plan_tiles, alignment-free test)
         // one long row: per segment (part order), fixed-assignment partials +
         // fixed block tree, accumulated in part order
         double yr = 0.0;
