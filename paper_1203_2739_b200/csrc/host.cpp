@@ -90,6 +90,7 @@ struct PanelPlan {
     int32_t gather_na = 0;            // x gathers bypass L1 allocation (SPMV_PN_GATHER_NA at create)
     int32_t ring = 0;                 // register-ring depth (SPMV_PN_RING at create; 0 = default)
     int32_t pf = 0;                   // L2 prefetch distance in epochs (SPMV_PN_PF at create; 0 = default)
+    int32_t persist = 0;              // persistent CTAs (SPMV_PN_PERSIST at create)
     bool ok() const { return panels > 0; }
 };
 
@@ -589,6 +590,7 @@ static spmv_status_t plan_pn(spmv_plan_s* h, PanelPlan& pl, const std::vector<in
     if (const char* e = getenv("SPMV_PN_GATHER_NA")) pl.gather_na = atoi(e);
     if (const char* e = getenv("SPMV_PN_RING")) pl.ring = atoi(e);   // measurements: 8, 12 or 16
     if (const char* e = getenv("SPMV_PN_PF")) pl.pf = atoi(e);       // measurements: epochs ahead
+    if (const char* e = getenv("SPMV_PN_PERSIST")) pl.persist = atoi(e);
     if (!part) {
         h->bytes_stream = (12 * 32 + 4) * G + 8 * h->m_loc;
         h->kernel = 7;
@@ -1171,6 +1173,7 @@ static void fill_pn_args(const PanelPlan& pl, spmvb::PnArgs& X) {
     X.gather_na = pl.gather_na;
     X.ring = pl.ring;
     X.pf_epochs = pl.pf;
+    X.persist = pl.persist;
 }
 
 static spmv_status_t run(spmv_handle_t h, const double* x, double* y, uint32_t flags, cudaStream_t st,

@@ -203,7 +203,8 @@ struct PnArgs {
     int32_t max_split_n;          // largest split_n over the panels (shared-memory copy of the descriptors)
     int32_t pf_epochs;        // epochs of the group stream prefetched into L2 ahead (0 = default)
     int32_t gather_na;        // x gathers L1::no_allocate (plan choice; 0 = allocate)
-    int32_t ring;             // register-ring depth in steps (8, 12 or 16; 0 = 12)
+    int32_t ring;             // register-ring depth in steps (8, 12 or 16; 0 = default)
+    int32_t persist;          // 1: one CTA per SM walks the panels (measurement switch)
 };
 cudaError_t launch_panel(const PnArgs& a, cudaStream_t s);
 

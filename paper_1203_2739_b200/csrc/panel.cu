@@ -73,215 +73,220 @@ __device__ __forceinline__ double ld_x(const double* p, uint64_t pol) {
 // 4 no L2 prefetch of the group stream, 6 gathers of a fixed 2 MB window (no
 // dependence on the loaded indices' values), 24 no next-panel prefetch,
 // 25 x gathers L1::no_allocate
-template <int MODE, int KD_ = kDefD, int KGD_ = 4, bool XS = true>
+template <int MODE, int KD_ = kDefD, int KGD_ = 4, bool XS = true, bool PERSIST = false>
 __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
-    constexpr int kD = KD_;                              // steps (groups) in flight per warp
-    constexpr int kGD = KGD_;                            // gathers issued this many steps ahead
-    // the ring is refilled four slots at a time after the last step of a warp's
-    // epoch, so kD - 3..kD steps are loaded ahead; a gather needs its step's
-    // index loaded: kGD <= kD - 4
-    static_assert(kPnB == 4 && kD % 4 == 0 && kGD >= 1 && kGD <= kD - 4, "ring geometry");
-    extern __shared__ __align__(16) double ys[];
-    const int p = blockIdx.x;
-    const PnPanel d = A.panel[p];
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    for (int i = tid; i < ((d.nslots + 15) & ~15); i += kT) ys[i] = 0.0;   // the panel's y slots
-    // virtual-row slot lists of the panel's split rows, copied to shared memory
-    // once (the epilogue folds them)
-    uint16_t* ssl = reinterpret_cast<uint16_t*>(ys + A.max_rows + 1);
-    int32_t* sdesc = reinterpret_cast<int32_t*>(ssl + ((A.max_sslots + 7) & ~7));   // (first, count, row) per split row
-    for (int i = tid; i < d.sslot_n; i += kT) ssl[i] = A.split_slots[d.sslot0 + i];
-    for (int i = tid; i < d.split_n; i += kT) {
-        const int e = d.split_off + i;
-        sdesc[3 * i] = A.split_first[e] - d.sslot0;
-        sdesc[3 * i + 1] = A.split_cnt[e];
-        sdesc[3 * i + 2] = A.split_row[e];
-    }
-    __syncthreads();
+    // one panel per CTA, or (PERSIST) one CTA per SM walking panels
+    // blockIdx.x, + gridDim.x, ...
+    for (int p = blockIdx.x; p < A.n_panels; p += gridDim.x) {
+        constexpr int kD = KD_;                              // steps (groups) in flight per warp
+        constexpr int kGD = KGD_;                            // gathers issued this many steps ahead
+        // the ring is refilled four slots at a time after the last step of a warp's
+        // epoch, so kD - 3..kD steps are loaded ahead; a gather needs its step's
+        // index loaded: kGD <= kD - 4
+        static_assert(kPnB == 4 && kD % 4 == 0 && kGD >= 1 && kGD <= kD - 4, "ring geometry");
+        extern __shared__ __align__(16) double ys[];
+        const PnPanel d = A.panel[p];
+        const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+        for (int i = tid; i < ((d.nslots + 15) & ~15); i += kT) ys[i] = 0.0;   // the panel's y slots
+        // virtual-row slot lists of the panel's split rows, copied to shared memory
+        // once (the epilogue folds them)
+        uint16_t* ssl = reinterpret_cast<uint16_t*>(ys + A.max_rows + 1);
+        int32_t* sdesc = reinterpret_cast<int32_t*>(ssl + ((A.max_sslots + 7) & ~7));   // (first, count, row) per split row
+        for (int i = tid; i < d.sslot_n; i += kT) ssl[i] = A.split_slots[d.sslot0 + i];
+        for (int i = tid; i < d.split_n; i += kT) {
+            const int e = d.split_off + i;
+            sdesc[3 * i] = A.split_first[e] - d.sslot0;
+            sdesc[3 * i + 1] = A.split_cnt[e];
+            sdesc[3 * i + 2] = A.split_row[e];
+        }
+        __syncthreads();
 
-    const uint64_t pol = pol_evict_first();
-    const uint64_t polx = pol_evict_last();   // x is the reused operand
-    const int PF = A.pf_epochs > 0 ? A.pf_epochs : kPF;
-    const int T = d.ne * kPnB;                       // steps per warp
+        const uint64_t pol = pol_evict_first();
+        const uint64_t polx = pol_evict_last();   // x is the reused operand
+        const int PF = A.pf_epochs > 0 ? A.pf_epochs : kPF;
+        const int T = d.ne * kPnB;                       // steps per warp
 
-    double rv[kD];
-    uint32_t ri[kD];
-    int32_t rb[kD];
-    double rx[kGD];
-    // running stream pointers: the warp's block of the next epoch to load
-    // (the stream is padded by kPnPadGroups groups, so the ring may read
-    // ahead past the panel's last epoch without bounds checks)
-    const int64_t blk0 = (int64_t)d.g0 * 32 + warp * 128;
-    const double* vp = A.gval + blk0 + lane * 2;
-    const uint32_t* ip = A.gidx + blk0 + lane * 4;
-    const int4* bp = reinterpret_cast<const int4*>(A.gbase4 + d.g0) + warp;
-    auto load4 = [&](int u) {   // the next epoch's four steps into ring slots u..u+3
-        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
-                     : "=d"(rv[u]), "=d"(rv[u + 1]) : "l"(vp), "l"(pol));
-        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
-                     : "=d"(rv[u + 2]), "=d"(rv[u + 3]) : "l"(vp + 64), "l"(pol));
-        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
-                     : "=r"(ri[u]), "=r"(ri[u + 1]), "=r"(ri[u + 2]), "=r"(ri[u + 3]) : "l"(ip), "l"(pol));
-        asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(rb[u]), "=r"(rb[u + 1]), "=r"(rb[u + 2]), "=r"(rb[u + 3]) : "l"(bp));
-        vp += kPnWarps * 128;
-        ip += kPnWarps * 128;
-        bp += kPnWarps;
-    };
-    double racc = 0.0;
-    auto gather = [&](uint32_t i, int32_t b) -> double {
-        if (MODE == 1) return 1.0;
-        if (MODE == 6) return __ldg(A.x_lo + ((b + (int)(i & 0xFFF)) & 0x3FFFF));
-        // unconditional: a padding lane reads x[base] (valid) and adds 0 * x into
-        // the scratch y slot -- a predicated-off load behind a branch made the
-        // warp wait for the gather at the branch (measured 1.6x slower)
-        // XS: x is split at x_split between two buffers (world > 1: interior |
-        // gathered border); world 1 reads one vector (no select per gather)
-        // column = base + delta (non-negative, < 2^31): one unsigned 32-bit add
-        // and one wide multiply-add form the address
-        const uint32_t c = (uint32_t)b + (i & kDeltaMask);
-        const double* xa = !XS ? A.x_lo + c
-                               : (int32_t)c < A.x_split ? A.x_lo + c : A.x_hi + (c - (uint32_t)A.x_split);
-        if (MODE == 25) return ld_x_na(xa, polx);
-        return ld_x(xa, polx);
-    };
-    // L2 prefetch of the panel's group stream kPF epochs ahead (one bulk
-    // prefetch per array per epoch, issued by thread 0): the register ring
-    // then waits for L2, not HBM, latency -- the x gathers depend on the
-    // loaded indices, so their distance is what bounds the pipeline.
-    // Past the panel's last epoch it prefetches the first epochs of panel
-    // p + gridDim.x -- about the panel the block scheduler starts next, on
-    // whichever SM frees first -- so a new CTA's ring does not fill from HBM.
-    int nx_g0 = 0, nx_ne = 0;
-    if (tid == 0 && MODE != 24 && p + (int)gridDim.x < A.n_panels) {
-        nx_g0 = A.panel[p + gridDim.x].g0;
-        nx_ne = A.panel[p + gridDim.x].ne;
-    }
-    auto prefetch_epoch = [&](int e) {
-        if (tid != 0) return;
-        int64_t g;
-        if (e < d.ne) g = (int64_t)d.g0 + (int64_t)e * kPnEpoch;
-        else if (e - d.ne < nx_ne) g = (int64_t)nx_g0 + (int64_t)(e - d.ne) * kPnEpoch;
-        else return;
-        // normal priority: an evict_first prefetch is the first victim of the next one
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.gval + g * 32), "r"(kPnEpoch * 32 * 8)
-                     : "memory");
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.gidx + g * 32), "r"(kPnEpoch * 32 * 4)
-                     : "memory");
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.gbase4 + g), "r"(kPnEpoch * 4) : "memory");
-    };
-    if (MODE != 4) {
-        for (int e = 0; e < PF; ++e) prefetch_epoch(e);
-        // this panel's slice of the next SB block's x(C_k), kept in L2 (evict_last)
-        if (tid == 32 && d.pf_len > 0) {
-            const uint64_t pl = pol_evict_last();
-            // 16-byte aligned start and length (bulk prefetch granularity)
-            const uintptr_t a0 = reinterpret_cast<uintptr_t>(A.x_lo + d.pf_col) & ~uintptr_t(15);
-            const uintptr_t a1 = reinterpret_cast<uintptr_t>(A.x_lo + d.pf_col + d.pf_len) & ~uintptr_t(15);
-            for (uintptr_t a = a0; a < a1; a += 32768) {
-                const uint32_t n = (uint32_t)(a1 - a < 32768 ? a1 - a : 32768);
-                asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(a), "r"(n), "l"(pl)
-                             : "memory");
+        double rv[kD];
+        uint32_t ri[kD];
+        int32_t rb[kD];
+        double rx[kGD];
+        // running stream pointers: the warp's block of the next epoch to load
+        // (the stream is padded by kPnPadGroups groups, so the ring may read
+        // ahead past the panel's last epoch without bounds checks)
+        const int64_t blk0 = (int64_t)d.g0 * 32 + warp * 128;
+        const double* vp = A.gval + blk0 + lane * 2;
+        const uint32_t* ip = A.gidx + blk0 + lane * 4;
+        const int4* bp = reinterpret_cast<const int4*>(A.gbase4 + d.g0) + warp;
+        auto load4 = [&](int u) {   // the next epoch's four steps into ring slots u..u+3
+            asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+                         : "=d"(rv[u]), "=d"(rv[u + 1]) : "l"(vp), "l"(pol));
+            asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+                         : "=d"(rv[u + 2]), "=d"(rv[u + 3]) : "l"(vp + 64), "l"(pol));
+            asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                         : "=r"(ri[u]), "=r"(ri[u + 1]), "=r"(ri[u + 2]), "=r"(ri[u + 3]) : "l"(ip), "l"(pol));
+            asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(rb[u]), "=r"(rb[u + 1]), "=r"(rb[u + 2]), "=r"(rb[u + 3]) : "l"(bp));
+            vp += kPnWarps * 128;
+            ip += kPnWarps * 128;
+            bp += kPnWarps;
+        };
+        double racc = 0.0;
+        auto gather = [&](uint32_t i, int32_t b) -> double {
+            if (MODE == 1) return 1.0;
+            if (MODE == 6) return __ldg(A.x_lo + ((b + (int)(i & 0xFFF)) & 0x3FFFF));
+            // unconditional: a padding lane reads x[base] (valid) and adds 0 * x into
+            // the scratch y slot -- a predicated-off load behind a branch made the
+            // warp wait for the gather at the branch (measured 1.6x slower)
+            // XS: x is split at x_split between two buffers (world > 1: interior |
+            // gathered border); world 1 reads one vector (no select per gather)
+            // column = base + delta (non-negative, < 2^31): one unsigned 32-bit add
+            // and one wide multiply-add form the address
+            const uint32_t c = (uint32_t)b + (i & kDeltaMask);
+            const double* xa = !XS ? A.x_lo + c
+                                   : (int32_t)c < A.x_split ? A.x_lo + c : A.x_hi + (c - (uint32_t)A.x_split);
+            if (MODE == 25) return ld_x_na(xa, polx);
+            return ld_x(xa, polx);
+        };
+        // L2 prefetch of the panel's group stream kPF epochs ahead (one bulk
+        // prefetch per array per epoch, issued by thread 0): the register ring
+        // then waits for L2, not HBM, latency -- the x gathers depend on the
+        // loaded indices, so their distance is what bounds the pipeline.
+        // Past the panel's last epoch it prefetches the first epochs of panel
+        // p + gridDim.x -- about the panel the block scheduler starts next, on
+        // whichever SM frees first -- so a new CTA's ring does not fill from HBM.
+        int nx_g0 = 0, nx_ne = 0;
+        if (tid == 0 && MODE != 24 && p + (int)gridDim.x < A.n_panels) {
+            nx_g0 = A.panel[p + gridDim.x].g0;
+            nx_ne = A.panel[p + gridDim.x].ne;
+        }
+        auto prefetch_epoch = [&](int e) {
+            if (tid != 0) return;
+            int64_t g;
+            if (e < d.ne) g = (int64_t)d.g0 + (int64_t)e * kPnEpoch;
+            else if (e - d.ne < nx_ne) g = (int64_t)nx_g0 + (int64_t)(e - d.ne) * kPnEpoch;
+            else return;
+            // normal priority: an evict_first prefetch is the first victim of the next one
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.gval + g * 32), "r"(kPnEpoch * 32 * 8)
+                         : "memory");
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.gidx + g * 32), "r"(kPnEpoch * 32 * 4)
+                         : "memory");
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.gbase4 + g), "r"(kPnEpoch * 4) : "memory");
+        };
+        if (MODE != 4) {
+            for (int e = 0; e < PF; ++e) prefetch_epoch(e);
+            // this panel's slice of the next SB block's x(C_k), kept in L2 (evict_last)
+            if (tid == 32 && d.pf_len > 0) {
+                const uint64_t pl = pol_evict_last();
+                // 16-byte aligned start and length (bulk prefetch granularity)
+                const uintptr_t a0 = reinterpret_cast<uintptr_t>(A.x_lo + d.pf_col) & ~uintptr_t(15);
+                const uintptr_t a1 = reinterpret_cast<uintptr_t>(A.x_lo + d.pf_col + d.pf_len) & ~uintptr_t(15);
+                for (uintptr_t a = a0; a < a1; a += 32768) {
+                    const uint32_t n = (uint32_t)(a1 - a < 32768 ? a1 - a : 32768);
+                    asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(a), "r"(n), "l"(pl)
+                                 : "memory");
+                }
             }
         }
-    }
-#pragma unroll
-    for (int u = 0; u < kD; u += 4) load4(u);
-#pragma unroll
-    for (int u = 0; u < kGD; ++u) rx[u] = gather(ri[u], rb[u]);
+    #pragma unroll
+        for (int u = 0; u < kD; u += 4) load4(u);
+    #pragma unroll
+        for (int u = 0; u < kGD; ++u) rx[u] = gather(ri[u], rb[u]);
 
-    auto step = [&](int u) {   // consume ring slot u (compile-time)
-        const uint32_t i = ri[u];
-        if (MODE == 2) {
-            racc = fma(rv[u], rx[u % kGD], racc);
-        } else {
-            // padding lanes carry the scratch slot (host upload), value 0
-            const int r = (int)(i >> kPnDeltaBits);
-            ys[r] = fma(rv[u], rx[u % kGD], ys[r]);
+        auto step = [&](int u) {   // consume ring slot u (compile-time)
+            const uint32_t i = ri[u];
+            if (MODE == 2) {
+                racc = fma(rv[u], rx[u % kGD], racc);
+            } else {
+                // padding lanes carry the scratch slot (host upload), value 0
+                const int r = (int)(i >> kPnDeltaBits);
+                ys[r] = fma(rv[u], rx[u % kGD], ys[r]);
+            }
+        };
+        auto epoch_end = [&](int t) {
+            if (MODE != 3) __syncthreads();
+            if (MODE != 4) prefetch_epoch(t / kPnB + PF);
+        };
+        // whole ring turns without bounds checks: loads and gathers past the
+        // panel's end read the next panel's (or the pad's) valid stream
+        int t0 = 0;
+        for (; t0 + kD <= T; t0 += kD) {
+    #pragma unroll
+            for (int u = 0; u < kD; ++u) {
+                step(u);
+                // after the warp's last step of an epoch: refill its four slots with
+                // the steps kD later
+                if (u % 4 == 3) load4(u - 3);
+                rx[u % kGD] = gather(ri[(u + kGD) % kD], rb[(u + kGD) % kD]);
+                if (u % kPnB == kPnB - 1) epoch_end(t0 + u);   // epoch boundary
+            }
         }
-    };
-    auto epoch_end = [&](int t) {
-        if (MODE != 3) __syncthreads();
-        if (MODE != 4) prefetch_epoch(t / kPnB + PF);
-    };
-    // whole ring turns without bounds checks: loads and gathers past the
-    // panel's end read the next panel's (or the pad's) valid stream
-    int t0 = 0;
-    for (; t0 + kD <= T; t0 += kD) {
-#pragma unroll
-        for (int u = 0; u < kD; ++u) {
+        // the last T - t0 (0, 4 or 8) steps are already in the ring
+    #pragma unroll
+        for (int u = 0; u < kD - 4; ++u) {
+            if (t0 + u >= T) break;
             step(u);
-            // after the warp's last step of an epoch: refill its four slots with
-            // the steps kD later
-            if (u % 4 == 3) load4(u - 3);
-            rx[u % kGD] = gather(ri[(u + kGD) % kD], rb[(u + kGD) % kD]);
-            if (u % kPnB == kPnB - 1) epoch_end(t0 + u);   // epoch boundary
+            if (u + kGD < kD) rx[u % kGD] = gather(ri[(u + kGD) % kD], rb[(u + kGD) % kD]);
+            if (u % kPnB == kPnB - 1) epoch_end(t0 + u);
         }
-    }
-    // the last T - t0 (0, 4 or 8) steps are already in the ring
-#pragma unroll
-    for (int u = 0; u < kD - 4; ++u) {
-        if (t0 + u >= T) break;
-        step(u);
-        if (u + kGD < kD) rx[u % kGD] = gather(ri[(u + kGD) % kD], rb[(u + kGD) % kD]);
-        if (u % kPnB == kPnB - 1) epoch_end(t0 + u);
-    }
-    if (MODE == 2 && racc == 1.2345) ys[0] = racc;
-    // epilogue: y[row] = ys[slot(row)].  The slot loads are batched 16 per
-    // thread (clamped addresses, no branch) and the first batch is issued
-    // before the barrier, so their latency is not paid once per row.
-    constexpr int EB = 16;
-    uint16_t sl[EB];
-    const uint16_t* r2s = A.row2slot + d.row0;
-    const int nrl = d.nrows;
-    auto load_slots = [&](int i0) {
-#pragma unroll
-        for (int k = 0; k < EB; ++k) sl[k] = r2s[min(i0 + k * kT, nrl - 1)];
-    };
-    load_slots(tid);
-    __syncthreads();
+        if (MODE == 2 && racc == 1.2345) ys[0] = racc;
+        // epilogue: y[row] = ys[slot(row)].  The slot loads are batched 16 per
+        // thread (clamped addresses, no branch) and the first batch is issued
+        // before the barrier, so their latency is not paid once per row.
+        constexpr int EB = 16;
+        uint16_t sl[EB];
+        const uint16_t* r2s = A.row2slot + d.row0;
+        const int nrl = d.nrows;
+        auto load_slots = [&](int i0) {
+    #pragma unroll
+            for (int k = 0; k < EB; ++k) sl[k] = r2s[min(i0 + k * kT, nrl - 1)];
+        };
+        load_slots(tid);
+        __syncthreads();
 
-    double mx = 0.0;
-    for (int i0 = tid; i0 < nrl; i0 += EB * kT) {
-        if (i0 != tid) load_slots(i0);
-#pragma unroll
-        for (int k = 0; k < EB; ++k) {
-            const int i = i0 + k * kT;
-            if (i < nrl && sl[k] < 0x8000) {        // split rows: below
-                const double v = ys[sl[k]];
-                A.y[d.row0 + i] = v;
-                mx = fmax(mx, fabs(v));
+        double mx = 0.0;
+        for (int i0 = tid; i0 < nrl; i0 += EB * kT) {
+            if (i0 != tid) load_slots(i0);
+    #pragma unroll
+            for (int k = 0; k < EB; ++k) {
+                const int i = i0 + k * kT;
+                if (i < nrl && sl[k] < 0x8000) {        // split rows: below
+                    const double v = ys[sl[k]];
+                    A.y[d.row0 + i] = v;
+                    mx = fmax(mx, fabs(v));
+                }
             }
         }
-    }
-    // rows split into virtual rows (long rows; a split handle's (row, part)
-    // segments): up to kPnFoldSeq slots, one thread per row adds them in fold
-    // order (part order); longer rows one warp each, lanes sum strided
-    // slots, fixed xor tree.  Both orders are fixed by the plan (deterministic).
-    for (int k = tid; k < d.split_short; k += kT) {
-        const int f = sdesc[3 * k], c = sdesc[3 * k + 1];
-        double v = ys[ssl[f]];
-        for (int j = 1; j < c; ++j) v += ys[ssl[f + j]];
-        A.y[d.row0 + sdesc[3 * k + 2]] = v;
-        mx = fmax(mx, fabs(v));
-    }
-    for (int k = d.split_short + warp; k < d.split_n; k += NW) {
-        const int f = sdesc[3 * k], c = sdesc[3 * k + 1];
-        double v = 0.0;
-        for (int j = lane; j < c; j += 32) v += ys[ssl[f + j]];
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-        if (lane == 0) {
+        // rows split into virtual rows (long rows; a split handle's (row, part)
+        // segments): up to kPnFoldSeq slots, one thread per row adds them in fold
+        // order (part order); longer rows one warp each, lanes sum strided
+        // slots, fixed xor tree.  Both orders are fixed by the plan (deterministic).
+        for (int k = tid; k < d.split_short; k += kT) {
+            const int f = sdesc[3 * k], c = sdesc[3 * k + 1];
+            double v = ys[ssl[f]];
+            for (int j = 1; j < c; ++j) v += ys[ssl[f + j]];
             A.y[d.row0 + sdesc[3 * k + 2]] = v;
             mx = fmax(mx, fabs(v));
         }
-    }
-    if (A.maxabs_slots) {
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-        if (lane == 0 && mx > 0.0)
-            atomicMax(A.maxabs_slots + ((p * NW + warp) & (kMaxSlots - 1)) * kSlotStride,
-                      (unsigned long long)__double_as_longlong(mx));
+        for (int k = d.split_short + warp; k < d.split_n; k += NW) {
+            const int f = sdesc[3 * k], c = sdesc[3 * k + 1];
+            double v = 0.0;
+            for (int j = lane; j < c; j += 32) v += ys[ssl[f + j]];
+    #pragma unroll
+            for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+            if (lane == 0) {
+                A.y[d.row0 + sdesc[3 * k + 2]] = v;
+                mx = fmax(mx, fabs(v));
+            }
+        }
+        if (A.maxabs_slots) {
+    #pragma unroll
+            for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+            if (lane == 0 && mx > 0.0)
+                atomicMax(A.maxabs_slots + ((p * NW + warp) & (kMaxSlots - 1)) * kSlotStride,
+                          (unsigned long long)__double_as_longlong(mx));
+        }
+        if (!PERSIST) break;
+        __syncthreads();   // the epilogue's reads of ys before the next panel zeroes it
     }
 }
 
@@ -339,6 +344,10 @@ cudaError_t launch_panel(const PnArgs& a, cudaStream_t s) {
         attr((const void*)spmv_panel_kernel<0, 8, 3, true>);
         attr((const void*)spmv_panel_kernel<25, 8, 2, true>);
         attr((const void*)spmv_panel_kernel<25, 8, 3, true>);
+        attr((const void*)spmv_panel_kernel<0, 8, 4, true, true>);
+        attr((const void*)spmv_panel_kernel<0, 8, 4, false, true>);
+        attr((const void*)spmv_panel_kernel<25, 8, 4, true, true>);
+        attr((const void*)spmv_panel_kernel<25, 8, 4, false, true>);
         attr((const void*)spmv_panel_kernel<0, 8, 4>);
         attr((const void*)spmv_panel_kernel<0, 16, 4>);
         attr((const void*)spmv_panel_kernel<0, 16, 8>);
@@ -358,6 +367,30 @@ cudaError_t launch_panel(const PnArgs& a, cudaStream_t s) {
     case 21: spmv_panel_kernel<0, 16, 8><<<b.n_panels, kT, smem, s>>>(b); break;
     default: {
         const bool xs = b.x_split != INT32_MAX;
+        if (b.persist && b.gather_na == 0 && (b.ring == 0 || b.ring == 8)) {   // measurement switch
+            static int nsm = 0;
+            if (!nsm) {
+                int dev = 0;
+                cudaGetDevice(&dev);
+                cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+            }
+            const int grid = std::min(b.n_panels, nsm);
+            if (xs) spmv_panel_kernel<0, 8, 4, true, true><<<grid, kT, smem, s>>>(b);
+            else spmv_panel_kernel<0, 8, 4, false, true><<<grid, kT, smem, s>>>(b);
+            return cudaGetLastError();
+        }
+        if (b.persist && b.gather_na && (b.ring == 0 || b.ring == 8)) {
+            static int nsm2 = 0;
+            if (!nsm2) {
+                int dev = 0;
+                cudaGetDevice(&dev);
+                cudaDeviceGetAttribute(&nsm2, cudaDevAttrMultiProcessorCount, dev);
+            }
+            const int grid = std::min(b.n_panels, nsm2);
+            if (xs) spmv_panel_kernel<25, 8, 4, true, true><<<grid, kT, smem, s>>>(b);
+            else spmv_panel_kernel<25, 8, 4, false, true><<<grid, kT, smem, s>>>(b);
+            return cudaGetLastError();
+        }
         // ring: steps in flight 8 / 12 / 16 with gathers 4 steps ahead; 1208 /
         // 1608: 12 / 16 with gathers 8 ahead; 802 / 803: 8 with gathers 2 / 3
         // ahead (measurements)

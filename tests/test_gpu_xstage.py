@@ -177,3 +177,20 @@ def test_panel_x_split_path(monkeypatch, name):
     y2 = gpu_apply(h2, xh, p.m)
     assert np.array_equal(y1.view(np.int64), y2.view(np.int64))
     assert_parity(y2, yh_ref, S, what=f"x-split path/{name}")
+
+
+@pytest.mark.parametrize("name", ["c5s", "c4s"])
+def test_persistent_panels(monkeypatch, name):
+    """SPMV_PN_PERSIST: one CTA per SM walks the panels (measurement switch);
+    same plan, same per-row order, so y equals the one-CTA-per-panel launch
+    bit for bit."""
+    monkeypatch.setenv("SPMV_KERNEL", "panel")
+    monkeypatch.setenv("SPMV_PN_ROWS", "700")
+    p = synth.make(name, variant="real")
+    x = p.x()
+    xh, yh_ref, S = oracle_permuted(p, x)
+    y1 = gpu_apply(create(p), xh, p.m)
+    monkeypatch.setenv("SPMV_PN_PERSIST", "1")
+    y2 = gpu_apply(create(p), xh, p.m)
+    assert np.array_equal(y1.view(np.int64), y2.view(np.int64))
+    assert_parity(y2, yh_ref, S, what=f"persistent/{name}")
