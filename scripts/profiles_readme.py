@@ -48,9 +48,9 @@ C3 multiple-SpMxV (`r01_c3_split.json`, L2 flushed, SpMxV alone): single SpMxV
 sequence {c3['split_literal_cold_ms']:.4f} ms ({c3['split_literal_cold_ms'] / c3['split_fused_cold_ms']:.1f}× the fused pass).
 
 `roofline.traffic` in a bench line is read from `ncu_traffic.json` (DRAM bytes per launch of the
-`--set full` capture); the lines above were printed before that file was updated to this round's
-final capture (C5 16.22 GB, C4 0.80 GB per launch, vs 14.72 / 0.66 GB algorithmic: group
-padding, per-group bases, the row→slot map and the x prefetch).
+`--set full` capture of the same kernel, previous round-end run): C5 16.22 GB, C4 0.80 GB per
+launch vs 14.72 / 0.66 GB algorithmic (group padding, per-group bases, the row→slot map and the x
+prefetch).
 
 Kernel evidence: `r01_panel_c5_c4.md` (the C5 and C4 panel kernels, ncu `--set full`, per-SASS
 memory counters), `r01_launches_c5.csv` (launch list of the C5 bench command), `r01_c5_rowtile.md`
