@@ -52,6 +52,12 @@ sequence {c3['split_literal_cold_ms']:.4f} ms ({c3['split_literal_cold_ms'] / c3
 launch vs 14.72 / 0.66 GB algorithmic (group padding, per-group bases, the row→slot map and the x
 prefetch).
 
+Reproduce on a B200: `R=rNN bash scripts/final_round.sh` (GPU tests, smoke, the five bench lines,
+the reference arm, the C3 split comparison, the power-drift trace, the C5 launch list and the
+C5/C4 ncu captures, into `gpurun_out/`), then `python scripts/panel_md.py rNN` and
+`python scripts/profiles_readme.py` after copying the lines here.  Interleaved A/B of plan or
+library variants: `scripts/ab_inter.py`.
+
 Kernel evidence: `r01_panel_c5_c4.md` (the C5 and C4 panel kernels, ncu `--set full`, per-SASS
 memory counters), `r01_launches_c5.csv` (launch list of the C5 bench command), `r01_c5_rowtile.md`
 (row-tile kernel on C5, earlier in the round), `r01_micro.json`, `r01_gather_modes.json`,
