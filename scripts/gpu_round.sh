@@ -1,4 +1,3 @@
 python -m paper_1203_2739_b200.build > /dev/null
-cd scripts
-ROUNDS=6 timeout 900 python ab_inter.py c2 "" "SPMV_TILE_NNZ=1700" "SPMV_TILE_NNZ=1400" "SPMV_TILE_NNZ=1024" "SPMV_TILE_NNZ=700" 2>&1 | tail -1
-ROUNDS=6 timeout 900 python ab_inter.py c1 "" "SPMV_TILE_NNZ=1024" "SPMV_TILE_NNZ=512" "SPMV_TILE_NNZ=256" 2>&1 | tail -1
+timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
