@@ -210,17 +210,47 @@ def oracle_sample(p, target_s: float, nthreads: int, start_row: int = 0, max_row
         rows = int(min(p.m, max(rows * 2, rows * target_s / max(dt, 1e-3) * 1.1)))
 
 
-def cpu_leg(args, p, split, x_gpu, y_gpu):
-    """The only place the timed arm touches oracle/: the CPU baseline and the
-    sampled, teacher-forced parity check of the last timed step."""
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_one_core(p, target_s: float):
+    """The oracle on ONE pinned host core (sched_setaffinity): the paper's
+    single-threaded setting (OSKI on one core)."""
+    old = os.sched_getaffinity(0)
+    core = min(old)
+    try:
+        os.sched_setaffinity(0, {core})
+        return oracle_sample(p, target_s, 1), core
+    finally:
+        os.sched_setaffinity(0, old)
+
+
+def cpu_leg(args, p, split, x_gpu, y_gpu, m_gpu=None, xn_gpu=None):
+    """The only place the timed arm touches oracle/: the CPU baseline (all
+    cores and one pinned core) and the teacher-forced parity check of the last
+    timed step (y_t on sampled rows, m_t and x_{t+1} on every entry)."""
     import oracle
     cpu = parity = None
     if not args.no_cpu_baseline:
-        nthreads = os.cpu_count() or 1
+        nthreads = len(os.sched_getaffinity(0)) or os.cpu_count() or 1
         r = oracle_sample(p, args.cpu_seconds, nthreads)
+        r1, core = oracle_one_core(p, max(2.0, args.cpu_seconds / 2))
         cpu = {"value": r["gflops"], "unit": "GFLOP/s", "cores": nthreads, "kind": "oracle",
+               "cpu_model": cpu_model(), "nproc": os.cpu_count(),
                "sample": f"{r['rows']} consecutive original-order rows ({r['nnz']} nnz) of {args.workload}, "
-                         f"oracle.spmv (serial per-row fp64, rows over {nthreads} threads), {r['seconds']:.1f} s"}
+                         f"oracle.spmv (serial per-row fp64, rows over {nthreads} threads), {r['seconds']:.1f} s",
+               "one_core": {"value": r1["gflops"], "unit": "GFLOP/s", "cores": 1, "pinned_core": core,
+                            "sample": f"{r1['rows']} rows ({r1['nnz']} nnz), 1 thread pinned with "
+                                      f"sched_setaffinity, {r1['seconds']:.1f} s (the paper's single-core "
+                                      "setting, P:L142)"}}
     if not args.no_parity and x_gpu is not None:
         rng = np.random.default_rng(1234)
         nsamp = min(p.m, args.parity_rows)
@@ -237,7 +267,18 @@ def cpu_leg(args, p, split, x_gpu, y_gpu):
             yref = oracle.split(p.row_ptr, p.col, p.val, p.parts, p.n_parts, x_orig)[orow]
         nbad, worst, _ = oracle.check(y_gpu[prow], yref, S)
         parity = {"rows_checked": int(nsamp), "failures": int(nbad), "max_err_over_S": worst,
-                  "tol": 1e-12, "teacher_forced": True}
+                  "tol": 1e-12, "teacher_forced": True, "step": "last timed step"}
+        if m_gpu is not None and xn_gpu is not None:
+            # a9: m_t = max |y_t| exactly (over all rows), x_{t+1} = y_t / m_t bitwise (every entry)
+            y_orig = oracle.unpermute_y(p.row_perm, y_gpu) if p.row_perm is not None else y_gpu
+            m_ref = oracle.maxabs(y_orig)
+            xn_orig = xn_gpu[p.col_perm] if p.col_perm is not None else xn_gpu
+            xn_ref = oracle.scale(y_orig, m_gpu)
+            parity["maxabs_exact"] = bool(m_gpu == m_ref)
+            parity["x_next_bitwise"] = bool(np.array_equal(xn_orig.view(np.int64), xn_ref.view(np.int64)))
+            parity["x_next_entries"] = int(len(xn_ref))
+            if not (parity["maxabs_exact"] and parity["x_next_bitwise"]):
+                parity["failures"] += 1
     return cpu, parity
 
 
@@ -248,7 +289,7 @@ def run_reference(args, rank, world):
     if rank != 0:
         return 0
     p = make_problem(args.workload, 0, 1)
-    nthreads = os.cpu_count() or 1
+    nthreads = len(os.sched_getaffinity(0)) or os.cpu_count() or 1
     import oracle
     # calibrate a per-step sample of ~1 s (bounded), then time W + K steps
     cal = oracle_sample(p, 1.0, nthreads)
@@ -267,7 +308,7 @@ def run_reference(args, rank, world):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": args.workload, "desc": WORKLOAD_DESC[args.workload]},
             "cpu_baseline": {"value": gf, "unit": "GFLOP/s", "cores": nthreads, "kind": "oracle",
-                             "sample": sample},
+                             "cpu_model": cpu_model(), "sample": sample},
             "e2e": {"value": gf, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     del oracle
@@ -280,6 +321,7 @@ def run_reference(args, rank, world):
 def run_ours(args, rank, world, local_rank):
     import torch
     import paper_1203_2739_b200 as sp
+    from paper_1203_2739_b200 import diag
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -339,12 +381,9 @@ def run_ours(args, rank, world, local_rank):
         sp.spmv_maxabs(h, md, stream=stream)
         sp.spmv_normalize(h, yd, md, xnext, stream=stream)
 
-    # our kernels per step: the SpMxV tile kernel, the long-row kernel when the
-    # matrix has rows longer than a tile (row-tile family), max-abs finish and
-    # x-update for the power iterations
-    long_launch = 1 if (info["n_long_rows"] > 0 and not split and info["kernel"] in (0, 3, 5, 8)
-                        and os.environ.get("SPMV_LONG")) else 0
-    launches_per_step = 1 + long_launch + (2 if power else 0)
+    # our kernels per step: the SpMxV kernel (panel or row-tile), max-abs finish
+    # and x-update for the power iterations
+    launches_per_step = 1 + (2 if power else 0)
     cur = 0
     for _ in range(args.warmup):
         if l2_flush:
@@ -396,11 +435,14 @@ def run_ours(args, rank, world, local_rank):
     ms_per_step = total_ms / K
     gflops = 2.0 * p.nnz / (ms_per_step * 1e-3) / 1e9
 
-    # device copies of the last step's x_t and y_t for the CPU leg's parity check
+    # device copies of the last step's x_t, y_t, m_t and x_{t+1} for the CPU
+    # leg's parity check (teacher-forced: the oracle recomputes from x_t)
     if not power:
         x_last = xbuf[cur]
     y_gpu = yd.cpu().numpy() if world == 1 else None
     x_gpu = x_last.cpu().numpy() if world == 1 else None
+    m_gpu = float(md.item()) if (power and world == 1) else None
+    xn_gpu = xbuf[cur].cpu().numpy() if (power and world == 1) else None
 
     # ---------------- e2e through the C ABI with host buffers
     # Every step copies its input x from pinned host memory and reads its
@@ -502,11 +544,11 @@ def run_ours(args, rank, world, local_rank):
         sink = torch.zeros(1, dtype=torch.float64, device=dev)
         cnt = 8 << 30
         for _ in range(2):
-            sp.spmv_diag_micro(1, 0, gb, gb.numel() * 8, cnt, sink, stream=stream)
+            diag.micro(1, 0, gb, gb.numel() * 8, cnt, sink, stream=stream)
         g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         g0.record(stream)
         for _ in range(3):
-            sp.spmv_diag_micro(1, 0, gb, gb.numel() * 8, cnt, sink, stream=stream)
+            diag.micro(1, 0, gb, gb.numel() * 8, cnt, sink, stream=stream)
         g1.record(stream)
         torch.cuda.synchronize()
         fpeak = 3 * cnt / (g0.elapsed_time(g1) * 1e-3) / 1e9
@@ -516,18 +558,18 @@ def run_ours(args, rank, world, local_rank):
                   "bytes_per_launch": fbytes,
                   "note": "group stream + distinct 32-byte x sectors of the gathers (plan-time count) per launch / "
                           "SpMxV time; peak = 128-bit LDG stream over a 16 MB L2-resident buffer, measured in this "
-                          "run (spmv_diag_micro kind 1)"}
+                          "run (libspmv_diag.so spmv_diag_micro kind 1)"}
         del gb
     if not args.no_gather_peak and info["kernel"] != 7:   # the panel kernel does not gather once per nonzero
         gx = torch.rand(4 << 20, dtype=torch.float64, device=dev)      # 32 MB, L2-resident
         sink = torch.zeros(1, dtype=torch.float64, device=dev)
         cnt = 1 << 29
         for _ in range(2):
-            sp.spmv_diag_gather_mode(gx, cnt, 0, sink)
+            diag.gather_mode(gx, cnt, 0, sink, stream=stream)
         g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         g0.record(stream)
         for _ in range(3):
-            sp.spmv_diag_gather_mode(gx, cnt, 0, sink)
+            diag.gather_mode(gx, cnt, 0, sink, stream=stream)
         g1.record(stream)
         torch.cuda.synchronize()
         gpeak = 3 * cnt / (g0.elapsed_time(g1) * 1e-3) / 1e9
@@ -559,7 +601,7 @@ def run_ours(args, rank, world, local_rank):
     # ---------------- CPU leg (rank 0, N = 1 only): oracle baseline + sampled parity
     cpu, parity = None, None
     if rank == 0 and world == 1:
-        cpu, parity = cpu_leg(args, p, split, x_gpu, y_gpu)
+        cpu, parity = cpu_leg(args, p, split, x_gpu, y_gpu, m_gpu, xn_gpu)
 
     # ---------------- warm-L2 time (C1-C3 are otherwise timed with L2 flushed)
     extra = {}
@@ -589,20 +631,11 @@ def run_ours(args, rank, world, local_rank):
         xs_ = torch.from_numpy(np.ascontiguousarray(x)).to(dev)
         ys_ = torch.empty(p.m, dtype=torch.float64, device=dev)
 
-        def time_scrambled(kernel_env):
-            # SPMV_KERNEL is read at create: "rowtile" keeps the input CSR order
-            # (the paper's unordered baseline); "" lets the default planner run,
-            # whose panels sort each row panel's nonzeros by column by themselves
-            old = os.environ.get("SPMV_KERNEL")
-            if kernel_env:
-                os.environ["SPMV_KERNEL"] = kernel_env
-            try:
-                hs = sp.spmv_create(p.m, p.n, p.row_ptr, p.col, p.val)
-            finally:
-                if old is None:
-                    os.environ.pop("SPMV_KERNEL", None)
-                else:
-                    os.environ["SPMV_KERNEL"] = old
+        def time_scrambled(kernel):
+            # "rowtile" keeps the input CSR order (the paper's unordered
+            # baseline); "auto" lets the default planner run, whose panels sort
+            # each row panel's nonzeros by column by themselves
+            hs = sp.spmv_create(p.m, p.n, p.row_ptr, p.col, p.val, options=dict(kernel=kernel))
             kern = sp.spmv_get_info(hs)["kernel"]
             for _ in range(3):
                 sp.spmv_apply(hs, xs_, ys_, stream=stream)
@@ -619,7 +652,7 @@ def run_ours(args, rank, world, local_rank):
             return statistics.median(tms), KERNEL_NAMES.get(kern, str(kern))
 
         sms, skern = time_scrambled("rowtile")
-        pms, pkern = time_scrambled("")
+        pms, pkern = time_scrambled("auto")
         extra["reordering"] = {"scrambled_spmv_ms": sms, "reordered_spmv_ms": avg_spmv_ms,
                                "speedup": sms / avg_spmv_ms,
                                "scrambled_kernel": skern + " on the input (scrambled) CSR order, no blocks",

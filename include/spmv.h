@@ -59,7 +59,8 @@ typedef enum {
  * border_owner_ptr (optional, K+1 entries, may be NULL): block k owns border
  *   columns [border_owner_ptr[k], border_owner_ptr[k+1]) (absolute permuted
  *   column ids inside C_B) for the multi-GPU x layout; NULL = K equal slices
- *   C_B.start + floor(k |C_B| / K). */
+ *   C_B.start + floor(k |C_B| / K).  row_border_owner_ptr: the same for the
+ *   DB row border R_B (multi-GPU y layout of DB handles). */
 enum { SPMV_SB = 1, SPMV_DB = 2 };
 typedef struct {
     int32_t kind;
@@ -67,6 +68,9 @@ typedef struct {
     const int64_t* row_block_ptr;     /* K+2 */
     const int64_t* col_block_ptr;     /* K+2 */
     const int64_t* border_owner_ptr;  /* K+1 or NULL */
+    const int64_t* row_border_owner_ptr;  /* DB only, K+1 or NULL: block k owns border rows
+                                             [p[k], p[k+1]) of R_B for the multi-GPU y layout;
+                                             NULL = K equal slices R_B.start + floor(k |R_B| / K) */
 } spmv_blocks_t;
 
 /* Multi-GPU bootstrap: one process per GPU; every rank calls spmv_create with
@@ -74,8 +78,17 @@ typedef struct {
  * (made by spmv_nccl_unique_id on one rank and broadcast by the caller).
  * Rank g owns the contiguous diagonal blocks [floor(K g / world),
  * floor(K (g+1) / world)), their rows, their interior columns and their owned
- * border slices (spmv_shard_plan).  This is the row-slice decomposition
- * y_k <- R_k x of P:L79. */
+ * border slices (spmv_shard_plan).
+ *   SB (Eq.(1)): the row-slice decomposition y_k <- R_k x of P:L79; the only
+ *   exchange is the border x(C_B) (all-gathered every apply).
+ *   DB (Eq.(5)) -- the multiple-SpMxV across GPUs (f1): part k of
+ *   the split is block k's diagonal block plus its border slices (n_parts == K,
+ *   or n_parts == 0: the 2D block assignment -- a nonzero of block row i goes
+ *   to i's block, of a border row to its interior column's block, border x
+ *   border to the row's border slice); rank g computes its parts' products,
+ *   the border rows' per-part temporaries travel to the owner of the row,
+ *   which folds them in part order.
+ * All ranks must issue the same sequence of apply calls (collective). */
 typedef struct {
     int32_t rank;
     int32_t world;
@@ -92,6 +105,28 @@ enum {
     SPMV_SPLIT_LITERAL = 4     /* split_apply only: K separate passes y <- y + A^k x (the unfused    */
                                /* literal sequence of P:L109), instead of the fused pass            */
 };
+
+/* Create-time options (spmv_create_ex; NULL = all defaults).  Zero means
+ * "automatic" in every field. */
+enum { SPMV_KERNEL_AUTO = 0, SPMV_KERNEL_PANEL = 1, SPMV_KERNEL_ROWTILE = 2 };
+enum { SPMV_SPLIT_AUTO = 0, SPMV_SPLIT_PANEL = 1, SPMV_SPLIT_ROWS = 2 };
+enum { SPMV_EXCHANGE_AUTO = 0, SPMV_EXCHANGE_NCCL = 1, SPMV_EXCHANGE_P2P = 2 };
+typedef struct {
+    int32_t struct_size;     /* sizeof(spmv_options_t) (forward compatibility), or 0 */
+    int32_t kernel;          /* single SpMxV: AUTO = column-sorted panels unless the plan pads > 25 %
+                                (then row tiles); PANEL forces the panels (whatever the padding);
+                                ROWTILE forces row tiles */
+    int32_t panel_rows;      /* y slots per panel; 0 = automatic (whole waves of ~16 K-slot panels) */
+    int32_t split_kernel;    /* fused multiple-SpMxV: AUTO / PANEL (a y slot per (row, part) segment) /
+                                ROWS (row-major part segments, row tiles) */
+    int32_t exchange;        /* world > 1: AUTO = P2P when every GPU pair has peer access and stream
+                                memory operations are available, else NCCL.  P2P: copy-engine pushes of
+                                the border slices into the peers' buffers (CUDA IPC) with device flags,
+                                overlapped with the interior epochs of the kernel (a4, f2).  NCCL:
+                                ncclAllGather / grouped send-recv on a comm stream, joined before
+                                the kernel */
+    int32_t reserved[11];
+} spmv_options_t;
 
 /* spmv_create -- ingest, validate, permute and plan (once; not per SpMxV).
  *   m, n, nnz     : matrix dimensions and nonzero count (m, n >= 0; nnz >= 0)
@@ -116,13 +151,26 @@ spmv_status_t spmv_create(int64_t m, int64_t n, int64_t nnz,
                           const spmv_dist_t* dist,
                           spmv_handle_t* out);
 
+/* spmv_create_ex -- spmv_create with options (NULL = spmv_create). */
+spmv_status_t spmv_create_ex(int64_t m, int64_t n, int64_t nnz,
+                             const int64_t* row_ptr, const int32_t* col_idx, const double* val,
+                             const int32_t* row_perm, const int32_t* col_perm,
+                             const spmv_blocks_t* blocks,
+                             int32_t n_parts, const int32_t* part_of_nnz,
+                             const spmv_dist_t* dist, const spmv_options_t* options,
+                             spmv_handle_t* out);
+
 /* spmv_apply -- single-SpMxV y^ <- A^ x^, asynchronous on `stream`.
  *   x : device double[x_len]; PERMUTED: x^ (1 GPU: n entries; world > 1: the
  *       rank's owned x, see spmv_info_t); ORIGINAL: x in the user's order
  *   y : device double[y_len]; overwritten (not accumulated); must not alias x
+ *       (world > 1: the rank's owned rows, y_local_len entries)
  *   Both must be 8-byte aligned.  No host synchronisation, no allocation:
  *   CUDA-graph capturable (1 GPU).  With world > 1 the border-column x
- *   entries are exchanged with NCCL over NVLink before the local SpMxV.
+ *   entries are exchanged over NVLink (P2P copy engines or NCCL); on a DB
+ *   handle the border rows' per-part temporaries are exchanged and folded in
+ *   part order too (the multiple-SpMxV across GPUs).  x must not
+ *   change until the call's work on `stream` has completed.
  * Errors: SPMV_ERR_USAGE, SPMV_ERR_DATA (length mismatch), SPMV_ERR_UNSUPPORTED,
  *         SPMV_ERR_INTERNAL. */
 spmv_status_t spmv_apply(spmv_handle_t h, const double* x, int64_t x_len,
@@ -130,10 +178,10 @@ spmv_status_t spmv_apply(spmv_handle_t h, const double* x, int64_t x_len,
 
 /* spmv_split_apply -- multiple-SpMxV y = 0; y <- y + A^k x, k = 1..K
  * (P:L107-109), in PERMUTED space (or ORIGINAL with the flag).  Default: one
- * fused pass that walks every row tile's part segments in part order and
- * keeps y on chip; SPMV_SPLIT_LITERAL: K passes, y read-modify-written in
- * global memory.  Errors as spmv_apply, plus SPMV_ERR_UNSUPPORTED when the
- * handle has no split. */
+ * fused pass that keeps every (row, part) temporary on chip and adds them to
+ * y in part order, one y store per row; SPMV_SPLIT_LITERAL: K passes, y
+ * read-modify-written in global memory (world 1).  Errors as spmv_apply, plus
+ * SPMV_ERR_UNSUPPORTED when the handle has no split. */
 spmv_status_t spmv_split_apply(spmv_handle_t h, const double* x, int64_t x_len,
                                double* y, int64_t y_len, uint32_t flags, void* stream);
 
@@ -146,46 +194,49 @@ spmv_status_t spmv_destroy(spmv_handle_t h);
 
 typedef struct {
     int64_t m, n, nnz;            /* global (whole matrix) */
-    int64_t m_local, nnz_local;   /* this rank's rows / nonzeros (== global at world 1) */
-    int64_t row_begin;            /* first global permuted row owned by this rank */
+    int64_t m_local, nnz_local;   /* this rank's compute rows / nonzeros (== global at world 1) */
+    int64_t row_begin;            /* first global permuted row of the rank's blocks */
     int64_t x_local_len;          /* length of x passed to apply on this rank (PERMUTED) */
     int64_t x_interior_begin;     /* global permuted column of x_local[0] */
     int64_t x_interior_len;       /* interior columns at the front of x_local */
     int64_t x_border_begin;       /* global permuted column of the owned border slice */
     int64_t x_border_len;         /* owned border slice length (tail of x_local) */
     int64_t border_total;         /* |C_B| */
-    int64_t n_tiles;              /* row tiles of the SpMxV kernel */
-    int64_t n_long_rows;          /* rows handled by the long-row path */
+    int64_t n_tiles;              /* row tiles (row-tile kernel) */
+    int64_t n_long_rows;          /* rows longer than a tile */
     int64_t bytes_alg;            /* 12 nnz + 4 (m+1) + 8 m + 8 n_touched, local */
     int64_t bytes_alg_split;      /* same for the fused split pass (0 without a split) */
     int64_t split_segments;       /* (row, part) segments of the split layout */
-    int64_t xs_panels;            /* panel kernels (7, 6): panels (0 when the row-tile kernel is used) */
-    int64_t xs_groups;            /* panel kernels: 32-entry groups */
-    int64_t xs_pad_slots;         /* panel kernels: padding slots among them */
+    int64_t panels;               /* panel kernel: panels (0 when the row-tile kernel is used) */
+    int64_t groups;               /* panel kernel: 32-entry groups */
+    int64_t pad_slots;            /* panel kernel: padding slots among them */
     int64_t bytes_stream;         /* device bytes the apply kernel actually reads + writes (no x reuse) */
     int32_t n_parts, rank, world, kind;
     int32_t has_owner_map;        /* spmv_normalize is available */
-    int32_t kernel;               /* single-SpMxV kernel: 7 column-sorted panels (default: SB handles at
-                                     any world size, any matrix at world 1, when the plan pads < 25 %),
-                                     0 row-tile (otherwise); the others are measurement variants
-                                     (SPMV_KERNEL environment variable at create) */
-    int32_t split_kernel;         /* fused multiple-SpMxV kernel: 7 column-sorted panels with one y slot
-                                     per (row, part) segment (default), 3 row-major part segments,
-                                     1 part-major tiles; 0 without a split */
-    int32_t reserved;
-    int64_t gather_sectors;       /* panel kernel (7): distinct 32-byte x sectors its gathers request per
-                                     launch (counted at plan time); with bytes_stream, the bytes that cross
-                                     L2 -> SM per launch (the kernel's second roofline) */
+    int32_t kernel;               /* single-SpMxV kernel: 7 column-sorted panels, 0 row tiles */
+    int32_t split_kernel;         /* fused multiple-SpMxV: 7 panels with one y slot per (row, part)
+                                     segment, 3 row-major part segments; 0 without a split */
+    int32_t exchange;             /* world > 1: 1 NCCL, 2 P2P copy engines (overlapped), 3 loopback (test) */
+    int64_t gather_sectors;       /* panel kernel: distinct 32-byte x sectors its gathers request per
+                                     launch (plan time); with bytes_stream, the bytes that cross L2 -> SM */
+    int64_t y_local_len;          /* length of y passed to apply on this rank */
+    int64_t y_border_begin;       /* DB world > 1: global permuted row of the owned border-row slice */
+    int64_t y_border_len;         /*   (tail of y_local) */
+    int64_t deferred;             /* panel kernel: nonzeros deferred to a later epoch (repeated row) */
+    int64_t y_wavefronts_x1000;   /* panel kernel: predicted shared-memory wavefronts per y access x 1000 */
+    int64_t exchange_timeouts;    /* world > 1 P2P: device-side flag waits that timed out (should be 0;
+                                     reading it synchronises the device) */
 } spmv_info_t;
 
 spmv_status_t spmv_get_info(spmv_handle_t h, spmv_info_t* info);
 
-/* Shard plan of the multi-GPU SB layout (host-only, no GPU needed; the same
+/* Shard plan of the multi-GPU layout (host-only, no GPU needed; the same
  * routine spmv_create uses).  Rank `rank` of `world` owns blocks
  * [block_begin, block_end) = [floor(K r / world), floor(K (r+1) / world)),
- * rows [row_begin, row_end), x_local = [interior columns
- * x_interior_begin .. +x_interior_len | owned border slice x_border_begin ..
- * +x_border_len] (all PERMUTED global ids).  world == 1: the whole matrix. */
+ * rows [row_begin, row_end) (+ DB: border rows [y_border_begin, +y_border_len)),
+ * x_local = [interior columns x_interior_begin .. +x_interior_len | owned
+ * border slice x_border_begin .. +x_border_len] (all PERMUTED global ids).
+ * world == 1: the whole matrix. */
 typedef struct {
     int64_t block_begin, block_end;
     int64_t row_begin, row_end;
@@ -193,6 +244,8 @@ typedef struct {
     int64_t x_border_begin, x_border_len;
     int64_t x_local_len;
     int64_t border_begin, border_total;   /* C_B */
+    int64_t y_border_begin, y_border_len; /* DB: owned slice of R_B */
+    int64_t y_local_len;
 } spmv_shard_t;
 
 spmv_status_t spmv_shard_plan(const spmv_blocks_t* blocks, int64_t m, int64_t n, int32_t rank, int32_t world,
@@ -209,83 +262,6 @@ spmv_status_t spmv_shard_plan(const spmv_blocks_t* blocks, int64_t m, int64_t n,
 spmv_status_t spmv_maxabs(spmv_handle_t h, double* m_dev, void* stream);
 spmv_status_t spmv_normalize(spmv_handle_t h, const double* y, const double* m_dev,
                              double* x_next, void* stream);
-
-/* Debug hook: copies the device copy of the PERMUTED local CSR back to host
- * (row_ptr as int64[m_local+1] relative to the rank's first nonzero,
- * col as GLOBAL permuted column ids int32[nnz_local], val double[nnz_local]).
- * Synchronous.  Used by tests to check the ingest bit-exactly. */
-spmv_status_t spmv_debug_copy_csr(spmv_handle_t h, int64_t* row_ptr, int32_t* col, double* val);
-
-/* Diagnostics for the measurement harness: roofline
- * microkernels, asynchronous on `stream`, results written to *out_dev only to
- * keep the loads alive.  They bound what the SpMxV kernel can reach:
- *   spmv_diag_read   : 128-bit read stream over `bytes` of device memory (HBM read peak)
- *   spmv_diag_gather : `count` random 8-byte gathers from x[0..n) (x-gather rate)
- *   spmv_diag_csr    : over the handle's device CSR (world 1): mode 0 streams
- *                      col/val only; mode 1 also gathers x[col] (no row sums);
- *                      mode 2 gathers x[col mod 2^20] (8 MB window); mode 3
- *                      gathers independent of col (no load-to-load dependency). */
-spmv_status_t spmv_diag_read(const void* buf, int64_t bytes, int32_t blocks_per_sm, double* out_dev, void* stream);
-spmv_status_t spmv_diag_gather(const double* x, int64_t n, int64_t count, double* out_dev, void* stream);
-spmv_status_t spmv_diag_gather_mode(const double* x, int64_t n, int64_t count, int32_t mode, int32_t blocks_per_sm,
-                                    double* out_dev, void* stream);   /* gather flavours 0..7, see diag.cu */
-spmv_status_t spmv_diag_csr(spmv_handle_t h, const double* x, int32_t mode, double* out_dev, void* stream);
-/* Host-only test hook of the x-staged kernel's planner (plan_xs.cpp): packs a
- * PERMUTED CSR (rows sorted by column, world-1 column ids) with an SB
- * descriptor into panels/groups exactly as spmv_create does, decodes the
- * packed streams again and compares them with the CSR bit for bit (and the
- * format's invariants).  stats[6] = panels, interior groups, border groups,
- * interior padding slots, border padding slots, nonzeros packed.  OK when the
- * round trip is exact; INTERNAL (message in spmv_last_error) when not;
- * UNSUPPORTED when the matrix does not fit the format. */
-spmv_status_t spmv_xs_plan_check(int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
-                                 const spmv_blocks_t* blocks, int64_t rows_target, int64_t* stats);
-
-/* Host-only test hook of the column-sorted panel kernel's planner
- * (plan_panel.cpp): packs a PERMUTED CSR (world-1 column ids) into panels
- * (the row ranges of `blocks`, or the whole matrix when blocks is NULL) of
- * about rows_target rows, decodes the groups again and compares them with the
- * CSR bit for bit, checking that no row repeats within an epoch.
- * stats[8] = panels, groups, padding slots, deferred nonzeros, epochs,
- * nonzeros packed, and 1000 x the mean predicted shared-memory wavefronts of
- * a group's y access with natural / bank-coloured y slots.  OK on an exact
- * round trip; INTERNAL otherwise. */
-spmv_status_t spmv_pn_plan_check(int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
-                                 const spmv_blocks_t* blocks, int64_t rows_target, int64_t* stats);
-
-/* Host-only test hook of the multi-GPU determinism of the panel plan (SURVEY
- * 8(e)): for each rank of `world`, builds that rank's local CSR of a PERMUTED
- * SB matrix (its blocks' rows; columns in the rank's x layout [interior |
- * C_B]), plans its panels exactly as spmv_create does (sms = the SM count the
- * whole-wave rule assumes) and hashes, per block, the panels' row ranges and
- * every group's (global row, virtual-row rank, global column, value bits) in
- * issue order.  out[r * K + k] = rank r's hash of block k, 0 for blocks it
- * does not own.  Equal hashes at world 1 and world G mean equal summation
- * orders, so y is bit-identical across GPU counts.  USAGE / DATA on bad
- * arguments (blocks must be SB). */
-spmv_status_t spmv_pn_shard_hash(int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
-                                 const spmv_blocks_t* blocks, int32_t world, int32_t sms, int64_t* out);
-
-/* Test hook of the multi-GPU path on one GPU.  With SPMV_TEST_RANKS_NO_NCCL
- * set in the environment, spmv_create accepts a dist descriptor whose
- * nccl_unique_id is NULL: the handle is rank `rank` of `world` (its shard,
- * local CSR, x layout and panel plan exactly as on a real multi-GPU run) but
- * has no communicator; its apply skips the border all-gather, and the test
- * supplies the full x(C_B) the all-gather would deliver through this call
- * (`x_border`: device pointer, `len` = |C_B| doubles, copied; the apply still
- * writes the rank's own slice into place first).  USAGE on a handle that is
- * not such a test rank or on a length mismatch. */
-spmv_status_t spmv_test_set_border(spmv_handle_t h, const double* x_border, int64_t len);
-
-/* Design microbenchmarks (diag2.cu): kind 1 L2->SM LDG.128 bandwidth over the
- * L2-resident `buf` (`bytes` long, `count` bytes read in total); kind 2 bulk-copy
- * L2->shared bandwidth, param = cluster size 1/2/4/8 (multicast when > 1),
- * `count` bytes delivered per launch over all CTAs; kind 3 shared-memory
- * y[r] += v*x[c] updates (`buf` unused, `count` updates, param 0 random /
- * 1 conflict-free); kind 4 L2 gathers with `param` lanes per 128-byte line
- * (`buf` = x of `bytes`, `count` gathers).  USAGE on bad arguments. */
-spmv_status_t spmv_diag_micro(int32_t kind, int32_t param, const void* buf, int64_t bytes, int64_t count,
-                              double* out_dev, void* stream);
 
 /* Writes a fresh 128-byte NCCL unique id into out (len >= 128). */
 spmv_status_t spmv_nccl_unique_id(void* out, size_t len);

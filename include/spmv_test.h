@@ -1,0 +1,74 @@
+/*
+ * spmv_test.h -- test and debug hooks of libspmv_b200.so.  NOT part of the
+ * user-facing ABI (include/spmv.h): the parity tests use them to read the
+ * library's internal state back and to run the multi-GPU path on one GPU.
+ * They never change what spmv_create / spmv_apply compute for a handle made
+ * through include/spmv.h.
+ */
+#ifndef SPMV_B200_TEST_H
+#define SPMV_B200_TEST_H
+
+#include "spmv.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Copies the device copy of the PERMUTED local CSR back to host (row_ptr as
+ * int64[m_local+1] relative to the rank's first nonzero, col as GLOBAL
+ * permuted column ids int32[nnz_local], val double[nnz_local]).  Synchronous.
+ * World > 1 DB handles: the local compute rows (block rows, then the
+ * border-row temporaries' segments).  Checks the ingest (a1) bit-exactly. */
+spmv_status_t spmv_debug_copy_csr(spmv_handle_t h, int64_t* row_ptr, int32_t* col, double* val);
+
+/* Host-only round trip of the column-sorted panel kernel's planner
+ * (plan_panel.cpp): packs a PERMUTED CSR (world-1 column ids) into panels
+ * (the row ranges of `blocks`, or the whole matrix when blocks is NULL) of
+ * about rows_target rows, decodes the groups again and compares them with the
+ * CSR bit for bit, checking that no row repeats within an epoch, that groups
+ * never mix interior and border columns, that border groups come last and
+ * that every panel fits shared memory.  stats[10] = panels, groups, padding
+ * slots, deferred nonzeros, epochs, nonzeros packed, 1000 x the mean predicted
+ * shared-memory wavefronts of a group's y access with natural / bank-coloured
+ * y slots, the largest panel's shared memory bytes, panels with border
+ * groups.  OK on an exact round trip; INTERNAL otherwise. */
+spmv_status_t spmv_pn_plan_check(int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
+                                 const spmv_blocks_t* blocks, int64_t rows_target, int64_t* stats);
+
+/* Host-only check of the multi-GPU determinism of the SB panel plan (SURVEY
+ * 8(e)): for each rank of `world`, builds that rank's local CSR of a PERMUTED
+ * SB matrix (its blocks' rows; columns in the rank's x layout [interior |
+ * C_B]), plans its panels exactly as spmv_create does (sms = the SM count the
+ * whole-wave rule assumes) and hashes, per block, the panels' row ranges and
+ * every group's (global row, virtual-row rank, global column, value bits) in
+ * issue order.  out[r * K + k] = rank r's hash of block k, 0 for blocks it
+ * does not own.  Equal hashes at world 1 and world G mean equal summation
+ * orders, so y is bit-identical across GPU counts. */
+spmv_status_t spmv_pn_shard_hash(int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
+                                 const spmv_blocks_t* blocks, int32_t world, int32_t sms, int64_t* out);
+
+/* Rank `rank` of `world` of the multi-GPU path, built on the current device
+ * WITHOUT a communicator (shard, local CSR, x / y layouts, plans exactly as a
+ * real multi-GPU rank), for the loopback fake of SURVEY §4: create all
+ * `world` ranks in one process, then link them with spmv_test_loopback_link.
+ * dist->nccl_unique_id is ignored. */
+spmv_status_t spmv_test_create_rank(int64_t m, int64_t n, int64_t nnz, const int64_t* row_ptr, const int32_t* col_idx,
+                                     const double* val, const int32_t* row_perm, const int32_t* col_perm,
+                                     const spmv_blocks_t* blocks, int32_t n_parts, const int32_t* part_of_nnz,
+                                     const spmv_dist_t* dist, const spmv_options_t* options, spmv_handle_t* out);
+
+/* Links `world` test ranks (handles[r] is rank r) into one loopback group:
+ * every rank's exchange then runs the P2P protocol of the multi-GPU path --
+ * copy-engine pushes of its border slices (and DB temporaries) into the
+ * other ranks' buffers, stream-memory-operation flags, the kernel's device
+ * wait before its first border epoch -- with the peers' buffers on the same
+ * GPU.  Each rank must then be applied on its own stream, ranks in any order
+ * (the same number of applies per rank).  USAGE when a handle is not a test
+ * rank of that world or the ranks disagree; UNSUPPORTED without stream
+ * memory operations. */
+spmv_status_t spmv_test_loopback_link(spmv_handle_t* handles, int32_t world);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPMV_B200_TEST_H */

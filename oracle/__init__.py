@@ -5,7 +5,7 @@ Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
 no code with the CUDA path in ``paper_1203_2739_b200/`` and never imports it.
 
 Every routine is a thin ctypes shim over ``oracle.c`` (plain C, fp64,
-``-O2 -ffp-contract=off``); each C function cites the PAPER.md passage it
+``-O3 -ffp-contract=off``); each C function cites the PAPER.md passage it
 follows (P:Lnn = /root/reference/PAPER.md line nn).  Parity status of each
 function is listed in DESIGN.md "Oracle pins"; none is "parity unpinned".
 """
@@ -25,10 +25,10 @@ TOL = 1e-12   # north_star: |y - y_ref| <= 1e-12 * sum_j |a_ij x_j| per entry
 
 
 def build(force: bool = False) -> str:
-    """Compile oracle.c (gcc -O2 -ffp-contract=off, OpenMP for row-parallel timing)."""
+    """Compile oracle.c (gcc -O3 -ffp-contract=off, OpenMP for row-parallel timing)."""
     if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
         tmp = _SO + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp",
+        subprocess.check_call(["gcc", "-O3", "-ffp-contract=off", "-fno-fast-math", "-fopenmp",
                                "-fPIC", "-shared", "-o", tmp, _SRC, "-lm"])
         os.replace(tmp, _SO)
     return _SO

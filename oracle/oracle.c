@@ -9,7 +9,7 @@
  * code, header, table or helper with the CUDA path (paper_1203_2739_b200/),
  * and neither side includes or imports the other.
  *
- * Build: gcc -O2 -ffp-contract=off (no -ffast-math): every multiply and every
+ * Build: gcc -O3 -ffp-contract=off (no -ffast-math): every multiply and every
  * add rounds separately, in the order written, IEEE round-to-nearest (A21).
  *
  * What it computes:

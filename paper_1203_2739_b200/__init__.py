@@ -7,9 +7,12 @@ kernels, the NCCL border exchange, the power-iteration glue -- runs in the
 library.  There is no CPU or PyTorch fallback: if the library is missing,
 importing the binding's entry points raises.
 
-Names follow the ABI: ``spmv_create``, ``spmv_apply``, ``spmv_split_apply``,
-``spmv_destroy`` plus the helpers ``spmv_get_info``, ``spmv_maxabs``,
-``spmv_normalize``, ``spmv_debug_copy_csr``, ``spmv_nccl_unique_id``.
+Names follow the ABI: ``spmv_create`` (-> ``spmv_create_ex``), ``spmv_apply``,
+``spmv_split_apply``, ``spmv_destroy`` plus the helpers ``spmv_get_info``,
+``spmv_maxabs``, ``spmv_normalize``, ``spmv_shard_plan``,
+``spmv_nccl_unique_id``.  The test hooks of ``include/spmv_test.h`` are in
+``paper_1203_2739_b200.testing``; the measurement microkernels
+(``include/spmv_diag.h``, a separate library) in ``paper_1203_2739_b200.diag``.
 Vectors are CUDA float64 torch tensors (or raw device addresses); the stream
 argument is a ``torch.cuda.Stream``, a raw ``cudaStream_t`` int, or None for
 torch's current stream.
@@ -22,7 +25,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("SPMV_LIB") or os.path.join(_HERE, "libspmv_b200.so")   # SPMV_LIB: A/B builds
+LIB_PATH = os.path.join(_HERE, "libspmv_b200.so")
 
 SPMV_OK, SPMV_ERR_USAGE, SPMV_ERR_DATA, SPMV_ERR_INTERNAL, SPMV_ERR_UNSUPPORTED = range(5)
 SPMV_SB, SPMV_DB = 1, 2
@@ -31,11 +34,16 @@ SPMV_VEC_ORIGINAL = 1
 SPMV_FUSE_MAXABS = 2
 SPMV_SPLIT_LITERAL = 4
 
-EXPORTED = ["spmv_create", "spmv_apply", "spmv_split_apply", "spmv_destroy", "spmv_get_info",
-            "spmv_maxabs", "spmv_normalize", "spmv_debug_copy_csr", "spmv_nccl_unique_id",
-            "spmv_status_string", "spmv_last_error", "spmv_version", "spmv_shard_plan",
-            "spmv_diag_read", "spmv_diag_gather", "spmv_diag_csr", "spmv_diag_gather_mode", "spmv_diag_micro",
-            "spmv_xs_plan_check", "spmv_pn_plan_check", "spmv_pn_shard_hash", "spmv_test_set_border"]
+EXPORTED = ["spmv_create", "spmv_create_ex", "spmv_apply", "spmv_split_apply", "spmv_destroy", "spmv_get_info",
+            "spmv_maxabs", "spmv_normalize", "spmv_nccl_unique_id", "spmv_status_string", "spmv_last_error",
+            "spmv_version", "spmv_shard_plan"]
+# include/spmv_test.h (test and debug hooks, same library)
+EXPORTED_TEST = ["spmv_debug_copy_csr", "spmv_pn_plan_check", "spmv_pn_shard_hash", "spmv_test_create_rank",
+                 "spmv_test_loopback_link"]
+
+KERNELS = {"auto": 0, "panel": 1, "rowtile": 2}
+SPLIT_KERNELS = {"auto": 0, "panel": 1, "rows": 2}
+EXCHANGES = {"auto": 0, "nccl": 1, "p2p": 2}
 
 
 class SpmvError(RuntimeError):
@@ -47,7 +55,13 @@ class SpmvError(RuntimeError):
 class _Blocks(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int32), ("K", ctypes.c_int32),
                 ("row_block_ptr", ctypes.c_void_p), ("col_block_ptr", ctypes.c_void_p),
-                ("border_owner_ptr", ctypes.c_void_p)]
+                ("border_owner_ptr", ctypes.c_void_p), ("row_border_owner_ptr", ctypes.c_void_p)]
+
+
+class _Options(ctypes.Structure):
+    _fields_ = [("struct_size", ctypes.c_int32), ("kernel", ctypes.c_int32), ("panel_rows", ctypes.c_int32),
+                ("split_kernel", ctypes.c_int32), ("exchange", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 11)]
 
 
 class _Dist(ctypes.Structure):
@@ -59,14 +73,15 @@ class spmv_info_t(ctypes.Structure):
     _fields_ = [(k, ctypes.c_int64) for k in (
         "m", "n", "nnz", "m_local", "nnz_local", "row_begin", "x_local_len", "x_interior_begin",
         "x_interior_len", "x_border_begin", "x_border_len", "border_total", "n_tiles", "n_long_rows",
-        "bytes_alg", "bytes_alg_split", "split_segments", "xs_panels", "xs_groups", "xs_pad_slots",
+        "bytes_alg", "bytes_alg_split", "split_segments", "panels", "groups", "pad_slots",
         "bytes_stream")] + [
         (k, ctypes.c_int32) for k in ("n_parts", "rank", "world", "kind", "has_owner_map", "kernel",
-                                      "split_kernel")] + [
-        ("reserved", ctypes.c_int32), ("gather_sectors", ctypes.c_int64)]
+                                      "split_kernel", "exchange")] + [
+        (k, ctypes.c_int64) for k in ("gather_sectors", "y_local_len", "y_border_begin", "y_border_len",
+                                      "deferred", "y_wavefronts_x1000", "exchange_timeouts")]
 
     def as_dict(self) -> dict:
-        return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
+        return {k: getattr(self, k) for k, _ in self._fields_}
 
 
 _lib = None
@@ -82,29 +97,27 @@ def lib():
         L = ctypes.CDLL(LIB_PATH)
         vp, i64, i32, u32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint32
         L.spmv_create.argtypes = [i64, i64, i64, vp, vp, vp, vp, vp, vp, i32, vp, vp, ctypes.POINTER(vp)]
+        L.spmv_create_ex.argtypes = [i64, i64, i64, vp, vp, vp, vp, vp, vp, i32, vp, vp, vp, ctypes.POINTER(vp)]
         L.spmv_apply.argtypes = [vp, vp, i64, vp, i64, u32, vp]
         L.spmv_split_apply.argtypes = [vp, vp, i64, vp, i64, u32, vp]
         L.spmv_destroy.argtypes = [vp]
         L.spmv_get_info.argtypes = [vp, ctypes.POINTER(spmv_info_t)]
         L.spmv_maxabs.argtypes = [vp, vp, vp]
         L.spmv_normalize.argtypes = [vp, vp, vp, vp, vp]
-        L.spmv_debug_copy_csr.argtypes = [vp, vp, vp, vp]
         L.spmv_nccl_unique_id.argtypes = [vp, ctypes.c_size_t]
-        L.spmv_diag_read.argtypes = [vp, i64, i32, vp, vp]
-        L.spmv_diag_gather.argtypes = [vp, i64, i64, vp, vp]
-        L.spmv_diag_csr.argtypes = [vp, vp, i32, vp, vp]
-        L.spmv_diag_gather_mode.argtypes = [vp, i64, i64, i32, i32, vp, vp]
-        L.spmv_diag_micro.argtypes = [i32, i32, vp, i64, i64, vp, vp]
-        L.spmv_xs_plan_check.argtypes = [i64, i64, vp, vp, vp, vp, i64, vp]
-        L.spmv_pn_plan_check.argtypes = [i64, i64, vp, vp, vp, vp, i64, vp]
-        L.spmv_pn_shard_hash.argtypes = [i64, i64, vp, vp, vp, vp, i32, i32, vp]
-        L.spmv_test_set_border.argtypes = [vp, vp, i64]
         L.spmv_shard_plan.argtypes = [vp, i64, i64, i32, i32, vp]
         L.spmv_status_string.argtypes = [i32]
         L.spmv_status_string.restype = ctypes.c_char_p
         L.spmv_last_error.argtypes = []
         L.spmv_last_error.restype = ctypes.c_char_p
         L.spmv_version.restype = i32
+        L.spmv_debug_copy_csr.argtypes = [vp, vp, vp, vp]
+        L.spmv_pn_plan_check.argtypes = [i64, i64, vp, vp, vp, vp, i64, vp]
+        L.spmv_pn_shard_hash.argtypes = [i64, i64, vp, vp, vp, vp, i32, i32, vp]
+        L.spmv_test_create_rank.argtypes = [i64, i64, i64, vp, vp, vp, vp, vp, vp, i32, vp, vp, vp, ctypes.POINTER(vp)]
+        L.spmv_test_loopback_link.argtypes = [vp, i32]
+        for name in EXPORTED_TEST:
+            getattr(L, name).restype = i32
         for name in EXPORTED:
             if name not in ("spmv_status_string", "spmv_last_error", "spmv_version"):
                 getattr(L, name).restype = i32
@@ -179,35 +192,45 @@ def _h(h) -> ctypes.c_void_p:
     return ctypes.c_void_p(p)
 
 
-def spmv_create(m: int, n: int, row_ptr, col_idx, val, row_perm=None, col_perm=None, blocks=None,
-                parts=None, n_parts: int = 0, dist=None) -> Handle:
-    """Ingest an ORIGINAL-space CSR plus old->new permutations (P:L55).
+def _blocks_struct(blocks, keep):
+    if blocks is None:
+        return None
+    rbp = _np(blocks["row_block_ptr"], np.int64)
+    cbp = _np(blocks["col_block_ptr"], np.int64)
+    bop = _np(blocks.get("border_owner_ptr"), np.int64)
+    rop = _np(blocks.get("row_border_owner_ptr"), np.int64)
+    b = _Blocks(int(blocks["kind"]), int(blocks["K"]), rbp.ctypes.data, cbp.ctypes.data,
+                None if bop is None else bop.ctypes.data, None if rop is None else rop.ctypes.data)
+    keep += [rbp, cbp, bop, rop, b]
+    return ctypes.byref(b)
 
-    blocks: dict(kind=1|2, K=.., row_block_ptr=[K+2], col_block_ptr=[K+2],
-    border_owner_ptr=[K+1] or None) in PERMUTED space.  parts: int32 part id
-    per nonzero in input order (split Pi).  dist: dict(rank, world,
-    device, nccl_unique_id=bytes(128)) for one-process-per-GPU runs."""
+
+def _options_struct(options, keep):
+    if not options:
+        return None
+    o = _Options()
+    o.struct_size = ctypes.sizeof(_Options)
+    o.kernel = KERNELS[options.get("kernel", "auto")]
+    o.panel_rows = int(options.get("panel_rows", 0))
+    o.split_kernel = SPLIT_KERNELS[options.get("split_kernel", "auto")]
+    o.exchange = EXCHANGES[options.get("exchange", "auto")]
+    keep.append(o)
+    return ctypes.byref(o)
+
+
+def _create_args(m, n, row_ptr, col_idx, val, row_perm, col_perm, blocks, parts, n_parts, dist, options, keep):
     rp = _np(row_ptr, np.int64)
     ci = _np(col_idx, np.int32)
     va = _np(val, np.float64)
     pr = _np(row_perm, np.int32)
     pc = _np(col_perm, np.int32)
     pa = _np(parts, np.int32)
+    keep += [rp, ci, va, pr, pc, pa]
     nnz = int(rp[-1]) if rp is not None and len(rp) else 0
-    keep = []
-    bptr = None
-    if blocks is not None:
-        rbp = _np(blocks["row_block_ptr"], np.int64)
-        cbp = _np(blocks["col_block_ptr"], np.int64)
-        bop = _np(blocks.get("border_owner_ptr"), np.int64)
-        keep += [rbp, cbp, bop]
-        b = _Blocks(int(blocks["kind"]), int(blocks["K"]), rbp.ctypes.data, cbp.ctypes.data,
-                    None if bop is None else bop.ctypes.data)
-        keep.append(b)
-        bptr = ctypes.byref(b)
+    bptr = _blocks_struct(blocks, keep)
     dptr = None
     if dist is not None:
-        uid_ptr = None   # None: the single-process rank emulation of the tests (SPMV_TEST_RANKS_NO_NCCL)
+        uid_ptr = None
         if dist.get("nccl_unique_id") is not None:
             uid = ctypes.create_string_buffer(bytes(dist["nccl_unique_id"]), 128)
             keep.append(uid)
@@ -215,86 +238,42 @@ def spmv_create(m: int, n: int, row_ptr, col_idx, val, row_perm=None, col_perm=N
         d = _Dist(int(dist["rank"]), int(dist["world"]), int(dist.get("device", 0)), 0, uid_ptr)
         keep.append(d)
         dptr = ctypes.byref(d)
+    return (m, n, nnz, _addr(rp), _addr(ci), _addr(va), _addr(pr), _addr(pc), bptr,
+            int(n_parts if pa is not None else 0), _addr(pa), dptr, _options_struct(options, keep))
+
+
+def spmv_create(m: int, n: int, row_ptr, col_idx, val, row_perm=None, col_perm=None, blocks=None,
+                parts=None, n_parts: int = 0, dist=None, options=None) -> Handle:
+    """Ingest an ORIGINAL-space CSR plus old->new permutations (P:L55).
+
+    blocks: dict(kind=1|2, K=.., row_block_ptr=[K+2], col_block_ptr=[K+2],
+    border_owner_ptr=[K+1] or None, row_border_owner_ptr=[K+1] or None) in
+    PERMUTED space.  parts: int32 part id per nonzero in input order (split Pi,
+    P:L107).  dist: dict(rank, world, device, nccl_unique_id=bytes(128)) for
+    one-process-per-GPU runs.  options: dict(kernel="auto"|"panel"|"rowtile",
+    panel_rows=int, split_kernel="auto"|"panel"|"rows", exchange="auto"|"nccl"|"p2p")
+    (spmv_options_t)."""
+    keep = []
+    args = _create_args(m, n, row_ptr, col_idx, val, row_perm, col_perm, blocks, parts, n_parts, dist, options, keep)
     out = ctypes.c_void_p(0)
-    st = lib().spmv_create(m, n, nnz, _addr(rp), _addr(ci), _addr(va), _addr(pr), _addr(pc), bptr,
-                           int(n_parts if pa is not None else 0), _addr(pa), dptr, ctypes.byref(out))
-    _check(st, "spmv_create")
+    _check(lib().spmv_create_ex(*args, ctypes.byref(out)), "spmv_create")
     return Handle(out.value)
-
-
-def spmv_xs_plan_check(m: int, n: int, row_ptr, col, val, blocks, rows_target: int) -> dict:
-    """Host-only round trip of the x-staged planner (see spmv.h); raises on mismatch."""
-    rp = _np(row_ptr, np.int64)
-    ci = _np(col, np.int32)
-    va = _np(val, np.float64)
-    rbp = _np(blocks["row_block_ptr"], np.int64)
-    cbp = _np(blocks["col_block_ptr"], np.int64)
-    b = _Blocks(int(blocks["kind"]), int(blocks["K"]), rbp.ctypes.data, cbp.ctypes.data, None)
-    stats = np.zeros(6, dtype=np.int64)
-    _check(lib().spmv_xs_plan_check(m, n, _addr(rp), _addr(ci), _addr(va), ctypes.byref(b), rows_target,
-                                    stats.ctypes.data), "spmv_xs_plan_check")
-    return dict(zip(("panels", "groups_i", "groups_b", "pad_i", "pad_b", "entries"), (int(v) for v in stats)))
 
 
 class _Shard(ctypes.Structure):
     _fields_ = [(k, ctypes.c_int64) for k in (
         "block_begin", "block_end", "row_begin", "row_end", "x_interior_begin", "x_interior_len",
-        "x_border_begin", "x_border_len", "x_local_len", "border_begin", "border_total")]
+        "x_border_begin", "x_border_len", "x_local_len", "border_begin", "border_total",
+        "y_border_begin", "y_border_len", "y_local_len")]
 
 
 def spmv_shard_plan(blocks, m: int, n: int, rank: int, world: int) -> dict:
     """Host-side SB shard plan of rank `rank` of `world` (see spmv.h)."""
-    rbp = _np(blocks["row_block_ptr"], np.int64)
-    cbp = _np(blocks["col_block_ptr"], np.int64)
-    bop = _np(blocks.get("border_owner_ptr"), np.int64)
-    b = _Blocks(int(blocks["kind"]), int(blocks["K"]), rbp.ctypes.data, cbp.ctypes.data,
-                None if bop is None else bop.ctypes.data)
-    out = _Shard()
-    _check(lib().spmv_shard_plan(ctypes.byref(b), m, n, rank, world, ctypes.byref(out)), "spmv_shard_plan")
-    return {k: int(getattr(out, k)) for k, _ in _Shard._fields_}
-
-
-def spmv_pn_plan_check(m: int, n: int, row_ptr, col, val, blocks, rows_target: int) -> dict:
-    """Host-only round trip of the column-sorted panel planner (see spmv.h); raises on mismatch."""
-    rp = _np(row_ptr, np.int64)
-    ci = _np(col, np.int32)
-    va = _np(val, np.float64)
     keep = []
-    bptr = None
-    if blocks is not None:
-        rbp = _np(blocks["row_block_ptr"], np.int64)
-        cbp = _np(blocks["col_block_ptr"], np.int64)
-        b = _Blocks(int(blocks["kind"]), int(blocks["K"]), rbp.ctypes.data, cbp.ctypes.data, None)
-        keep += [rbp, cbp, b]
-        bptr = ctypes.byref(b)
-    stats = np.zeros(8, dtype=np.int64)
-    _check(lib().spmv_pn_plan_check(m, n, _addr(rp), _addr(ci), _addr(va), bptr, rows_target, stats.ctypes.data),
-           "spmv_pn_plan_check")
-    d = dict(zip(("panels", "groups", "pads", "deferred", "epochs", "entries"), (int(v) for v in stats[:6])))
-    d["y_wavefronts_natural"] = stats[6] / 1000.0
-    d["y_wavefronts_coloured"] = stats[7] / 1000.0
-    return d
-
-
-def spmv_pn_shard_hash(m: int, n: int, row_ptr, col, val, blocks, world: int, sms: int = 148) -> np.ndarray:
-    """Host-only: per-rank, per-block hashes of the panel plan's summation order (see spmv.h);
-    returns an int64 array [world, K]."""
-    rp = _np(row_ptr, np.int64)
-    ci = _np(col, np.int32)
-    va = _np(val, np.float64)
-    rbp = _np(blocks["row_block_ptr"], np.int64)
-    cbp = _np(blocks["col_block_ptr"], np.int64)
-    b = _Blocks(int(blocks["kind"]), int(blocks["K"]), rbp.ctypes.data, cbp.ctypes.data, None)
-    out = np.zeros((world, int(blocks["K"])), dtype=np.int64)
-    _check(lib().spmv_pn_shard_hash(m, n, _addr(rp), _addr(ci), _addr(va), ctypes.byref(b), world, sms,
-                                    out.ctypes.data), "spmv_pn_shard_hash")
-    return out
-
-
-def spmv_test_set_border(h, x_border):
-    """Test hook (single-process rank emulation): the full x(C_B) the border exchange would gather."""
-    _check(lib().spmv_test_set_border(_h(h), ctypes.c_void_p(_dev(x_border)), int(x_border.numel())),
-           "spmv_test_set_border")
+    b = _blocks_struct(blocks, keep)
+    out = _Shard()
+    _check(lib().spmv_shard_plan(b, m, n, rank, world, ctypes.byref(out)), "spmv_shard_plan")
+    return {k: int(getattr(out, k)) for k, _ in _Shard._fields_}
 
 
 def spmv_apply(h, x, y, flags: int = 0, stream=None, x_len: int | None = None, y_len: int | None = None):
@@ -336,46 +315,10 @@ def spmv_normalize(h, y, m_dev, x_next, stream=None):
            "spmv_normalize")
 
 
-def spmv_debug_copy_csr(h):
-    """The device copy of the permuted local CSR, back on the host."""
-    info = spmv_get_info(h)
-    rp = np.empty(info["m_local"] + 1, np.int64)
-    col = np.empty(info["nnz_local"], np.int32)
-    val = np.empty(info["nnz_local"], np.float64)
-    _check(lib().spmv_debug_copy_csr(_h(h), _addr(rp), _addr(col), _addr(val)), "spmv_debug_copy_csr")
-    return rp, col, val
-
-
 def spmv_nccl_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     _check(lib().spmv_nccl_unique_id(buf, 128), "spmv_nccl_unique_id")
     return buf.raw
-
-
-def spmv_diag_read(buf, nbytes: int, out, blocks_per_sm: int = 4, stream=None):
-    _check(lib().spmv_diag_read(ctypes.c_void_p(buf.data_ptr()), nbytes, blocks_per_sm, ctypes.c_void_p(_dev(out)),
-                                ctypes.c_void_p(_stream(stream))), "spmv_diag_read")
-
-
-def spmv_diag_gather(x, count: int, out, stream=None):
-    _check(lib().spmv_diag_gather(ctypes.c_void_p(_dev(x)), x.numel(), count, ctypes.c_void_p(_dev(out)),
-                                  ctypes.c_void_p(_stream(stream))), "spmv_diag_gather")
-
-
-def spmv_diag_gather_mode(x, count: int, mode: int, out, blocks_per_sm: int = 8, stream=None):
-    _check(lib().spmv_diag_gather_mode(ctypes.c_void_p(_dev(x)), x.numel(), count, mode, blocks_per_sm,
-                                       ctypes.c_void_p(_dev(out)), ctypes.c_void_p(_stream(stream))),
-           "spmv_diag_gather_mode")
-
-
-def spmv_diag_micro(kind: int, param: int, buf, nbytes: int, count: int, out, stream=None):
-    _check(lib().spmv_diag_micro(kind, param, ctypes.c_void_p(_dev(buf) if buf is not None else 0), nbytes, count,
-                                 ctypes.c_void_p(_dev(out)), ctypes.c_void_p(_stream(stream))), "spmv_diag_micro")
-
-
-def spmv_diag_csr(h, x, mode: int, out, stream=None):
-    _check(lib().spmv_diag_csr(_h(h), ctypes.c_void_p(_dev(x)), mode, ctypes.c_void_p(_dev(out)),
-                               ctypes.c_void_p(_stream(stream))), "spmv_diag_csr")
 
 
 def spmv_status_string(s: int) -> str:

@@ -33,18 +33,20 @@ def _nccl_dir() -> str:
 
 SOURCES = {
     "kernels.cu": "cu",
-    "diag.cu": "cu",
-    "diag2.cu": "cu",
-    "pipe.cu": "cu",
     "rowtile.cu": "cu",
     "split.cu": "cu",
-    "xstage.cu": "cu",
     "panel.cu": "cu",
     "plan_panel.cpp": "cpp",
-    "plan_xs.cpp": "cpp",
     "host.cpp": "cpp",
+    "exchange.cpp": "cpp",
+    "test_hooks.cpp": "cpp",
 }
-HEADERS = ["internal.h", "plan_xs.h", "plan_panel.h", os.path.join("..", "..", "include", "spmv.h")]
+HEADERS = ["internal.h", "plan_panel.h", "handle.h", "exchange.h", os.path.join("..", "..", "include", "spmv.h"),
+           os.path.join("..", "..", "include", "spmv_test.h")]
+# measurement microkernels: a separate library (include/spmv_diag.h), not the SpMxV path
+DIAG_DIR = os.path.join(HERE, "diag")
+DIAG_SOURCES = ["diag.cu", "diag2.cu", "api.cu"]
+DIAG_LIB = os.path.join(HERE, "libspmv_diag.so")
 
 
 def _newer(target: str, deps) -> bool:
@@ -57,8 +59,7 @@ def _newer(target: str, deps) -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     nccl = _nccl_dir()
-    defs = os.environ.get("SPMV_BUILD_DEFS", "").split()   # A/B builds only (e.g. -DSPMV_PN_B=8)
-    inc = defs + ["-I" + CSRC, "-I" + os.path.join(ROOT, "include"), "-I" + os.path.join(nccl, "include"),
+    inc = ["-I" + CSRC, "-I" + os.path.join(ROOT, "include"), "-I" + os.path.join(nccl, "include"),
            "-I" + os.path.join(CUDA, "include")]
     hdrs = [os.path.join(CSRC, h) for h in HEADERS]
     objs = []
@@ -96,7 +97,36 @@ def build(force: bool = False, verbose: bool = False) -> str:
             sys.stdout.write(r.stdout + r.stderr)
             raise RuntimeError("link failed")
         os.replace(tmp, LIB)
+    build_diag(force, verbose)
     return LIB
+
+
+def build_diag(force: bool = False, verbose: bool = False) -> str:
+    """libspmv_diag.so: the measurement microkernels bench.py uses for its live peaks."""
+    os.makedirs(BUILD, exist_ok=True)
+    objs = []
+    hdrs = [os.path.join(DIAG_DIR, "diag.h"), os.path.join(ROOT, "include", "spmv_diag.h")]
+    for src in DIAG_SOURCES:
+        s = os.path.join(DIAG_DIR, src)
+        o = os.path.join(BUILD, "diag_" + src + ".o")
+        objs.append(o)
+        if not force and not _newer(o, [s, __file__] + hdrs):
+            continue
+        cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-c", s, "-o", o,
+               "-I" + DIAG_DIR, "-I" + os.path.join(ROOT, "include")]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if verbose or r.returncode:
+            sys.stdout.write(r.stdout + r.stderr)
+        if r.returncode:
+            raise RuntimeError(f"compile failed: diag/{src}")
+    if force or _newer(DIAG_LIB, objs):
+        tmp = DIAG_LIB + f".tmp{os.getpid()}"
+        r = subprocess.run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs], capture_output=True, text=True)
+        if r.returncode:
+            sys.stdout.write(r.stdout + r.stderr)
+            raise RuntimeError("link failed: libspmv_diag.so")
+        os.replace(tmp, DIAG_LIB)
+    return DIAG_LIB
 
 
 if __name__ == "__main__":

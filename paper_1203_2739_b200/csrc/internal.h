@@ -1,5 +1,6 @@
 // internal.h -- shared between the host library (host.cpp) and the kernels
-// (kernels.cu).  Not part of the ABI (include/spmv.h is).
+// (kernels.cu, rowtile.cu, split.cu, panel.cu).  Not part of the ABI
+// (include/spmv.h is).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -17,6 +18,7 @@ constexpr int kTileRows = 512;
 constexpr int kTileShort = 1;      // >= 1: every row has <= kShortRow nonzeros; value = lanes per row
 constexpr int kTileGeneral = 0;
 constexpr int kShortRow = 32;
+constexpr int kMaxDevices = 64;     // per-device caches (SM count, kernel attributes)
 constexpr int kMaxSlots = 1024;      // max-abs accumulator slots (spread atomics)
 constexpr int kSlotStride = 16;    // 16 x 8 B = 128 B apart
 
@@ -41,14 +43,14 @@ struct TileArgs {
     unsigned long long* maxabs_slots;   // nullptr or kMaxSlots*kSlotStride
 };
 
-cudaError_t launch_tiles(const TileArgs& a, bool split, bool xsplit, cudaStream_t s);
-
-// Persistent warp-specialised single-SpMxV kernel (pipe.cu).
-struct PipeArgs {
+// Row-tile single-SpMxV kernel (rowtile.cu): one 256-thread CTA per row tile
+// (the fallback when the panel plan is rejected, and the row-major fused
+// split, split.cu).
+struct RowTileArgs {
     const int32_t* tile_row;   // [T+1]
     const int32_t* tile_nnz;   // [T+1] = row_ptr[tile_row[t]]
-    const int32_t* tile_cls;   // [T] kTileShort / kTileGeneral
-    const int32_t* rowptr;     // [m+1+4]
+    const int32_t* tile_cls;   // [T] kTileShort.. (lanes per row) / kTileGeneral
+    const int32_t* rowptr;     // [m+1+pad]
     const int32_t* col;        // [nnz+pad]
     const double* val;         // [nnz+pad]
     const double* x_lo;
@@ -57,18 +59,8 @@ struct PipeArgs {
     int32_t n_tiles;
     double* y;
     unsigned long long* maxabs_slots;
-    int* tile_counter;         // zeroed by launch_pipe before every launch
-    int32_t gmode;             // x gather flavour (measurements): 0 ld.global.nc, 1 + L2 evict_last,
-                               // 2 + L1 no_allocate and L2 evict_last
-    const int32_t* long_tiles; // tiles holding one row longer than a tile (run by launch_longrows), or
-                               // nullptr: the tile kernel runs them itself
 };
-cudaError_t launch_longrows(const PipeArgs& a, int32_t n_long, bool xsplit, cudaStream_t s);
-cudaError_t launch_pipe(const PipeArgs& a, bool xsplit, cudaStream_t s);
-// Default single-SpMxV kernel (rowtile.cu): one 512-thread CTA per row tile.
-using RowTileArgs = PipeArgs;
-cudaError_t launch_rowtile(const RowTileArgs& a, bool xsplit, int threads, cudaStream_t s, bool lin = false);
-cudaError_t launch_rowseg(const RowTileArgs& a, bool xsplit, cudaStream_t s);
+cudaError_t launch_rowtile(const RowTileArgs& a, bool xsplit, cudaStream_t s);
 // Fused / literal multiple-SpMxV kernel (split.cu), K <= 64 parts.
 constexpr int kMaxParts = 64;
 cudaError_t launch_split(const TileArgs& a, bool xsplit, cudaStream_t s);
@@ -76,60 +68,17 @@ cudaError_t launch_split(const TileArgs& a, bool xsplit, cudaStream_t s);
 // segments in part order, each summed into its own temporary (split.cu).
 cudaError_t launch_split_rows(const RowTileArgs& a, const int32_t* row_seg, const int32_t* seg_ptr, bool xsplit,
                               cudaStream_t s);
-size_t pipe_smem_bytes();
 // x^[c] = x[colinv[c]]   (ORIGINAL-mode x preparation, a3)
 cudaError_t launch_gather(const double* src, const int32_t* idx, double* dst, int64_t n, cudaStream_t s);
+// DB split across GPUs: y[i] = fold of tin[fpos[fptr[i]..fptr[i+1])] in order (f1)
+cudaError_t launch_fold(const double* tin, const int32_t* fptr, const int32_t* fpos, double* y, int64_t n,
+                        unsigned long long* slots, cudaStream_t s);
 // max over slots -> *out
 cudaError_t launch_maxabs_finish(const unsigned long long* slots, double* out, cudaStream_t s);
 // x_next[c] = y[owner[c]] / *m   (power-iteration glue, a9)
 cudaError_t launch_normalize(const double* y, const int32_t* owner, const double* m, double* x_next,
                              int64_t n, cudaStream_t s);
-int kernel_num_sms();
-
-// ---------------------------------------------------------------------------
-// x-staged single-SpMxV (xstage.cu, plan_xs.cpp).  A panel is a
-// run of rows of one SB block; its interior columns C_k are streamed through
-// shared memory in chunks of kXsW columns by the bulk-copy engine, its y rows
-// live in shared memory, and its nonzeros are pre-packed into 32-entry groups
-// (one per lane) with distinct rows and spread shared-memory banks.  Border
-// (C_B) nonzeros are gathered from L2.
-constexpr int kXsWarps = 16;                 // consumer warps; each owns a row range
-constexpr int kXsStages = 3;                 // x chunk ring
-constexpr int kXsW = 2048;                   // columns per chunk (multiple of 16)
-constexpr int kXsStageStride = kXsW + 16;    // doubles per stage buffer
-constexpr int kXsRowsMax = 22528;            // y rows per panel (shared memory)
-constexpr uint32_t kXsDummy = 0xFFFFFFFFu;   // padding slot
-static_assert(kXsW % 16 == 0, "chunk width must keep the bank map shift-invariant");
-
-struct XsPanel {
-    int32_t row0;      // first local row
-    int32_t nrows;     // rows in the panel (<= kXsRowsMax)
-    int32_t col0;      // first interior column (local id); chunk j starts at col0 + j*kXsW
-    int32_t col_end;   // one past the last interior column
-    int32_t nch;       // chunks
-    int32_t u_base;    // offset of this panel's per-warp chunk tables in XsArgs::U
-    int32_t rw;        // rows per warp (warp w owns [w*rw, min((w+1)*rw, nrows)))
-    int32_t pad;
-};
-
-struct XsArgs {
-    const XsPanel* panel;
-    int32_t n_panels;
-    int32_t cbits;            // border index: (row_in_warp << cbits) | border column
-    const int32_t* wg;        // [P*NW+1] interior groups of (panel, warp), contiguous
-    const int32_t* wb;        // [P*NW+1] border groups of (panel, warp)
-    const int32_t* U;         // per (panel, warp): nch entries, U[j] = first group with min chunk >= j
-    const double* gval;       // [groups*32]
-    const uint32_t* gidx;     // [groups*32] (row_in_panel << 16) | offset from its group's first chunk
-    const double* bval;
-    const uint32_t* bidx;
-    const double* x;          // interior columns: x[col]
-    const double* xg;         // border columns: xg[border column]
-    double* y;                // local rows
-    unsigned long long* maxabs_slots;
-};
-cudaError_t launch_xstage(const XsArgs& a, cudaStream_t s);
-size_t xstage_smem_bytes();
+int kernel_num_sms();   // SMs of the current device
 
 // ---------------------------------------------------------------------------
 // Column-sorted panel SpMxV (panel.cu, plan_panel.cpp): the
@@ -141,10 +90,7 @@ size_t xstage_smem_bytes();
 // shared-memory y updates of one epoch never race, and a CTA barrier
 // separates epochs.
 constexpr int kPnWarps = 16;                 // warps per panel CTA
-#ifndef SPMV_PN_B
-#define SPMV_PN_B 4
-#endif
-constexpr int kPnB = SPMV_PN_B;              // groups per warp per epoch
+constexpr int kPnB = 4;                      // groups per warp per epoch (4 beat 8)
 constexpr int kPnEpoch = kPnWarps * kPnB;    // groups per epoch
 constexpr int kPnPadGroups = 4 * kPnEpoch;  // zero groups after the stream (ring read-ahead, <= 16 steps)
 constexpr int kPnRowsMax = 28672;            // y rows per panel (224 KB of shared memory)
@@ -168,16 +114,13 @@ struct PnPanel {
     int32_t sslot0;    // their virtual rows' slots: split_slots[sslot0, sslot0 + sslot_n)
     int32_t sslot_n;
     int32_t split_short; // split rows [0, split_short) have <= kPnFoldSeq virtual rows (folded by one thread)
+    int32_t bepoch;    // first epoch with a border-column (x_split side) group; ne if none.  Interior
+                       // groups come first (the planner's column order), so at world > 1 the border-x
+                       // exchange overlaps epochs [0, bepoch) (a4)
 };
-#ifndef SPMV_PN_FOLDSEQ
-#define SPMV_PN_FOLDSEQ 32
-#endif
-constexpr int kPnFoldSeq = SPMV_PN_FOLDSEQ;   // virtual rows a thread folds sequentially
-#ifndef SPMV_PN_VMAX
-#define SPMV_PN_VMAX 32
-#endif
+constexpr int kPnFoldSeq = 32;               // virtual rows a thread folds sequentially
 constexpr int kPnSplitAt = 32;               // a row with more nonzeros is split into interleaved
-constexpr int kPnVMax = SPMV_PN_VMAX;        // virtual rows of <= kPnVMax nonzeros (own y slots,
+constexpr int kPnVMax = 32;                  // virtual rows of <= kPnVMax nonzeros (own y slots,
                                              // folded in order in the epilogue)
 
 struct PnArgs {
@@ -201,21 +144,27 @@ struct PnArgs {
     const int32_t* split_row;     // [split rows] panel-local row
     int32_t max_sslots;           // largest sslot_n over the panels (shared-memory copy)
     int32_t max_split_n;          // largest split_n over the panels (shared-memory copy of the descriptors)
-    int32_t pf_epochs;        // epochs of the group stream prefetched into L2 ahead (0 = default)
-    int32_t gather_na;        // x gathers L1::no_allocate (plan choice; 0 = allocate)
-    int32_t ring;             // register-ring depth in steps (8, 12 or 16; 0 = default)
-    int32_t persist;          // 1: one CTA per SM walks the panels (measurement switch)
+    int32_t gather_na;        // x gathers L1::no_allocate (plan choice: SB handles; 0 = allocate)
+    // DB across GPUs: rows >= y_split are the border-row temporaries, written to y_hi[row - y_split]
+    // (and left out of the max-abs fold)
+    double* y_hi;
+    int32_t y_split;
+    // world > 1 with the P2P exchange (a4): before its first border epoch a CTA waits until
+    // ready[q] - seq >= 0 (wrap-safe) for every rank q != self; a wait that times out adds 1 to
+    // *err and goes on (no hang).  ready == nullptr: no wait (world 1, or the exchange completed
+    // before the launch)
+    const int32_t* ready;
+    int32_t world, self, seq;
+    int32_t* err;
 };
+// Dynamic shared memory of a panel CTA: its y slots (+ the padding lanes'
+// scratch slot), the split rows' slot lists (u16) and their (first, count,
+// row) descriptors.  The planner caps every panel at kPnSmemMax (ADVICE r1:
+// split rows add bytes beyond the slots) and the launch re-checks it.
+constexpr int64_t kPnSmemMax = 227 * 1024;
+inline int64_t panel_smem_bytes(int64_t slots16, int64_t sslots, int64_t split_n) {
+    return (slots16 + 1) * 8 + ((sslots + 7) & ~int64_t(7)) * 2 + split_n * 12;
+}
 cudaError_t launch_panel(const PnArgs& a, cudaStream_t s);
-
-// roofline microkernels (diag.cu)
-cudaError_t diag_read(const void* buf, int64_t bytes, double* out, int blocks_per_sm, cudaStream_t s);
-cudaError_t diag_gather(const double* x, int64_t n, int64_t count, double* out, cudaStream_t s);
-cudaError_t diag_gather_mode(const double* x, int64_t n, int64_t count, int mode, int blocks_per_sm, double* out,
-                             cudaStream_t s);
-cudaError_t diag_csr(const int32_t* col, const double* val, const double* x, int64_t nnz, int mode, double* out,
-                     cudaStream_t s);
-cudaError_t diag_micro(int kind, int param, const void* buf, int64_t bytes, int64_t count, double* out,
-                       cudaStream_t s);
 
 }  // namespace spmvb

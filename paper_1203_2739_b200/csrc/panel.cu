@@ -22,9 +22,8 @@
 // flight (L1 no-allocate, L2 evict-first: the matrix is read once) and
 // issues the x gathers kGD steps ahead of their use.  The epilogue writes y
 // once per row and folds max |y|.
+#include <atomic>
 #include <cstdint>
-#include <algorithm>
-#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "internal.h"
@@ -60,6 +59,19 @@ __device__ __forceinline__ double ld_x(const double* p, uint64_t pol) {
     asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
     return v;
 }
+// world > 1: the border buffer is written by the exchange while the kernel
+// runs (before the CTA's border epochs), so its reads are coherent weak loads,
+// not the read-only (.nc) path, and never allocate in L1
+__device__ __forceinline__ double ld_x_co(const double* p, uint64_t pol) {
+    double v;
+    asm volatile("ld.global.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ int32_t ld_acquire_sys(const int32_t* p) {
+    int32_t v;
+    asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 // Group stream layout (host.cpp upload_panel_stream): the kPnB = 4 groups a
 // warp runs in one epoch form a 128-entry block, (epoch e, warp w) at
 // g0 * 32 + (e * 16 + w) * 128: values as two (step, lane, step & 1) pairs
@@ -68,18 +80,15 @@ __device__ __forceinline__ double ld_x(const double* p, uint64_t pol) {
 // issues 4 stream loads per epoch (2 value, 1 index, 1 base quad) instead of
 // 9, so fewer L1 requests carry the same bytes.
 //
-// MODE (ablation, measurements only; 0 = the kernel): 1 no x gathers (x = 1),
-// 2 no shared-memory y update (register sum), 3 no epoch barriers (racy),
-// 4 no L2 prefetch of the group stream, 6 gathers of a fixed 2 MB window (no
-// dependence on the loaded indices' values), 24 no next-panel prefetch,
-// 25 x gathers L1::no_allocate
-template <int MODE, int KD_ = kDefD, int KGD_ = 4, bool XS = true, bool PERSIST = false>
+// NA: x gathers L1::no_allocate (SB handles: a panel's gathers rarely revisit
+// a line across groups); XS: x split over two buffers at x_split (world > 1:
+// interior | gathered border).
+template <bool NA, bool XS>
 __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
-    // one panel per CTA, or (PERSIST) one CTA per SM walking panels
-    // blockIdx.x, + gridDim.x, ...
-    for (int p = blockIdx.x; p < A.n_panels; p += gridDim.x) {
-        constexpr int kD = KD_;                              // steps (groups) in flight per warp
-        constexpr int kGD = KGD_;                            // gathers issued this many steps ahead
+    {   // one panel per CTA
+        const int p = blockIdx.x;
+        constexpr int kD = kDefD;                            // steps (groups) in flight per warp
+        constexpr int kGD = 4;                               // gathers issued this many steps ahead
         // the ring is refilled four slots at a time after the last step of a warp's
         // epoch, so kD - 3..kD steps are loaded ahead; a gather needs its step's
         // index loaded: kGD <= kD - 4
@@ -103,7 +112,7 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
 
         const uint64_t pol = pol_evict_first();
         const uint64_t polx = pol_evict_last();   // x is the reused operand
-        const int PF = A.pf_epochs > 0 ? A.pf_epochs : kPF;
+        constexpr int PF = kPF;
         const int T = d.ne * kPnB;                       // steps per warp
 
         double rv[kD];
@@ -130,10 +139,7 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
             ip += kPnWarps * 128;
             bp += kPnWarps;
         };
-        double racc = 0.0;
         auto gather = [&](uint32_t i, int32_t b) -> double {
-            if (MODE == 1) return 1.0;
-            if (MODE == 6) return __ldg(A.x_lo + ((b + (int)(i & 0xFFF)) & 0x3FFFF));
             // unconditional: a padding lane reads x[base] (valid) and adds 0 * x into
             // the scratch y slot -- a predicated-off load behind a branch made the
             // warp wait for the gather at the branch (measured 1.6x slower)
@@ -144,8 +150,29 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
             const uint32_t c = (uint32_t)b + (i & kDeltaMask);
             const double* xa = !XS ? A.x_lo + c
                                    : (int32_t)c < A.x_split ? A.x_lo + c : A.x_hi + (c - (uint32_t)A.x_split);
-            if (MODE == 25) return ld_x_na(xa, polx);
-            return ld_x(xa, polx);
+            return XS ? ld_x_co(xa, polx) : NA ? ld_x_na(xa, polx) : ld_x(xa, polx);
+        };
+        // a4 (world > 1, P2P exchange): the border x(C_B) of this apply may
+        // still be in flight over NVLink while the interior epochs run.  A
+        // gather is issued one epoch ahead of its step, so the CTA waits for
+        // every peer's ready flag at the end of epoch bepoch - 2 (before the
+        // first border gather), thread 0 polling with acquire loads, the rest
+        // at the epoch barrier.  Bounded: a timeout counts in *err, no hang.
+        const bool must_wait = XS && A.ready != nullptr && d.bepoch < d.ne;
+        auto border_wait = [&]() {
+            if (tid == 0) {
+                for (int q = 0; q < A.world; ++q) {
+                    if (q == A.self) continue;
+                    uint32_t it = 0;
+                    while ((int32_t)(ld_acquire_sys(A.ready + q) - A.seq) < 0) {
+                        __nanosleep(128);
+                        if (++it > (1u << 25)) {   // ~ seconds: the peer is gone
+                            atomicAdd(A.err, 1);
+                            break;
+                        }
+                    }
+                }
+            }
         };
         // L2 prefetch of the panel's group stream kPF epochs ahead (one bulk
         // prefetch per array per epoch, issued by thread 0): the register ring
@@ -155,7 +182,7 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
         // p + gridDim.x -- about the panel the block scheduler starts next, on
         // whichever SM frees first -- so a new CTA's ring does not fill from HBM.
         int nx_g0 = 0, nx_ne = 0;
-        if (tid == 0 && MODE != 24 && p + (int)gridDim.x < A.n_panels) {
+        if (tid == 0 && p + (int)gridDim.x < A.n_panels) {
             nx_g0 = A.panel[p + gridDim.x].g0;
             nx_ne = A.panel[p + gridDim.x].ne;
         }
@@ -172,7 +199,7 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
                          : "memory");
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.gbase4 + g), "r"(kPnEpoch * 4) : "memory");
         };
-        if (MODE != 4) {
+        {
             for (int e = 0; e < PF; ++e) prefetch_epoch(e);
             // this panel's slice of the next SB block's x(C_k), kept in L2 (evict_last)
             if (tid == 32 && d.pf_len > 0) {
@@ -189,22 +216,27 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
         }
     #pragma unroll
         for (int u = 0; u < kD; u += 4) load4(u);
+        if (must_wait && d.bepoch == 0) {
+            border_wait();
+            __syncthreads();
+        }
     #pragma unroll
         for (int u = 0; u < kGD; ++u) rx[u] = gather(ri[u], rb[u]);
+        if (must_wait && d.bepoch == 1) {
+            border_wait();
+            __syncthreads();
+        }
 
         auto step = [&](int u) {   // consume ring slot u (compile-time)
             const uint32_t i = ri[u];
-            if (MODE == 2) {
-                racc = fma(rv[u], rx[u % kGD], racc);
-            } else {
-                // padding lanes carry the scratch slot (host upload), value 0
-                const int r = (int)(i >> kPnDeltaBits);
-                ys[r] = fma(rv[u], rx[u % kGD], ys[r]);
-            }
+            // padding lanes carry the scratch slot (host upload), value 0
+            const int r = (int)(i >> kPnDeltaBits);
+            ys[r] = fma(rv[u], rx[u % kGD], ys[r]);
         };
         auto epoch_end = [&](int t) {
-            if (MODE != 3) __syncthreads();
-            if (MODE != 4) prefetch_epoch(t / kPnB + PF);
+            if (must_wait && t / kPnB + 2 == d.bepoch) border_wait();
+            __syncthreads();
+            prefetch_epoch(t / kPnB + PF);
         };
         // whole ring turns without bounds checks: loads and gathers past the
         // panel's end read the next panel's (or the pad's) valid stream
@@ -228,7 +260,6 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
             if (u + kGD < kD) rx[u % kGD] = gather(ri[(u + kGD) % kD], rb[(u + kGD) % kD]);
             if (u % kPnB == kPnB - 1) epoch_end(t0 + u);
         }
-        if (MODE == 2 && racc == 1.2345) ys[0] = racc;
         // epilogue: y[row] = ys[slot(row)].  The slot loads are batched 16 per
         // thread (clamped addresses, no branch) and the first batch is issued
         // before the barrier, so their latency is not paid once per row.
@@ -243,6 +274,9 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
         load_slots(tid);
         __syncthreads();
 
+        // DB across GPUs: a panel of border-row temporaries writes them to y_hi
+        const bool tpanel = d.row0 >= A.y_split;
+        double* const yb = tpanel ? A.y_hi - A.y_split : A.y;
         double mx = 0.0;
         for (int i0 = tid; i0 < nrl; i0 += EB * kT) {
             if (i0 != tid) load_slots(i0);
@@ -251,7 +285,7 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
                 const int i = i0 + k * kT;
                 if (i < nrl && sl[k] < 0x8000) {        // split rows: below
                     const double v = ys[sl[k]];
-                    A.y[d.row0 + i] = v;
+                    yb[d.row0 + i] = v;
                     mx = fmax(mx, fabs(v));
                 }
             }
@@ -264,7 +298,7 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
             const int f = sdesc[3 * k], c = sdesc[3 * k + 1];
             double v = ys[ssl[f]];
             for (int j = 1; j < c; ++j) v += ys[ssl[f + j]];
-            A.y[d.row0 + sdesc[3 * k + 2]] = v;
+            yb[d.row0 + sdesc[3 * k + 2]] = v;
             mx = fmax(mx, fabs(v));
         }
         for (int k = d.split_short + warp; k < d.split_n; k += NW) {
@@ -274,19 +308,17 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
     #pragma unroll
             for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
             if (lane == 0) {
-                A.y[d.row0 + sdesc[3 * k + 2]] = v;
+                yb[d.row0 + sdesc[3 * k + 2]] = v;
                 mx = fmax(mx, fabs(v));
             }
         }
-        if (A.maxabs_slots) {
+        if (A.maxabs_slots && !tpanel) {
     #pragma unroll
             for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
             if (lane == 0 && mx > 0.0)
                 atomicMax(A.maxabs_slots + ((p * NW + warp) & (kMaxSlots - 1)) * kSlotStride,
                           (unsigned long long)__double_as_longlong(mx));
         }
-        if (!PERSIST) break;
-        __syncthreads();   // the epilogue's reads of ys before the next panel zeroes it
     }
 }
 
@@ -294,130 +326,32 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
 
 cudaError_t launch_panel(const PnArgs& a, cudaStream_t s) {
     if (a.n_panels <= 0) return cudaSuccess;
-    static int mode = -1;
-    // only the panel's y in shared memory: the rest of the 256 KB L1/shared
-    // array stays L1, which holds the global loads in flight
-    const size_t smem = (size_t)(a.max_rows + 1) * sizeof(double)     // + the padding lanes' scratch slot
-                        + (size_t)((a.max_sslots + 7) & ~7) * 2           // split rows' slot lists
-                        + (size_t)a.max_split_n * 12;                     // and their (first, count, row)
-    if (mode < 0) {
-        const char* e = getenv("SPMV_PN_MODE");   // ablations for measurements only
-        mode = e ? atoi(e) : 0;
-        const int smax = 227 * 1024;
-        cudaError_t r = cudaSuccess;
-        auto attr = [&](const void* k) {
-            if (r == cudaSuccess) r = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
-        };
-        attr((const void*)spmv_panel_kernel<0>);
-        attr((const void*)spmv_panel_kernel<1>);
-        attr((const void*)spmv_panel_kernel<2>);
-        attr((const void*)spmv_panel_kernel<3>);
-        attr((const void*)spmv_panel_kernel<4>);
-        attr((const void*)spmv_panel_kernel<6>);
-        attr((const void*)spmv_panel_kernel<24>);
-        attr((const void*)spmv_panel_kernel<25>);
-        attr((const void*)spmv_panel_kernel<0, 12, 4, false>);
-        attr((const void*)spmv_panel_kernel<25, 12, 4, false>);
-        attr((const void*)spmv_panel_kernel<25, 12, 4, true>);
-        attr((const void*)spmv_panel_kernel<0, 12, 4, true>);
-        attr((const void*)spmv_panel_kernel<0, 8, 4, false>);
-        attr((const void*)spmv_panel_kernel<0, 16, 4, false>);
-        attr((const void*)spmv_panel_kernel<25, 8, 4, false>);
-        attr((const void*)spmv_panel_kernel<25, 16, 4, false>);
-        attr((const void*)spmv_panel_kernel<25, 8, 4, true>);
-        attr((const void*)spmv_panel_kernel<25, 16, 4, true>);
-        attr((const void*)spmv_panel_kernel<0, 8, 4, true>);
-        attr((const void*)spmv_panel_kernel<0, 16, 4, true>);
-        attr((const void*)spmv_panel_kernel<0, 12, 8, false>);
-        attr((const void*)spmv_panel_kernel<0, 16, 8, false>);
-        attr((const void*)spmv_panel_kernel<25, 12, 8, false>);
-        attr((const void*)spmv_panel_kernel<25, 16, 8, false>);
-        attr((const void*)spmv_panel_kernel<0, 12, 8, true>);
-        attr((const void*)spmv_panel_kernel<0, 16, 8, true>);
-        attr((const void*)spmv_panel_kernel<25, 12, 8, true>);
-        attr((const void*)spmv_panel_kernel<25, 16, 8, true>);
-        attr((const void*)spmv_panel_kernel<0, 8, 2, false>);
-        attr((const void*)spmv_panel_kernel<0, 8, 3, false>);
-        attr((const void*)spmv_panel_kernel<25, 8, 2, false>);
-        attr((const void*)spmv_panel_kernel<25, 8, 3, false>);
-        attr((const void*)spmv_panel_kernel<0, 8, 2, true>);
-        attr((const void*)spmv_panel_kernel<0, 8, 3, true>);
-        attr((const void*)spmv_panel_kernel<25, 8, 2, true>);
-        attr((const void*)spmv_panel_kernel<25, 8, 3, true>);
-        attr((const void*)spmv_panel_kernel<0, 8, 4, true, true>);
-        attr((const void*)spmv_panel_kernel<0, 8, 4, false, true>);
-        attr((const void*)spmv_panel_kernel<25, 8, 4, true, true>);
-        attr((const void*)spmv_panel_kernel<25, 8, 4, false, true>);
-        attr((const void*)spmv_panel_kernel<0, 8, 4>);
-        attr((const void*)spmv_panel_kernel<0, 16, 4>);
-        attr((const void*)spmv_panel_kernel<0, 16, 8>);
-        if (r != cudaSuccess) return r;
+    // only the panel's y (and split-row fold lists) in shared memory: the rest
+    // of the 256 KB L1/shared array stays L1, which holds the loads in flight
+    const int64_t smem = panel_smem_bytes(a.max_rows, a.max_sslots, a.max_split_n);
+    if (smem > kPnSmemMax) return cudaErrorInvalidValue;   // the planner never builds such a panel
+    // the opt-in shared-memory limit is a per-device function attribute: set
+    // it once per device (a process may hold handles on several GPUs)
+    static std::atomic<int> ready[kMaxDevices];
+    int dev = 0;
+    cudaError_t r = cudaGetDevice(&dev);
+    if (r != cudaSuccess) return r;
+    const int di = dev < kMaxDevices ? dev : kMaxDevices - 1;
+    if (!ready[di].load(std::memory_order_acquire) || dev >= kMaxDevices) {
+        const int smax = (int)kPnSmemMax;
+        for (const void* k : {(const void*)spmv_panel_kernel<false, false>, (const void*)spmv_panel_kernel<false, true>,
+                              (const void*)spmv_panel_kernel<true, false>, (const void*)spmv_panel_kernel<true, true>})
+            if ((r = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smax)) != cudaSuccess)
+                return r;
+        ready[di].store(1, std::memory_order_release);
     }
-    PnArgs b = a;
-    switch (mode) {
-    case 1: spmv_panel_kernel<1><<<b.n_panels, kT, smem, s>>>(b); break;
-    case 2: spmv_panel_kernel<2><<<b.n_panels, kT, smem, s>>>(b); break;
-    case 3: spmv_panel_kernel<3><<<b.n_panels, kT, smem, s>>>(b); break;
-    case 4: spmv_panel_kernel<4><<<b.n_panels, kT, smem, s>>>(b); break;
-    case 6: spmv_panel_kernel<6><<<b.n_panels, kT, smem, s>>>(b); break;
-    case 24: spmv_panel_kernel<24><<<b.n_panels, kT, smem, s>>>(b); break;
-    case 25: spmv_panel_kernel<25><<<b.n_panels, kT, smem, s>>>(b); break;
-    case 22: spmv_panel_kernel<0, 8, 4><<<b.n_panels, kT, smem, s>>>(b); break;     // ring depth variants
-    case 18: spmv_panel_kernel<0, 16, 4><<<b.n_panels, kT, smem, s>>>(b); break;
-    case 21: spmv_panel_kernel<0, 16, 8><<<b.n_panels, kT, smem, s>>>(b); break;
-    default: {
-        const bool xs = b.x_split != INT32_MAX;
-        if (b.persist && b.gather_na == 0 && (b.ring == 0 || b.ring == 8)) {   // measurement switch
-            static int nsm = 0;
-            if (!nsm) {
-                int dev = 0;
-                cudaGetDevice(&dev);
-                cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-            }
-            const int grid = std::min(b.n_panels, nsm);
-            if (xs) spmv_panel_kernel<0, 8, 4, true, true><<<grid, kT, smem, s>>>(b);
-            else spmv_panel_kernel<0, 8, 4, false, true><<<grid, kT, smem, s>>>(b);
-            return cudaGetLastError();
-        }
-        if (b.persist && b.gather_na && (b.ring == 0 || b.ring == 8)) {
-            static int nsm2 = 0;
-            if (!nsm2) {
-                int dev = 0;
-                cudaGetDevice(&dev);
-                cudaDeviceGetAttribute(&nsm2, cudaDevAttrMultiProcessorCount, dev);
-            }
-            const int grid = std::min(b.n_panels, nsm2);
-            if (xs) spmv_panel_kernel<25, 8, 4, true, true><<<grid, kT, smem, s>>>(b);
-            else spmv_panel_kernel<25, 8, 4, false, true><<<grid, kT, smem, s>>>(b);
-            return cudaGetLastError();
-        }
-        // ring: steps in flight 8 / 12 / 16 with gathers 4 steps ahead; 1208 /
-        // 1608: 12 / 16 with gathers 8 ahead; 802 / 803: 8 with gathers 2 / 3
-        // ahead (measurements)
-        const int rd = b.ring == 8 || b.ring == 12 || b.ring == 16 || b.ring == 1208 || b.ring == 1608 ||
-                       b.ring == 802 || b.ring == 803 ? b.ring : kDefD;
-#define SPMV_PN_LAUNCH(M, D, G)                                                           \
-    (xs ? (spmv_panel_kernel<M, D, G, true><<<b.n_panels, kT, smem, s>>>(b), 0)          \
-        : (spmv_panel_kernel<M, D, G, false><<<b.n_panels, kT, smem, s>>>(b), 0))
-        if (b.gather_na) {
-            if (rd == 12) SPMV_PN_LAUNCH(25, 12, 4);
-            else if (rd == 16) SPMV_PN_LAUNCH(25, 16, 4);
-            else if (rd == 1208) SPMV_PN_LAUNCH(25, 12, 8);
-            else if (rd == 1608) SPMV_PN_LAUNCH(25, 16, 8);
-            else if (rd == 802) SPMV_PN_LAUNCH(25, 8, 2);
-            else if (rd == 803) SPMV_PN_LAUNCH(25, 8, 3);
-            else SPMV_PN_LAUNCH(25, 8, 4);
-        } else {
-            if (rd == 12) SPMV_PN_LAUNCH(0, 12, 4);
-            else if (rd == 16) SPMV_PN_LAUNCH(0, 16, 4);
-            else if (rd == 1208) SPMV_PN_LAUNCH(0, 12, 8);
-            else if (rd == 1608) SPMV_PN_LAUNCH(0, 16, 8);
-            else if (rd == 802) SPMV_PN_LAUNCH(0, 8, 2);
-            else if (rd == 803) SPMV_PN_LAUNCH(0, 8, 3);
-            else SPMV_PN_LAUNCH(0, 8, 4);
-        }
-#undef SPMV_PN_LAUNCH
-    }
+    const bool xs = a.x_split != INT32_MAX;
+    if (a.gather_na) {
+        if (xs) spmv_panel_kernel<true, true><<<a.n_panels, kT, smem, s>>>(a);
+        else spmv_panel_kernel<true, false><<<a.n_panels, kT, smem, s>>>(a);
+    } else {
+        if (xs) spmv_panel_kernel<false, true><<<a.n_panels, kT, smem, s>>>(a);
+        else spmv_panel_kernel<false, false><<<a.n_panels, kT, smem, s>>>(a);
     }
     return cudaGetLastError();
 }

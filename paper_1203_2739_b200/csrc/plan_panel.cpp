@@ -121,8 +121,7 @@ void colour_slots(int32_t nr, const std::vector<Ent>& ents, int64_t G, std::vect
             cnt[g * 16 + b2]++;
         }
     };
-    static const int kSweeps = getenv("SPMV_PN_SWEEPS") ? atoi(getenv("SPMV_PN_SWEEPS")) : 2;
-    static const int kTries = getenv("SPMV_PN_TRIES") ? atoi(getenv("SPMV_PN_TRIES")) : 3;
+    constexpr int kSweeps = 2, kTries = 3;
     for (int sw = 0; sw < kSweeps; ++sw)
         for (int32_t i = 0; i < nr; ++i) {
             const int32_t r = (int32_t)((i * 40503ull + sw * 7919ull) % (uint64_t)nr);   // fixed visiting order
@@ -259,8 +258,15 @@ void build_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col
             const int32_t vr = vbase[r] + evr[i];
             ents[i] = {vr, col[e], val[e]};
             // rotated sweep: panels of one block start at different columns, so
-            // concurrently running CTAs do not all hit the same x lines (L2 slices)
-            keys[i] = ((uint64_t)((uint32_t)col[e] - (uint32_t)P.rot) << 32) | (uint64_t)i;
+            // concurrently running CTAs do not all hit the same x lines (L2
+            // slices); columns >= x_split (the border C_B, Eq.(1)) come after
+            // every interior column, so a panel's border groups form its last
+            // epochs -- at world > 1 the border-x exchange then overlaps the
+            // interior groups (a4)
+            const int64_t c = col[e];
+            const uint64_t rel = c >= x_split ? (uint64_t(1) << 31) | (uint64_t)(c - x_split)
+                                              : (uint64_t)(c >= P.rot ? c - P.rot : c - P.rot + x_split);
+            keys[i] = (rel << 32) | (uint64_t)i;
         }
     std::sort(keys.begin(), keys.end());
     P.entries = n;
@@ -316,12 +322,6 @@ void build_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col
             em.close();
             ++ng;
         }
-        if (getenv("SPMV_PN_DEBUG") && P.desc.row0 == 0) {
-            int64_t filled = 0;
-            for (int64_t q = (int64_t)gents.size() - 32 * ng; q < (int64_t)gents.size(); ++q) filled += gents[q].row >= 0;
-            fprintf(stderr, "epoch %d: groups %d entries %lld deferred-queue %zu pos %lld/%lld\n", epoch, ng,
-                    (long long)filled, deferred.size(), (long long)pos, (long long)n);
-        }
         while (ng < kPnEpoch) {   // all-dummy groups complete the epoch
             em.close();
             ++ng;
@@ -345,13 +345,7 @@ void build_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col
         P.ywf0 = G ? w / G : 0;
     }
     std::vector<uint16_t> v2s;
-    if (getenv("SPMV_PN_NOCOLOUR")) {
-        v2s.resize(nr);
-        for (int32_t r = 0; r < (int32_t)nr; ++r) v2s[r] = (uint16_t)r;
-        slot = ident;
-    } else {
-        colour_slots((int32_t)nr, gents, G, v2s, slot);
-    }
+    colour_slots((int32_t)nr, gents, G, v2s, slot);
     // real rows -> slot, or -> split entry (virtual rows' slots in fold order)
     // split rows with <= kPnFoldSeq virtual rows first (the epilogue folds
     // those one thread per row, sequentially), then the longer ones (a warp each)
@@ -388,6 +382,14 @@ void build_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col
         P.gsectors += ns;
     }
     P.ywf1 = G ? w / G : 0;
+    // first epoch holding a border (x_split side) group: at world > 1 the
+    // kernel waits for the border-x exchange before it (a4)
+    P.desc.bepoch = epoch;
+    for (int64_t g = 0; g < G; ++g)
+        if ((int64_t)gbases[g] >= x_split) {
+            P.desc.bepoch = (int32_t)(g / kPnEpoch);
+            break;
+        }
     P.gbase4.resize(P.gbase.size());
     for (int32_t e = 0; e < epoch; ++e)
         for (int w = 0; w < kPnWarps; ++w)
@@ -438,22 +440,31 @@ bool plan_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col,
         const int64_t np0 = std::max<int64_t>(np_of[k], 1);
         const int64_t Rk = (S + np0 - 1) / np0;   // this range's slots per panel
         const int64_t cap = std::min<int64_t>(Rk + Rk / 4, kPnRowsMax);
+        // shared memory of a panel (panel_smem_bytes): 8 B per y slot, plus 2 B
+        // per slot and 12 B per row for rows split into virtual rows (the
+        // epilogue's fold lists); a panel never exceeds kPnSmemMax, whatever
+        // the cut mode (rows of 33-64 nonzeros need ~16 B per slot)
+        auto smem_of = [](int64_t s) -> int64_t { return 8 * s + (s > 1 ? 2 * s + 12 : 0); };
+        const int64_t smem_cap = kPnSmemMax - 8 * 16 - 8 - 16;   // slack for the rounding of slots / lists
         auto make_cuts = [&](bool by_bytes) {
             std::vector<int64_t> cut(1, rg.first);
             const int64_t tot = by_bytes ? C : S;
-            int64_t acc = 0, ps = 0, pi = 1;
+            int64_t acc = 0, ps = 0, pb = 0, pi = 1;
             for (int64_t r = rg.first; r < rg.second; ++r) {
                 const int64_t s = slots_of(r);
-                if (by_bytes && ps > 0 && ps + s > cap) {   // slot cap: cut before r
+                if (ps > 0 && ((by_bytes && ps + s > cap) || pb + smem_of(s) > smem_cap)) {   // caps: cut before r
                     cut.push_back(r);
                     ps = 0;
+                    pb = 0;
                     while (pi < np0 && acc >= tot * pi / np0) ++pi;
                 }
                 acc += by_bytes ? 12 * (rp[r + 1] - rp[r]) + 10 * s : s;
                 ps += s;
+                pb += smem_of(s);
                 if (pi < np0 && acc >= tot * pi / np0 && r + 1 < rg.second) {
                     cut.push_back(r + 1);
                     ps = 0;
+                    pb = 0;
                     while (pi < np0 && acc >= tot * pi / np0) ++pi;
                 }
             }
@@ -486,7 +497,7 @@ bool plan_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col,
             PnPanelData d;
             d.desc.row0 = (int32_t)a;
             d.desc.nrows = (int32_t)(e - a);
-            if (xcols && k < xcols->size() && getenv("SPMV_PN_NOROT") == nullptr) {
+            if (xcols && k < xcols->size()) {
                 const int64_t c0 = (*xcols)[k].first, c1 = (*xcols)[k].second;
                 d.rot = (int32_t)(c0 + (c1 - c0) * p / np);
             }

@@ -37,9 +37,6 @@
 namespace spmvb {
 namespace {
 
-constexpr int kRT = 512;                 // threads per tile CTA (one quad each)
-static_assert(kRT * 4 == kTileNnz, "one quad per thread");
-
 __device__ __forceinline__ uint64_t pol_evict_first() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -60,28 +57,6 @@ __device__ __forceinline__ double2 ld_v2d(const double* ptr, uint64_t pol) {
     return r;
 }
 
-__device__ __forceinline__ double gx(const double* p, int gmode, uint64_t pl) {
-    double v;
-    if (gmode == 1) {
-        asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pl));
-    } else if (gmode == 2) {
-        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pl));
-    } else {
-        v = __ldg(p);
-    }
-    return v;
-}
-
-template <bool XSPLIT>
-__device__ __forceinline__ double ldx(const RowTileArgs& A, int c) {
-    uint64_t pl = 0;
-    if (A.gmode) asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pl));
-    if (XSPLIT) return c < A.x_split ? gx(A.x_lo + c, A.gmode, pl) : gx(A.x_hi + (c - A.x_split), A.gmode, pl);
-    return gx(A.x_lo + c, A.gmode, pl);
-}
-
-
-
 // fixed gather flavour of the default path (no run-time switch, no branch):
 // L1 no-allocate (a gathered line is not reused inside a tile) and L2
 // evict-last (x is the reused operand)
@@ -96,8 +71,9 @@ __device__ __forceinline__ double ldx2(const RowTileArgs& A, int c) {
     return v;
 }
 
-template <int NT>
-struct RTSmemT {
+constexpr int NT = 256;                  // threads per tile CTA
+constexpr int kNT = NT;
+struct RTSmem {
     double prod[kTileNnz];          // product of position p (nonzero a4 + p)
     int32_t so[kTileRows + 1];      // row_ptr[r0 + j] - a4
     int32_t longrows[kTileRows];    // general tiles: rows with > 32 nonzeros
@@ -105,26 +81,11 @@ struct RTSmemT {
     double red[NT / 32];
 };
 
-__device__ __forceinline__ int32_t ld_s32(const int32_t* ptr, uint64_t pol) {
-    int32_t r;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(r) : "l"(ptr), "l"(pol));
-    return r;
-}
-__device__ __forceinline__ double ld_f64(const double* ptr, uint64_t pol) {
-    double r;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(ptr), "l"(pol));
-    return r;
-}
-
 // NT threads per tile CTA; each thread streams QPT = 512/NT quads.
-// LIN: lane-consecutive positions instead of quads (thread t takes positions
-// t, t+NT, ...): the same coalesced stream, but the 32 gathers of one warp
-// instruction are for 32 consecutive nonzeros, so sorted columns of a long
-// row share 128-byte lines (C4's banded rows).
-template <bool XSPLIT, int NT, bool LIN>
-__global__ void __launch_bounds__(NT, (NT == 512 ? 3 : NT == 256 ? 6 : 8)) spmv_rowtile_kernel(const RowTileArgs A) {
+template <bool XSPLIT>
+__global__ void __launch_bounds__(NT, 6) spmv_rowtile_kernel(const RowTileArgs A) {
     constexpr int QPT = 512 / NT;
-    __shared__ __align__(16) RTSmemT<NT> sm;
+    __shared__ __align__(16) RTSmem sm;
     const int t = blockIdx.x;
     const int tid = threadIdx.x;
     const int r0 = A.tile_row[t], r1 = A.tile_row[t + 1];
@@ -137,27 +98,9 @@ __global__ void __launch_bounds__(NT, (NT == 512 ? 3 : NT == 256 ? 6 : 8)) spmv_
 
     if (b - a + 3 > kTileNnz) {   // long row: planned as one (host plan_tiles, alignment-free test)
         // ------------------------------------------- one long row (> a tile)
-        if (A.long_tiles) return;                   // done by spmv_longrow_kernel
         const int64_t qa = a >> 2, qb = ((int64_t)b + 3) >> 2;
         double acc = 0.0;
-        if (LIN) {
-            for (int64_t e = a + tid; e < b; e += 4 * NT) {
-                double v[4], xv[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int64_t f = e + u * NT;
-                    v[u] = 0.0;
-                    if (f < b) {
-                        v[u] = ld_f64(A.val + f, pol);
-                        xv[u] = ldx<XSPLIT>(A, ld_s32(A.col + f, pol));
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    if (e + u * NT < b) acc += v[u] * xv[u];
-            }
-        }
-        for (int64_t q = qa + tid; !LIN && q < qb; q += NT) {
+        for (int64_t q = qa + tid; q < qb; q += NT) {
             // all four gathers unconditional (the quad's columns are valid), products masked
             const int4 c = ld_v4(A.col + 4 * q, pol);
             const double2 v0 = ld_v2d(A.val + 4 * q, pol);
@@ -188,31 +131,7 @@ __global__ void __launch_bounds__(NT, (NT == 512 ? 3 : NT == 256 ? 6 : 8)) spmv_
     // ------------------------------------------------ stage products, so[]
     for (int j = tid; j <= nr; j += NT) sm.so[j] = A.rowptr[r0 + j] - a4;
     if (tid == 0) sm.nlong = 0;
-    if (LIN) {
-        const int lo = a - a4, hi = b - a4;
-        constexpr int PPT = kTileNnz / NT;   // positions per thread
-        int32_t c[PPT];
-        double v[PPT];
-#pragma unroll
-        for (int k = 0; k < PPT; ++k) {
-            const int p = tid + k * NT;
-            if (p >= lo && p < hi) {
-                c[k] = ld_s32(A.col + a4 + p, pol);
-                v[k] = ld_f64(A.val + a4 + p, pol);
-            }
-        }
-        double xv[PPT];
-#pragma unroll
-        for (int k = 0; k < PPT; ++k) {
-            const int p = tid + k * NT;
-            if (p >= lo && p < hi) xv[k] = ldx<XSPLIT>(A, c[k]);
-        }
-#pragma unroll
-        for (int k = 0; k < PPT; ++k) {
-            const int p = tid + k * NT;
-            if (p >= lo && p < hi) sm.prod[p] = v[k] * xv[k];
-        }
-    } else {
+    {
         // Branch-free staging: every thread loads its QPT quads and gathers all
         // 4 x values unconditionally -- quads past the tile end are clamped to
         // the tile's first quad (a valid address), positions outside
@@ -311,273 +230,12 @@ __global__ void __launch_bounds__(NT, (NT == 512 ? 3 : NT == 256 ? 6 : 8)) spmv_
     }
 }
 
-// ---------------------------------------------------------------------------
-// spmv_rowseg_kernel: same tile geometry and streaming as above, but the
-// products never touch shared memory (the L1TEX pipe is shared by the x
-// gathers and shared-memory wavefronts; ncu: 69 % busy on C5 with staging).
-// Thread q keeps the products of positions 4q..4q+3 in registers and walks
-// them against the tile's row offsets: rows that start and end inside its
-// quad are stored at once; a row running across threads is completed with a
-// segmented inclusive scan over the threads (warp shuffles, then one carry
-// per warp through shared memory), in a fixed order -- deterministic.
-// ---------------------------------------------------------------------------
-struct SegSmem {
-    int32_t so[kTileRows + 1];
-    double wv[kRT / 32];            // per warp: scan value at lane 31
-    int32_t wf[kRT / 32];           // per warp: a chain reset happened in the warp
-    int32_t wh[kRT / 32];           // per warp: lane 31 carries a row into the next warp
-    double red[kRT / 32];
-};
-
-template <bool XSPLIT>
-__global__ void __launch_bounds__(kRT, 3) spmv_rowseg_kernel(const RowTileArgs A) {
-    __shared__ __align__(16) SegSmem sm;
-    const int t = blockIdx.x;
-    const int tid = threadIdx.x;
-    const int lane = tid & 31, warp = tid >> 5;
-    const int r0 = A.tile_row[t], r1 = A.tile_row[t + 1];
-    const int a = A.tile_nnz[t], b = A.tile_nnz[t + 1];
-    const int nr = r1 - r0;
-    const int a4 = a & ~3;
-    const uint64_t pol = pol_evict_first();
-    double mx = 0.0;
-
-    if (b - a + 3 > kTileNnz) {   // long row: planned as one (host plan_tiles, alignment-free test)
-        // ------------------------------------------- one long row (> a tile)
-        const int64_t qa = a >> 2, qb = ((int64_t)b + 3) >> 2;
-        double acc = 0.0;
-        for (int64_t q = qa + tid; q < qb; q += kRT) {
-            const int4 c = ld_v4(A.col + 4 * q, pol);
-            const double2 v0 = ld_v2d(A.val + 4 * q, pol);
-            const double2 v1 = ld_v2d(A.val + 4 * q + 2, pol);
-            const int64_t g = 4 * q;
-            if (g + 0 >= a && g + 0 < b) acc += v0.x * ldx<XSPLIT>(A, c.x);
-            if (g + 1 >= a && g + 1 < b) acc += v0.y * ldx<XSPLIT>(A, c.y);
-            if (g + 2 >= a && g + 2 < b) acc += v1.x * ldx<XSPLIT>(A, c.z);
-            if (g + 3 >= a && g + 3 < b) acc += v1.y * ldx<XSPLIT>(A, c.w);
-        }
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-        if (lane == 0) sm.red[warp] = acc;
-        __syncthreads();
-        if (tid == 0) {
-            double tot = 0.0;
-            for (int w = 0; w < kRT / 32; ++w) tot += sm.red[w];
-            A.y[r0] = tot;
-            if (A.maxabs_slots && tot != 0.0)
-                atomicMax(A.maxabs_slots + (t & (kMaxSlots - 1)) * kSlotStride,
-                          (unsigned long long)__double_as_longlong(fabs(tot)));
-        }
-        return;
-    }
-
-    // -------------------------------------------- stream, gather, products
-    for (int j = tid; j <= nr; j += kRT) sm.so[j] = A.rowptr[r0 + j] - a4;
-    const int pq = 4 * tid;
-    const int lo = a - a4, hi = b - a4;
-    const int e_lo = max(pq, lo), e_hi = min(pq + 4, hi);
-    const bool act = e_lo < e_hi;
-    double pv[4] = {0.0, 0.0, 0.0, 0.0};
-    if (a4 + pq < b) {
-        const int4 c = ld_v4(A.col + a4 + pq, pol);
-        const double2 v0 = ld_v2d(A.val + a4 + pq, pol);
-        const double2 v1 = ld_v2d(A.val + a4 + pq + 2, pol);
-        const double x0 = (pq + 0 >= lo && pq + 0 < hi) ? ldx<XSPLIT>(A, c.x) : 0.0;
-        const double x1 = (pq + 1 >= lo && pq + 1 < hi) ? ldx<XSPLIT>(A, c.y) : 0.0;
-        const double x2 = (pq + 2 >= lo && pq + 2 < hi) ? ldx<XSPLIT>(A, c.z) : 0.0;
-        const double x3 = (pq + 3 >= lo && pq + 3 < hi) ? ldx<XSPLIT>(A, c.w) : 0.0;
-        pv[0] = v0.x * x0; pv[1] = v0.y * x1; pv[2] = v1.x * x2; pv[3] = v1.y * x3;
-    }
-    __syncthreads();                                     // so[] staged
-
-    for (int r = tid; r < nr; r += kRT)                  // empty rows: y = +0 (A5)
-        if (sm.so[r] == sm.so[r + 1]) A.y[r0 + r] = 0.0;
-
-    // ------------------------------------------------ walk the quad
-    double v = 0.0;          // scan input: chain value leaving this thread
-    bool f = true;           // chain reset at this thread
-    bool carry = false;      // this thread's last row continues in the next thread
-    int head_row = -1;
-    double head_sum = 0.0;
-    bool head_ends = false;
-    if (act) {
-        int lo_r = 0, hi_r = nr - 1;                     // last row with so(r) <= e_lo
-        while (lo_r < hi_r) {
-            const int mid = (lo_r + hi_r + 1) >> 1;
-            if (sm.so[mid] <= e_lo) lo_r = mid; else hi_r = mid - 1;
-        }
-        int row = lo_r;
-        int end = sm.so[row + 1];
-        head_row = row;
-        bool in_head = true;
-        double cur = 0.0;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int p = pq + u;
-            if (p >= e_lo && p < e_hi) {
-                while (p >= end) {
-                    if (in_head) { head_sum = cur; head_ends = true; in_head = false; }
-                    else { A.y[r0 + row] = cur; mx = fmax(mx, fabs(cur)); }   // row inside the quad
-                    cur = 0.0;
-                    ++row;
-                    end = sm.so[row + 1];
-                }
-                cur += pv[u];
-            }
-        }
-        if (in_head) {                                   // one row covers the whole quad
-            head_sum = cur;
-            if (end <= e_hi) head_ends = true;           // ... and ends here
-            else { f = false; carry = true; v = cur; }   // ... and runs on: pass the chain
-        } else if (end <= e_hi) {                        // last row also ends here
-            A.y[r0 + row] = cur;
-            mx = fmax(mx, fabs(cur));
-        } else {                                         // last row runs on: start a chain
-            carry = true;
-            v = cur;
-        }
-    }
-
-    // -------------------------- segmented inclusive scan of chain values
-    double S = v;
-    bool F = f;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const double Su = __shfl_up_sync(0xffffffffu, S, d);
-        const bool Fu = __shfl_up_sync(0xffffffffu, F ? 1 : 0, d) != 0;
-        if (lane >= d) {
-            if (!F) S = Su + S;
-            F = F || Fu;
-        }
-    }
-    if (lane == 31) {
-        sm.wv[warp] = S;
-        sm.wf[warp] = F ? 1 : 0;
-        sm.wh[warp] = carry ? 1 : 0;
-    }
-    __syncthreads();
-    // carry into this warp's lane 0: out_k = wf[k] ? wv[k] : c + wv[k],
-    // c = wh[k] ? out_k : 0, over earlier warps in order (fixed order)
-    double cin = 0.0;
-    for (int k = 0; k < warp; ++k) {
-        const double out = sm.wf[k] ? sm.wv[k] : cin + sm.wv[k];
-        cin = sm.wh[k] ? out : 0.0;
-    }
-    const double Sfull = F ? S : cin + S;
-    const double Sprev = __shfl_up_sync(0xffffffffu, Sfull, 1);
-    const bool cprev = __shfl_up_sync(0xffffffffu, carry ? 1 : 0, 1) != 0;
-    const double carry_in = (lane == 0) ? cin : (cprev ? Sprev : 0.0);
-    if (act && head_ends) {
-        const double tot = carry_in + head_sum;
-        A.y[r0 + head_row] = tot;
-        mx = fmax(mx, fabs(tot));
-    }
-    if (A.maxabs_slots) {
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-        if (lane == 0 && mx > 0.0)
-            atomicMax(A.maxabs_slots + ((t * (kRT / 32) + warp) & (kMaxSlots - 1)) * kSlotStride,
-                      (unsigned long long)__double_as_longlong(mx));
-    }
-}
-
-// ---------------------------------------------------------------------------
-// spmv_longrow_kernel: rows longer than a tile (CTA-per-row class), one CTA
-// each, launched over the list of long tiles.  Each thread keeps LQ quads of
-// the row in flight (all stream loads, then all gathers), which the tile
-// kernel's register budget (6 CTAs/SM) cannot afford; fixed assignment and
-// fixed block tree (deterministic).
-template <bool XSPLIT>
-__global__ void __launch_bounds__(256, 2) spmv_longrow_kernel(const RowTileArgs A) {
-    constexpr int NT = 256, LQ = 4;
-    __shared__ double red[NT / 32];
-    const int t = A.long_tiles[blockIdx.x];
-    const int tid = threadIdx.x;
-    const int r0 = A.tile_row[t];
-    const int a = A.tile_nnz[t], b = A.tile_nnz[t + 1];
-    const uint64_t pol = pol_evict_first();
-    const int64_t qa = a >> 2, qb = ((int64_t)b + 3) >> 2;
-    double acc = 0.0;
-    for (int64_t q0 = qa + tid; q0 < qb; q0 += (int64_t)LQ * NT) {
-        int4 c[LQ];
-        double2 v0[LQ], v1[LQ];
-#pragma unroll
-        for (int u = 0; u < LQ; ++u) {
-            const int64_t q = q0 + (int64_t)u * NT;
-            if (q < qb) {
-                c[u] = ld_v4(A.col + 4 * q, pol);
-                v0[u] = ld_v2d(A.val + 4 * q, pol);
-                v1[u] = ld_v2d(A.val + 4 * q + 2, pol);
-            }
-        }
-        double xv[LQ][4];
-#pragma unroll
-        for (int u = 0; u < LQ; ++u) {
-            const int64_t g = 4 * (q0 + (int64_t)u * NT);
-            if (q0 + (int64_t)u * NT < qb) {
-                (void)g;
-                xv[u][0] = ldx2<XSPLIT>(A, c[u].x);
-                xv[u][1] = ldx2<XSPLIT>(A, c[u].y);
-                xv[u][2] = ldx2<XSPLIT>(A, c[u].z);
-                xv[u][3] = ldx2<XSPLIT>(A, c[u].w);
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < LQ; ++u) {
-            const int64_t g = 4 * (q0 + (int64_t)u * NT);
-            if (q0 + (int64_t)u * NT < qb) {
-                if (g + 0 >= a && g + 0 < b) acc += v0[u].x * xv[u][0];
-                if (g + 1 >= a && g + 1 < b) acc += v0[u].y * xv[u][1];
-                if (g + 2 >= a && g + 2 < b) acc += v1[u].x * xv[u][2];
-                if (g + 3 >= a && g + 3 < b) acc += v1[u].y * xv[u][3];
-            }
-        }
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-    if ((tid & 31) == 0) red[tid >> 5] = acc;
-    __syncthreads();
-    if (tid == 0) {
-        double tot = 0.0;
-        for (int w = 0; w < NT / 32; ++w) tot += red[w];
-        A.y[r0] = tot;
-        if (A.maxabs_slots && tot != 0.0)
-            atomicMax(A.maxabs_slots + (t & (kMaxSlots - 1)) * kSlotStride,
-                      (unsigned long long)__double_as_longlong(fabs(tot)));
-    }
-}
-
 }  // namespace
 
-cudaError_t launch_longrows(const RowTileArgs& a, int32_t n_long, bool xsplit, cudaStream_t s) {
-    if (n_long <= 0 || !a.long_tiles) return cudaSuccess;
-    if (xsplit) spmv_longrow_kernel<true><<<n_long, 256, 0, s>>>(a);
-    else spmv_longrow_kernel<false><<<n_long, 256, 0, s>>>(a);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_rowtile(const RowTileArgs& a, bool xsplit, int nt, cudaStream_t s, bool lin) {
+cudaError_t launch_rowtile(const RowTileArgs& a, bool xsplit, cudaStream_t s) {
     if (a.n_tiles <= 0) return cudaSuccess;
-    if (lin) {
-        if (xsplit) spmv_rowtile_kernel<true, 256, true><<<a.n_tiles, 256, 0, s>>>(a);
-        else spmv_rowtile_kernel<false, 256, true><<<a.n_tiles, 256, 0, s>>>(a);
-    } else if (nt == 256) {
-        if (xsplit) spmv_rowtile_kernel<true, 256, false><<<a.n_tiles, 256, 0, s>>>(a);
-        else spmv_rowtile_kernel<false, 256, false><<<a.n_tiles, 256, 0, s>>>(a);
-    } else if (nt == 128) {
-        if (xsplit) spmv_rowtile_kernel<true, 128, false><<<a.n_tiles, 128, 0, s>>>(a);
-        else spmv_rowtile_kernel<false, 128, false><<<a.n_tiles, 128, 0, s>>>(a);
-    } else {
-        if (xsplit) spmv_rowtile_kernel<true, 512, false><<<a.n_tiles, 512, 0, s>>>(a);
-        else spmv_rowtile_kernel<false, 512, false><<<a.n_tiles, 512, 0, s>>>(a);
-    }
-    return cudaGetLastError();
-}
-
-cudaError_t launch_rowseg(const RowTileArgs& a, bool xsplit, cudaStream_t s) {
-    if (a.n_tiles <= 0) return cudaSuccess;
-    if (xsplit) spmv_rowseg_kernel<true><<<a.n_tiles, kRT, 0, s>>>(a);
-    else spmv_rowseg_kernel<false><<<a.n_tiles, kRT, 0, s>>>(a);
+    if (xsplit) spmv_rowtile_kernel<true><<<a.n_tiles, kNT, 0, s>>>(a);
+    else spmv_rowtile_kernel<false><<<a.n_tiles, kNT, 0, s>>>(a);
     return cudaGetLastError();
 }
 

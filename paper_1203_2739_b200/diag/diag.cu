@@ -2,13 +2,10 @@
 // "N13"): they bound what the SpMxV kernel can reach on this matrix.
 //   read    : a pure 128-bit read stream (HBM read peak; SpMxV is ~95% reads)
 //   gather  : random 8-byte gathers from an L2-resident vector (x-gather rate)
-//   csr     : mode 0 streams the handle's col/val only (no x),
-//             mode 1 streams col/val and gathers x[col] (no row reduction):
-//             the speed of light of the SpMxV memory pattern on this matrix.
 #include <cstdint>
 #include <cuda_runtime.h>
 
-#include "internal.h"
+#include "diag.h"
 
 namespace spmvb {
 namespace {
@@ -162,53 +159,6 @@ __global__ void __launch_bounds__(256) gather_smem_kernel(const double* __restri
     if (acc == 1.2345) out[0] = acc;
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(256) csr_stream_kernel(const int32_t* __restrict__ col, const double* __restrict__ val,
-                                                         const double* __restrict__ x, int64_t nq, double* out) {
-    // one CTA per 512 consecutive quads, launched in order (no drift)
-    const uint64_t pol = pol_first();
-    double acc = 0.0;
-    const int64_t stride = blockDim.x;
-    for (int64_t q = blockIdx.x * 512ll + threadIdx.x; q < nq && q < blockIdx.x * 512ll + 512; q += 2 * stride) {
-        const bool two = q + stride < nq;
-        const int4 c0 = ldv4(col + 4 * q, pol);
-        const int4 a0 = ldv4(val + 4 * q, pol), b0 = ldv4(val + 4 * q + 2, pol);
-        int4 c1 = c0, a1 = a0, b1 = b0;
-        if (two) {
-            c1 = ldv4(col + 4 * (q + stride), pol);
-            a1 = ldv4(val + 4 * (q + stride), pol);
-            b1 = ldv4(val + 4 * (q + stride) + 2, pol);
-        }
-        const double v[8] = {__hiloint2double(a0.y, a0.x), __hiloint2double(a0.w, a0.z),
-                             __hiloint2double(b0.y, b0.x), __hiloint2double(b0.w, b0.z),
-                             __hiloint2double(a1.y, a1.x), __hiloint2double(a1.w, a1.z),
-                             __hiloint2double(b1.y, b1.x), __hiloint2double(b1.w, b1.z)};
-        const int c[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-        if (MODE == 0) {
-#pragma unroll
-            for (int u = 0; u < 8; ++u) acc += v[u] + (double)c[u];
-        } else if (MODE == 2) {     // same stream, gathers folded into an 8 MB window
-            double xv[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) xv[u] = __ldg(x + (c[u] & ((1 << 20) - 1)));
-#pragma unroll
-            for (int u = 0; u < 8; ++u) acc += v[u] * xv[u];
-        } else if (MODE == 3) {     // gathers only at independent addresses (no dependency on col)
-            double xv[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) xv[u] = __ldg(x + (((q * 8 + u) * 2654435761ull) & ((1 << 20) - 1)));
-#pragma unroll
-            for (int u = 0; u < 8; ++u) acc += v[u] * xv[u];
-        } else {
-            double xv[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) xv[u] = __ldg(x + c[u]);
-#pragma unroll
-            for (int u = 0; u < 8; ++u) acc += v[u] * xv[u];
-        }
-    }
-    if (acc == 1.2345) out[0] = acc;
-}
 
 int sms() {
     int dev = 0, n = 0;
@@ -252,19 +202,6 @@ cudaError_t diag_gather_mode(const double* x, int64_t n, int64_t count, int mode
         gather_smem_kernel<<<grid, 256, 12288 * 8, s>>>(x, pt, out);
         break;
     default: return cudaErrorInvalidValue;
-    }
-    return cudaGetLastError();
-}
-
-cudaError_t diag_csr(const int32_t* col, const double* val, const double* x, int64_t nnz, int mode, double* out,
-                     cudaStream_t s) {
-    const int64_t nq = (nnz + 3) / 4;
-    const int grid = (int)((nq + 511) / 512);
-    switch (mode) {
-    case 0: csr_stream_kernel<0><<<grid, 256, 0, s>>>(col, val, x, nq, out); break;
-    case 1: csr_stream_kernel<1><<<grid, 256, 0, s>>>(col, val, x, nq, out); break;
-    case 2: csr_stream_kernel<2><<<grid, 256, 0, s>>>(col, val, x, nq, out); break;
-    default: csr_stream_kernel<3><<<grid, 256, 0, s>>>(col, val, x, nq, out); break;
     }
     return cudaGetLastError();
 }

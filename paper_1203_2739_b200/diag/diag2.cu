@@ -12,7 +12,7 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
-#include "internal.h"
+#include "diag.h"
 
 namespace spmvb {
 namespace {

@@ -1,0 +1,73 @@
+"""Test and debug hooks of libspmv_b200.so (``include/spmv_test.h``).
+
+Argument marshalling only, like the main binding.  The parity tests use these
+to read the device CSR back, to round-trip the panel planner on the host, and
+to run the multi-GPU path on one GPU (the loopback fake of SURVEY.md §4:
+``test_create_rank`` + ``loopback_link``).  Nothing here changes what a handle
+made by ``spmv_create`` computes.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import Handle, _addr, _blocks_struct, _check, _create_args, _h, _np, lib, spmv_get_info
+
+
+def debug_copy_csr(h):
+    """The device copy of the permuted local CSR, back on the host (global column ids)."""
+    info = spmv_get_info(h)
+    rp = np.empty(info["m_local"] + 1, np.int64)
+    col = np.empty(info["nnz_local"], np.int32)
+    val = np.empty(info["nnz_local"], np.float64)
+    _check(lib().spmv_debug_copy_csr(_h(h), _addr(rp), _addr(col), _addr(val)), "spmv_debug_copy_csr")
+    return rp, col, val
+
+
+def pn_plan_check(m: int, n: int, row_ptr, col, val, blocks, rows_target: int) -> dict:
+    """Host-only round trip of the column-sorted panel planner; raises on mismatch."""
+    rp = _np(row_ptr, np.int64)
+    ci = _np(col, np.int32)
+    va = _np(val, np.float64)
+    keep = []
+    bptr = _blocks_struct(blocks, keep)
+    stats = np.zeros(10, dtype=np.int64)
+    _check(lib().spmv_pn_plan_check(m, n, _addr(rp), _addr(ci), _addr(va), bptr, rows_target, stats.ctypes.data),
+           "spmv_pn_plan_check")
+    d = dict(zip(("panels", "groups", "pads", "deferred", "epochs", "entries"), (int(v) for v in stats[:6])))
+    d["y_wavefronts_natural"] = stats[6] / 1000.0
+    d["y_wavefronts_coloured"] = stats[7] / 1000.0
+    d["smem_max"] = int(stats[8])
+    d["panels_with_border"] = int(stats[9])
+    return d
+
+
+def pn_shard_hash(m: int, n: int, row_ptr, col, val, blocks, world: int, sms: int = 148) -> np.ndarray:
+    """Host-only: per-rank, per-block hashes of the SB panel plan's summation order; int64 [world, K]."""
+    rp = _np(row_ptr, np.int64)
+    ci = _np(col, np.int32)
+    va = _np(val, np.float64)
+    keep = []
+    bptr = _blocks_struct(blocks, keep)
+    out = np.zeros((world, int(blocks["K"])), dtype=np.int64)
+    _check(lib().spmv_pn_shard_hash(m, n, _addr(rp), _addr(ci), _addr(va), bptr, world, sms, out.ctypes.data),
+           "spmv_pn_shard_hash")
+    return out
+
+
+def test_create_rank(m: int, n: int, row_ptr, col_idx, val, rank: int, world: int, row_perm=None, col_perm=None,
+                     blocks=None, parts=None, n_parts: int = 0, device: int = 0, options=None) -> Handle:
+    """Rank `rank` of `world` on the current GPU without a communicator (loopback fake)."""
+    keep = []
+    args = _create_args(m, n, row_ptr, col_idx, val, row_perm, col_perm, blocks, parts, n_parts,
+                        dict(rank=rank, world=world, device=device), options, keep)
+    out = ctypes.c_void_p(0)
+    _check(lib().spmv_test_create_rank(*args, ctypes.byref(out)), "spmv_test_create_rank")
+    return Handle(out.value)
+
+
+def loopback_link(handles) -> None:
+    """Link test ranks 0..G-1 (in order) into one loopback group (P2P protocol on one GPU)."""
+    arr = (ctypes.c_void_p * len(handles))(*[_h(h).value for h in handles])
+    _check(lib().spmv_test_loopback_link(arr, len(handles)), "spmv_test_loopback_link")

@@ -4,7 +4,7 @@ import json, os, sys
 import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1203_2739_b200 as sp, synth
-from roofline import timeit
+from timing import timeit
 p = synth.make("c3")
 h = sp.spmv_create(p.m, p.n, p.row_ptr, p.col, p.val, blocks=p.blocks, parts=p.parts, n_parts=p.n_parts)
 info = sp.spmv_get_info(h)

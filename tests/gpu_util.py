@@ -13,6 +13,14 @@ def create(prob, **kw):
                           n_parts=prob.n_parts, **kw)
 
 
+PANEL = dict(kernel="panel")
+
+
+def panel(rows):
+    """spmv_options_t forcing the column-sorted panel kernel at `rows` y slots per panel."""
+    return dict(kernel="panel", split_kernel="panel", panel_rows=rows)
+
+
 def oracle_permuted(prob, x):
     """Oracle y and S for original-space x, mapped to PERMUTED space:
     y^[row_perm[i]] = y[i]; plus x^ (x^[col_perm[j]] = x[j])."""

@@ -22,22 +22,13 @@ import paper_1203_2739_b200 as sp
 import synth
 
 
-class Shard(ctypes.Structure):
-    _fields_ = [(k, ctypes.c_int64) for k in (
-        "block_begin", "block_end", "row_begin", "row_end", "x_interior_begin", "x_interior_len",
-        "x_border_begin", "x_border_len", "x_local_len", "border_begin", "border_total")]
+class _S:
+    def __init__(self, d):
+        self.__dict__.update(d)
 
 
 def shard_plan(p, rank, world):
-    b = p.blocks
-    rbp = np.ascontiguousarray(b["row_block_ptr"], np.int64)
-    cbp = np.ascontiguousarray(b["col_block_ptr"], np.int64)
-    blk = sp._Blocks(1, b["K"], rbp.ctypes.data, cbp.ctypes.data, None)
-    s = Shard()
-    st = sp.lib().spmv_shard_plan(ctypes.byref(blk), ctypes.c_int64(p.m), ctypes.c_int64(p.n), rank, world,
-                                  ctypes.byref(s))
-    assert st == 0
-    return s
+    return _S(sp.spmv_shard_plan(p.blocks, p.m, p.n, rank, world))
 
 
 def _worker(rank, world, port, name, result_q):

@@ -1,0 +1,139 @@
+"""GPU parity of the SB default kernel -- column-sorted panels (panel.cu),
+y in shared memory, epoch barriers -- against the CPU oracle (oracle/), forced
+onto small panels through spmv_options_t: odd block widths, blocks without a
+border, empty and dense rows, bit-exact integer data, determinism, the fused
+multiple-SpMxV on panels and the row-major fallback."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1203_2739_b200 as sp
+import synth
+from gpu_util import assert_parity, create, gpu_apply, oracle_permuted
+from gpu_util import panel
+from test_plan_cpu import _c5_like, _random_sb
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+@pytest.fixture(scope="module", autouse=True)
+def cuda():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    sp.lib()
+
+
+def _run(m, n, rp, col, val, blocks, x, flags=0, rows=700):
+    h = sp.spmv_create(m, n, rp, col, val, blocks=blocks, options=panel(rows))
+    assert sp.spmv_get_info(h)["kernel"] == 7
+    return h, gpu_apply(h, x, m, flags=flags)
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+@pytest.mark.parametrize("variant", ["int", "real"])
+def test_random_sb_odd_blocks(seed, variant):
+    m, n, rp, col, val, blocks = _random_sb(seed, 4, [37, 600, 1201, 90], [1, 2047, 2049, 5001], 333, 0.01, 0.01)
+    rng = np.random.default_rng(seed + 10)
+    if variant == "int":
+        val = rng.integers(-4, 5, len(val)).astype(np.float64)
+        x = rng.integers(-4, 5, n).astype(np.float64)
+    else:
+        x = rng.uniform(-1, 1, n)
+    yref, S = oracle.spmv(rp, col, val, x)
+    _, y = _run(m, n, rp, col, val, blocks, x)
+    assert_parity(y, yref, S, exact=(variant == "int"), what=f"random_sb/{seed}/{variant}")
+
+
+def test_no_border_dense_rows():
+    m, n, rp, col, val, blocks = _random_sb(5, 3, [40, 1, 300], [3000, 17, 4100], 0, 0.3, 0.0)
+    x = np.random.default_rng(3).uniform(-1, 1, n)
+    yref, S = oracle.spmv(rp, col, val, x)
+    _, y = _run(m, n, rp, col, val, blocks, x)
+    assert_parity(y, yref, S, what="no_border")
+
+
+@pytest.mark.parametrize("name", ["c5s", "c2s"])
+@pytest.mark.parametrize("variant", ["int", "dyadic", "real"])
+def test_presets(name, variant):
+    p = synth.make(name, variant=variant)
+    x = p.x()
+    xh, yh_ref, S = oracle_permuted(p, x)
+    h = create(p, options=panel(700))
+    assert sp.spmv_get_info(h)["kernel"] == 7
+    yh = gpu_apply(h, xh, p.m)
+    assert_parity(yh, yh_ref, S, exact=(variant != "real"), what=f"panel/{name}/{variant}")
+
+
+@pytest.mark.parametrize("variant", ["int", "real"])
+def test_c5_like_default_geometry(variant):
+    """The SB default (panel kernel) on a C5-shaped block pair, at the panel size
+    the default plan picks for full C5 (16,384 rows; this small matrix would
+    otherwise get 1,024-row panels)."""
+    p = _c5_like(seed=3)
+    if variant == "int":
+        rng = np.random.default_rng(1)
+        p.val[:] = rng.integers(-4, 5, p.nnz)
+    x = synth.vector(p.n, 3, 0, variant)
+    yref, S = oracle.spmv(p.row_ptr, p.col, p.val, x, nthreads=oracle.max_threads())
+    h = create(p, options=dict(panel_rows=16384))
+    info = sp.spmv_get_info(h)
+    assert info["kernel"] == 7 and info["pad_slots"] < 0.05 * 32 * info["groups"]
+    y = gpu_apply(h, x, p.m)
+    assert_parity(y, yref, S, exact=(variant == "int"), what=f"c5_like/{variant}")
+
+
+@pytest.mark.parametrize("name", ["c5s", "c4s"])
+def test_deterministic(name):
+    p = synth.make(name)
+    h = create(p, options=panel(2000))
+    x = torch.from_numpy(oracle.permute_x(p.col_perm, p.x()) if p.col_perm is not None else p.x()).cuda()
+    y = torch.empty(p.m, dtype=torch.float64, device="cuda")
+    sp.spmv_apply(h, x, y)
+    y1 = y.clone()
+    for _ in range(3):
+        sp.spmv_apply(h, x, y)
+    torch.cuda.synchronize()
+    assert torch.equal(y, y1), "run-to-run deterministic"
+
+
+@pytest.mark.parametrize("variant", ["int", "real"])
+def test_split_on_panels(variant):
+    """Fused multiple-SpMxV on the panel kernel: each (row, part) segment is its
+    own virtual row, folded per row.  Forced onto small panels."""
+    p = synth.make("c3s", variant=variant)
+    x = p.x()
+    h = create(p, options=panel(900))
+    assert sp.spmv_get_info(h)["split_kernel"] == 7
+    y = gpu_apply(h, x, p.m, split=True)
+    yref = oracle.split(p.row_ptr, p.col, p.val, p.parts, p.n_parts, x)
+    S = oracle.spmv(p.row_ptr, p.col, p.val, x)[1]
+    assert_parity(y, yref, S, exact=(variant == "int"), what=f"split-on-panels/{variant}")
+    # literal sequence and single SpMxV on the same handle agree with the oracle too
+    yl = gpu_apply(h, x, p.m, flags=sp.SPMV_SPLIT_LITERAL, split=True)
+    assert_parity(yl, yref, S, exact=(variant == "int"), what="literal")
+
+
+def test_split_on_panels_random_parts():
+    p = synth.make("c4s", variant="int")      # rows up to 3,000 nonzeros: long segments split further
+    rng = np.random.default_rng(7)
+    parts = rng.integers(0, 5, p.nnz).astype(np.int32)
+    x = p.x()
+    h = sp.spmv_create(p.m, p.n, p.row_ptr, p.col, p.val, parts=parts, n_parts=5, options=panel(3000))
+    y = gpu_apply(h, x, p.m, split=True)
+    yref = oracle.split(p.row_ptr, p.col, p.val, parts, 5, x)
+    assert_parity(y, yref, None, exact=True, what="split-on-panels/random parts")
+
+
+def test_split_rowmajor_kernel():
+    """The row-major segment kernel (used when the panel plan is rejected)."""
+    p = synth.make("c3s", variant="int")
+    x = p.x()
+    h = create(p, options=dict(split_kernel="rows"))
+    assert sp.spmv_get_info(h)["split_kernel"] == 3
+    y = gpu_apply(h, x, p.m, split=True)
+    yref = oracle.split(p.row_ptr, p.col, p.val, p.parts, p.n_parts, x)
+    assert_parity(y, yref, None, exact=True, what="split row-major")
+
+

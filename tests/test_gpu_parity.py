@@ -7,8 +7,9 @@ import pytest
 
 import oracle
 import paper_1203_2739_b200 as sp
+import paper_1203_2739_b200.testing as T
 import synth
-from gpu_util import assert_parity, create, gpu_apply, oracle_permuted
+from gpu_util import assert_parity, create, gpu_apply, oracle_permuted, panel
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -26,7 +27,7 @@ def cuda():
 def test_ingest_bit_exact(name):
     p = synth.make(name)
     h = create(p)
-    rp, col, val = sp.spmv_debug_copy_csr(h)
+    rp, col, val = T.debug_copy_csr(h)
     o = oracle.permute(p.m, p.n, p.row_ptr, p.col, p.val, p.row_perm, p.col_perm)
     assert np.array_equal(rp, o[0])
     assert np.array_equal(col, o[1])
@@ -78,21 +79,19 @@ def _edge_matrix(lengths, n, seed=0, variant="int"):
                                   "single", "all_empty", "ragged_mix"])
 @pytest.mark.parametrize("variant", ["int", "real"])
 @pytest.mark.parametrize("kernel", ["default", "panel"])
-def test_edge_shapes(monkeypatch, case, variant, kernel):
+def test_edge_shapes(case, variant, kernel):
     """Row lengths at every tile/class boundary +-1, rows longer than a tile,
     empty rows, m != n (Table 1's rectangular group), odd row
     starts (exercise the 128-bit quad peeling).  kernel=panel forces the
     column-sorted panel kernel on small panels (virtual rows of very long
     rows, the warp fold of rows with > 32 of them, empty panels' rows)."""
-    if kernel == "panel":
-        monkeypatch.setenv("SPMV_KERNEL", "panel")
-        monkeypatch.setenv("SPMV_PN_ROWS", "700")
-    T = 2048   # kTileNnz
+    opts = panel(700) if kernel == "panel" else None
+    TN = 2048   # kTileNnz
     rng = np.random.default_rng(5)
     if case == "tile_edges":
-        lengths, n = [1, 3, T - 1, T, T + 1, 2, 5, T - 3, 7, 4 * T + 1, 1, 0, 33, 31, 32], 20000
+        lengths, n = [1, 3, TN - 1, TN, TN + 1, 2, 5, TN - 3, 7, 4 * TN + 1, 1, 0, 33, 31, 32], 20000
     elif case == "long_rows":
-        lengths, n = [10000, 1, 6000, 2 * T, 3], 12000
+        lengths, n = [10000, 1, 6000, 2 * TN, 3], 12000
     elif case == "empty_rows":
         lengths, n = list(rng.choice([0, 0, 0, 1, 2, 17], 3000)), 500
     elif case == "rect_wide":
@@ -104,11 +103,13 @@ def test_edge_shapes(monkeypatch, case, variant, kernel):
     elif case == "all_empty":
         lengths, n = [0] * 1000, 77
     else:
-        lengths, n = list(rng.integers(0, 600, 400)) + [T + 5] + list(rng.integers(0, 3, 2000)), 4000
+        lengths, n = list(rng.integers(0, 600, 400)) + [TN + 5] + list(rng.integers(0, 3, 2000)), 4000
     rp, col, val, x = _edge_matrix(lengths, n, variant=variant)
     m = len(lengths)
     y_ref, S = oracle.spmv(rp, col, val, x)
-    h = sp.spmv_create(m, n, rp, col, val)
+    h = sp.spmv_create(m, n, rp, col, val, options=opts)
+    if kernel == "panel" and case not in ("all_empty",):
+        assert sp.spmv_get_info(h)["kernel"] == 7
     y = gpu_apply(h, x, m)
     assert_parity(y, y_ref, S, exact=(variant == "int"), what=case)
 
@@ -164,11 +165,9 @@ def test_split_k1_and_random_parts():
     assert np.array_equal(gpu_apply(h5, x, p.m, split=True, flags=sp.SPMV_SPLIT_LITERAL), y_ref)
 
 
-def test_split_on_panels_edges(monkeypatch):
+def test_split_on_panels_edges():
     """Fused split on forced small panels: K = 1, parts that never occur, rows
     whose nonzeros all sit in one part, empty rows, long segments."""
-    monkeypatch.setenv("SPMV_KERNEL", "panel")
-    monkeypatch.setenv("SPMV_PN_ROWS", "700")
     lengths = [0, 1, 40, 3000, 0, 7, 33, 2] * 150
     rp, col, val, x = _edge_matrix(lengths, 5000, seed=3)
     m, nnz = len(lengths), int(rp[-1])
@@ -181,7 +180,7 @@ def test_split_on_panels_edges(monkeypatch):
         "random": (rng.integers(0, 9, nnz).astype(np.int32), 9),
     }
     for what, (parts, K) in cases.items():
-        h = sp.spmv_create(m, 5000, rp, col, val, parts=parts, n_parts=K)
+        h = sp.spmv_create(m, 5000, rp, col, val, parts=parts, n_parts=K, options=panel(700))
         assert sp.spmv_get_info(h)["split_kernel"] == 7, what
         ys = gpu_apply(h, x, m, split=True)
         assert np.array_equal(ys, oracle.split(rp, col, val, parts, K, x)), what
@@ -201,33 +200,78 @@ def test_split_with_permutation():
 
 
 # ------------------------------------------------ power iteration glue (a9)
-def test_power_iteration_teacher_forced():
-    p = synth.make("c5s")
-    h = create(p)
+def _c5_like(seed=3):
+    """Two C5-shaped SB blocks (identity perms) at the production panel size."""
+    synth.PRESETS["_c5like_pi"] = lambda **kw: synth._sb(2, 40_000, 39_200, 400, 12, 20, 0, 3, **kw)
+    return synth.make("_c5like_pi", scramble=0, seed=seed)
+
+
+def _teacher_forced(p, opts, steps, split=False, expect_kernel=None):
+    """Teacher-forced power iteration: at every step the
+    oracle recomputes A x_t (or the split sum) from the GPU's own x_t and
+    checks y_t within the north_star tolerance; m_t must equal the oracle's
+    max |y_t| of the GPU's y_t exactly, and x_{t+1} must equal y_t / m_t bit
+    for bit (IEEE division)."""
+    h = create(p, options=opts)
     info = sp.spmv_get_info(h)
     assert info["has_owner_map"] == 1
+    if expect_kernel is not None:
+        assert (info["split_kernel"] if split else info["kernel"]) == expect_kernel
     x = p.x()
-    xh = torch.from_numpy(oracle.permute_x(p.col_perm, x)).cuda()
+    xh = torch.from_numpy(oracle.permute_x(p.col_perm, x) if p.col_perm is not None else x.copy()).cuda()
     yh = torch.empty(p.m, dtype=torch.float64, device="cuda")
     md = torch.empty(1, dtype=torch.float64, device="cuda")
-    for t in range(6):
-        sp.spmv_apply(h, xh, yh, sp.SPMV_FUSE_MAXABS)
+    nth = oracle.max_threads()
+    for t in range(steps):
+        (sp.spmv_split_apply if split else sp.spmv_apply)(h, xh, yh, sp.SPMV_FUSE_MAXABS)
         sp.spmv_maxabs(h, md)
         xn = torch.empty_like(xh)
         sp.spmv_normalize(h, yh, md, xn)
         torch.cuda.synchronize()
-        # teacher forcing: the oracle recomputes A x_t from the GPU's own x_t
         xg = xh.cpu().numpy()
-        x_orig = np.empty_like(xg)
-        x_orig[:] = xg[p.col_perm]            # x[j] = x^[col_perm[j]]
-        y_ref, S = oracle.spmv(p.row_ptr, p.col, p.val, x_orig)
-        y_gpu = oracle.unpermute_y(p.row_perm, yh.cpu().numpy())
+        x_orig = xg[p.col_perm] if p.col_perm is not None else xg      # x[j] = x^[col_perm[j]]
+        y_ref, S = oracle.spmv(p.row_ptr, p.col, p.val, x_orig, nthreads=nth)
+        if split:
+            y_ref = oracle.split(p.row_ptr, p.col, p.val, p.parts, p.n_parts, x_orig)
+        yg = yh.cpu().numpy()
+        y_gpu = oracle.unpermute_y(p.row_perm, yg) if p.row_perm is not None else yg
         assert_parity(y_gpu, y_ref, S, what=f"step {t}")
         m_gpu = float(md.item())
-        assert m_gpu == oracle.maxabs(y_gpu)                     # exact max
-        xn_ref = oracle.scale(y_gpu, m_gpu)                      # x_{t+1}[j] = y_t[j] / m_t
-        assert np.array_equal(xn.cpu().numpy()[p.col_perm], xn_ref)
+        assert m_gpu == oracle.maxabs(y_gpu), f"step {t}: max |y| folded on the GPU"
+        xn_ref = oracle.scale(y_gpu, m_gpu)                             # x_{t+1}[j] = y_t[j] / m_t
+        xnh = xn.cpu().numpy()
+        xn_orig = xnh[p.col_perm] if p.col_perm is not None else xnh
+        assert np.array_equal(xn_orig.view(np.int64), xn_ref.view(np.int64)), f"step {t}: x-update"
         xh = xn
+    sp.spmv_destroy(h)
+
+
+def test_power_iteration_teacher_forced():
+    """c5s on its default kernel (the row-tile fallback at this size)."""
+    _teacher_forced(synth.make("c5s"), None, 6)
+
+
+def test_power_iteration_panel_c5_geometry():
+    """The production kernel of C5 -- column-sorted panels at the full-C5 panel
+    size (16,384 slots), SB border groups -- with the max |y| fold of its
+    epilogue (untested on the default kernel)."""
+    _teacher_forced(_c5_like(), panel(16384), 4, expect_kernel=7)
+
+
+def test_power_iteration_panel_c4_virtual_rows():
+    """C4's power-law rows on forced panels: rows above 32 nonzeros are split
+    into virtual rows, folded by one thread (<= 32 of them) or a warp (more);
+    both epilogue folds feed the max."""
+    p = synth.make("c4s")
+    assert int(np.diff(p.row_ptr).max()) > 32 * 32   # some rows get > 32 virtual rows (warp fold)
+    _teacher_forced(p, panel(2000), 4, expect_kernel=7)
+
+
+def test_power_iteration_split_fused_maxabs():
+    """The fused multiple-SpMxV on panels with SPMV_FUSE_MAXABS: the (row,
+    part) fold of the epilogue feeds the max; teacher-forced against the
+    oracle's literal split sequence."""
+    _teacher_forced(synth.make("c3s"), panel(900), 3, split=True, expect_kernel=7)
 
 
 # ------------------------------------------------------------ API behaviour
@@ -285,3 +329,18 @@ def test_full_size_parity(name):
     if p.parts is not None:
         ys_ref = oracle.split(p.row_ptr, p.col, p.val, p.parts, p.n_parts, x)
         assert_parity(gpu_apply(h, xh, p.m, split=True), ys_ref, S, what=name + " split")
+
+
+def test_full_size_power_c4():
+    """BASELINE config C4 at full size (4 M rows, 48 M nonzeros) on its default
+    kernel: three teacher-forced power steps, every entry, m_t exact and
+    x_{t+1} bitwise."""
+    _teacher_forced(synth.make("c4"), None, 3, expect_kernel=7)
+
+
+def test_full_size_power_c5():
+    """BASELINE config C5 at full size (64 M rows, 1.12e9 nonzeros, hidden
+    permutation) on its default kernel (panels, plan of the bench): two
+    teacher-forced power steps checked on all 64 M rows (the bench
+    samples 200,000 rows), m_t exact and x_{t+1} bitwise."""
+    _teacher_forced(synth.make("c5"), None, 2, expect_kernel=7)

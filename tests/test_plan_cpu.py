@@ -1,21 +1,15 @@
-"""Host-only checks of the x-staged kernel's planner (plan_xs.cpp): the packed
-panel/group streams decode back to the permuted CSR bit for bit, with the
-format's invariants (distinct rows per group, <= 2 consecutive chunks per
-group, zero-valued padding).  The kernel itself is checked on the GPU
-(test_gpu_parity.py)."""
+"""Host-only checks of the column-sorted panel planner (plan_panel.cpp): the
+packed groups decode back to the permuted CSR bit for bit, with the format's
+invariants (distinct rows per epoch, groups on one side of the border split,
+border groups last, every panel within 227 KB of shared memory), and the SB
+plan does not depend on the GPU count.  The kernel itself is checked on the
+GPU (tests/test_gpu_*.py)."""
 import numpy as np
 import pytest
 
 import paper_1203_2739_b200 as sp
+import paper_1203_2739_b200.testing as T
 import synth
-
-
-@pytest.mark.parametrize("name,target", [("c5s", 2000), ("c5s", 700), ("c2s", 300), ("c2s", 5000)])
-def test_plan_round_trip_presets(name, target):
-    p = synth.make(name, scramble=0)          # SB form in permuted order (rows sorted)
-    st = sp.spmv_xs_plan_check(p.m, p.n, p.row_ptr, p.col, p.val, p.blocks, target)
-    assert st["entries"] == p.nnz
-    assert st["panels"] >= p.blocks["K"]
 
 
 def _random_sb(seed, K, rows, cols, border, dens_int, dens_b):
@@ -40,23 +34,6 @@ def _random_sb(seed, K, rows, cols, border, dens_int, dens_b):
     return m, n, np.array(rp, dtype=np.int64), np.concatenate(col), np.concatenate(val), blocks
 
 
-@pytest.mark.parametrize("seed", [0, 1, 2])
-def test_plan_round_trip_random_sb(seed):
-    # block widths straddle chunk boundaries (kXsW = 2048): 1, 2047, 2049, 5001 columns
-    m, n, rp, col, val, blocks = _random_sb(seed, 4, [37, 600, 1201, 90], [1, 2047, 2049, 5001], 333, 0.01, 0.01)
-    st = sp.spmv_xs_plan_check(m, n, rp, col, val, blocks, 256)
-    assert st["entries"] == len(col)
-
-
-def test_plan_dense_rows_and_empty_rows():
-    # rows with many entries per chunk (each row's entries land in distinct groups)
-    # and empty rows/blocks without border columns
-    m, n, rp, col, val, blocks = _random_sb(5, 3, [40, 1, 300], [3000, 17, 4100], 0, 0.3, 0.0)
-    st = sp.spmv_xs_plan_check(m, n, rp, col, val, blocks, 512)
-    assert st["entries"] == len(col)
-    assert st["groups_b"] == 0
-
-
 # ---------------------------------------------------------------- panel planner
 def _c5_like(K=2, rows=60_000, cols=58_800, border=1_200, seed=0):
     synth.PRESETS["_c5like"] = lambda **kw: synth._sb(K, rows, cols, border // K, 12, 20, 0, 3, **kw)
@@ -66,7 +43,7 @@ def _c5_like(K=2, rows=60_000, cols=58_800, border=1_200, seed=0):
 @pytest.mark.parametrize("target", [30_000, 7_000])
 def test_panel_plan_round_trip_c5_like(target):
     p = _c5_like()
-    st = sp.spmv_pn_plan_check(p.m, p.n, p.row_ptr, p.col, p.val, p.blocks, target)
+    st = T.pn_plan_check(p.m, p.n, p.row_ptr, p.col, p.val, p.blocks, target)
     assert st["entries"] == p.nnz
     assert st["epochs"] * 64 == st["groups"]
     # big panels: little padding, few deferred nonzeros (the kernel's premise)
@@ -80,13 +57,13 @@ def test_panel_plan_round_trip_small(name, target):
     # small panels pad heavily (the library then keeps the row-tile kernel),
     # but the round trip must still be exact; c4s has rows of up to 3,000 nonzeros
     p = synth.make(name) if name == "c4s" else synth.make(name, scramble=0)
-    st = sp.spmv_pn_plan_check(p.m, p.n, p.row_ptr, p.col, p.val, p.blocks if name != "c4s" else None, target)
+    st = T.pn_plan_check(p.m, p.n, p.row_ptr, p.col, p.val, p.blocks if name != "c4s" else None, target)
     assert st["entries"] == p.nnz
 
 
 def test_panel_plan_random_sb_odd_blocks():
     m, n, rp, col, val, blocks = _random_sb(7, 4, [37, 600, 1201, 90], [1, 2047, 2049, 5001], 333, 0.01, 0.01)
-    st = sp.spmv_pn_plan_check(m, n, rp, col, val, blocks, 400)
+    st = T.pn_plan_check(m, n, rp, col, val, blocks, 400)
     assert st["entries"] == len(col)
 
 
@@ -113,7 +90,7 @@ def test_panel_plan_rank_local_layout(world, rank):
               "row_block_ptr": np.array([rbp[k] - r0 for k in range(k0, k1 + 1)] + [r1 - r0], dtype=np.int64),
               "col_block_ptr": np.array([cbp[k] - q0 for k in range(k0, k1 + 1)] + [nint + sh["border_total"]],
                                         dtype=np.int64)}
-    st = sp.spmv_pn_plan_check(r1 - r0, nint + sh["border_total"], rp, loc, val_g[a:b], blocks, 1500)
+    st = T.pn_plan_check(r1 - r0, nint + sh["border_total"], rp, loc, val_g[a:b], blocks, 1500)
     assert st["entries"] == b - a
 
 
@@ -132,13 +109,38 @@ def test_panel_plan_independent_of_gpu_count(name):
     -- y is then bit-identical across GPU counts."""
     p = synth.make(name, scramble=0)
     K = p.blocks["K"]
-    ref = sp.spmv_pn_shard_hash(p.m, p.n, p.row_ptr, p.col, p.val, p.blocks, 1)[0]
+    ref = T.pn_shard_hash(p.m, p.n, p.row_ptr, p.col, p.val, p.blocks, 1)[0]
     assert np.all(ref != 0)
     for world in (2, 4):
-        h = sp.spmv_pn_shard_hash(p.m, p.n, p.row_ptr, p.col, p.val, p.blocks, world)
+        h = T.pn_shard_hash(p.m, p.n, p.row_ptr, p.col, p.val, p.blocks, world)
         owned = (h != 0).sum(axis=0)
         assert np.all(owned == 1), f"each block on exactly one rank (world {world})"
         assert np.array_equal(h.sum(axis=0), ref), f"world {world} plans differ from world 1"
     # the hash has teeth: another whole-wave count cuts other panels
-    other = sp.spmv_pn_shard_hash(p.m, p.n, p.row_ptr, p.col, p.val, p.blocks, 1, sms=1)[0]
+    other = T.pn_shard_hash(p.m, p.n, p.row_ptr, p.col, p.val, p.blocks, 1, sms=1)[0]
     assert not np.array_equal(other, ref)
+
+
+def test_panel_smem_cap_split_rows():
+    """rows of 33-64 nonzeros become two virtual rows, and a
+    split row also costs 2 B per slot and 12 B per row of fold lists, so a
+    panel of ~16 K slots can exceed 227 KB; the planner must cut panels by
+    shared-memory bytes, whatever the slot target."""
+    rng = np.random.default_rng(11)
+    m = n = 40_000
+    L = 40
+    col = np.concatenate([np.sort(rng.choice(n, L, replace=False)) for _ in range(m)]).astype(np.int32)
+    rp = np.arange(0, (m + 1) * L, L, dtype=np.int64)
+    val = rng.uniform(-1, 1, m * L)
+    st = T.pn_plan_check(m, n, rp, col, val, None, 16384)
+    assert st["entries"] == m * L
+    assert st["smem_max"] <= 227 * 1024
+
+
+def test_border_groups_last():
+    """Columns of C_B (Eq.(1)) come after every interior column in each panel,
+    so the border groups form the panel's last epochs (the world > 1 exchange
+    overlaps the interior epochs); the check itself runs in pn_plan_check."""
+    p = _c5_like()
+    st = T.pn_plan_check(p.m, p.n, p.row_ptr, p.col, p.val, p.blocks, 7_000)
+    assert st["panels_with_border"] == st["panels"]
