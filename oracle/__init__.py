@@ -67,6 +67,8 @@ def _load():
         L.oracle_split_lambda.argtypes = [i64, i64, vp, vp, vp, i32, ctypes.POINTER(i64),
                                           ctypes.POINTER(i64)]
         L.oracle_split_lambda.restype = None
+        L.oracle_sbfs.argtypes = [i64, i64, vp, vp, i32, vp, vp, vp, vp, vp, vp]
+        L.oracle_sbfs.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -204,3 +206,19 @@ def split_lambda(m, n, row_ptr, col, parts, K):
     a, b = ctypes.c_int64(0), ctypes.c_int64(0)
     _load().oracle_split_lambda(m, n, _p(row_ptr), _p(col), _p(parts), K, ctypes.byref(a), ctypes.byref(b))
     return int(a.value), int(b.value)
+
+
+def sbfs(m, n, row_ptr, col, K):
+    """sBFS ordering + SB extraction (reading R5).  Returns dict with
+    row_perm, col_perm (old -> new), row_block_ptr, col_block_ptr (K+2 each)
+    and the plain BFS numbers bfs_row, bfs_col."""
+    row_ptr, col = _c(row_ptr, np.int64), _c(col, np.int32)
+    out = dict(row_perm=np.empty(m, np.int32), col_perm=np.empty(n, np.int32),
+               row_block_ptr=np.empty(K + 2, np.int64), col_block_ptr=np.empty(K + 2, np.int64),
+               bfs_row=np.empty(m, np.int32), bfs_col=np.empty(n, np.int32))
+    rc = _load().oracle_sbfs(m, n, _p(row_ptr), _p(col), K, _p(out["row_perm"]), _p(out["col_perm"]),
+                             _p(out["row_block_ptr"]), _p(out["col_block_ptr"]), _p(out["bfs_row"]),
+                             _p(out["bfs_col"]))
+    if rc:
+        raise ValueError("oracle.sbfs: bad arguments")
+    return out

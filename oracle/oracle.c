@@ -278,6 +278,129 @@ void oracle_split_lambda(int64_t m, int64_t n, const int64_t* row_ptr, const int
     *sum_lc = sc;
 }
 
+/* ------------------------------------------------------------------------ */
+/* sBFS ordering (section 5.1): "we apply BFS on the
+ * bipartite graph representation of the matrix, so that the resulting BFS
+ * orders on the row and column vertices determine row and column
+ * reorderings, respectively."  Reading R5 fixes what the paper
+ * leaves open, as the textbook queue BFS:
+ *   - vertices: rows r_0..r_{m-1} and columns c_0..c_{n-1}; edge (r_i, c_j)
+ *     for every stored entry a_ij;
+ *   - the root is the lowest-numbered unvisited row; a popped vertex appends
+ *     its unvisited neighbours in ascending number; when the queue empties the
+ *     next root is again the lowest-numbered unvisited row; columns no row
+ *     touches come last, ascending;
+ *   - new row number = position among the rows in visiting order; columns
+ *     likewise.  row_perm / col_perm are old -> new (reading A1).
+ * Then the SB extraction (Eq.(1)) with K blocks (reading R5):
+ *   - new row r goes to block min(K-1, floor(K * P(r) / nnz)), P(r) = stored
+ *     entries of the rows numbered below r (floor(K * r / m) when nnz = 0);
+ *   - a column all of whose rows lie in one block k is interior to block k,
+ *     any other column (two or more blocks, or none) is a border column;
+ *   - columns are renumbered: block 0's interior columns, ..., block K-1's,
+ *     then the border columns C_B, each group in BFS column order.
+ * Outputs row_perm[m], col_perm[n] (the SB order, old -> new),
+ * row_block_ptr[K+2] (R_B empty), col_block_ptr[K+2] (the last range is C_B),
+ * and bfs_row[m], bfs_col[n]: the plain BFS numbers before the extraction.
+ * Returns 0, or 1 on bad arguments. */
+int oracle_sbfs(int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col, int32_t K,
+                int32_t* row_perm, int32_t* col_perm, int64_t* row_block_ptr, int64_t* col_block_ptr,
+                int32_t* bfs_row, int32_t* bfs_col) {
+    if (m < 0 || n < 0 || K < 1) return 1;
+    const int64_t nnz = row_ptr[m];
+    /* row adjacency sorted ascending (input rows may be unsorted) */
+    int32_t* radj = (int32_t*)malloc(sizeof(int32_t) * (size_t)(nnz > 0 ? nnz : 1));
+    memcpy(radj, col, sizeof(int32_t) * (size_t)nnz);
+    for (int64_t i = 0; i < m; ++i) {   /* insertion sort per row: plain and obviously correct */
+        for (int64_t t = row_ptr[i] + 1; t < row_ptr[i + 1]; ++t) {
+            int32_t v = radj[t];
+            int64_t u = t - 1;
+            while (u >= row_ptr[i] && radj[u] > v) { radj[u + 1] = radj[u]; --u; }
+            radj[u + 1] = v;
+        }
+    }
+    /* column adjacency: rows in ascending order (counting pass over rows in order) */
+    int64_t* cptr = (int64_t*)calloc((size_t)n + 1, sizeof(int64_t));
+    for (int64_t t = 0; t < nnz; ++t) cptr[col[t] + 1] += 1;
+    for (int64_t j = 0; j < n; ++j) cptr[j + 1] += cptr[j];
+    int32_t* cadj = (int32_t*)malloc(sizeof(int32_t) * (size_t)(nnz > 0 ? nnz : 1));
+    int64_t* fill = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+    for (int64_t j = 0; j < n; ++j) fill[j] = cptr[j];
+    for (int64_t i = 0; i < m; ++i)
+        for (int64_t t = row_ptr[i]; t < row_ptr[i + 1]; ++t) cadj[fill[col[t]]++] = (int32_t)i;
+    /* queue BFS; queue entries: v >= 0 row v, v < 0 column -v-1 */
+    int64_t* queue = (int64_t*)malloc(sizeof(int64_t) * (size_t)(m + n > 0 ? m + n : 1));
+    for (int64_t i = 0; i < m; ++i) bfs_row[i] = -1;
+    for (int64_t j = 0; j < n; ++j) bfs_col[j] = -1;
+    int64_t head = 0, tail = 0, nr = 0, nc = 0, next_root = 0;
+    while (nr < m) {
+        while (bfs_row[next_root] >= 0) ++next_root;      /* lowest unvisited row */
+        bfs_row[next_root] = (int32_t)nr++;
+        queue[tail++] = next_root;
+        while (head < tail) {
+            const int64_t u = queue[head++];
+            if (u >= 0) {
+                for (int64_t t = row_ptr[u]; t < row_ptr[u + 1]; ++t) {
+                    const int32_t j = radj[t];
+                    if (bfs_col[j] < 0) { bfs_col[j] = (int32_t)nc++; queue[tail++] = -(int64_t)j - 1; }
+                }
+            } else {
+                const int64_t j = -u - 1;
+                for (int64_t t = cptr[j]; t < cptr[j + 1]; ++t) {
+                    const int32_t i = cadj[t];
+                    if (bfs_row[i] < 0) { bfs_row[i] = (int32_t)nr++; queue[tail++] = i; }
+                }
+            }
+        }
+    }
+    for (int64_t j = 0; j < n; ++j)
+        if (bfs_col[j] < 0) bfs_col[j] = (int32_t)nc++;   /* untouched columns, ascending */
+    /* SB extraction: blocks of the BFS row order by nonzero prefix */
+    int64_t* len_new = (int64_t*)malloc(sizeof(int64_t) * (size_t)(m > 0 ? m : 1));
+    for (int64_t i = 0; i < m; ++i) len_new[bfs_row[i]] = row_ptr[i + 1] - row_ptr[i];
+    int32_t* blk_new = (int32_t*)malloc(sizeof(int32_t) * (size_t)(m > 0 ? m : 1));
+    int64_t P = 0;
+    for (int64_t r = 0; r < m; ++r) {
+        int64_t b = nnz > 0 ? (int64_t)(((__int128)K * P) / nnz) : (K * r) / (m > 0 ? m : 1);
+        if (b > K - 1) b = K - 1;
+        blk_new[r] = (int32_t)b;
+        P += len_new[r];
+    }
+    for (int32_t k = 0; k <= K + 1; ++k) row_block_ptr[k] = m;
+    for (int64_t r = m - 1; r >= 0; --r) row_block_ptr[blk_new[r]] = r;
+    for (int32_t k = K - 1; k >= 0; --k)          /* empty blocks start where the next one does */
+        if (row_block_ptr[k] > row_block_ptr[k + 1]) row_block_ptr[k] = row_block_ptr[k + 1];
+    row_block_ptr[0] = 0;
+    /* column classes: -1 none yet, k one block, K two or more / none */
+    int32_t* cls = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
+    for (int64_t j = 0; j < n; ++j) cls[j] = -1;
+    for (int64_t i = 0; i < m; ++i) {
+        const int32_t b = blk_new[bfs_row[i]];
+        for (int64_t t = row_ptr[i]; t < row_ptr[i + 1]; ++t) {
+            const int32_t j = col[t];
+            if (cls[j] == -1) cls[j] = b;
+            else if (cls[j] != b) cls[j] = K;
+        }
+    }
+    for (int64_t j = 0; j < n; ++j) if (cls[j] == -1) cls[j] = K;
+    /* column numbering: by (class, BFS column number) */
+    int32_t* by_bfs = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
+    for (int64_t j = 0; j < n; ++j) by_bfs[bfs_col[j]] = (int32_t)j;
+    int64_t q = 0;
+    for (int32_t k = 0; k <= K; ++k) {
+        col_block_ptr[k] = q;
+        for (int64_t c = 0; c < n; ++c) {
+            const int32_t j = by_bfs[c];
+            if (cls[j] == k) col_perm[j] = (int32_t)q++;
+        }
+    }
+    col_block_ptr[K + 1] = n;
+    for (int64_t i = 0; i < m; ++i) row_perm[i] = bfs_row[i];
+    free(radj); free(cptr); free(cadj); free(fill); free(queue); free(len_new); free(blk_new); free(cls);
+    free(by_bfs);
+    return 0;
+}
+
 int oracle_max_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();
