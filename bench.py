@@ -660,6 +660,50 @@ def run_ours(args, rank, world, local_rank):
                                "scrambled_default_kernel": pkern + " on the scrambled matrix, no blocks "
                                                            "(the panel's own column sort recovers part of the locality)",
                                "note": "same matrix and x: input order vs SB-reordered (Table 2 analog, P:L51-55)"}
+        if not args.no_sbfs:
+            # f4: the order produced on the GPU instead of received -- the sBFS
+            # analog + SB extraction with the planted form's K --
+            # and its Table 3 analog: the ordering (+ ingest)
+            # time in SpMxVs of the unordered matrix, and the SpMxVs it
+            # takes to amortize against the unordered SpMxV
+            K = int(p.blocks["K"])
+            torch.cuda.synchronize()
+            t0 = time.time()
+            g = sp.spmv_order_sbfs(p.m, p.n, p.row_ptr, p.col, K)
+            t_order = time.time() - t0
+            t0 = time.time()
+            hb = sp.spmv_create(p.m, p.n, p.row_ptr, p.col, p.val, row_perm=g["row_perm"], col_perm=g["col_perm"],
+                                blocks=g["blocks"])
+            t_create = time.time() - t0
+            xb_ = torch.empty(p.n, dtype=torch.float64, device=dev)
+            xb_[torch.from_numpy(g["col_perm"].astype(np.int64)).to(dev)] = torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+            ys_ = torch.empty(p.m, dtype=torch.float64, device=dev)
+            for _ in range(3):
+                sp.spmv_apply(hb, xb_, ys_, stream=stream)
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(10)]
+            for a_, b_ in evs:
+                if l2_flush:
+                    flush_buf.fill_(1.0)
+                a_.record(stream)
+                sp.spmv_apply(hb, xb_, ys_, stream=stream)
+                b_.record(stream)
+            torch.cuda.synchronize()
+            bms = statistics.median([a_.elapsed_time(b_) for a_, b_ in evs])
+            bkern = KERNEL_NAMES.get(sp.spmv_get_info(hb)["kernel"], "?")
+            sp.spmv_destroy(hb)
+            gain = sms - bms
+            extra["reordering"]["sbfs"] = {
+                "K": K, "border_cols": int(g["border_cols"]), "planted_border_cols": int(p.n - p.blocks["col_block_ptr"][K]),
+                "bfs_levels": int(g["levels"]), "components": int(g["components"]),
+                "order_device_ms": g["bfs_ms"] + g["extract_ms"], "order_wall_s": t_order, "create_s": t_create,
+                "spmv_ms": bms, "kernel": bkern, "speedup_vs_scrambled": sms / bms,
+                "overhead_spmvs": (t_order * 1e3) / sms, "overhead_with_create_spmvs": ((t_order + t_create) * 1e3) / sms,
+                "amortization_spmvs": ((t_order * 1e3) / gain) if gain > 0 else None,
+                "amortization_with_create_spmvs": (((t_order + t_create) * 1e3) / gain) if gain > 0 else None,
+                "note": "spmv_order_sbfs on the scrambled input (GPU BFS on the bipartite graph + SB extraction), "
+                        "then spmv_create with that order; overhead in unordered SpMxVs and amortization = "
+                        "ordering time / (unordered - sBFS-ordered SpMxV time), Table 3's definition"}
+            del xb_
         del xs_, ys_
 
     # ---------------- cuSPARSE comparator (informational): the
@@ -752,6 +796,7 @@ def main():
     ap.add_argument("--no-gather-peak", action="store_true")
     ap.add_argument("--no-reorder-ref", action="store_true", help="skip the scrambled-order reference timing")
     ap.add_argument("--no-cusparse", action="store_true", help="skip the cuSPARSE comparator timing")
+    ap.add_argument("--no-sbfs", action="store_true", help="skip the GPU sBFS ordering (f4) timing")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--parity-rows", type=int, default=200000)
     ap.add_argument("--e2e-steps", type=int, default=10)

@@ -263,6 +263,45 @@ spmv_status_t spmv_maxabs(spmv_handle_t h, double* m_dev, void* stream);
 spmv_status_t spmv_normalize(spmv_handle_t h, const double* y, const double* m_dev,
                              double* x_next, void* stream);
 
+/* ---------------------------------------------------------------------- */
+/* Producing the reordering.                               */
+
+/* spmv_order_sbfs -- the sBFS ordering of P:L134 (section 5.1: BFS on the
+ * bipartite graph of A, whose row and column visiting orders give the row
+ * and column reorderings) computed on the current CUDA device, followed by
+ * the extraction of a K-way SB form (Eq.(1)), so the outputs feed
+ * spmv_create directly (kind SPMV_SB).  Definition (reading R5):
+ *   - the BFS root is the lowest-numbered unvisited row; a visited vertex
+ *     enqueues its unvisited neighbours in ascending number; when the queue
+ *     empties the next root is the lowest unvisited row; columns no row
+ *     touches are numbered last, ascending;
+ *   - new row r joins block min(K-1, floor(K * P(r) / nnz)), P(r) = stored
+ *     entries of the rows numbered below r (rows split by nonzeros);
+ *   - a column all of whose rows lie in block k is interior to block k;
+ *     every other column (two or more blocks, or none) is a border column;
+ *     columns are numbered block by block, then C_B, each in BFS order.
+ * Arguments (all HOST arrays; synchronous; the device work is this call's):
+ *   m, n, nnz, row_ptr[m+1] (int64), col_idx[nnz]: the ORIGINAL-space CSR
+ *     (rows need not be sorted; validated: DATA on a bad row_ptr / column);
+ *   K >= 1: number of SB diagonal blocks;
+ *   row_perm[m], col_perm[n]: receive the old->new permutations (A1);
+ *   row_block_ptr[K+2], col_block_ptr[K+2]: receive the block descriptor in
+ *     permuted space (R_B empty; [col_block_ptr[K], n) is C_B);
+ *   info: optional timings and statistics (NULL allowed).
+ * Errors: USAGE (bad arguments), DATA (invalid CSR), UNSUPPORTED (m or n
+ * beyond int32), INTERNAL (CUDA / out of device memory). */
+typedef struct {
+    double bfs_ms;           /* device time of the CSC build and the BFS (CUDA events) */
+    double extract_ms;       /* device time of the SB extraction */
+    int64_t levels;          /* BFS levels expanded (row and column levels) */
+    int64_t components;      /* BFS roots with entries */
+    int64_t border_cols;     /* |C_B| of the extracted SB form */
+} spmv_order_info_t;
+
+spmv_status_t spmv_order_sbfs(int64_t m, int64_t n, int64_t nnz, const int64_t* row_ptr, const int32_t* col_idx,
+                              int32_t K, int32_t* row_perm, int32_t* col_perm,
+                              int64_t* row_block_ptr, int64_t* col_block_ptr, spmv_order_info_t* info);
+
 /* Writes a fresh 128-byte NCCL unique id into out (len >= 128). */
 spmv_status_t spmv_nccl_unique_id(void* out, size_t len);
 

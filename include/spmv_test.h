@@ -27,11 +27,12 @@ spmv_status_t spmv_debug_copy_csr(spmv_handle_t h, int64_t* row_ptr, int32_t* co
  * about rows_target rows, decodes the groups again and compares them with the
  * CSR bit for bit, checking that no row repeats within an epoch, that groups
  * never mix interior and border columns, that border groups come last and
- * that every panel fits shared memory.  stats[10] = panels, groups, padding
+ * that every panel fits shared memory.  stats[11] = panels, groups, padding
  * slots, deferred nonzeros, epochs, nonzeros packed, 1000 x the mean predicted
  * shared-memory wavefronts of a group's y access with natural / bank-coloured
  * y slots, the largest panel's shared memory bytes, panels with border
- * groups.  OK on an exact round trip; INTERNAL otherwise. */
+ * groups, distinct 32-byte x sectors over all groups' gathers.  OK on an
+ * exact round trip; INTERNAL otherwise. */
 spmv_status_t spmv_pn_plan_check(int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
                                  const spmv_blocks_t* blocks, int64_t rows_target, int64_t* stats);
 
@@ -67,6 +68,15 @@ spmv_status_t spmv_test_create_rank(int64_t m, int64_t n, int64_t nnz, const int
  * rank of that world or the ranks disagree; UNSUPPORTED without stream
  * memory operations. */
 spmv_status_t spmv_test_loopback_link(spmv_handle_t* handles, int32_t world);
+
+/* The apply stream of a linked loopback test rank (created by
+ * spmv_test_loopback_link right after the rank's comm stream, so the ranks'
+ * streams do not share the GPU's hardware work queues when
+ * CUDA_DEVICE_MAX_CONNECTIONS >= 2 * world): a rank's apply blocks its stream
+ * until the peers' pushes land, and a peer's push queued behind that wait on
+ * a shared queue would never run.  USAGE for a handle that is not a linked
+ * test rank. */
+spmv_status_t spmv_test_rank_stream(spmv_handle_t h, void** stream);
 
 #ifdef __cplusplus
 }

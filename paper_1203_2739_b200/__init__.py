@@ -10,7 +10,8 @@ importing the binding's entry points raises.
 Names follow the ABI: ``spmv_create`` (-> ``spmv_create_ex``), ``spmv_apply``,
 ``spmv_split_apply``, ``spmv_destroy`` plus the helpers ``spmv_get_info``,
 ``spmv_maxabs``, ``spmv_normalize``, ``spmv_shard_plan``,
-``spmv_nccl_unique_id``.  The test hooks of ``include/spmv_test.h`` are in
+``spmv_nccl_unique_id``, and ``spmv_order_sbfs`` (f4: the sBFS ordering + SB
+extraction that produces the permutations and blocks).  The test hooks of ``include/spmv_test.h`` are in
 ``paper_1203_2739_b200.testing``; the measurement microkernels
 (``include/spmv_diag.h``, a separate library) in ``paper_1203_2739_b200.diag``.
 Vectors are CUDA float64 torch tensors (or raw device addresses); the stream
@@ -36,10 +37,10 @@ SPMV_SPLIT_LITERAL = 4
 
 EXPORTED = ["spmv_create", "spmv_create_ex", "spmv_apply", "spmv_split_apply", "spmv_destroy", "spmv_get_info",
             "spmv_maxabs", "spmv_normalize", "spmv_nccl_unique_id", "spmv_status_string", "spmv_last_error",
-            "spmv_version", "spmv_shard_plan"]
+            "spmv_version", "spmv_shard_plan", "spmv_order_sbfs"]
 # include/spmv_test.h (test and debug hooks, same library)
 EXPORTED_TEST = ["spmv_debug_copy_csr", "spmv_pn_plan_check", "spmv_pn_shard_hash", "spmv_test_create_rank",
-                 "spmv_test_loopback_link"]
+                 "spmv_test_loopback_link", "spmv_test_rank_stream"]
 
 KERNELS = {"auto": 0, "panel": 1, "rowtile": 2}
 SPLIT_KERNELS = {"auto": 0, "panel": 1, "rows": 2}
@@ -84,6 +85,11 @@ class spmv_info_t(ctypes.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class spmv_order_info_t(ctypes.Structure):
+    _fields_ = [("bfs_ms", ctypes.c_double), ("extract_ms", ctypes.c_double), ("levels", ctypes.c_int64),
+                ("components", ctypes.c_int64), ("border_cols", ctypes.c_int64)]
+
+
 _lib = None
 
 
@@ -111,11 +117,13 @@ def lib():
         L.spmv_last_error.argtypes = []
         L.spmv_last_error.restype = ctypes.c_char_p
         L.spmv_version.restype = i32
+        L.spmv_order_sbfs.argtypes = [i64, i64, i64, vp, vp, i32, vp, vp, vp, vp, ctypes.POINTER(spmv_order_info_t)]
         L.spmv_debug_copy_csr.argtypes = [vp, vp, vp, vp]
         L.spmv_pn_plan_check.argtypes = [i64, i64, vp, vp, vp, vp, i64, vp]
         L.spmv_pn_shard_hash.argtypes = [i64, i64, vp, vp, vp, vp, i32, i32, vp]
         L.spmv_test_create_rank.argtypes = [i64, i64, i64, vp, vp, vp, vp, vp, vp, i32, vp, vp, vp, ctypes.POINTER(vp)]
         L.spmv_test_loopback_link.argtypes = [vp, i32]
+        L.spmv_test_rank_stream.argtypes = [vp, vp]
         for name in EXPORTED_TEST:
             getattr(L, name).restype = i32
         for name in EXPORTED:
@@ -327,3 +335,22 @@ def spmv_status_string(s: int) -> str:
 
 def spmv_version() -> int:
     return int(lib().spmv_version())
+
+
+def spmv_order_sbfs(m: int, n: int, row_ptr, col, K: int) -> dict:
+    """sBFS ordering + SB extraction on the current CUDA device (f4).
+    Host CSR in, host permutations (old -> new) and an SB block descriptor out
+    (``blocks`` is ready for ``spmv_create``), plus the device timings."""
+    rp = _np(row_ptr, np.int64)
+    ci = _np(col, np.int32)
+    rperm = np.empty(m, np.int32)
+    cperm = np.empty(n, np.int32)
+    rbp = np.empty(K + 2, np.int64)
+    cbp = np.empty(K + 2, np.int64)
+    info = spmv_order_info_t()
+    _check(lib().spmv_order_sbfs(m, n, int(rp[-1]), _addr(rp), _addr(ci), K, _addr(rperm), _addr(cperm),
+                                 _addr(rbp), _addr(cbp), ctypes.byref(info)), "spmv_order_sbfs")
+    return {"row_perm": rperm, "col_perm": cperm, "row_block_ptr": rbp, "col_block_ptr": cbp,
+            "blocks": {"kind": SPMV_SB, "K": K, "row_block_ptr": rbp, "col_block_ptr": cbp},
+            "bfs_ms": info.bfs_ms, "extract_ms": info.extract_ms, "levels": info.levels,
+            "components": info.components, "border_cols": info.border_cols}

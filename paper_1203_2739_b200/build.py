@@ -36,6 +36,7 @@ SOURCES = {
     "rowtile.cu": "cu",
     "split.cu": "cu",
     "panel.cu": "cu",
+    "order.cu": "cu",
     "plan_panel.cpp": "cpp",
     "host.cpp": "cpp",
     "exchange.cpp": "cpp",
@@ -62,6 +63,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     inc = ["-I" + CSRC, "-I" + os.path.join(ROOT, "include"), "-I" + os.path.join(nccl, "include"),
            "-I" + os.path.join(CUDA, "include")]
     hdrs = [os.path.join(CSRC, h) for h in HEADERS]
+    # build-time experiments only (e.g. "-DSPMV_PN_PEND=64"); the library reads no environment at run time
+    defs = os.environ.get("SPMV_BUILD_DEFS", "").split()
     objs = []
     for src, kind in SOURCES.items():
         s = os.path.join(CSRC, src)
@@ -71,10 +74,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
             continue
         if kind == "cu":
             cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-                   "--expt-relaxed-constexpr", "-Xptxas", "-v", "-c", s, "-o", o, *inc]
+                   "--expt-relaxed-constexpr", "-Xptxas", "-v", "-c", s, "-o", o, *inc, *defs]
         else:
             cmd = ["g++", "-O2", "-std=c++17", "-fPIC", "-fopenmp", "-Wall", "-Wno-unused-function",
-                   "-c", s, "-o", o, *inc]
+                   "-c", s, "-o", o, *inc, *defs]
         if verbose:
             print(" ".join(cmd), flush=True)
         r = subprocess.run(cmd, capture_output=True, text=True)

@@ -267,14 +267,32 @@ spmv_status_t xchg_loopback_link(spmv_plan_s** hs, int world) {
             h->xb.bytes != hs[0]->xb.bytes)
             return fail(SPMV_ERR_USAGE, "loopback_link: handle %d is not test rank %d of world %d", r, r, world);
     }
+    // On one GPU every rank's streams share the device's hardware work
+    // queues; a stream blocked in a wait on a peer's flag (DB: the fold waits
+    // for the peers' temporaries) would also block whatever else sits in its
+    // queue -- possibly the very push it waits for.  Streams are assigned to
+    // the queues round-robin in creation order, so each rank's comm stream
+    // and an apply stream for the test (spmv_test_rank_stream) are created
+    // here back to back: with CUDA_DEVICE_MAX_CONNECTIONS >= 2 * world they
+    // get queues of their own (on a real multi-GPU run each rank has its own
+    // device and no such aliasing exists).
     for (int r = 0; r < world; ++r) {
         spmv_plan_s* h = hs[r];
         DeviceGuard g(h->device);
         h->peer.assign(world, XBufs{});
         for (int q = 0; q < world; ++q) h->peer[q] = hs[q]->xb;
         h->xmode = kXLoopback;
+        if (h->comm_stream) {
+            cudaStreamDestroy(h->comm_stream);
+            h->comm_stream = nullptr;
+        }
+        if (h->test_stream) {
+            cudaStreamDestroy(h->test_stream);
+            h->test_stream = nullptr;
+        }
         spmv_status_t s = make_streams(h);
         if (s) return s;
+        CUDA_TRY(cudaStreamCreateWithFlags(&h->test_stream, cudaStreamNonBlocking));
     }
     return SPMV_OK;
 }
@@ -404,6 +422,8 @@ void xchg_release(spmv_plan_s* h) {
     for (void* p : h->ipc_opened) cudaIpcCloseMemHandle(p);
     h->ipc_opened.clear();
     if (h->comm_stream) cudaStreamDestroy(h->comm_stream);
+    if (h->test_stream) cudaStreamDestroy(h->test_stream);
+    h->test_stream = nullptr;
     if (h->ev_x) cudaEventDestroy(h->ev_x);
     if (h->ev_comm) cudaEventDestroy(h->ev_comm);
     if (h->ev_kernel) cudaEventDestroy(h->ev_kernel);

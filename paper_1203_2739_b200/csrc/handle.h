@@ -160,6 +160,7 @@ struct spmv_plan_s {
     ncclComm_t comm = nullptr;
     bool test_rank = false;           // created by spmv_test_create_rank (no communicator)
     cudaStream_t comm_stream = nullptr;
+    cudaStream_t test_stream = nullptr;   // loopback test ranks: the apply stream the test uses (own queue)
     cudaEvent_t ev_x = nullptr, ev_comm = nullptr, ev_kernel = nullptr;
     int32_t seq = 0;                  // applies issued (all ranks issue the same sequence)
     std::vector<int64_t> bord_off, bord_cnt;   // per rank: owned C_B slice (offset inside C_B, length)

@@ -292,8 +292,8 @@ spmv_status_t plan_pn(spmv_plan_s* h, PanelPlan& pl, const std::vector<int64_t>&
     pl.max_rows = max_rows;
     pl.max_sslots = max_ss;
     pl.max_split_n = max_sn;
-    // padding lanes: the planner's dummy index becomes the scratch y slot
-    // max_rows (delta 0: a valid x read, times the value 0)
+    // padding lanes: the planner's dummy index of bank b becomes the scratch
+    // y slot max_rows + b (delta 0: a valid x read, times the value 0)
     const uint32_t dummy_dev = (uint32_t)pl.max_rows << kPnDeltaBits;
     std::vector<double> tv;
     std::vector<uint32_t> ti;
@@ -313,7 +313,7 @@ spmv_status_t plan_pn(spmv_plan_s* h, PanelPlan& pl, const std::vector<int64_t>&
                 for (int l = 0; l < 32; ++l) {
                     tv[blk + (b / 2) * 64 + l * 2 + (b & 1)] = D.gval[g * 32 + l];
                     const uint32_t i = D.gidx[g * 32 + l];
-                    ti[blk + l * 4 + b] = i == kPnDummy ? dummy_dev : i;
+                    ti[blk + l * 4 + b] = pn_is_dummy(i) ? dummy_dev + (((i >> kPnDeltaBits) - kPnDummyRow) << kPnDeltaBits) : i;
                 }
             }
             CUDA_TRY(cudaMemcpy(pl.d_gval + g0 * 32, tv.data(), ng * 32 * 8, cudaMemcpyHostToDevice));

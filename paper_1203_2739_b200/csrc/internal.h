@@ -89,7 +89,10 @@ int kernel_num_sms();   // SMs of the current device
 // epochs of kPnB groups per warp; the rows of an epoch are distinct, so the
 // shared-memory y updates of one epoch never race, and a CTA barrier
 // separates epochs.
-constexpr int kPnWarps = 16;                 // warps per panel CTA
+#ifndef SPMV_PN_WARPS
+#define SPMV_PN_WARPS 16
+#endif
+constexpr int kPnWarps = SPMV_PN_WARPS;      // warps per panel CTA
 constexpr int kPnB = 4;                      // groups per warp per epoch (4 beat 8)
 constexpr int kPnEpoch = kPnWarps * kPnB;    // groups per epoch
 constexpr int kPnPadGroups = 4 * kPnEpoch;  // zero groups after the stream (ring read-ahead, <= 16 steps)
@@ -98,8 +101,14 @@ constexpr int kPnRowsTarget = 16384;         // default panel size: 128 KB of y,
                                              // 256 KB L1/shared array stays L1 (measured best, §5.3)
 constexpr int kPnRowBits = 15;               // idx = (row_in_panel << 17) | (col - group base)
 constexpr int kPnDeltaBits = 17;
-constexpr uint32_t kPnDummy = 0xFFFE0000u;   // row field 0x7FFF (-> scratch y slot), delta 0 (a valid x
-                                             // address): padding lanes run the same code branch-free
+// Padding lanes run the same code branch-free: their index holds delta 0 (a
+// valid x address, times the value 0) and a row field 0x7FF0 + b, which the
+// upload maps to scratch y slot max_rows + b -- the planner picks b among the
+// 8-byte banks its half-warp leaves free, so padding never adds a y bank
+// conflict.
+constexpr uint32_t kPnDummyRow = 0x7FF0;
+constexpr uint32_t pn_dummy(int bank) { return (kPnDummyRow + (uint32_t)bank) << 17; }
+constexpr bool pn_is_dummy(uint32_t i) { return (i >> 17) >= kPnDummyRow; }
 
 struct PnPanel {
     int32_t row0;      // first local row
@@ -119,6 +128,11 @@ struct PnPanel {
                        // exchange overlaps epochs [0, bepoch) (a4)
 };
 constexpr int kPnFoldSeq = 32;               // virtual rows a thread folds sequentially
+#ifndef SPMV_PN_PEND
+#define SPMV_PN_PEND 32
+#endif
+constexpr int kPnPend = SPMV_PN_PEND;        // planner: bank-blocked nonzeros an epoch keeps pending before
+                                             // it closes a group early (y bank conflicts vs padding)
 constexpr int kPnSplitAt = 32;               // a row with more nonzeros is split into interleaved
 constexpr int kPnVMax = 32;                  // virtual rows of <= kPnVMax nonzeros (own y slots,
                                              // folded in order in the epilogue)
@@ -134,8 +148,8 @@ struct PnArgs {
     const double* x_hi;
     double* y;
     unsigned long long* maxabs_slots;
-    int32_t max_rows;         // largest panel's y slots (a multiple of 16); slot max_rows is the padding
-                              // lanes' scratch; shared memory = 8 * (max_rows + 1) bytes (the rest stays L1)
+    int32_t max_rows;         // largest panel's y slots (a multiple of 16); slots max_rows + 0..15 are the
+                              // padding lanes' scratch (one per bank); shared memory = panel_smem_bytes
     const uint16_t* row2slot; // [local rows] y slot of each row within its panel (bank colouring), or
                               // 0x8000 | k: row split into virtual rows, see split_*
     const int32_t* split_first;   // [split rows] first entry in split_slots (absolute)
@@ -158,12 +172,12 @@ struct PnArgs {
     int32_t* err;
 };
 // Dynamic shared memory of a panel CTA: its y slots (+ the padding lanes'
-// scratch slot), the split rows' slot lists (u16) and their (first, count,
+// 16 scratch slots), the split rows' slot lists (u16) and their (first, count,
 // row) descriptors.  The planner caps every panel at kPnSmemMax (ADVICE r1:
 // split rows add bytes beyond the slots) and the launch re-checks it.
 constexpr int64_t kPnSmemMax = 227 * 1024;
 inline int64_t panel_smem_bytes(int64_t slots16, int64_t sslots, int64_t split_n) {
-    return (slots16 + 1) * 8 + ((sslots + 7) & ~int64_t(7)) * 2 + split_n * 12;
+    return (slots16 + 16) * 8 + ((sslots + 7) & ~int64_t(7)) * 2 + split_n * 12;
 }
 cudaError_t launch_panel(const PnArgs& a, cudaStream_t s);
 

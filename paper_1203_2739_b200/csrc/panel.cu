@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
         for (int i = tid; i < ((d.nslots + 15) & ~15); i += kT) ys[i] = 0.0;   // the panel's y slots
         // virtual-row slot lists of the panel's split rows, copied to shared memory
         // once (the epilogue folds them)
-        uint16_t* ssl = reinterpret_cast<uint16_t*>(ys + A.max_rows + 1);
+        uint16_t* ssl = reinterpret_cast<uint16_t*>(ys + A.max_rows + 16);
         int32_t* sdesc = reinterpret_cast<int32_t*>(ssl + ((A.max_sslots + 7) & ~7));   // (first, count, row) per split row
         for (int i = tid; i < d.sslot_n; i += kT) ssl[i] = A.split_slots[d.sslot0 + i];
         for (int i = tid; i < d.split_n; i += kT) {

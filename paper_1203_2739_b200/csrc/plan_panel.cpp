@@ -101,6 +101,21 @@ void colour_slots(int32_t nr, const std::vector<Ent>& ents, int64_t G, std::vect
         rs ^= rs << 13; rs ^= rs >> 7; rs ^= rs << 17;
         return rs;
     };
+#ifndef SPMV_PN_WPOW
+#define SPMV_PN_WPOW 3
+#endif
+#ifndef SPMV_PN_SWEEPS
+#define SPMV_PN_SWEEPS 2
+#endif
+#ifndef SPMV_PN_TRIES
+#define SPMV_PN_TRIES 3
+#endif
+    int64_t W[34];
+    for (int c = 0; c < 34; ++c) {
+        int64_t v = 1;
+        for (int k = 0; k < SPMV_PN_WPOW; ++k) v *= c;
+        W[c] = v;
+    }
     auto gain_move = [&](int32_t r, int b1, int b2, int32_t other) {
         // cost change of moving r from b1 to b2 (groups also holding `other` are skipped: swapped pair cancels)
         int64_t d = 0;
@@ -110,7 +125,7 @@ void colour_slots(int32_t nr, const std::vector<Ent>& ents, int64_t G, std::vect
             for (int32_t u = rg_ptr[other]; u < rg_ptr[other + 1]; ++u)
                 if (rg[u] == g) { both = true; break; }
             if (both) continue;
-            d += 2 * ((int)cnt[g * 16 + b2] - (int)cnt[g * 16 + b1] + 1);
+            d += W[cnt[g * 16 + b2] + 1] - W[cnt[g * 16 + b2]] + W[cnt[g * 16 + b1] - 1] - W[cnt[g * 16 + b1]];
         }
         return d;
     };
@@ -121,7 +136,7 @@ void colour_slots(int32_t nr, const std::vector<Ent>& ents, int64_t G, std::vect
             cnt[g * 16 + b2]++;
         }
     };
-    constexpr int kSweeps = 2, kTries = 3;
+    constexpr int kSweeps = SPMV_PN_SWEEPS, kTries = SPMV_PN_TRIES;
     for (int sw = 0; sw < kSweeps; ++sw)
         for (int32_t i = 0; i < nr; ++i) {
             const int32_t r = (int32_t)((i * 40503ull + sw * 7919ull) % (uint64_t)nr);   // fixed visiting order
@@ -156,37 +171,89 @@ void colour_slots(int32_t nr, const std::vector<Ent>& ents, int64_t G, std::vect
     }
 }
 
-// Predicted wavefronts of one warp-wide 64-bit y access for a group whose
-// lanes were assigned by emit_group (sum over the half-warps of the largest
-// bank multiplicity).
+// Predicted wavefronts of one warp-wide 64-bit y access of a packed group: a
+// 64-bit shared-memory access is served per half-warp, one wavefront per
+// distinct address in the most loaded 8-byte bank (slot mod 16; lanes on the
+// same address merge -- the padding lanes of a half share one scratch slot).
 double y_wavefronts(const uint32_t* idx) {
     double w = 0;
     for (int h = 0; h < 2; ++h) {
         int c[16] = {0}, m = 0;
-        for (int l = h * 16; l < h * 16 + 16; ++l)
-            if (idx[l] != kPnDummy) m = std::max(m, ++c[(idx[l] >> kPnDeltaBits) & 15]);
+        bool dummy[16] = {};
+        for (int l = h * 16; l < h * 16 + 16; ++l) {
+            const uint32_t r = idx[l] >> kPnDeltaBits;
+            if (pn_is_dummy(idx[l])) {
+                const int b = (int)(r - kPnDummyRow);
+                if (!dummy[b]) m = std::max(m, ++c[b]);
+                dummy[b] = true;
+            } else {
+                m = std::max(m, ++c[r & 15]);
+            }
+        }
         w += std::max(m, 1);
     }
     return w;
 }
 
-// lanes: entries sorted by slot bank alternate between the half-warps
+// Lanes of a group: with c_b entries in bank b (slot mod 16), half-warp 0
+// takes a_b of them and half 1 the rest, each half at most 16 lanes, chosen
+// to minimise max_b a_b + max_b (c_b - a_b) -- the access's wavefronts (an
+// alternating split pays 4 for two banks of 3 entries, this one 3).  Each
+// half's padding lanes share the scratch slot of its least loaded bank.
 void emit_group(const Ent* e, int32_t base, const std::vector<int32_t>& slot, PnPanelData& P) {
-    Ent s[32];
-    int n = 0;
+    int c[16] = {0}, n = 0, m = 0;
+    const Ent* byb[16][32];
     for (int k = 0; k < 32; ++k)
-        if (e[k].row >= 0) s[n++] = e[k];
-    std::stable_sort(s, s + n, [&](const Ent& a, const Ent& b) { return (slot[a.row] & 15) < (slot[b.row] & 15); });
+        if (e[k].row >= 0) {
+            const int b = slot[e[k].row] & 15;
+            byb[b][c[b]++] = &e[k];
+            m = std::max(m, c[b]);
+            ++n;
+        }
+    int a[16] = {0};
+    bool found = false;
+    for (int S = m; S <= 2 * m + 2 && !found; ++S)
+        for (int T0 = (S + 1) / 2; T0 <= S && !found; ++T0) {
+            const int T1 = S - T0;
+            int lo_s = 0, hi_s = 0;
+            bool ok = true;
+            for (int b = 0; b < 16 && ok; ++b) {
+                const int lo = std::max(0, c[b] - T1), hi = std::min(c[b], T0);
+                ok = lo <= hi;
+                lo_s += lo;
+                hi_s += hi;
+            }
+            if (!ok || lo_s > 16 || hi_s < n - 16) continue;
+            int tot = 0;
+            for (int b = 0; b < 16; ++b) tot += (a[b] = std::max(0, c[b] - T1));
+            for (int b = 0; b < 16 && tot < n - 16; ++b) {
+                const int add = std::min(std::min(c[b], T0) - a[b], n - 16 - tot);
+                a[b] += add;
+                tot += add;
+            }
+            found = true;
+        }
     uint32_t idx[32];
     double val[32];
-    for (int l = 0; l < 32; ++l) {
-        idx[l] = kPnDummy;
-        val[l] = 0.0;
-    }
-    for (int k = 0; k < n; ++k) {
-        const int lane = (k & 1) * 16 + (k >> 1);
-        idx[lane] = ((uint32_t)slot[s[k].row] << kPnDeltaBits) | (uint32_t)(s[k].col - base);
-        val[lane] = s[k].v;
+    int nh[2] = {0, 0}, load[2][16] = {};
+    for (int b = 0; b < 16; ++b)
+        for (int j = 0; j < c[b]; ++j) {
+            const int h = j < a[b] ? 0 : 1;
+            const Ent& x = *byb[b][j];
+            const int lane = h * 16 + nh[h]++;
+            idx[lane] = ((uint32_t)slot[x.row] << kPnDeltaBits) | (uint32_t)(x.col - base);
+            val[lane] = x.v;
+            ++load[h][b];
+        }
+    for (int h = 0; h < 2; ++h) {
+        int bmin = 0;
+        for (int b = 1; b < 16; ++b)
+            if (load[h][b] < load[h][bmin]) bmin = b;
+        while (nh[h] < 16) {
+            const int lane = h * 16 + nh[h]++;
+            idx[lane] = pn_dummy(bmin);
+            val[lane] = 0.0;
+        }
     }
     P.gval.insert(P.gval.end(), val, val + 32);
     P.gidx.insert(P.gidx.end(), idx, idx + 32);
@@ -445,7 +512,7 @@ bool plan_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col,
         // epilogue's fold lists); a panel never exceeds kPnSmemMax, whatever
         // the cut mode (rows of 33-64 nonzeros need ~16 B per slot)
         auto smem_of = [](int64_t s) -> int64_t { return 8 * s + (s > 1 ? 2 * s + 12 : 0); };
-        const int64_t smem_cap = kPnSmemMax - 8 * 16 - 8 - 16;   // slack for the rounding of slots / lists
+        const int64_t smem_cap = kPnSmemMax - 8 * 16 - 8 * 16 - 16;   // slack: rounding of slots / lists, scratch slots
         auto make_cuts = [&](bool by_bytes) {
             std::vector<int64_t> cut(1, rg.first);
             const int64_t tot = by_bytes ? C : S;
@@ -626,7 +693,7 @@ bool verify_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& co
                 for (int l = 0; l < 32; ++l) {
                     const uint32_t i = P.gidx[g * 32 + l];
                     const double v = P.gval[g * 32 + l];
-                    if (i == kPnDummy) {
+                    if (pn_is_dummy(i)) {
                         if (v != 0.0) e = "dummy slot with a value";
                         continue;
                     }

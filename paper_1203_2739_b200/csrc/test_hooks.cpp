@@ -70,7 +70,7 @@ spmv_status_t spmv_pn_plan_check(int64_t m, int64_t n, const int64_t* row_ptr, c
         stats[0] = st.panels; stats[1] = st.groups; stats[2] = st.pads;
         stats[3] = st.deferred; stats[4] = st.epochs; stats[5] = st.entries;
         stats[6] = (int64_t)(st.ywf0 * 1000.0); stats[7] = (int64_t)(st.ywf1 * 1000.0);
-        stats[8] = smax; stats[9] = with_border;
+        stats[8] = smax; stats[9] = with_border; stats[10] = st.gsectors;
         if (st.entries != nnz) return fail(SPMV_ERR_INTERNAL, "pn_plan_check: plan holds %lld of %lld nonzeros",
                                            (long long)st.entries, (long long)nnz);
         if (smax > kPnSmemMax) return fail(SPMV_ERR_INTERNAL, "pn_plan_check: a panel needs %lld B of shared memory",
@@ -152,7 +152,7 @@ spmv_status_t spmv_pn_shard_hash(int64_t m, int64_t n, const int64_t* row_ptr, c
                 for (int64_t g = 0; g < G; ++g)
                     for (int l = 0; l < 32; ++l) {
                         const uint32_t i = P.gidx[g * 32 + l];
-                        if (i == kPnDummy) continue;
+                        if (pn_is_dummy(i)) continue;
                         const int32_t sl = (int32_t)(i >> kPnDeltaBits);
                         const int64_t lc = (int64_t)P.gbase[g] + (i & ((1u << kPnDeltaBits) - 1));
                         int64_t gc = lc;
@@ -186,6 +186,13 @@ spmv_status_t spmv_test_create_rank(int64_t m, int64_t n, int64_t nnz, const int
 spmv_status_t spmv_test_loopback_link(spmv_handle_t* handles, int32_t world) {
     if (!handles || world < 2) return fail(SPMV_ERR_USAGE, "loopback_link: bad arguments");
     return xchg_loopback_link(handles, world);
+}
+
+spmv_status_t spmv_test_rank_stream(spmv_handle_t h, void** stream) {
+    if (!valid(h) || !stream) return fail(SPMV_ERR_USAGE, "rank_stream: bad arguments");
+    if (!h->test_rank || !h->test_stream) return fail(SPMV_ERR_USAGE, "rank_stream: not a linked test rank");
+    *stream = (void*)h->test_stream;
+    return SPMV_OK;
 }
 
 }  // extern "C"

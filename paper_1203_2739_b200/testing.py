@@ -32,7 +32,7 @@ def pn_plan_check(m: int, n: int, row_ptr, col, val, blocks, rows_target: int) -
     va = _np(val, np.float64)
     keep = []
     bptr = _blocks_struct(blocks, keep)
-    stats = np.zeros(10, dtype=np.int64)
+    stats = np.zeros(11, dtype=np.int64)
     _check(lib().spmv_pn_plan_check(m, n, _addr(rp), _addr(ci), _addr(va), bptr, rows_target, stats.ctypes.data),
            "spmv_pn_plan_check")
     d = dict(zip(("panels", "groups", "pads", "deferred", "epochs", "entries"), (int(v) for v in stats[:6])))
@@ -40,6 +40,7 @@ def pn_plan_check(m: int, n: int, row_ptr, col, val, blocks, rows_target: int) -
     d["y_wavefronts_coloured"] = stats[7] / 1000.0
     d["smem_max"] = int(stats[8])
     d["panels_with_border"] = int(stats[9])
+    d["gather_sectors"] = int(stats[10])
     return d
 
 
@@ -71,3 +72,11 @@ def loopback_link(handles) -> None:
     """Link test ranks 0..G-1 (in order) into one loopback group (P2P protocol on one GPU)."""
     arr = (ctypes.c_void_p * len(handles))(*[_h(h).value for h in handles])
     _check(lib().spmv_test_loopback_link(arr, len(handles)), "spmv_test_loopback_link")
+
+
+def rank_stream(h):
+    """The apply stream of a linked loopback test rank, as a torch.cuda.ExternalStream."""
+    import torch
+    out = ctypes.c_void_p(0)
+    _check(lib().spmv_test_rank_stream(_h(h), ctypes.byref(out)), "spmv_test_rank_stream")
+    return torch.cuda.ExternalStream(out.value)

@@ -202,7 +202,7 @@ def test_split_with_permutation():
 # ------------------------------------------------ power iteration glue (a9)
 def _c5_like(seed=3):
     """Two C5-shaped SB blocks (identity perms) at the production panel size."""
-    synth.PRESETS["_c5like_pi"] = lambda **kw: synth._sb(2, 40_000, 39_200, 400, 12, 20, 0, 3, **kw)
+    synth.PRESETS["_c5like_pi"] = lambda **kw: synth._sb(2, 40_000, 39_200, 800, 12, 20, 0, 3, **kw)
     return synth.make("_c5like_pi", scramble=0, seed=seed)
 
 

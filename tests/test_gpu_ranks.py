@@ -66,7 +66,7 @@ def y_rows(info):
 
 def apply_ranks(hs, infos, xls, split=False, flags=0):
     """One apply per rank, each on its own stream (as on its own GPU)."""
-    streams = [torch.cuda.Stream() for _ in hs]
+    streams = [T.rank_stream(h) for h in hs]   # each rank's own hardware queue (spmv_test_rank_stream)
     ys = []
     for h, i, xl, s in zip(hs, infos, xls, streams):
         xd = xl if torch.is_tensor(xl) else torch.from_numpy(np.ascontiguousarray(xl)).cuda()
@@ -248,7 +248,7 @@ def test_exchange_overlaps_interior():
     x = p.x()
     xl = [torch.from_numpy(x_local(x, i)).cuda() for i in infos]
     ys = [torch.empty(i["y_local_len"], dtype=torch.float64, device="cuda") for i in infos]
-    s0, s1 = torch.cuda.Stream(), torch.cuda.Stream()
+    s0, s1 = T.rank_stream(hs[0]), T.rank_stream(hs[1])
     ev = lambda: torch.cuda.Event(enable_timing=True)   # noqa: E731
 
     def both(delay_s):
