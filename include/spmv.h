@@ -125,7 +125,11 @@ typedef struct {
                                 overlapped with the interior epochs of the kernel (a4, f2).  NCCL:
                                 ncclAllGather / grouped send-recv on a comm stream, joined before
                                 the kernel */
-    int32_t reserved[11];
+    int32_t index16;         /* f3 (ICSR-style index compression): AUTO (0) = row-tile handles
+                                stream 16-bit tile-local column ids (10 B per nonzero instead of 12)
+                                whenever every row tile's columns fit two 65,536-id windows (an SB
+                                block tile: C_k and C_B, Eq.(1)); 1 = off (32-bit ids) */
+    int32_t reserved[10];
 } spmv_options_t;
 
 /* spmv_create -- ingest, validate, permute and plan (once; not per SpMxV).
@@ -226,6 +230,8 @@ typedef struct {
     int64_t y_wavefronts_x1000;   /* panel kernel: predicted shared-memory wavefronts per y access x 1000 */
     int64_t exchange_timeouts;    /* world > 1 P2P: device-side flag waits that timed out (should be 0;
                                      reading it synchronises the device) */
+    int64_t index_bytes;          /* row-tile kernel: bytes per column id it streams (2 with the f3
+                                     16-bit tile-local ids, else 4) */
 } spmv_info_t;
 
 spmv_status_t spmv_get_info(spmv_handle_t h, spmv_info_t* info);

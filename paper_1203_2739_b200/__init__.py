@@ -61,8 +61,8 @@ class _Blocks(ctypes.Structure):
 
 class _Options(ctypes.Structure):
     _fields_ = [("struct_size", ctypes.c_int32), ("kernel", ctypes.c_int32), ("panel_rows", ctypes.c_int32),
-                ("split_kernel", ctypes.c_int32), ("exchange", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 11)]
+                ("split_kernel", ctypes.c_int32), ("exchange", ctypes.c_int32), ("index16", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 10)]
 
 
 class _Dist(ctypes.Structure):
@@ -79,7 +79,7 @@ class spmv_info_t(ctypes.Structure):
         (k, ctypes.c_int32) for k in ("n_parts", "rank", "world", "kind", "has_owner_map", "kernel",
                                       "split_kernel", "exchange")] + [
         (k, ctypes.c_int64) for k in ("gather_sectors", "y_local_len", "y_border_begin", "y_border_len",
-                                      "deferred", "y_wavefronts_x1000", "exchange_timeouts")]
+                                      "deferred", "y_wavefronts_x1000", "exchange_timeouts", "index_bytes")]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -222,6 +222,10 @@ def _options_struct(options, keep):
     o.panel_rows = int(options.get("panel_rows", 0))
     o.split_kernel = SPLIT_KERNELS[options.get("split_kernel", "auto")]
     o.exchange = EXCHANGES[options.get("exchange", "auto")]
+    o.index16 = int(options.get("index16", 0))
+    unknown = set(options) - {"kernel", "panel_rows", "split_kernel", "exchange", "index16"}
+    if unknown:
+        raise ValueError(f"unknown spmv options: {sorted(unknown)}")
     keep.append(o)
     return ctypes.byref(o)
 

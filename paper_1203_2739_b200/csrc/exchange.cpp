@@ -20,6 +20,9 @@
 //     before its first border epoch (panel.cu) -- the exchange overlaps the
 //     interior compute.  A push of apply seq waits (stream wait-value) until
 //     the peer reported done >= seq - 2, i.e. finished reading that parity.
+//     DB: the temporaries are pushed the same way after the kernel, and the
+//     fold kernel waits for the peers' tready flags on the device (bounded),
+//     so no apply stream ever blocks on a peer's progress.
 //   * NCCL: in-place ncclAllGather (grouped broadcasts for unequal slices) and
 //     grouped send/recv of the temporaries, on the apply stream before / after
 //     the kernel (no overlap: an SpMxV kernel spinning on a flag could keep an
@@ -179,7 +182,18 @@ spmv_status_t xchg_alloc(spmv_plan_s* h) {
     if (s) return s;
     CUDA_TRY(cudaMemset(base, 0, L.bytes));
     h->xb = view_of(base, L);
+    void* hp = nullptr;
+    CUDA_TRY(cudaHostAlloc(&hp, 64, cudaHostAllocMapped));
+    h->xb.herr_host = static_cast<int32_t*>(hp);
+    *h->xb.herr_host = 0;
+    void* dp = nullptr;
+    CUDA_TRY(cudaHostGetDevicePointer(&dp, hp, 0));
+    h->xb.herr = static_cast<int32_t*>(dp);
     return SPMV_OK;
+}
+
+bool xchg_failed(const spmv_plan_s* h) {
+    return h->xb.herr_host && *reinterpret_cast<volatile int32_t*>(h->xb.herr_host) != 0;
 }
 
 spmv_status_t xchg_agree(spmv_plan_s* h, spmv_status_t local, spmv_status_t* agreed) {
@@ -347,6 +361,7 @@ spmv_status_t xchg_pre(spmv_plan_s* h, const double* x, cudaStream_t st, XView& 
     v.ready = h->xb.ready;
     v.seq = seq;
     v.err = h->xb.err;
+    v.herr = h->xb.herr;
     return SPMV_OK;
 }
 
@@ -366,7 +381,7 @@ spmv_status_t xchg_post(spmv_plan_s* h, double* y, unsigned long long* slots, cu
             if (h->t_recv_cnt[r]) NCCL_TRY(ncclRecv(tin + h->t_recv_off[r], h->t_recv_cnt[r], ncclFloat64, r, h->comm, st));
         }
         NCCL_TRY(ncclGroupEnd());
-        CUDA_TRY(launch_fold(tin, h->d_fold_ptr, h->d_fold_pos, y + h->m_blk, h->y_bord_len, slots, st));
+        CUDA_TRY(launch_fold(tin, h->d_fold_ptr, h->d_fold_pos, y + h->m_blk, h->y_bord_len, FoldWait{}, slots, st));
         return SPMV_OK;
     }
     const int32_t seq = h->seq;
@@ -391,9 +406,15 @@ spmv_status_t xchg_post(spmv_plan_s* h, double* y, unsigned long long* slots, cu
             if ((s = write_val(h->comm_stream, h->peer[r].tready + me, seq))) return s;
         }
         CUDA_TRY(cudaEventRecord(h->ev_comm, h->comm_stream));
-        for (int r = 0; r < h->world; ++r)
-            if (r != me && (s = wait_geq(st, h->xb.tready + r, seq))) return s;
-        CUDA_TRY(launch_fold(tin, h->d_fold_ptr, h->d_fold_pos, y + h->m_blk, h->y_bord_len, slots, st));
+        // the fold kernel waits for the peers' tready flags on the device
+        FoldWait fw;
+        fw.ready = h->xb.tready;
+        fw.world = h->world;
+        fw.self = me;
+        fw.seq = seq;
+        fw.err = h->xb.err;
+        fw.herr = h->xb.herr;
+        CUDA_TRY(launch_fold(tin, h->d_fold_ptr, h->d_fold_pos, y + h->m_blk, h->y_bord_len, fw, slots, st));
         for (int r = 0; r < h->world; ++r)
             if (r != me && (s = write_val(st, h->peer[r].tdone + me, seq))) return s;
     }
@@ -419,6 +440,8 @@ int64_t xchg_timeouts(spmv_plan_s* h) {
 }
 
 void xchg_release(spmv_plan_s* h) {
+    if (h->xb.herr_host) cudaFreeHost(h->xb.herr_host);
+    h->xb.herr_host = h->xb.herr = nullptr;
     for (void* p : h->ipc_opened) cudaIpcCloseMemHandle(p);
     h->ipc_opened.clear();
     if (h->comm_stream) cudaStreamDestroy(h->comm_stream);

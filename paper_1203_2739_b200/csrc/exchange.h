@@ -13,6 +13,7 @@ struct XView {
     const int32_t* ready = nullptr;
     int32_t seq = 0;
     int32_t* err = nullptr;
+    int32_t* herr = nullptr;   // host-mapped sticky flag (set on a timed-out wait)
 };
 
 spmv_status_t xchg_alloc(spmv_plan_s* h);                                        // create: buffers
@@ -22,6 +23,7 @@ spmv_status_t xchg_pre(spmv_plan_s* h, const double* x, cudaStream_t st, XView& 
 spmv_status_t xchg_post(spmv_plan_s* h, double* y, unsigned long long* slots, cudaStream_t st);   // after it
 spmv_status_t xchg_allreduce_max(spmv_plan_s* h, double* m_dev, cudaStream_t st);
 int64_t xchg_timeouts(spmv_plan_s* h);
+bool xchg_failed(const spmv_plan_s* h);   // a device-side exchange wait timed out (no synchronisation)
 void xchg_release(spmv_plan_s* h);
 spmv_status_t xchg_loopback_link(spmv_plan_s** hs, int world);
 bool stream_memops_available();

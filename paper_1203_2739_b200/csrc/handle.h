@@ -96,6 +96,9 @@ struct XBufs {
     int32_t* tready = nullptr;            // [world] tready[q] = seq: rank q's border-row temporaries landed
     int32_t* tdone = nullptr;             // [world] tdone[q] = seq: rank q folded its temporaries of apply seq
     int32_t* err = nullptr;               // [1] device-side wait timeouts
+    int32_t* herr = nullptr;              // host-mapped flag (device address) set by a timed-out wait: the
+                                          // next apply reports it without a synchronisation (sticky error)
+    int32_t* herr_host = nullptr;         // the same flag's host address (cudaHostAlloc, mapped)
 };
 
 }  // namespace spmvb
@@ -122,6 +125,7 @@ struct spmv_plan_s {
     int32_t n_parts = 0;
     int64_t n_seg = 0;
     int64_t bytes_alg = 0, bytes_alg_split = 0, bytes_stream = 0;
+    int64_t index_bytes = 4;          // row-tile column ids: 4, or 2 with the f3 16-bit ids
     bool has_perm = false;
     bool has_owner = false;
     int kernel = 0;                   // 7 column-sorted panels, 0 row tiles
@@ -129,6 +133,8 @@ struct spmv_plan_s {
     // device arrays (one allocation each)
     int32_t* d_rowptr = nullptr;      // [m_loc+1]
     int32_t* d_col = nullptr;         // [nnz_loc + pad] local column ids
+    uint16_t* d_col16 = nullptr;      // f3: [nnz_loc + pad] 16-bit tile-local column ids (or nullptr)
+    int4* d_tile_base = nullptr;      // f3: [T] per tile (lo, hi, split, largest column)
     double* d_val = nullptr;          // [nnz_loc + pad]
     int32_t* d_tile_row = nullptr;    // [T+1]
     int32_t* d_tile_nnz = nullptr;    // [T+1] row_ptr[tile_row[t]]

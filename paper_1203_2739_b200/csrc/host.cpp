@@ -72,6 +72,8 @@ template spmv_status_t dalloc<double>(spmv_plan_s*, double**, size_t);
 template spmv_status_t dalloc<int32_t>(spmv_plan_s*, int32_t**, size_t);
 template spmv_status_t dalloc<char>(spmv_plan_s*, char**, size_t);
 template spmv_status_t upload<int32_t>(spmv_plan_s*, int32_t**, const int32_t*, size_t, size_t);
+template spmv_status_t upload<uint16_t>(spmv_plan_s*, uint16_t**, const uint16_t*, size_t, size_t);
+template spmv_status_t upload<int4>(spmv_plan_s*, int4**, const int4*, size_t, size_t);
 
 void free_plan(spmv_plan_s* h) {
     if (!h) return;
@@ -598,6 +600,24 @@ spmv_status_t create_impl(int64_t m, int64_t n, int64_t nnz, const int64_t* row_
 
     DeviceGuard dg(h->device);
     if (!dg.ok()) return fail(SPMV_ERR_INTERNAL, "cannot select device %d", h->device);
+    // Every kernel of the apply path is loaded now, not at its first launch
+    // (CUDA's lazy loading): on a multi-GPU run a rank's kernel spins on a
+    // peer's exchange flag, and a module load can wait for the kernels
+    // running on the device -- a peer's first launch of, e.g., the DB fold
+    // kernel would then stall the exchange until the device-side waits time
+    // out (found by the loopback tests).
+    {
+        static std::atomic<int> loaded[kMaxDevices];
+        const int di = h->device >= 0 && h->device < kMaxDevices ? h->device : kMaxDevices - 1;
+        if (!loaded[di].load(std::memory_order_acquire)) {
+            for (cudaError_t (*f)() : {preload_kernels_misc, preload_kernels_panel, preload_kernels_rowtile,
+                                       preload_kernels_split}) {
+                const cudaError_t e = f();
+                if (e != cudaSuccess) return fail(SPMV_ERR_INTERNAL, "kernel preload: %s", cudaGetErrorString(e));
+            }
+            loaded[di].store(1, std::memory_order_release);
+        }
+    }
 
     // ---------------------------------------------- NCCL bootstrap (a4)
     if (world > 1 && !test_rank) {
@@ -816,6 +836,60 @@ spmv_status_t create_impl(int64_t m, int64_t n, int64_t nnz, const int64_t* row_
             if ((s = upload(h, &h->d_tile_cls, tile_cls.data(), T))) return s;
         }
         h->bytes_stream = 12 * nnz_loc + 4 * (m_loc + 1) + 8 * m_loc;
+
+        // ------------------- f3: 16-bit tile-local column ids (row tiles)
+        // The ICSR idea of P:L43 (fewer index bytes per nonzero) in the form
+        // the SB layout allows: a row tile never crosses an SB block, so its
+        // columns lie in its block's interior C_k and the border C_B (Eq.(1))
+        // -- two windows.  Per tile, the windows are cut at the largest gap
+        // between its distinct columns; id u = c - lo for c in the low window,
+        // split + (c - hi_start) in the high one, decoded on the device as
+        // u + (u < split ? lo : hi) with hi = hi_start - split.  Used when
+        // every tile's windows fit 65,536 ids together (C1, C2): the kernel
+        // then streams 2 + 8 bytes per nonzero instead of 4 + 8.  Integer
+        // decoding: the same columns, the same summation order (bit-identical).
+        h->index_bytes = 4;
+        if (h->opt.index16 == 0 && T > 0 && nnz_loc > 0) {
+            std::vector<uint16_t> c16(nnz_loc + kPad, 0);
+            std::vector<int4> tb(T);
+            std::atomic<int> fits{1};
+#pragma omp parallel
+            {
+                std::vector<int32_t> cs;
+#pragma omp for schedule(dynamic, 16)
+                for (int64_t t = 0; t < T; ++t) {
+                    if (!fits.load(std::memory_order_relaxed)) continue;
+                    const int64_t a = rp[tile_row[t]], b = rp[tile_row[t + 1]];
+                    cs.assign(pcol.begin() + a, pcol.begin() + b);
+                    std::sort(cs.begin(), cs.end());
+                    cs.erase(std::unique(cs.begin(), cs.end()), cs.end());
+                    int32_t lo = cs.empty() ? 0 : cs.front(), split = 65536, hi = lo;
+                    if (!cs.empty() && (int64_t)cs.back() - lo >= 65536) {
+                        size_t g = 0;   // largest gap: between cs[g] and cs[g + 1]
+                        for (size_t q = 1; q + 1 < cs.size(); ++q)
+                            if (cs[q + 1] - cs[q] > cs[g + 1] - cs[g]) g = q;
+                        const int64_t lenA = (int64_t)cs[g] - lo + 1, lenB = (int64_t)cs.back() - cs[g + 1] + 1;
+                        if (lenA + lenB > 65536) {
+                            fits = 0;
+                            continue;
+                        }
+                        split = (int32_t)lenA;
+                        hi = cs[g + 1] - split;
+                    }
+                    tb[t] = make_int4(lo, hi, split, cs.empty() ? 0 : cs.back());
+                    for (int64_t e = a; e < b; ++e) {
+                        const int32_t c = pcol[e];
+                        c16[e] = (uint16_t)(c - lo < split ? c - lo : c - hi);
+                    }
+                }
+            }
+            if (fits) {
+                if ((s = upload(h, &h->d_col16, c16.data(), nnz_loc + kPad))) return s;
+                if ((s = upload(h, &h->d_tile_base, tb.data(), T))) return s;
+                h->index_bytes = 2;
+                h->bytes_stream -= 2 * nnz_loc;
+            }
+        }
 
         // -------------------------------------------- split layout (a8)
         // Within each row tile the nonzeros are regrouped part-major: for k =
@@ -1207,6 +1281,9 @@ spmv_status_t run(spmv_handle_t h, const double* x, double* y, uint32_t flags, c
     XView xv;
     xv.x_hi = xk;
     xv.x_split = INT32_MAX;
+    if (h->world > 1 && xchg_failed(h))   // sticky: a peer stopped answering in an earlier apply
+        return fail(SPMV_ERR_INTERNAL, "a border exchange timed out in an earlier apply (a peer is gone); "
+                                       "its results were invalid");
     if (h->world > 1) {
         spmv_status_t s = xchg_pre(h, xk, st, xv);
         if (s) return s;
@@ -1254,6 +1331,7 @@ spmv_status_t run(spmv_handle_t h, const double* x, double* y, uint32_t flags, c
         X.self = h->rank;
         X.seq = xv.seq;
         X.err = xv.err;
+        X.herr = xv.herr;
         CUDA_TRY(launch_panel(X, st));
     } else if (!split) {
         RowTileArgs P{};
@@ -1262,6 +1340,8 @@ spmv_status_t run(spmv_handle_t h, const double* x, double* y, uint32_t flags, c
         P.tile_cls = h->d_tile_cls;
         P.rowptr = h->d_rowptr;
         P.col = h->d_col;
+        P.col16 = h->d_col16;
+        P.tile_base = h->d_tile_base;
         P.val = h->d_val;
         P.x_lo = xk;
         P.x_hi = xv.x_hi;
@@ -1344,6 +1424,7 @@ spmv_status_t spmv_get_info(spmv_handle_t h, spmv_info_t* info) {
     info->y_border_begin = h->y_bord_begin;
     info->y_border_len = h->y_bord_len;
     info->exchange_timeouts = xchg_timeouts(h);
+    info->index_bytes = h->index_bytes;
     return SPMV_OK;
 }
 

@@ -59,6 +59,10 @@ struct RowTileArgs {
     int32_t n_tiles;
     double* y;
     unsigned long long* maxabs_slots;
+    // f3: 16-bit tile-local column ids (nullptr: col is used).  Tile t's id u
+    // decodes to min(u + (u < tile_base[t].z ? tile_base[t].x : tile_base[t].y), tile_base[t].w)
+    const uint16_t* col16;     // [nnz+pad]
+    const int4* tile_base;     // [T] (lo, hi, split, largest column of the tile)
 };
 cudaError_t launch_rowtile(const RowTileArgs& a, bool xsplit, cudaStream_t s);
 // Fused / literal multiple-SpMxV kernel (split.cu), K <= 64 parts.
@@ -70,8 +74,16 @@ cudaError_t launch_split_rows(const RowTileArgs& a, const int32_t* row_seg, cons
                               cudaStream_t s);
 // x^[c] = x[colinv[c]]   (ORIGINAL-mode x preparation, a3)
 cudaError_t launch_gather(const double* src, const int32_t* idx, double* dst, int64_t n, cudaStream_t s);
-// DB split across GPUs: y[i] = fold of tin[fpos[fptr[i]..fptr[i+1])] in order (f1)
-cudaError_t launch_fold(const double* tin, const int32_t* fptr, const int32_t* fpos, double* y, int64_t n,
+// DB split across GPUs: y[i] = fold of tin[fpos[fptr[i]..fptr[i+1])] in order (f1).  With
+// w.ready set (P2P exchange) the kernel first waits on the device until
+// ready[q] - seq >= 0 for every peer q != self (bounded; a timeout adds 1 to *err).
+struct FoldWait {
+    const int32_t* ready = nullptr;
+    int32_t world = 1, self = 0, seq = 0;
+    int32_t* err = nullptr;
+    int32_t* herr = nullptr;   // host-mapped sticky flag, also set on a timeout
+};
+cudaError_t launch_fold(const double* tin, const int32_t* fptr, const int32_t* fpos, double* y, int64_t n, FoldWait w,
                         unsigned long long* slots, cudaStream_t s);
 // max over slots -> *out
 cudaError_t launch_maxabs_finish(const unsigned long long* slots, double* out, cudaStream_t s);
@@ -79,6 +91,11 @@ cudaError_t launch_maxabs_finish(const unsigned long long* slots, double* out, c
 cudaError_t launch_normalize(const double* y, const int32_t* owner, const double* m, double* x_next,
                              int64_t n, cudaStream_t s);
 int kernel_num_sms();   // SMs of the current device
+// Eager loading of every SpMxV-path kernel on the current device (per .cu file)
+cudaError_t preload_kernels_misc();
+cudaError_t preload_kernels_panel();
+cudaError_t preload_kernels_rowtile();
+cudaError_t preload_kernels_split();
 
 // ---------------------------------------------------------------------------
 // Column-sorted panel SpMxV (panel.cu, plan_panel.cpp): the
@@ -170,6 +187,7 @@ struct PnArgs {
     const int32_t* ready;
     int32_t world, self, seq;
     int32_t* err;
+    int32_t* herr;            // host-mapped sticky flag, also set on a timeout (the next apply reports it)
 };
 // Dynamic shared memory of a panel CTA: its y slots (+ the padding lanes'
 // 16 scratch slots), the split rows' slot lists (u16) and their (first, count,

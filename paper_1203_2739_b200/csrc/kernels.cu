@@ -64,13 +64,38 @@ __global__ void normalize_scalar_kernel(const double* __restrict__ y, const int3
 // DB split across GPUs (f1): y_i = 0, then y_i <- y_i + tmp_k for
 // the row's received per-part temporaries in part order (fold lists built at
 // create), one thread per owned border row; max |y| folded like the SpMxV's.
-__global__ void __launch_bounds__(256) fold_kernel(const double* __restrict__ tin, const int32_t* __restrict__ fptr,
+// P2P exchange (ready != nullptr): the peers' temporaries arrive over NVLink
+// while earlier work runs; every CTA first waits (thread 0, acquire loads,
+// bounded: a timeout counts in *err) until ready[q] - seq >= 0 for every peer
+// q -- a device-side wait, so no stream ever blocks on a peer (a blocked
+// stream can hold up unrelated work queued behind it) -- and then reads tin
+// through L2 (ld.cg: written by the peers' copy engines).
+__global__ void __launch_bounds__(256) fold_kernel(const double* tin, const int32_t* __restrict__ fptr,
                                                    const int32_t* __restrict__ fpos, double* __restrict__ y,
-                                                   int64_t n, unsigned long long* slots) {
+                                                   int64_t n, unsigned long long* slots, FoldWait w) {
+    if (w.ready) {
+        if (threadIdx.x == 0)
+            for (int q = 0; q < w.world; ++q) {
+                if (q == w.self) continue;
+                uint32_t it = 0;
+                for (;;) {
+                    int32_t v;
+                    asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(w.ready + q) : "memory");
+                    if (v - w.seq >= 0) break;
+                    __nanosleep(256);
+                    if (++it > (1u << 24)) {   // ~ seconds: the peer is gone
+                        atomicAdd(w.err, 1);
+                        if (w.herr) *reinterpret_cast<volatile int32_t*>(w.herr) = 1;
+                        break;
+                    }
+                }
+            }
+        __syncthreads();
+    }
     double mx = 0.0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         double v = 0.0;
-        for (int32_t j = fptr[i]; j < fptr[i + 1]; ++j) v = v + tin[fpos[j]];
+        for (int32_t j = fptr[i]; j < fptr[i + 1]; ++j) v = v + __ldcg(tin + fpos[j]);
         y[i] = v;
         mx = fmax(mx, fabs(v));
     }
@@ -111,10 +136,10 @@ cudaError_t launch_gather(const double* src, const int32_t* idx, double* dst, in
     return cudaGetLastError();
 }
 
-cudaError_t launch_fold(const double* tin, const int32_t* fptr, const int32_t* fpos, double* y, int64_t n,
+cudaError_t launch_fold(const double* tin, const int32_t* fptr, const int32_t* fpos, double* y, int64_t n, FoldWait w,
                         unsigned long long* slots, cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
-    fold_kernel<<<grid_for(n, 256), 256, 0, s>>>(tin, fptr, fpos, y, n, slots);
+    fold_kernel<<<grid_for(n, 256), 256, 0, s>>>(tin, fptr, fpos, y, n, slots, w);
     return cudaGetLastError();
 }
 
@@ -132,6 +157,21 @@ cudaError_t launch_normalize(const double* y, const int32_t* owner, const double
         normalize_kernel<<<grid_for((n + 3) / 4, 256), 256, 0, s>>>(y, owner, m, x_next, n);
     }
     return cudaGetLastError();
+}
+
+
+// Loads this file's kernels now (cudaFuncGetAttributes forces the lazy loader):
+// a kernel first launched while a peer rank's kernel spins on an exchange flag
+// would otherwise load its module then, and a module load can wait for the
+// running kernels -- the spinning one included (see host.cpp preload_kernels).
+cudaError_t preload_kernels_misc() {
+    cudaFuncAttributes fa;
+    for (const void* k : {(const void*)gather_kernel, (const void*)maxabs_finish_kernel, (const void*)normalize_kernel,
+                          (const void*)normalize_scalar_kernel, (const void*)fold_kernel}) {
+        const cudaError_t e = cudaFuncGetAttributes(&fa, k);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 }  // namespace spmvb

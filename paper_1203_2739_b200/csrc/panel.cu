@@ -168,6 +168,7 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
                         __nanosleep(128);
                         if (++it > (1u << 25)) {   // ~ seconds: the peer is gone
                             atomicAdd(A.err, 1);
+                            if (A.herr) *reinterpret_cast<volatile int32_t*>(A.herr) = 1;
                             break;
                         }
                     }
@@ -354,6 +355,21 @@ cudaError_t launch_panel(const PnArgs& a, cudaStream_t s) {
         else spmv_panel_kernel<false, false><<<a.n_panels, kT, smem, s>>>(a);
     }
     return cudaGetLastError();
+}
+
+
+// Loads this file's kernels now (cudaFuncGetAttributes forces the lazy loader):
+// a kernel first launched while a peer rank's kernel spins on an exchange flag
+// would otherwise load its module then, and a module load can wait for the
+// running kernels -- the spinning one included (see host.cpp preload_kernels).
+cudaError_t preload_kernels_panel() {
+    cudaFuncAttributes fa;
+    for (const void* k : {(const void*)spmv_panel_kernel<false, false>, (const void*)spmv_panel_kernel<false, true>,
+                          (const void*)spmv_panel_kernel<true, false>, (const void*)spmv_panel_kernel<true, true>}) {
+        const cudaError_t e = cudaFuncGetAttributes(&fa, k);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 }  // namespace spmvb

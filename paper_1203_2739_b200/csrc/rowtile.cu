@@ -27,6 +27,8 @@
 //      for rows <= 32, warp-per-row (fixed lane assignment and tree) for
 //      longer rows;
 //   3. y is stored coalesced; max |y| is folded per warp (one atomicMax).
+// f3 (C16): with 16-bit tile-local column ids the stream is 10 B per nonzero
+// (an 8-byte quad of ids + two 16-byte value pairs per four nonzeros).
 // Rows longer than a tile get a tile of their own (CTA-per-row class): all
 // threads stream the row with a fixed assignment and a fixed tree.
 #include <cstdint>
@@ -48,6 +50,18 @@ __device__ __forceinline__ int4 ld_v4(const int32_t* ptr, uint64_t pol) {
                  : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                  : "l"(ptr), "l"(pol));
     return r;
+}
+// f3: four 16-bit tile-local column ids (8 bytes), decoded with the tile's
+// two windows: u + (u < split ? lo : hi), capped at the tile's largest column
+// (the quads at a tile's ends also hold a neighbour tile's ids, whose
+// products are masked; the cap keeps their gathers inside x)
+__device__ __forceinline__ int4 ld_v4c16(const uint16_t* ptr, uint64_t pol, const int4 tb) {
+    unsigned short u0, u1, u2, u3;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u16 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=h"(u0), "=h"(u1), "=h"(u2), "=h"(u3)
+                 : "l"(ptr), "l"(pol));
+    auto dec = [&](int u) { return min(u + (u < tb.z ? tb.x : tb.y), tb.w); };
+    return make_int4(dec(u0), dec(u1), dec(u2), dec(u3));
 }
 __device__ __forceinline__ double2 ld_v2d(const double* ptr, uint64_t pol) {
     double2 r;
@@ -82,7 +96,8 @@ struct RTSmem {
 };
 
 // NT threads per tile CTA; each thread streams QPT = 512/NT quads.
-template <bool XSPLIT>
+// C16: the column ids are the f3 16-bit tile-local ids (col16 + tile_base).
+template <bool XSPLIT, bool C16>
 __global__ void __launch_bounds__(NT, 6) spmv_rowtile_kernel(const RowTileArgs A) {
     constexpr int QPT = 512 / NT;
     __shared__ __align__(16) RTSmem sm;
@@ -95,6 +110,8 @@ __global__ void __launch_bounds__(NT, 6) spmv_rowtile_kernel(const RowTileArgs A
     const int a4 = a & ~3;
     const uint64_t pol = pol_evict_first();
     double mx = 0.0;
+    const int4 tb = C16 ? A.tile_base[t] : make_int4(0, 0, 0, 0);
+    auto cols4 = [&](int64_t pos) { return C16 ? ld_v4c16(A.col16 + pos, pol, tb) : ld_v4(A.col + pos, pol); };
 
     if (b - a + 3 > kTileNnz) {   // long row: planned as one (host plan_tiles, alignment-free test)
         // ------------------------------------------- one long row (> a tile)
@@ -102,7 +119,7 @@ __global__ void __launch_bounds__(NT, 6) spmv_rowtile_kernel(const RowTileArgs A
         double acc = 0.0;
         for (int64_t q = qa + tid; q < qb; q += NT) {
             // all four gathers unconditional (the quad's columns are valid), products masked
-            const int4 c = ld_v4(A.col + 4 * q, pol);
+            const int4 c = cols4(4 * q);
             const double2 v0 = ld_v2d(A.val + 4 * q, pol);
             const double2 v1 = ld_v2d(A.val + 4 * q + 2, pol);
             const double x0 = ldx2<XSPLIT>(A, c.x), x1 = ldx2<XSPLIT>(A, c.y);
@@ -145,7 +162,7 @@ __global__ void __launch_bounds__(NT, 6) spmv_rowtile_kernel(const RowTileArgs A
         for (int k = 0; k < QPT; ++k) {
             const int p = 4 * (tid + k * NT);
             const int pq = (a4 + p < b) ? p : 0;
-            c[k] = ld_v4(A.col + a4 + pq, pol);
+            c[k] = cols4(a4 + pq);
             v0[k] = ld_v2d(A.val + a4 + pq, pol);
             v1[k] = ld_v2d(A.val + a4 + pq + 2, pol);
         }
@@ -234,9 +251,30 @@ __global__ void __launch_bounds__(NT, 6) spmv_rowtile_kernel(const RowTileArgs A
 
 cudaError_t launch_rowtile(const RowTileArgs& a, bool xsplit, cudaStream_t s) {
     if (a.n_tiles <= 0) return cudaSuccess;
-    if (xsplit) spmv_rowtile_kernel<true><<<a.n_tiles, kNT, 0, s>>>(a);
-    else spmv_rowtile_kernel<false><<<a.n_tiles, kNT, 0, s>>>(a);
+    const bool c16 = a.col16 != nullptr;
+    if (xsplit) {
+        if (c16) spmv_rowtile_kernel<true, true><<<a.n_tiles, kNT, 0, s>>>(a);
+        else spmv_rowtile_kernel<true, false><<<a.n_tiles, kNT, 0, s>>>(a);
+    } else {
+        if (c16) spmv_rowtile_kernel<false, true><<<a.n_tiles, kNT, 0, s>>>(a);
+        else spmv_rowtile_kernel<false, false><<<a.n_tiles, kNT, 0, s>>>(a);
+    }
     return cudaGetLastError();
+}
+
+
+// Loads this file's kernels now (cudaFuncGetAttributes forces the lazy loader):
+// a kernel first launched while a peer rank's kernel spins on an exchange flag
+// would otherwise load its module then, and a module load can wait for the
+// running kernels -- the spinning one included (see host.cpp preload_kernels).
+cudaError_t preload_kernels_rowtile() {
+    cudaFuncAttributes fa;
+    for (const void* k : {(const void*)spmv_rowtile_kernel<false, false>, (const void*)spmv_rowtile_kernel<false, true>,
+                          (const void*)spmv_rowtile_kernel<true, false>, (const void*)spmv_rowtile_kernel<true, true>}) {
+        const cudaError_t e = cudaFuncGetAttributes(&fa, k);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 }  // namespace spmvb

@@ -393,4 +393,19 @@ cudaError_t launch_split_rows(const RowTileArgs& a, const int32_t* row_seg, cons
     return cudaGetLastError();
 }
 
+
+// Loads this file's kernels now (cudaFuncGetAttributes forces the lazy loader):
+// a kernel first launched while a peer rank's kernel spins on an exchange flag
+// would otherwise load its module then, and a module load can wait for the
+// running kernels -- the spinning one included (see host.cpp preload_kernels).
+cudaError_t preload_kernels_split() {
+    cudaFuncAttributes fa;
+    for (const void* k : {(const void*)spmv_split_kernel<false>, (const void*)spmv_split_kernel<true>,
+                          (const void*)spmv_split_rows_kernel<false>, (const void*)spmv_split_rows_kernel<true>}) {
+        const cudaError_t e = cudaFuncGetAttributes(&fa, k);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
 }  // namespace spmvb

@@ -78,14 +78,17 @@ def _edge_matrix(lengths, n, seed=0, variant="int"):
 @pytest.mark.parametrize("case", ["tile_edges", "long_rows", "empty_rows", "rect_wide", "rect_tall",
                                   "single", "all_empty", "ragged_mix"])
 @pytest.mark.parametrize("variant", ["int", "real"])
-@pytest.mark.parametrize("kernel", ["default", "panel"])
+@pytest.mark.parametrize("kernel", ["default", "panel", "rowtile32"])
 def test_edge_shapes(case, variant, kernel):
     """Row lengths at every tile/class boundary +-1, rows longer than a tile,
     empty rows, m != n (Table 1's rectangular group), odd row
     starts (exercise the 128-bit quad peeling).  kernel=panel forces the
     column-sorted panel kernel on small panels (virtual rows of very long
-    rows, the warp fold of rows with > 32 of them, empty panels' rows)."""
-    opts = panel(700) if kernel == "panel" else None
+    rows, the warp fold of rows with > 32 of them, empty panels' rows).
+    The default here is the row-tile kernel with f3's 16-bit tile-local ids
+    (every case fits them; a tile's boundary quads hold a neighbour's ids);
+    rowtile32 forces 32-bit ids."""
+    opts = panel(700) if kernel == "panel" else dict(kernel="rowtile", index16=1) if kernel == "rowtile32" else None
     TN = 2048   # kTileNnz
     rng = np.random.default_rng(5)
     if case == "tile_edges":
@@ -344,3 +347,26 @@ def test_full_size_power_c5():
     teacher-forced power steps checked on all 64 M rows (the bench
     samples 200,000 rows), m_t exact and x_{t+1} bitwise."""
     _teacher_forced(synth.make("c5"), None, 2, expect_kernel=7)
+
+
+# ----------------------------------------------- f3: 16-bit column ids
+@pytest.mark.parametrize("name", ["c1", "c2s", "c5s", "c4s", "c2"])
+def test_index16_bitwise(name):
+    """f3 (ICSR-style index compression): the row-tile kernel with
+    16-bit tile-local column ids (two windows per tile: C_k and C_B for an SB
+    block tile) gives the same y bit for bit as with 32-bit ids (integer
+    decoding, same summation order), and matches the oracle."""
+    p = synth.make(name)
+    x = p.x()
+    xh, yh_ref, S = oracle_permuted(p, x)
+    ys = {}
+    for mode in (0, 1):
+        h = create(p, options=dict(kernel="rowtile", index16=mode))
+        info = sp.spmv_get_info(h)
+        ys[mode] = (gpu_apply(h, xh, p.m), info["index_bytes"])
+        sp.spmv_destroy(h)
+    assert ys[1][1] == 4
+    if name != "c4s":   # c4s: a long row's columns span > 65,536 ids -> stays 32-bit
+        assert ys[0][1] == 2, "16-bit ids expected"
+    assert np.array_equal(ys[0][0].view(np.int64), ys[1][0].view(np.int64))
+    assert_parity(ys[0][0], yh_ref, S, what=f"{name} 16-bit ids")

@@ -65,17 +65,16 @@ def y_rows(info):
 
 
 def apply_ranks(hs, infos, xls, split=False, flags=0):
-    """One apply per rank, each on its own stream (as on its own GPU)."""
+    """One apply per rank, each on its own stream (as on its own GPU).  All
+    inputs and outputs are allocated and ready before the first apply, so
+    nothing on the host waits between the ranks' applies (a rank's apply
+    completes only once its peers have pushed their slices)."""
     streams = [T.rank_stream(h) for h in hs]   # each rank's own hardware queue (spmv_test_rank_stream)
-    ys = []
-    for h, i, xl, s in zip(hs, infos, xls, streams):
-        xd = xl if torch.is_tensor(xl) else torch.from_numpy(np.ascontiguousarray(xl)).cuda()
-        yd = torch.full((i["y_local_len"],), float("nan"), dtype=torch.float64, device="cuda")
-        s.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(s):
-            (sp.spmv_split_apply if split else sp.spmv_apply)(h, xd, yd, flags, stream=s)
-            xd.record_stream(s)
-        ys.append(yd)
+    xds = [xl if torch.is_tensor(xl) else torch.from_numpy(np.ascontiguousarray(xl)).cuda() for xl in xls]
+    ys = [torch.full((i["y_local_len"],), float("nan"), dtype=torch.float64, device="cuda") for i in infos]
+    torch.cuda.synchronize()
+    for h, xd, yd, s in zip(hs, xds, ys, streams):
+        (sp.spmv_split_apply if split else sp.spmv_apply)(h, xd, yd, flags, stream=s)
     torch.cuda.synchronize()
     return ys
 
@@ -144,13 +143,20 @@ def test_sb_ranks_power_steps(world):
         xg = xg_next
 
 
-@pytest.mark.parametrize("name,world", [("c3s", 2), ("c3s", 4), ("c3", 8)])
+# C3's DB structure with K = 8 blocks, small enough that all eight ranks'
+# kernels are co-resident on the one GPU of the loopback fake: a rank's CTAs
+# spin (bounded) until every peer's slice lands, and on one GPU a peer whose
+# kernel cannot get an SM never pushes (full C3 at world 8 has 632 CTAs of
+# 1 per SM; on a real run each rank has a GPU of its own).
+synth.PRESETS["_c3w8"] = lambda **kw: synth._db(8, 3000, 1000, 10, 16, 0, 4, 10, 20, **kw)
+
+
+@pytest.mark.parametrize("name,world", [("c3s", 2), ("c3s", 4), ("_c3w8", 8)])
 @pytest.mark.parametrize("variant", ["int", "real"])
 def test_db_split_across_ranks(name, world, variant):
     """f1: the multiple-SpMxV across GPUs on C3's DB structure (K parts, A13's
-    2D block assignment; full C3 at world 8): part k on block k's rank,
-    border-row temporaries folded in part order by the row's owner
-    (P:L107-109)."""
+    2D block assignment): part k on block k's rank, border-row temporaries
+    folded in part order by the row's owner."""
     p = synth.make(name, variant=variant)
     x = p.x()
     y_ref = oracle.split(p.row_ptr, p.col, p.val, p.parts, p.n_parts, x)
@@ -169,6 +175,7 @@ def test_db_split_across_ranks(name, world, variant):
     for i, yd in zip(infos, ys):
         y[y_rows(i)] = yd.cpu().numpy()
     assert_parity(y, y_ref, S, exact=(variant == "int"), what="DB apply")
+    assert all(sp.spmv_get_info(h)["exchange_timeouts"] == 0 for h in hs)
 
 
 @pytest.mark.parametrize("world", [2, 4])
@@ -281,3 +288,23 @@ def test_exchange_overlaps_interior():
           f"peer's push began (interior share done early: {1 - t_tail / t_full:.2f})")
     assert t_tail < 0.7 * t_full, (t_tail, t_full)
     assert all(sp.spmv_get_info(h)["exchange_timeouts"] == 0 for h in hs)
+
+
+def test_peer_gone_is_sticky():
+    """A rank whose peer never applies: its kernel's device-side wait for the
+    border slice gives up after a bound (no hang), counts the timeout, and
+    the handle's next apply fails with SPMV_ERR_INTERNAL instead of
+    returning results computed from a stale border."""
+    p = synth.make("c5s", scramble=0)
+    hs, infos = make_ranks(p, 2)
+    x0 = torch.from_numpy(x_local(p.x(), infos[0])).cuda()
+    y0 = torch.empty(infos[0]["y_local_len"], dtype=torch.float64, device="cuda")
+    s0 = T.rank_stream(hs[0])
+    t0 = time.time()
+    sp.spmv_apply(hs[0], x0, y0, stream=s0)     # rank 1 never pushes its slice
+    torch.cuda.synchronize()
+    assert time.time() - t0 < 120
+    assert sp.spmv_get_info(hs[0])["exchange_timeouts"] > 0
+    with pytest.raises(sp.SpmvError) as e:
+        sp.spmv_apply(hs[0], x0, y0, stream=s0)
+    assert e.value.status == sp.SPMV_ERR_INTERNAL
