@@ -600,25 +600,6 @@ spmv_status_t create_impl(int64_t m, int64_t n, int64_t nnz, const int64_t* row_
 
     DeviceGuard dg(h->device);
     if (!dg.ok()) return fail(SPMV_ERR_INTERNAL, "cannot select device %d", h->device);
-    // Every kernel of the apply path is loaded now, not at its first launch
-    // (CUDA's lazy loading): on a multi-GPU run a rank's kernel spins on a
-    // peer's exchange flag, and a module load can wait for the kernels
-    // running on the device -- a peer's first launch of, e.g., the DB fold
-    // kernel would then stall the exchange until the device-side waits time
-    // out (found by the loopback tests).
-    {
-        static std::atomic<int> loaded[kMaxDevices];
-        const int di = h->device >= 0 && h->device < kMaxDevices ? h->device : kMaxDevices - 1;
-        if (!loaded[di].load(std::memory_order_acquire)) {
-            for (cudaError_t (*f)() : {preload_kernels_misc, preload_kernels_panel, preload_kernels_rowtile,
-                                       preload_kernels_split}) {
-                const cudaError_t e = f();
-                if (e != cudaSuccess) return fail(SPMV_ERR_INTERNAL, "kernel preload: %s", cudaGetErrorString(e));
-            }
-            loaded[di].store(1, std::memory_order_release);
-        }
-    }
-
     // ---------------------------------------------- NCCL bootstrap (a4)
     if (world > 1 && !test_rank) {
         ncclUniqueId id;
@@ -801,6 +782,25 @@ spmv_status_t create_impl(int64_t m, int64_t n, int64_t nnz, const int64_t* row_
             h->bytes_alg = 12 * nnz_loc + 4 * (m_loc + 1) + 8 * m_loc + 8 * nt;
             h->bytes_alg_split = 0;
             if (n_parts) h->bytes_alg_split = 12 * nnz_loc + 8 * m_loc + 8 * nt;   // + segment metadata below
+        }
+
+        // Every kernel of the apply path is loaded now, not at its first launch
+        // (CUDA's lazy loading): on a multi-GPU run a rank's kernel spins on a
+        // peer's exchange flag, and a module load can wait for the kernels
+        // running on the device -- a peer's first launch of, e.g., the DB fold
+        // kernel would then stall the exchange until the device-side waits time
+        // out (found by the loopback tests).
+        {
+            static std::atomic<int> loaded[kMaxDevices];
+            const int di = h->device >= 0 && h->device < kMaxDevices ? h->device : kMaxDevices - 1;
+            if (!loaded[di].load(std::memory_order_acquire)) {
+                for (cudaError_t (*f)() : {preload_kernels_misc, preload_kernels_panel, preload_kernels_rowtile,
+                                           preload_kernels_split}) {
+                    const cudaError_t e = f();
+                    if (e != cudaSuccess) return fail(SPMV_ERR_INTERNAL, "kernel preload: %s", cudaGetErrorString(e));
+                }
+                loaded[di].store(1, std::memory_order_release);
+            }
         }
 
         // ------------------------------------------------ device upload
