@@ -129,7 +129,13 @@ typedef struct {
                                 stream 16-bit tile-local column ids (10 B per nonzero instead of 12)
                                 whenever every row tile's columns fit two 65,536-id windows (an SB
                                 block tile: C_k and C_B, Eq.(1)); 1 = off (32-bit ids) */
-    int32_t reserved[10];
+    int32_t debug_checks;    /* 1 = run the checked variant of the panel kernel (compute-sanitizer is
+                                not available on this GPU pool): every y slot and x column it touches is
+                                bounds-checked, and every y update stamps its slot with the epoch in
+                                shared memory (atomicExch), so a row updated twice within one epoch --
+                                a violation of the planner's race-freedom invariant -- is counted;
+                                counts in spmv_info_t.debug_violations.  Slower; for tests */
+    int32_t reserved[9];
 } spmv_options_t;
 
 /* spmv_create -- ingest, validate, permute and plan (once; not per SpMxV).
@@ -232,6 +238,9 @@ typedef struct {
                                      reading it synchronises the device) */
     int64_t index_bytes;          /* row-tile kernel: bytes per column id it streams (2 with the f3
                                      16-bit tile-local ids, else 4) */
+    int64_t debug_violations[3];  /* debug_checks: y slots out of bounds, x columns out of bounds, rows
+                                     updated twice in one epoch (all 0 on a correct plan; reading them
+                                     synchronises the device) */
 } spmv_info_t;
 
 spmv_status_t spmv_get_info(spmv_handle_t h, spmv_info_t* info);

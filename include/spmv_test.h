@@ -69,6 +69,14 @@ spmv_status_t spmv_test_create_rank(int64_t m, int64_t n, int64_t nnz, const int
  * memory operations. */
 spmv_status_t spmv_test_loopback_link(spmv_handle_t* handles, int32_t world);
 
+/* Test of the debug checks (spmv_options_t.debug_checks): corrupts the panel
+ * plan of a panel handle on the device -- kind 1: a warp-1 entry of panel 0's
+ * first epoch takes the y slot of a warp-0 entry (a row updated twice in one
+ * epoch); 2: a y slot beyond the panel's shared memory; 3: a column delta
+ * beyond x for a matrix whose columns are fewer than the group base + 2^17.
+ * The handle's results are wrong afterwards; USAGE / UNSUPPORTED otherwise. */
+spmv_status_t spmv_test_corrupt_panel(spmv_handle_t h, int32_t kind);
+
 /* The apply stream of a linked loopback test rank (created by
  * spmv_test_loopback_link right after the rank's comm stream, so the ranks'
  * streams do not share the GPU's hardware work queues when

@@ -40,7 +40,7 @@ EXPORTED = ["spmv_create", "spmv_create_ex", "spmv_apply", "spmv_split_apply", "
             "spmv_version", "spmv_shard_plan", "spmv_order_sbfs"]
 # include/spmv_test.h (test and debug hooks, same library)
 EXPORTED_TEST = ["spmv_debug_copy_csr", "spmv_pn_plan_check", "spmv_pn_shard_hash", "spmv_test_create_rank",
-                 "spmv_test_loopback_link", "spmv_test_rank_stream"]
+                 "spmv_test_loopback_link", "spmv_test_rank_stream", "spmv_test_corrupt_panel"]
 
 KERNELS = {"auto": 0, "panel": 1, "rowtile": 2}
 SPLIT_KERNELS = {"auto": 0, "panel": 1, "rows": 2}
@@ -62,7 +62,7 @@ class _Blocks(ctypes.Structure):
 class _Options(ctypes.Structure):
     _fields_ = [("struct_size", ctypes.c_int32), ("kernel", ctypes.c_int32), ("panel_rows", ctypes.c_int32),
                 ("split_kernel", ctypes.c_int32), ("exchange", ctypes.c_int32), ("index16", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 10)]
+                ("debug_checks", ctypes.c_int32), ("reserved", ctypes.c_int32 * 9)]
 
 
 class _Dist(ctypes.Structure):
@@ -79,10 +79,13 @@ class spmv_info_t(ctypes.Structure):
         (k, ctypes.c_int32) for k in ("n_parts", "rank", "world", "kind", "has_owner_map", "kernel",
                                       "split_kernel", "exchange")] + [
         (k, ctypes.c_int64) for k in ("gather_sectors", "y_local_len", "y_border_begin", "y_border_len",
-                                      "deferred", "y_wavefronts_x1000", "exchange_timeouts", "index_bytes")]
+                                      "deferred", "y_wavefronts_x1000", "exchange_timeouts", "index_bytes")] + [
+        ("debug_violations", ctypes.c_int64 * 3)]
 
     def as_dict(self) -> dict:
-        return {k: getattr(self, k) for k, _ in self._fields_}
+        d = {k: getattr(self, k) for k, _ in self._fields_}
+        d["debug_violations"] = list(self.debug_violations)
+        return d
 
 
 class spmv_order_info_t(ctypes.Structure):
@@ -124,6 +127,7 @@ def lib():
         L.spmv_test_create_rank.argtypes = [i64, i64, i64, vp, vp, vp, vp, vp, vp, i32, vp, vp, vp, ctypes.POINTER(vp)]
         L.spmv_test_loopback_link.argtypes = [vp, i32]
         L.spmv_test_rank_stream.argtypes = [vp, vp]
+        L.spmv_test_corrupt_panel.argtypes = [vp, i32]
         for name in EXPORTED_TEST:
             getattr(L, name).restype = i32
         for name in EXPORTED:
@@ -223,7 +227,8 @@ def _options_struct(options, keep):
     o.split_kernel = SPLIT_KERNELS[options.get("split_kernel", "auto")]
     o.exchange = EXCHANGES[options.get("exchange", "auto")]
     o.index16 = int(options.get("index16", 0))
-    unknown = set(options) - {"kernel", "panel_rows", "split_kernel", "exchange", "index16"}
+    o.debug_checks = int(options.get("debug_checks", 0))
+    unknown = set(options) - {"kernel", "panel_rows", "split_kernel", "exchange", "index16", "debug_checks"}
     if unknown:
         raise ValueError(f"unknown spmv options: {sorted(unknown)}")
     keep.append(o)

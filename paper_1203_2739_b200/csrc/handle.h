@@ -133,6 +133,7 @@ struct spmv_plan_s {
     // device arrays (one allocation each)
     int32_t* d_rowptr = nullptr;      // [m_loc+1]
     int32_t* d_col = nullptr;         // [nnz_loc + pad] local column ids
+    unsigned long long* d_dbg = nullptr;   // debug_checks: violation counters [3]
     uint16_t* d_col16 = nullptr;      // f3: [nnz_loc + pad] 16-bit tile-local column ids (or nullptr)
     int4* d_tile_base = nullptr;      // f3: [T] per tile (lo, hi, split, largest column)
     double* d_val = nullptr;          // [nnz_loc + pad]

@@ -71,6 +71,7 @@ spmv_status_t upload(spmv_plan_s* h, T** out, const T* src, size_t count, size_t
 template spmv_status_t dalloc<double>(spmv_plan_s*, double**, size_t);
 template spmv_status_t dalloc<int32_t>(spmv_plan_s*, int32_t**, size_t);
 template spmv_status_t dalloc<char>(spmv_plan_s*, char**, size_t);
+template spmv_status_t dalloc<unsigned long long>(spmv_plan_s*, unsigned long long**, size_t);
 template spmv_status_t upload<int32_t>(spmv_plan_s*, int32_t**, const int32_t*, size_t, size_t);
 template spmv_status_t upload<uint16_t>(spmv_plan_s*, uint16_t**, const uint16_t*, size_t, size_t);
 template spmv_status_t upload<int4>(spmv_plan_s*, int4**, const int4*, size_t, size_t);
@@ -1072,6 +1073,10 @@ spmv_status_t create_impl(int64_t m, int64_t n, int64_t nnz, const int64_t* row_
 
         // ------------------------------------------------- misc buffers
         if ((s = dalloc(h, &h->d_slots, kMaxSlots * kSlotStride))) return s;
+        if (h->opt.debug_checks) {   // the checked panel kernel's violation counters
+            if ((s = dalloc(h, &h->d_dbg, 3))) return s;
+            CUDA_TRY(cudaMemset(h->d_dbg, 0, 3 * sizeof(unsigned long long)));
+        }
         CUDA_TRY(cudaMemset(h->d_slots, 0, kMaxSlots * kSlotStride * sizeof(unsigned long long)));
 
         // ---------------- DB across GPUs: temporaries and their fold lists (f1)
@@ -1332,6 +1337,8 @@ spmv_status_t run(spmv_handle_t h, const double* x, double* y, uint32_t flags, c
         X.seq = xv.seq;
         X.err = xv.err;
         X.herr = xv.herr;
+        X.dbg = h->d_dbg;
+        X.x_cols = h->world > 1 ? h->x_int_len + h->border_total : h->n;
         CUDA_TRY(launch_panel(X, st));
     } else if (!split) {
         RowTileArgs P{};
@@ -1425,6 +1432,16 @@ spmv_status_t spmv_get_info(spmv_handle_t h, spmv_info_t* info) {
     info->y_border_len = h->y_bord_len;
     info->exchange_timeouts = xchg_timeouts(h);
     info->index_bytes = h->index_bytes;
+    for (int k = 0; k < 3; ++k) info->debug_violations[k] = 0;
+    if (h->d_dbg) {
+        DeviceGuard g(h->device);
+        unsigned long long v[3] = {0, 0, 0};
+        if (cudaDeviceSynchronize() == cudaSuccess &&
+            cudaMemcpy(v, h->d_dbg, sizeof v, cudaMemcpyDeviceToHost) == cudaSuccess)
+            for (int k = 0; k < 3; ++k) info->debug_violations[k] = (int64_t)v[k];
+        else
+            cudaGetLastError();
+    }
     return SPMV_OK;
 }
 

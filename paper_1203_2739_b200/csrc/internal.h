@@ -188,6 +188,10 @@ struct PnArgs {
     int32_t world, self, seq;
     int32_t* err;
     int32_t* herr;            // host-mapped sticky flag, also set on a timeout (the next apply reports it)
+    // debug_checks (spmv_options_t): the checked kernel variant counts y slots out of bounds, x
+    // columns >= x_cols and rows updated twice in one epoch into dbg[0..2]
+    unsigned long long* dbg;
+    int64_t x_cols;
 };
 // Dynamic shared memory of a panel CTA: its y slots (+ the padding lanes'
 // 16 scratch slots), the split rows' slot lists (u16) and their (first, count,
@@ -197,6 +201,6 @@ constexpr int64_t kPnSmemMax = 227 * 1024;
 inline int64_t panel_smem_bytes(int64_t slots16, int64_t sslots, int64_t split_n) {
     return (slots16 + 16) * 8 + ((sslots + 7) & ~int64_t(7)) * 2 + split_n * 12;
 }
-cudaError_t launch_panel(const PnArgs& a, cudaStream_t s);
+cudaError_t launch_panel(const PnArgs& a, cudaStream_t s);   // a.dbg != nullptr: the checked variant
 
 }  // namespace spmvb

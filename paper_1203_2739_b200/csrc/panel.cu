@@ -83,7 +83,12 @@ __device__ __forceinline__ int32_t ld_acquire_sys(const int32_t* p) {
 // NA: x gathers L1::no_allocate (SB handles: a panel's gathers rarely revisit
 // a line across groups); XS: x split over two buffers at x_split (world > 1:
 // interior | gathered border).
-template <bool NA, bool XS>
+// CHK (spmv_options_t.debug_checks): every y slot and x column is bounds-
+// checked and every y update stamps its slot with the epoch (atomicExch in
+// shared memory), counting a row updated twice within one epoch -- the
+// planner's race-freedom invariant -- into A.dbg (compute-sanitizer is not
+// available on this GPU pool).
+template <bool NA, bool XS, bool CHK>
 __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
     {   // one panel per CTA
         const int p = blockIdx.x;
@@ -108,6 +113,9 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
             sdesc[3 * i + 1] = A.split_cnt[e];
             sdesc[3 * i + 2] = A.split_row[e];
         }
+        int32_t* stamp = sdesc + 3 * A.max_split_n;   // CHK only: epoch + 1 of each slot's last update
+        if (CHK)
+            for (int i = tid; i < A.max_rows + 16; i += kT) stamp[i] = 0;
         __syncthreads();
 
         const uint64_t pol = pol_evict_first();
@@ -147,7 +155,11 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
             // gathered border); world 1 reads one vector (no select per gather)
             // column = base + delta (non-negative, < 2^31): one unsigned 32-bit add
             // and one wide multiply-add form the address
-            const uint32_t c = (uint32_t)b + (i & kDeltaMask);
+            uint32_t c = (uint32_t)b + (i & kDeltaMask);
+            if (CHK && (int64_t)c >= A.x_cols) {
+                atomicAdd(A.dbg + 1, 1ull);
+                c = 0;
+            }
             const double* xa = !XS ? A.x_lo + c
                                    : (int32_t)c < A.x_split ? A.x_lo + c : A.x_hi + (c - (uint32_t)A.x_split);
             return XS ? ld_x_co(xa, polx) : NA ? ld_x_na(xa, polx) : ld_x(xa, polx);
@@ -228,10 +240,20 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
             __syncthreads();
         }
 
-        auto step = [&](int u) {   // consume ring slot u (compile-time)
+        auto step = [&](int u, int t) {   // consume ring slot u (compile-time) of step t
             const uint32_t i = ri[u];
             // padding lanes carry the scratch slot (host upload), value 0
             const int r = (int)(i >> kPnDeltaBits);
+            if (CHK) {
+                if (r >= A.max_rows + 16) {
+                    atomicAdd(A.dbg + 0, 1ull);
+                    return;
+                }
+                if (r < A.max_rows) {
+                    const int ep = t / kPnB + 1;
+                    if (atomicExch(stamp + r, ep) == ep) atomicAdd(A.dbg + 2, 1ull);
+                }
+            }
             ys[r] = fma(rv[u], rx[u % kGD], ys[r]);
         };
         auto epoch_end = [&](int t) {
@@ -245,7 +267,7 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
         for (; t0 + kD <= T; t0 += kD) {
     #pragma unroll
             for (int u = 0; u < kD; ++u) {
-                step(u);
+                step(u, t0 + u);
                 // after the warp's last step of an epoch: refill its four slots with
                 // the steps kD later
                 if (u % 4 == 3) load4(u - 3);
@@ -257,7 +279,7 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
     #pragma unroll
         for (int u = 0; u < kD - 4; ++u) {
             if (t0 + u >= T) break;
-            step(u);
+            step(u, t0 + u);
             if (u + kGD < kD) rx[u % kGD] = gather(ri[(u + kGD) % kD], rb[(u + kGD) % kD]);
             if (u % kPnB == kPnB - 1) epoch_end(t0 + u);
         }
@@ -285,6 +307,10 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
             for (int k = 0; k < EB; ++k) {
                 const int i = i0 + k * kT;
                 if (i < nrl && sl[k] < 0x8000) {        // split rows: below
+                    if (CHK && sl[k] >= A.max_rows) {
+                        atomicAdd(A.dbg + 0, 1ull);
+                        continue;
+                    }
                     const double v = ys[sl[k]];
                     yb[d.row0 + i] = v;
                     mx = fmax(mx, fabs(v));
@@ -325,12 +351,10 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
 
 }  // namespace
 
-cudaError_t launch_panel(const PnArgs& a, cudaStream_t s) {
-    if (a.n_panels <= 0) return cudaSuccess;
-    // only the panel's y (and split-row fold lists) in shared memory: the rest
-    // of the 256 KB L1/shared array stays L1, which holds the loads in flight
-    const int64_t smem = panel_smem_bytes(a.max_rows, a.max_sslots, a.max_split_n);
-    if (smem > kPnSmemMax) return cudaErrorInvalidValue;   // the planner never builds such a panel
+namespace {
+
+template <bool CHK>
+cudaError_t launch_panel_t(const PnArgs& a, cudaStream_t s, int64_t smem) {
     // the opt-in shared-memory limit is a per-device function attribute: set
     // it once per device (a process may hold handles on several GPUs)
     static std::atomic<int> ready[kMaxDevices];
@@ -340,32 +364,45 @@ cudaError_t launch_panel(const PnArgs& a, cudaStream_t s) {
     const int di = dev < kMaxDevices ? dev : kMaxDevices - 1;
     if (!ready[di].load(std::memory_order_acquire) || dev >= kMaxDevices) {
         const int smax = (int)kPnSmemMax;
-        for (const void* k : {(const void*)spmv_panel_kernel<false, false>, (const void*)spmv_panel_kernel<false, true>,
-                              (const void*)spmv_panel_kernel<true, false>, (const void*)spmv_panel_kernel<true, true>})
+        for (const void* k : {(const void*)spmv_panel_kernel<false, false, CHK>, (const void*)spmv_panel_kernel<false, true, CHK>,
+                              (const void*)spmv_panel_kernel<true, false, CHK>, (const void*)spmv_panel_kernel<true, true, CHK>})
             if ((r = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smax)) != cudaSuccess)
                 return r;
         ready[di].store(1, std::memory_order_release);
     }
     const bool xs = a.x_split != INT32_MAX;
     if (a.gather_na) {
-        if (xs) spmv_panel_kernel<true, true><<<a.n_panels, kT, smem, s>>>(a);
-        else spmv_panel_kernel<true, false><<<a.n_panels, kT, smem, s>>>(a);
+        if (xs) spmv_panel_kernel<true, true, CHK><<<a.n_panels, kT, smem, s>>>(a);
+        else spmv_panel_kernel<true, false, CHK><<<a.n_panels, kT, smem, s>>>(a);
     } else {
-        if (xs) spmv_panel_kernel<false, true><<<a.n_panels, kT, smem, s>>>(a);
-        else spmv_panel_kernel<false, false><<<a.n_panels, kT, smem, s>>>(a);
+        if (xs) spmv_panel_kernel<false, true, CHK><<<a.n_panels, kT, smem, s>>>(a);
+        else spmv_panel_kernel<false, false, CHK><<<a.n_panels, kT, smem, s>>>(a);
     }
     return cudaGetLastError();
 }
 
+}  // namespace
+
+cudaError_t launch_panel(const PnArgs& a, cudaStream_t s) {
+    if (a.n_panels <= 0) return cudaSuccess;
+    // only the panel's y (and split-row fold lists) in shared memory: the rest
+    // of the 256 KB L1/shared array stays L1, which holds the loads in flight
+    int64_t smem = panel_smem_bytes(a.max_rows, a.max_sslots, a.max_split_n);
+    if (a.dbg) smem += 4 * (int64_t)(a.max_rows + 16);   // the checked variant's epoch stamps
+    if (smem > kPnSmemMax) return cudaErrorInvalidValue;   // the planner never builds such a panel
+    return a.dbg ? launch_panel_t<true>(a, s, smem) : launch_panel_t<false>(a, s, smem);
+}
 
 // Loads this file's kernels now (cudaFuncGetAttributes forces the lazy loader):
 // a kernel first launched while a peer rank's kernel spins on an exchange flag
 // would otherwise load its module then, and a module load can wait for the
-// running kernels -- the spinning one included (see host.cpp preload_kernels).
+// running kernels -- the spinning one included (see host.cpp).
 cudaError_t preload_kernels_panel() {
     cudaFuncAttributes fa;
-    for (const void* k : {(const void*)spmv_panel_kernel<false, false>, (const void*)spmv_panel_kernel<false, true>,
-                          (const void*)spmv_panel_kernel<true, false>, (const void*)spmv_panel_kernel<true, true>}) {
+    for (const void* k : {(const void*)spmv_panel_kernel<false, false, false>, (const void*)spmv_panel_kernel<false, true, false>,
+                          (const void*)spmv_panel_kernel<true, false, false>, (const void*)spmv_panel_kernel<true, true, false>,
+                          (const void*)spmv_panel_kernel<false, false, true>, (const void*)spmv_panel_kernel<false, true, true>,
+                          (const void*)spmv_panel_kernel<true, false, true>, (const void*)spmv_panel_kernel<true, true, true>}) {
         const cudaError_t e = cudaFuncGetAttributes(&fa, k);
         if (e != cudaSuccess) return e;
     }

@@ -188,6 +188,30 @@ spmv_status_t spmv_test_loopback_link(spmv_handle_t* handles, int32_t world) {
     return xchg_loopback_link(handles, world);
 }
 
+spmv_status_t spmv_test_corrupt_panel(spmv_handle_t h, int32_t kind) {
+    if (!valid(h) || kind < 1 || kind > 3) return fail(SPMV_ERR_USAGE, "corrupt_panel: bad arguments");
+    if (h->kernel != 7 || !h->pn.ok()) return fail(SPMV_ERR_UNSUPPORTED, "corrupt_panel: not a panel handle");
+    DeviceGuard g(h->device);
+    // panel 0, epoch 0: warp 0's and warp 1's 128-entry blocks, (lane, step) -> l * 4 + b
+    PnPanel p0;
+    CUDA_TRY(cudaMemcpy(&p0, h->pn.d_panel, sizeof p0, cudaMemcpyDeviceToHost));
+    uint32_t blk[256];
+    uint32_t* dev = h->pn.d_gidx + (int64_t)p0.g0 * 32;
+    CUDA_TRY(cudaMemcpy(blk, dev, sizeof blk, cudaMemcpyDeviceToHost));
+    const uint32_t mask = (1u << kPnDeltaBits) - 1u;
+    int a = -1, b = -1;   // a real entry of warp 0 and one of warp 1
+    for (int q = 0; q < 128 && a < 0; ++q)
+        if ((blk[q] >> kPnDeltaBits) < (uint32_t)h->pn.max_rows) a = q;
+    for (int q = 128; q < 256 && b < 0; ++q)
+        if ((blk[q] >> kPnDeltaBits) < (uint32_t)h->pn.max_rows) b = q;
+    if (a < 0 || b < 0) return fail(SPMV_ERR_UNSUPPORTED, "corrupt_panel: epoch 0 too sparse");
+    if (kind == 1) blk[b] = (blk[a] & ~mask) | (blk[b] & mask);              // warp 1 updates warp 0's row
+    if (kind == 2) blk[b] = ((uint32_t)(h->pn.max_rows + 100) << kPnDeltaBits) | (blk[b] & mask);   // slot
+    if (kind == 3) blk[b] = (blk[b] & ~mask) | mask;                           // column delta 2^17 - 1
+    CUDA_TRY(cudaMemcpy(dev, blk, sizeof blk, cudaMemcpyHostToDevice));
+    return SPMV_OK;
+}
+
 spmv_status_t spmv_test_rank_stream(spmv_handle_t h, void** stream) {
     if (!valid(h) || !stream) return fail(SPMV_ERR_USAGE, "rank_stream: bad arguments");
     if (!h->test_rank || !h->test_stream) return fail(SPMV_ERR_USAGE, "rank_stream: not a linked test rank");

@@ -80,3 +80,8 @@ def rank_stream(h):
     out = ctypes.c_void_p(0)
     _check(lib().spmv_test_rank_stream(_h(h), ctypes.byref(out)), "spmv_test_rank_stream")
     return torch.cuda.ExternalStream(out.value)
+
+
+def corrupt_panel(h, kind: int) -> None:
+    """Corrupt a panel handle's plan on the device (tests of debug_checks)."""
+    _check(lib().spmv_test_corrupt_panel(_h(h), kind), "spmv_test_corrupt_panel")

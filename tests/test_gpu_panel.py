@@ -10,6 +10,7 @@ import pytest
 
 import oracle
 import paper_1203_2739_b200 as sp
+import paper_1203_2739_b200.testing as T
 import synth
 from gpu_util import assert_parity, create, gpu_apply, oracle_permuted
 from gpu_util import panel
@@ -137,3 +138,46 @@ def test_split_rowmajor_kernel():
     assert_parity(y, yref, None, exact=True, what="split row-major")
 
 
+
+
+# ---------------------------------------- debug checks (sanitizer stand-in)
+@pytest.mark.parametrize("name,opts,split", [
+    ("c5s", dict(kernel="panel", panel_rows=2000), False),
+    ("c4s", dict(kernel="panel", panel_rows=2000), False),
+    ("c1", dict(kernel="panel", panel_rows=700), False),
+    ("c3s", dict(split_kernel="panel", panel_rows=900), True),
+    ("_c5like_dbg", dict(kernel="panel", panel_rows=16384), False)])
+def test_debug_checks_clean(name, opts, split):
+    """compute-sanitizer is closed on this GPU pool, so the panel kernel has a
+    checked variant (spmv_options_t.debug_checks): every y slot and x column
+    bounds-checked, every y update stamping its slot with the epoch.  On the
+    planner's output it must count no violation -- the shared-memory y
+    updates of an epoch never race (distinct rows) -- and still match the
+    oracle."""
+    if name == "_c5like_dbg":
+        synth.PRESETS[name] = lambda **kw: synth._sb(2, 40_000, 39_200, 800, 12, 20, 0, 3, **kw)
+    p = synth.make(name)
+    h = create(p, options=dict(opts, debug_checks=1))
+    x = p.x()
+    if split:
+        y = gpu_apply(h, x, p.m, split=True)
+        assert_parity(y, oracle.split(p.row_ptr, p.col, p.val, p.parts, p.n_parts, x),
+                      oracle.spmv(p.row_ptr, p.col, p.val, x)[1], what=name)
+    else:
+        xh, yh, S = oracle_permuted(p, x)
+        assert_parity(gpu_apply(h, xh, p.m), yh, S, what=name)
+    assert sp.spmv_get_info(h)["debug_violations"] == [0, 0, 0]
+    sp.spmv_destroy(h)
+
+
+@pytest.mark.parametrize("kind,slot", [(1, 2), (2, 0), (3, 1)])
+def test_debug_checks_have_teeth(kind, slot):
+    """A corrupted plan is caught: a row updated twice in one epoch (a
+    shared-memory race), a y slot out of bounds, an x column out of bounds."""
+    p = synth.make("c5s", scramble=0)
+    h = create(p, options=dict(kernel="panel", panel_rows=2000, debug_checks=1))
+    T.corrupt_panel(h, kind)
+    gpu_apply(h, oracle_permuted(p, p.x())[0], p.m)
+    v = sp.spmv_get_info(h)["debug_violations"]
+    assert v[slot] > 0, v
+    sp.spmv_destroy(h)
