@@ -768,7 +768,10 @@ def run_ours(args, rank, world, local_rank):
             "gpu_launches": launches_per_step * K,
             "clocks": clk.summary(),
             "parity": parity,
-            "setup_s": {"generate": t_gen, "create": t_create},
+            "setup_s": {"generate": t_gen, "create": t_create,
+                        "create_phases": dict(zip(("validate_descriptor_shard", "permute", "tiles_csr_upload",
+                                                   "split_layouts", "panel_plans_upload", "maps_buffers"),
+                                                  [round(v, 3) for v in info["create_s"]]))},
             **extra,
         }
         print(json.dumps(line), flush=True)

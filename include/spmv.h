@@ -241,6 +241,10 @@ typedef struct {
     int64_t debug_violations[3];  /* debug_checks: y slots out of bounds, x columns out of bounds, rows
                                      updated twice in one epoch (all 0 on a correct plan; reading them
                                      synchronises the device) */
+    double create_s[6];           /* spmv_create's wall time by phase (s): validation + descriptor +
+                                     shard; permutation of the rows; tiles + CSR upload; split layouts;
+                                     panel plans + upload; maps and buffers (the ingest cost of Table 3's
+                                     amortization) */
 } spmv_info_t;
 
 spmv_status_t spmv_get_info(spmv_handle_t h, spmv_info_t* info);

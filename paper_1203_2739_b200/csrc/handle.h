@@ -126,6 +126,7 @@ struct spmv_plan_s {
     int64_t n_seg = 0;
     int64_t bytes_alg = 0, bytes_alg_split = 0, bytes_stream = 0;
     int64_t index_bytes = 4;          // row-tile column ids: 4, or 2 with the f3 16-bit ids
+    double create_s[6] = {0, 0, 0, 0, 0, 0};   // spmv_info_t.create_s
     bool has_perm = false;
     bool has_owner = false;
     int kernel = 0;                   // 7 column-sorted panels, 0 row tiles

@@ -16,6 +16,7 @@
 //   a9         : max-abs and x-update glue for the power iterations
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -430,6 +431,13 @@ spmv_status_t create_impl(int64_t m, int64_t n, int64_t nnz, const int64_t* row_
                           const double* val, const int32_t* row_perm, const int32_t* col_perm,
                           const spmv_blocks_t* blocks, int32_t n_parts, const int32_t* part_of_nnz,
                           const spmv_dist_t* dist, const spmv_options_t* options, bool test_rank, spmv_plan_s* h) {
+    // create phases (spmv_info_t.create_s): wall seconds since the previous mark
+    auto t_last = std::chrono::steady_clock::now();
+    auto mark = [&](int k) {
+        const auto now = std::chrono::steady_clock::now();
+        h->create_s[k] += std::chrono::duration<double>(now - t_last).count();
+        t_last = now;
+    };
     // ---------------------------------------------------------- arguments
     h->opt = default_options();
     if (options) {
@@ -611,6 +619,7 @@ spmv_status_t create_impl(int64_t m, int64_t n, int64_t nnz, const int64_t* row_
     // From here on every failure is local to this rank: it is recorded in
     // local_status and all ranks agree on the outcome at the end.
     spmv_status_t local_status = SPMV_OK;
+    mark(0);   // validation, block descriptor, shard, communicator
     auto run_local = [&]() -> spmv_status_t {
         // --------------------------------------- permute the local rows (a1)
         // new row p has the entries of old row row_inv[p], columns mapped
@@ -743,6 +752,7 @@ spmv_status_t create_impl(int64_t m, int64_t n, int64_t nnz, const int64_t* row_
             if (env == 2) return fail(SPMV_ERR_UNSUPPORTED, "DB across GPUs: part k must hold block k's rows");
         }
 
+        mark(1);   // permutation of the local rows
         // -------------------------------------- local column ids (x layout)
         // world 1: global permuted ids.  world > 1: [interior | full C_B]: the
         // kernel reads c < x_int_len from the user's x, the rest from the
@@ -892,6 +902,7 @@ spmv_status_t create_impl(int64_t m, int64_t n, int64_t nnz, const int64_t* row_
             }
         }
 
+        mark(2);   // tiles, CSR upload, f3 ids
         // -------------------------------------------- split layout (a8)
         // Within each row tile the nonzeros are regrouped part-major: for k =
         // 0..K-1, the tile's rows' part-k runs ("segments") in row order --
@@ -1007,6 +1018,7 @@ spmv_status_t create_impl(int64_t m, int64_t n, int64_t nnz, const int64_t* row_
             h->blk_slots = loc;
         }
 
+        mark(3);   // split layouts
         // ---------------- fused multiple-SpMxV on panels (a8): (row, part) virtual rows
         if (n_parts && !db_dist && nnz_loc > 0 && O.split_kernel != SPMV_SPLIT_ROWS) {
             if ((s = plan_pn(h, h->pns, rp, pcol, pval, rbp, cbp, &ppart,
@@ -1035,6 +1047,7 @@ spmv_status_t create_impl(int64_t m, int64_t n, int64_t nnz, const int64_t* row_
             return fail(SPMV_ERR_UNSUPPORTED, "world > 1 runs the panel kernel");
         }
 
+        mark(4);   // panel plans and their upload
         // -------------------------------------- ORIGINAL-mode maps (a3, a7)
         if (world == 1 && h->has_perm) {
             if ((s = upload(h, &h->d_colinv, col_inv.data(), n))) return s;
@@ -1156,6 +1169,7 @@ spmv_status_t create_impl(int64_t m, int64_t n, int64_t nnz, const int64_t* row_
         return SPMV_OK;
     };
     local_status = run_local();
+    mark(5);   // maps, buffers, exchange allocation
     if (world > 1 && !test_rank) {   // every rank returns the same status (after all planning)
         spmv_status_t agreed = SPMV_OK;
         spmv_status_t r = xchg_agree(h, local_status, &agreed);
@@ -1432,6 +1446,7 @@ spmv_status_t spmv_get_info(spmv_handle_t h, spmv_info_t* info) {
     info->y_border_len = h->y_bord_len;
     info->exchange_timeouts = xchg_timeouts(h);
     info->index_bytes = h->index_bytes;
+    for (int k = 0; k < 6; ++k) info->create_s[k] = h->create_s[k];
     for (int k = 0; k < 3; ++k) info->debug_violations[k] = 0;
     if (h->d_dbg) {
         DeviceGuard g(h->device);
