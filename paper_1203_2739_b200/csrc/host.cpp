@@ -299,35 +299,48 @@ spmv_status_t plan_pn(spmv_plan_s* h, PanelPlan& pl, const std::vector<int64_t>&
     // padding lanes: the planner's dummy index of bank b becomes the scratch
     // y slot max_rows + b (delta 0: a valid x read, times the value 0)
     const uint32_t dummy_dev = (uint32_t)pl.max_rows << kPnDeltaBits;
+    // device layout of the group stream (panel.cu): per (epoch, warp) a
+    // 128-entry block; values as (step pair, lane, step & 1), indices as
+    // (lane, step), so 16-byte loads cover 2 / 4 of a warp's steps.  Built for
+    // batches of consecutive panels in parallel (their groups are contiguous
+    // on the device), one copy per batch and array.
     std::vector<double> tv;
     std::vector<uint32_t> ti;
-    for (int64_t p = 0; p < P; ++p) {
-        PnPanelData& D = pd[p];
-        const int64_t g0 = D.desc.g0, ng = (int64_t)D.gbase.size();
-        if (ng) {
-            // device layout of the group stream (panel.cu): per (epoch, warp) a
-            // 128-entry block; values as (step pair, lane, step & 1), indices as
-            // (lane, step), so 16-byte loads cover 2 / 4 of a warp's steps
-            tv.resize(ng * 32);
-            ti.resize(ng * 32);
-            for (int64_t g = 0; g < ng; ++g) {
+    std::vector<int32_t> tb;
+    for (int64_t p0 = 0; p0 < P;) {
+        int64_t p1 = p0, ng = 0;
+        while (p1 < P && (ng == 0 || ng + (int64_t)pd[p1].gbase.size() <= (int64_t(1) << 20))) ng += (int64_t)pd[p1++].gbase.size();
+        const int64_t gb = pd[p0].desc.g0;
+        tv.resize(ng * 32);
+        ti.resize(ng * 32);
+        tb.resize(ng);
+#pragma omp parallel for schedule(dynamic, 1)
+        for (int64_t p = p0; p < p1; ++p) {
+            PnPanelData& D = pd[p];
+            const int64_t off = (int64_t)D.desc.g0 - gb, n = (int64_t)D.gbase.size();
+            for (int64_t g = 0; g < n; ++g) {
                 const int64_t q = g / kPnWarps, w = g % kPnWarps;   // g = (e * 4 + b) * 16 + w
                 const int64_t e = q / kPnB, b = q % kPnB;
-                const int64_t blk = (e * kPnWarps + w) * 128;
+                const int64_t blk = (off + (e * kPnWarps + w) * kPnB) * 32;
                 for (int l = 0; l < 32; ++l) {
                     tv[blk + (b / 2) * 64 + l * 2 + (b & 1)] = D.gval[g * 32 + l];
                     const uint32_t i = D.gidx[g * 32 + l];
-                    ti[blk + l * 4 + b] = pn_is_dummy(i) ? dummy_dev + (((i >> kPnDeltaBits) - kPnDummyRow) << kPnDeltaBits) : i;
+                    ti[blk + l * 4 + b] =
+                        pn_is_dummy(i) ? dummy_dev + (((i >> kPnDeltaBits) - kPnDummyRow) << kPnDeltaBits) : i;
                 }
             }
-            CUDA_TRY(cudaMemcpy(pl.d_gval + g0 * 32, tv.data(), ng * 32 * 8, cudaMemcpyHostToDevice));
-            CUDA_TRY(cudaMemcpy(pl.d_gidx + g0 * 32, ti.data(), ng * 32 * 4, cudaMemcpyHostToDevice));
-            CUDA_TRY(cudaMemcpy(pl.d_gbase4 + g0, D.gbase4.data(), ng * 4, cudaMemcpyHostToDevice));
+            std::copy(D.gbase4.begin(), D.gbase4.end(), tb.begin() + off);
+            std::vector<double>().swap(D.gval);
+            std::vector<uint32_t>().swap(D.gidx);
+            std::vector<int32_t>().swap(D.gbase);
+            std::vector<int32_t>().swap(D.gbase4);
         }
-        std::vector<double>().swap(D.gval);
-        std::vector<uint32_t>().swap(D.gidx);
-        std::vector<int32_t>().swap(D.gbase);
-        std::vector<int32_t>().swap(D.gbase4);
+        if (ng) {
+            CUDA_TRY(cudaMemcpy(pl.d_gval + gb * 32, tv.data(), ng * 32 * 8, cudaMemcpyHostToDevice));
+            CUDA_TRY(cudaMemcpy(pl.d_gidx + gb * 32, ti.data(), ng * 32 * 4, cudaMemcpyHostToDevice));
+            CUDA_TRY(cudaMemcpy(pl.d_gbase4 + gb, tb.data(), ng * 4, cudaMemcpyHostToDevice));
+        }
+        p0 = p1;
     }
     pl.panels = P;
     pl.groups = G;

@@ -116,15 +116,20 @@ void colour_slots(int32_t nr, const std::vector<Ent>& ents, int64_t G, std::vect
         for (int k = 0; k < SPMV_PN_WPOW; ++k) v *= c;
         W[c] = v;
     }
-    auto gain_move = [&](int32_t r, int b1, int b2, int32_t other) {
-        // cost change of moving r from b1 to b2 (groups also holding `other` are skipped: swapped pair cancels)
+    // groups of the swap partner, marked once per candidate pair (a group
+    // holding both rows of a swap keeps its counts: the moves cancel)
+    std::vector<uint32_t> gmark(std::max<int64_t>(G, 1), 0);
+    uint32_t tag = 0;
+    auto mark_groups = [&](int32_t r) {
+        ++tag;
+        for (int32_t q = rg_ptr[r]; q < rg_ptr[r + 1]; ++q) gmark[rg[q]] = tag;
+    };
+    auto gain_move = [&](int32_t r, int b1, int b2) {
+        // cost change of moving r from b1 to b2, skipping the marked groups
         int64_t d = 0;
         for (int32_t q = rg_ptr[r]; q < rg_ptr[r + 1]; ++q) {
             const int64_t g = rg[q];
-            bool both = false;
-            for (int32_t u = rg_ptr[other]; u < rg_ptr[other + 1]; ++u)
-                if (rg[u] == g) { both = true; break; }
-            if (both) continue;
+            if (gmark[g] == tag) continue;
             d += W[cnt[g * 16 + b2] + 1] - W[cnt[g * 16 + b2]] + W[cnt[g * 16 + b1] - 1] - W[cnt[g * 16 + b1]];
         }
         return d;
@@ -148,7 +153,10 @@ void colour_slots(int32_t nr, const std::vector<Ent>& ents, int64_t G, std::vect
                 const int b2 = (b1 + 1 + (int)(rnd() % 15)) & 15;
                 if (of_bank[b2].empty()) continue;
                 const int32_t s2 = of_bank[b2][rnd() % of_bank[b2].size()];
-                const int64_t d = gain_move(r, b1, b2, s2) + gain_move(s2, b2, b1, r);
+                mark_groups(s2);
+                int64_t d = gain_move(r, b1, b2);
+                mark_groups(r);
+                d += gain_move(s2, b2, b1);
                 if (d < best) { best = d; bs = s2; }
             }
             if (bs >= 0) {
@@ -200,20 +208,14 @@ double y_wavefronts(const uint32_t* idx) {
 // to minimise max_b a_b + max_b (c_b - a_b) -- the access's wavefronts (an
 // alternating split pays 4 for two banks of 3 entries, this one 3).  Each
 // half's padding lanes share the scratch slot of its least loaded bank.
-void emit_group(const Ent* e, int32_t base, const std::vector<int32_t>& slot, PnPanelData& P) {
-    int c[16] = {0}, n = 0, m = 0;
-    const Ent* byb[16][32];
-    for (int k = 0; k < 32; ++k)
-        if (e[k].row >= 0) {
-            const int b = slot[e[k].row] & 15;
-            byb[b][c[b]++] = &e[k];
-            m = std::max(m, c[b]);
-            ++n;
-        }
-    int a[16] = {0};
-    bool found = false;
-    for (int S = m; S <= 2 * m + 2 && !found; ++S)
-        for (int T0 = (S + 1) / 2; T0 <= S && !found; ++T0) {
+// The half-warp split of a group's banks: bank b's c_b entries, a_b of them
+// in half 0 -- minimising max_b a_b + max_b (c_b - a_b) with at most 16 lanes
+// per half.  Returns that cost (each half counted at least 1: the padding
+// lanes of a half share the scratch slot of its least loaded bank).
+int split_banks(const int c[16], int n, int m, int a[16]) {
+    for (int b = 0; b < 16; ++b) a[b] = 0;
+    for (int S = m; S <= 2 * m + 2; ++S)
+        for (int T0 = (S + 1) / 2; T0 <= S; ++T0) {
             const int T1 = S - T0;
             int lo_s = 0, hi_s = 0;
             bool ok = true;
@@ -231,8 +233,28 @@ void emit_group(const Ent* e, int32_t base, const std::vector<int32_t>& slot, Pn
                 a[b] += add;
                 tot += add;
             }
-            found = true;
+            int m0 = 0, m1 = 0;
+            for (int b = 0; b < 16; ++b) {
+                m0 = std::max(m0, a[b]);
+                m1 = std::max(m1, c[b] - a[b]);
+            }
+            return std::max(m0, 1) + std::max(m1, 1);
         }
+    return 2 * m;
+}
+
+void emit_group(const Ent* e, int32_t base, const std::vector<int32_t>& slot, PnPanelData& P) {
+    int c[16] = {0}, n = 0, m = 0;
+    const Ent* byb[16][32];
+    for (int k = 0; k < 32; ++k)
+        if (e[k].row >= 0) {
+            const int b = slot[e[k].row] & 15;
+            byb[b][c[b]++] = &e[k];
+            m = std::max(m, c[b]);
+            ++n;
+        }
+    int a[16];
+    split_banks(c, n, m, a);
     uint32_t idx[32];
     double val[32];
     int nh[2] = {0, 0}, load[2][16] = {};
@@ -402,12 +424,15 @@ void build_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col
     std::vector<int32_t> ident(nr);
     for (int32_t r = 0; r < (int32_t)nr; ++r) ident[r] = r;
     if (nr > 0x7FFF) return;   // caller rejects the plan (slot field)
-    {   // statistics: natural slots
-        PnPanelData tmp;
+    {   // statistics: predicted y wavefronts with natural slots (slot = virtual row)
         double w = 0;
         for (int64_t g = 0; g < G; ++g) {
-            emit_group(&gents[g * 32], gbases[g], ident, tmp);
-            w += y_wavefronts(&tmp.gidx[g * 32]);
+            int c[16] = {0}, n = 0, m = 0, a[16];
+            for (int k = 0; k < 32; ++k) {
+                const int32_t r = gents[g * 32 + k].row;
+                if (r >= 0) m = std::max(m, ++c[r & 15]), ++n;
+            }
+            w += split_banks(c, n, m, a);
         }
         P.ywf0 = G ? w / G : 0;
     }
