@@ -706,6 +706,42 @@ def run_ours(args, rank, world, local_rank):
             del xb_
         del xs_, ys_
 
+    # ---------------- the smem-staging effect: the x-staged
+    # kernel (each CTA stages its SB block's x(C_k) + x(C_B) in shared
+    # memory) against the default, same protocol; only where it fits
+    xs_fits = False
+    if world == 1 and p.blocks is not None and int(p.blocks.get("kind", 0)) == 1 and not split:
+        cb_ = np.asarray(p.blocks["col_block_ptr"])
+        K_ = int(p.blocks["K"])
+        xs_fits = int(np.max(np.diff(cb_[:K_ + 1]))) + int(cb_[K_ + 1] - cb_[K_]) <= 227 * 1024 // 8
+    if xs_fits:
+        try:
+            hx = sp.spmv_create(p.m, p.n, p.row_ptr, p.col, p.val, row_perm=p.row_perm, col_perm=p.col_perm,
+                                blocks=p.blocks, options=dict(kernel="xstaged"))
+        except sp.SpmvError:
+            hx = None
+        if hx is not None:
+            xq_ = torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+            yq_ = torch.empty(p.m, dtype=torch.float64, device=dev)
+            for _ in range(3):
+                sp.spmv_apply(hx, xq_, yq_, sp.SPMV_VEC_ORIGINAL, stream=stream)
+            xh_ = torch.empty_like(xq_)
+            xh_[torch.from_numpy(np.asarray(p.col_perm).astype(np.int64)).to(dev)] = xq_
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(10)]
+            for a_, b_ in evs:
+                if l2_flush:
+                    flush_buf.fill_(1.0)
+                a_.record(stream)
+                sp.spmv_apply(hx, xh_, yq_, stream=stream)
+                b_.record(stream)
+            torch.cuda.synchronize()
+            xms = statistics.median([a_.elapsed_time(b_) for a_, b_ in evs])
+            extra["xstaged"] = {"spmv_ms": xms, "default_spmv_ms": avg_spmv_ms, "speedup_vs_default": avg_spmv_ms / xms,
+                                "note": "x-staged kernel (block x in shared memory, 16-bit block-local ids) vs the "
+                                        "default kernel, same L2 protocol"}
+            sp.spmv_destroy(hx)
+            del xq_, yq_, xh_
+
     # ---------------- cuSPARSE comparator (informational): the
     # vendor CSR SpMV (torch.mv on a CSR tensor -> cusparseSpMV, fp64, int32
     # indices) on the same reordered matrix, same L2 protocol; not the product

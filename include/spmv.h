@@ -108,14 +108,17 @@ enum {
 
 /* Create-time options (spmv_create_ex; NULL = all defaults).  Zero means
  * "automatic" in every field. */
-enum { SPMV_KERNEL_AUTO = 0, SPMV_KERNEL_PANEL = 1, SPMV_KERNEL_ROWTILE = 2 };
+enum { SPMV_KERNEL_AUTO = 0, SPMV_KERNEL_PANEL = 1, SPMV_KERNEL_ROWTILE = 2, SPMV_KERNEL_XSTAGED = 3 };
 enum { SPMV_SPLIT_AUTO = 0, SPMV_SPLIT_PANEL = 1, SPMV_SPLIT_ROWS = 2 };
 enum { SPMV_EXCHANGE_AUTO = 0, SPMV_EXCHANGE_NCCL = 1, SPMV_EXCHANGE_P2P = 2 };
 typedef struct {
     int32_t struct_size;     /* sizeof(spmv_options_t) (forward compatibility), or 0 */
-    int32_t kernel;          /* single SpMxV: AUTO = column-sorted panels unless the plan pads > 25 %
+    int32_t kernel;          /* single SpMxV: AUTO = column-sorted panels unless their plan pads > 25 %
                                 (then row tiles); PANEL forces the panels (whatever the padding);
-                                ROWTILE forces row tiles */
+                                ROWTILE forces row tiles; XSTAGED (1 GPU, SB): each CTA stages its
+                                block's x(C_k) and x(C_B) in shared memory once and gathers from
+                                there (the cache-fit rule of P:L61) -- UNSUPPORTED when a block's x
+                                does not fit; not chosen by AUTO (slower than row tiles on C2) */
     int32_t panel_rows;      /* y slots per panel; 0 = automatic (whole waves of ~16 K-slot panels) */
     int32_t split_kernel;    /* fused multiple-SpMxV: AUTO / PANEL (a y slot per (row, part) segment) /
                                 ROWS (row-major part segments, row tiles) */
@@ -223,7 +226,8 @@ typedef struct {
     int64_t bytes_stream;         /* device bytes the apply kernel actually reads + writes (no x reuse) */
     int32_t n_parts, rank, world, kind;
     int32_t has_owner_map;        /* spmv_normalize is available */
-    int32_t kernel;               /* single-SpMxV kernel: 7 column-sorted panels, 0 row tiles */
+    int32_t kernel;               /* single-SpMxV kernel: 7 column-sorted panels, 0 row tiles,
+                                     8 x-staged (SB blocks' x in shared memory) */
     int32_t split_kernel;         /* fused multiple-SpMxV: 7 panels with one y slot per (row, part)
                                      segment, 3 row-major part segments; 0 without a split */
     int32_t exchange;             /* world > 1: 1 NCCL, 2 P2P copy engines (overlapped), 3 loopback (test) */

@@ -42,7 +42,7 @@ EXPORTED = ["spmv_create", "spmv_create_ex", "spmv_apply", "spmv_split_apply", "
 EXPORTED_TEST = ["spmv_debug_copy_csr", "spmv_pn_plan_check", "spmv_pn_shard_hash", "spmv_test_create_rank",
                  "spmv_test_loopback_link", "spmv_test_rank_stream", "spmv_test_corrupt_panel"]
 
-KERNELS = {"auto": 0, "panel": 1, "rowtile": 2}
+KERNELS = {"auto": 0, "panel": 1, "rowtile": 2, "xstaged": 3}
 SPLIT_KERNELS = {"auto": 0, "panel": 1, "rows": 2}
 EXCHANGES = {"auto": 0, "nccl": 1, "p2p": 2}
 

@@ -37,6 +37,7 @@ SOURCES = {
     "split.cu": "cu",
     "panel.cu": "cu",
     "order.cu": "cu",
+    "xstaged.cu": "cu",
     "plan_panel.cpp": "cpp",
     "host.cpp": "cpp",
     "exchange.cpp": "cpp",

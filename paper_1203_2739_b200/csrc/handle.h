@@ -136,6 +136,9 @@ struct spmv_plan_s {
     int32_t* d_col = nullptr;         // [nnz_loc + pad] local column ids
     unsigned long long* d_dbg = nullptr;   // debug_checks: violation counters [3]
     uint16_t* d_col16 = nullptr;      // f3: [nnz_loc + pad] 16-bit tile-local column ids (or nullptr)
+    uint16_t* d_colx = nullptr;       // x-staged kernel: [nnz_loc + pad] 16-bit block-local ids
+    spmvb::XsCta* d_xcta = nullptr;   // x-staged kernel: per CTA its tiles and x slices
+    int32_t xs_ncta = 0, xs_max_x = 0;
     int4* d_tile_base = nullptr;      // f3: [T] per tile (lo, hi, split, largest column)
     double* d_val = nullptr;          // [nnz_loc + pad]
     int32_t* d_tile_row = nullptr;    // [T+1]

@@ -76,6 +76,7 @@ template spmv_status_t dalloc<unsigned long long>(spmv_plan_s*, unsigned long lo
 template spmv_status_t upload<int32_t>(spmv_plan_s*, int32_t**, const int32_t*, size_t, size_t);
 template spmv_status_t upload<uint16_t>(spmv_plan_s*, uint16_t**, const uint16_t*, size_t, size_t);
 template spmv_status_t upload<int4>(spmv_plan_s*, int4**, const int4*, size_t, size_t);
+template spmv_status_t upload<XsCta>(spmv_plan_s*, XsCta**, const XsCta*, size_t, size_t);
 
 void free_plan(spmv_plan_s* h) {
     if (!h) return;
@@ -460,8 +461,9 @@ spmv_status_t create_impl(int64_t m, int64_t n, int64_t nnz, const int64_t* row_
         h->opt.struct_size = (int32_t)sizeof(spmv_options_t);
     }
     const spmv_options_t& O = h->opt;
-    if (O.kernel < 0 || O.kernel > 2 || O.split_kernel < 0 || O.split_kernel > 2 || O.exchange < 0 ||
-        O.exchange > 2 || O.panel_rows < 0)
+    if (O.kernel < 0 || O.kernel > 3 || O.split_kernel < 0 || O.split_kernel > 2 || O.exchange < 0 ||
+        O.exchange > 2 || O.panel_rows < 0 || O.index16 < 0 || O.index16 > 1 || O.debug_checks < 0 ||
+        O.debug_checks > 1)
         return fail(SPMV_ERR_USAGE, "bad options");
     if (m < 0 || n < 0 || nnz < 0) return fail(SPMV_ERR_USAGE, "negative dimension");
     if (!row_ptr) return fail(SPMV_ERR_USAGE, "row_ptr is NULL");
@@ -819,7 +821,7 @@ spmv_status_t create_impl(int64_t m, int64_t n, int64_t nnz, const int64_t* row_
             const int di = h->device >= 0 && h->device < kMaxDevices ? h->device : kMaxDevices - 1;
             if (!loaded[di].load(std::memory_order_acquire)) {
                 for (cudaError_t (*f)() : {preload_kernels_misc, preload_kernels_panel, preload_kernels_rowtile,
-                                           preload_kernels_split}) {
+                                           preload_kernels_split, preload_kernels_xstaged}) {
                     const cudaError_t e = f();
                     if (e != cudaSuccess) return fail(SPMV_ERR_INTERNAL, "kernel preload: %s", cudaGetErrorString(e));
                 }
@@ -1040,12 +1042,92 @@ spmv_status_t create_impl(int64_t m, int64_t n, int64_t nnz, const int64_t* row_
             if (world > 1 && !h->pns.ok())
                 return fail(SPMV_ERR_UNSUPPORTED, "world > 1: the split's panel plan cannot be built");
         }
+        // ------------------ single SpMxV: x-staged SB blocks (Eq.(1))
+        // world 1, SB: when every block's x(C_k) + x(C_B) fits one SM's shared
+        // memory beside the tile buffers, each CTA stages its block's slice
+        // once and gathers from shared memory (C2: 11,875 + 10,000 entries)
+        h->kernel = 0;
+        // (measured slower than the row tiles on C2, so only on request)
+        const bool xs_try = world == 1 && h->kind == SPMV_SB && nnz_loc > 0 && T > 0 &&
+                            O.kernel == SPMV_KERNEL_XSTAGED;
+        if (xs_try) {
+            const int64_t nB = cbp[K + 1] - cbp[K];
+            int64_t max_x = 0;
+            for (int k = 0; k < K; ++k) max_x = std::max<int64_t>(max_x, cbp[k + 1] - cbp[k] + nB);
+            const bool fits = xstaged_smem_bytes(max_x) <= kPnSmemMax && max_x <= 65536;
+            if (!fits && O.kernel == SPMV_KERNEL_XSTAGED)
+                return fail(SPMV_ERR_UNSUPPORTED, "x-staged kernel: a block's x(C_k) + x(C_B) (%lld entries) "
+                                                  "does not fit shared memory", (long long)max_x);
+            if (fits) {
+                // tiles of each block (tiles never cross a block: cuts at rbp)
+                std::vector<int32_t> tile_blk(T);
+                for (int64_t t = 0; t < T; ++t) tile_blk[t] = row_block(R0 + tile_row[t]);
+                bool ok = true;
+                for (int64_t t = 0; t < T && ok; ++t) ok = tile_blk[t] < K;
+                if (ok) {
+                    // block-local ids
+                    std::vector<uint16_t> cx(nnz_loc + kPad, 0);
+#pragma omp parallel for schedule(dynamic, 64)
+                    for (int64_t t = 0; t < T; ++t) {
+                        const int k = tile_blk[t];
+                        const int64_t q0 = cbp[k], nk = cbp[k + 1] - cbp[k];
+                        for (int64_t e = rp[tile_row[t]]; e < rp[tile_row[t + 1]]; ++e) {
+                            const int64_t c = pcol[e];
+                            cx[e] = (uint16_t)(c < cbp[K] ? c - q0 : nk + (c - cbp[K]));
+                        }
+                    }
+                    // CTAs: about one per SM, shared among the blocks by nonzeros,
+                    // each a contiguous run of its block's tiles balanced by nonzeros
+                    const int64_t sms = kernel_num_sms();
+                    std::vector<XsCta> ctas;
+                    int64_t t = 0;
+                    for (int k = 0; k < K; ++k) {
+                        const int64_t ta = t;
+                        while (t < T && tile_blk[t] == k) ++t;
+                        if (t == ta) continue;
+                        const int64_t za = rp[tile_row[ta]], zb = rp[tile_row[t]];
+                        const int64_t nc = std::max<int64_t>(1, std::min<int64_t>(t - ta,
+                                               (sms * (zb - za) + nnz_loc / 2) / std::max<int64_t>(nnz_loc, 1)));
+                        int64_t u = ta;
+                        for (int64_t j = 0; j < nc; ++j) {
+                            const int64_t target = za + (zb - za) * (j + 1) / nc;
+                            int64_t v = u + 1;
+                            while (v < t && rp[tile_row[v]] < target) ++v;
+                            if (j == nc - 1) v = t;
+                            if (v <= u) continue;
+                            XsCta c{};
+                            c.t0 = (int32_t)u;
+                            c.t1 = (int32_t)v;
+                            c.q0 = (int32_t)cbp[k];
+                            c.nk = (int32_t)(cbp[k + 1] - cbp[k]);
+                            c.qB = (int32_t)cbp[K];
+                            c.nB = (int32_t)nB;
+                            c.k = k;
+                            {   // lanes per row for the warp-independent form: ~ mean row length / 3
+                                const int64_t rows = tile_row[v] - tile_row[u];
+                                const int64_t nz = rp[tile_row[v]] - rp[tile_row[u]];
+                                int32_t V = 1;
+                                while (V < 32 && V * 3 < (rows ? nz / rows : 1)) V *= 2;
+                                c.pad = V;
+                            }
+                            ctas.push_back(c);
+                            u = v;
+                        }
+                    }
+                    if ((s = upload(h, &h->d_colx, cx.data(), nnz_loc + kPad))) return s;
+                    if ((s = upload(h, &h->d_xcta, ctas.data(), ctas.size()))) return s;
+                    h->xs_ncta = (int32_t)ctas.size();
+                    h->xs_max_x = (int32_t)max_x;
+                    h->kernel = 8;
+                    h->bytes_stream = 10 * nnz_loc + 4 * (m_loc + 1) + 8 * m_loc;
+                }
+            }
+        }
         // ------------------------------ single SpMxV: column-sorted panels (a5-a7)
         // any matrix at world 1 (C4: 0.18 vs 0.26 ms for the row-tile kernel);
         // small matrices fall back to row tiles through the padding test; at
         // world > 1 the panel kernel is the only one with the border wait
-        h->kernel = 0;
-        if (nnz_loc > 0 && O.kernel != SPMV_KERNEL_ROWTILE) {
+        if (h->kernel == 0 && nnz_loc > 0 && O.kernel != SPMV_KERNEL_ROWTILE && O.kernel != SPMV_KERNEL_XSTAGED) {
             std::string why;
             if ((s = plan_pn(h, h->pn, rp, pcol, pval, rbp, cbp, nullptr, O.kernel == SPMV_KERNEL_PANEL || world > 1,
                              &why)))
@@ -1367,6 +1449,21 @@ spmv_status_t run(spmv_handle_t h, const double* x, double* y, uint32_t flags, c
         X.dbg = h->d_dbg;
         X.x_cols = h->world > 1 ? h->x_int_len + h->border_total : h->n;
         CUDA_TRY(launch_panel(X, st));
+    } else if (!split && h->kernel == 8) {
+        XsArgs Q{};
+        Q.cta = h->d_xcta;
+        Q.n_cta = h->xs_ncta;
+        Q.max_x = h->xs_max_x;
+        Q.tile_row = h->d_tile_row;
+        Q.tile_nnz = h->d_tile_nnz;
+        Q.tile_cls = h->d_tile_cls;
+        Q.rowptr = h->d_rowptr;
+        Q.colx = h->d_colx;
+        Q.val = h->d_val;
+        Q.x = xk;
+        Q.y = yk;
+        Q.maxabs_slots = slots;
+        CUDA_TRY(launch_xstaged(Q, st));
     } else if (!split) {
         RowTileArgs P{};
         P.tile_row = h->d_tile_row;

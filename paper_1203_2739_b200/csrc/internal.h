@@ -65,6 +65,32 @@ struct RowTileArgs {
     const int4* tile_base;     // [T] (lo, hi, split, largest column of the tile)
 };
 cudaError_t launch_rowtile(const RowTileArgs& a, bool xsplit, cudaStream_t s);
+
+// x-staged SB kernel (xstaged.cu): one CTA per range of row tiles of one SB
+// block, x(C_k) and x(C_B) staged in shared memory, 16-bit block-local ids.
+struct XsCta {
+    int32_t t0, t1;    // its row tiles [t0, t1) (all of one block)
+    int32_t q0, nk;    // x(C_k) = x[q0, q0 + nk)
+    int32_t qB, nB;    // x(C_B) = x[qB, qB + nB)
+    int32_t k, pad;    // pad: lanes per row of the warp-independent form
+};
+struct XsArgs {
+    const XsCta* cta;
+    int32_t n_cta;
+    int32_t max_x;             // largest nk + nB (shared memory)
+    const int32_t* tile_row;   // rowtile.cu's tiles
+    const int32_t* tile_nnz;
+    const int32_t* tile_cls;   // lanes per row for 512 threads (kTileShort..32) / kTileGeneral
+    const int32_t* rowptr;
+    const uint16_t* colx;      // [nnz+pad] block-local ids: u < nk -> C_k[u], else C_B[u - nk]
+    const double* val;
+    const double* x;
+    double* y;
+    unsigned long long* maxabs_slots;
+};
+int64_t xstaged_smem_bytes(int64_t x_entries);
+cudaError_t launch_xstaged(const XsArgs& a, cudaStream_t s);
+cudaError_t preload_kernels_xstaged();
 // Fused / literal multiple-SpMxV kernel (split.cu), K <= 64 parts.
 constexpr int kMaxParts = 64;
 cudaError_t launch_split(const TileArgs& a, bool xsplit, cudaStream_t s);
