@@ -138,7 +138,10 @@ typedef struct {
                                 shared memory (atomicExch), so a row updated twice within one epoch --
                                 a violation of the planner's race-freedom invariant -- is counted;
                                 counts in spmv_info_t.debug_violations.  Slower; for tests */
-    int32_t reserved[9];
+    int32_t retain_csr;      /* 1 = keep the device copy of the permuted CSR even when the panel kernel
+                                does not read it (for spmv_debug_copy_csr); 0 (default) = a panel
+                                handle frees it after planning (C5: 13.7 GB less per GPU) */
+    int32_t reserved[8];
 } spmv_options_t;
 
 /* spmv_create -- ingest, validate, permute and plan (once; not per SpMxV).

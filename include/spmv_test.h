@@ -18,7 +18,9 @@ extern "C" {
  * int64[m_local+1] relative to the rank's first nonzero, col as GLOBAL
  * permuted column ids int32[nnz_local], val double[nnz_local]).  Synchronous.
  * World > 1 DB handles: the local compute rows (block rows, then the
- * border-row temporaries' segments).  Checks the ingest (a1) bit-exactly. */
+ * border-row temporaries' segments).  Checks the ingest (a1) bit-exactly.
+ * A panel-kernel handle keeps the device CSR only when created with
+ * spmv_options_t.retain_csr (else UNSUPPORTED). */
 spmv_status_t spmv_debug_copy_csr(spmv_handle_t h, int64_t* row_ptr, int32_t* col, double* val);
 
 /* Host-only round trip of the column-sorted panel kernel's planner

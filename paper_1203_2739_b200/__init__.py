@@ -62,7 +62,7 @@ class _Blocks(ctypes.Structure):
 class _Options(ctypes.Structure):
     _fields_ = [("struct_size", ctypes.c_int32), ("kernel", ctypes.c_int32), ("panel_rows", ctypes.c_int32),
                 ("split_kernel", ctypes.c_int32), ("exchange", ctypes.c_int32), ("index16", ctypes.c_int32),
-                ("debug_checks", ctypes.c_int32), ("reserved", ctypes.c_int32 * 9)]
+                ("debug_checks", ctypes.c_int32), ("retain_csr", ctypes.c_int32), ("reserved", ctypes.c_int32 * 8)]
 
 
 class _Dist(ctypes.Structure):
@@ -229,7 +229,9 @@ def _options_struct(options, keep):
     o.exchange = EXCHANGES[options.get("exchange", "auto")]
     o.index16 = int(options.get("index16", 0))
     o.debug_checks = int(options.get("debug_checks", 0))
-    unknown = set(options) - {"kernel", "panel_rows", "split_kernel", "exchange", "index16", "debug_checks"}
+    o.retain_csr = int(options.get("retain_csr", 0))
+    unknown = set(options) - {"kernel", "panel_rows", "split_kernel", "exchange", "index16", "debug_checks",
+                              "retain_csr"}
     if unknown:
         raise ValueError(f"unknown spmv options: {sorted(unknown)}")
     keep.append(o)

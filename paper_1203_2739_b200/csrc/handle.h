@@ -197,6 +197,7 @@ template <class T>
 spmv_status_t dalloc(spmv_plan_s* h, T** out, size_t count);
 template <class T>
 spmv_status_t upload(spmv_plan_s* h, T** out, const T* src, size_t count, size_t alloc_count = 0);
+void dfree(spmv_plan_s* h, void* p);   // frees one of the handle's allocations early
 void free_plan(spmv_plan_s* h);
 bool valid(spmv_handle_t h);
 

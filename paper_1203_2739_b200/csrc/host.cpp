@@ -69,6 +69,15 @@ spmv_status_t upload(spmv_plan_s* h, T** out, const T* src, size_t count, size_t
     if (count) CUDA_TRY(cudaMemcpy(*out, src, count * sizeof(T), cudaMemcpyHostToDevice));
     return SPMV_OK;
 }
+void dfree(spmv_plan_s* h, void* p) {
+    if (!p) return;
+    for (size_t i = 0; i < h->allocs.size(); ++i)
+        if (h->allocs[i] == p) {
+            cudaFree(p);
+            h->allocs.erase(h->allocs.begin() + (int64_t)i);
+            return;
+        }
+}
 template spmv_status_t dalloc<double>(spmv_plan_s*, double**, size_t);
 template spmv_status_t dalloc<int32_t>(spmv_plan_s*, int32_t**, size_t);
 template spmv_status_t dalloc<char>(spmv_plan_s*, char**, size_t);
@@ -463,7 +472,7 @@ spmv_status_t create_impl(int64_t m, int64_t n, int64_t nnz, const int64_t* row_
     const spmv_options_t& O = h->opt;
     if (O.kernel < 0 || O.kernel > 3 || O.split_kernel < 0 || O.split_kernel > 2 || O.exchange < 0 ||
         O.exchange > 2 || O.panel_rows < 0 || O.index16 < 0 || O.index16 > 1 || O.debug_checks < 0 ||
-        O.debug_checks > 1)
+        O.debug_checks > 1 || O.retain_csr < 0 || O.retain_csr > 1)
         return fail(SPMV_ERR_USAGE, "bad options");
     if (m < 0 || n < 0 || nnz < 0) return fail(SPMV_ERR_USAGE, "negative dimension");
     if (!row_ptr) return fail(SPMV_ERR_USAGE, "row_ptr is NULL");
@@ -1135,6 +1144,19 @@ spmv_status_t create_impl(int64_t m, int64_t n, int64_t nnz, const int64_t* row_
             if (h->pn.ok()) {
                 h->kernel = 7;
                 h->bytes_stream = (12 * 32 + 4) * h->pn.groups + 8 * h->m_loc;
+                // the panel kernel reads only its group stream: the device CSR
+                // copy (and the row tiles' 16-bit ids) would double the
+                // handle's memory (C5: 13.7 GB) -- released unless asked for
+                if (!O.retain_csr) {
+                    dfree(h, h->d_col);
+                    dfree(h, h->d_val);
+                    dfree(h, h->d_col16);
+                    dfree(h, h->d_tile_base);
+                    h->d_col = nullptr;
+                    h->d_val = nullptr;
+                    h->d_col16 = nullptr;
+                    h->d_tile_base = nullptr;
+                }
             } else if (world > 1) {
                 return fail(SPMV_ERR_UNSUPPORTED, "world > 1: the panel plan cannot be built (%s)", why.c_str());
             }

@@ -16,6 +16,8 @@ extern "C" {
 
 spmv_status_t spmv_debug_copy_csr(spmv_handle_t h, int64_t* row_ptr, int32_t* col, double* val) {
     if (!valid(h) || !row_ptr || (h->nnz_loc && (!col || !val))) return fail(SPMV_ERR_USAGE, "bad arguments");
+    if (h->nnz_loc && !h->d_col)
+        return fail(SPMV_ERR_UNSUPPORTED, "the device CSR was released (panel kernel); create with retain_csr");
     DeviceGuard g(h->device);
     CUDA_TRY(cudaDeviceSynchronize());
     std::vector<int32_t> rp(h->m_loc + 1);

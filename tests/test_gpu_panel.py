@@ -181,3 +181,25 @@ def test_debug_checks_have_teeth(kind, slot):
     v = sp.spmv_get_info(h)["debug_violations"]
     assert v[slot] > 0, v
     sp.spmv_destroy(h)
+
+
+def test_csr_released_on_panel_handles():
+    """A panel handle frees its device CSR copy after planning (the kernel
+    reads only its group stream; C5: 13.7 GB per GPU); the debug copy is then
+    refused, unless created with retain_csr, and the SpMxV is unaffected."""
+    p = synth.make("c5s", scramble=0)
+    x = p.x()
+    xh, yh, S = oracle_permuted(p, x)
+    h = create(p, options=panel(2000))
+    free0 = torch.cuda.mem_get_info()[0]
+    with pytest.raises(sp.SpmvError) as e:
+        T.debug_copy_csr(h)
+    assert e.value.status == sp.SPMV_ERR_UNSUPPORTED
+    assert_parity(gpu_apply(h, xh, p.m), yh, S, what="released CSR")
+    h2 = create(p, options=dict(panel(2000), retain_csr=1))
+    rp, col, val = T.debug_copy_csr(h2)
+    assert len(col) == p.nnz
+    assert np.array_equal(gpu_apply(h2, xh, p.m), gpu_apply(h, xh, p.m))
+    sp.spmv_destroy(h)
+    sp.spmv_destroy(h2)
+    assert free0 > 0

@@ -26,7 +26,7 @@ def cuda():
 @pytest.mark.parametrize("name", ["c1", "c2s", "c5s", "c3s"])
 def test_ingest_bit_exact(name):
     p = synth.make(name)
-    h = create(p)
+    h = create(p, options=dict(retain_csr=1))
     rp, col, val = T.debug_copy_csr(h)
     o = oracle.permute(p.m, p.n, p.row_ptr, p.col, p.val, p.row_perm, p.col_perm)
     assert np.array_equal(rp, o[0])

@@ -249,7 +249,8 @@ def test_exchange_overlaps_interior():
     slow peer would); once the slice lands, only the border epochs remain.
     Measured with CUDA events: the time rank 0 still needs after rank 1 starts
     pushing is well below rank 0's whole kernel time with every slice ready."""
-    synth.PRESETS["_overlap"] = lambda **kw: synth._sb(2, 400_000, 392_000, 4000, 12, 20, 0, 3, **kw)
+    # large enough that rank 0's kernel (~0.2 ms) dwarfs the push latency
+    synth.PRESETS["_overlap"] = lambda **kw: synth._sb(2, 1_200_000, 1_188_000, 12_000, 12, 20, 0, 3, **kw)
     p = synth.make("_overlap", scramble=0)
     hs, infos = make_ranks(p, 2)
     x = p.x()
