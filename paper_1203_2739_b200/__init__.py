@@ -40,7 +40,7 @@ EXPORTED = ["spmv_create", "spmv_create_ex", "spmv_apply", "spmv_split_apply", "
             "spmv_version", "spmv_shard_plan", "spmv_order_sbfs"]
 # include/spmv_test.h (test and debug hooks, same library)
 EXPORTED_TEST = ["spmv_debug_copy_csr", "spmv_pn_plan_check", "spmv_pn_shard_hash", "spmv_test_create_rank",
-                 "spmv_test_loopback_link", "spmv_test_rank_stream", "spmv_test_corrupt_panel"]
+                 "spmv_test_loopback_link", "spmv_test_rank_stream", "spmv_test_corrupt_panel", "spmv_test_panel_stamps"]
 
 KERNELS = {"auto": 0, "panel": 1, "rowtile": 2, "xstaged": 3}
 SPLIT_KERNELS = {"auto": 0, "panel": 1, "rows": 2}
@@ -129,6 +129,7 @@ def lib():
         L.spmv_test_loopback_link.argtypes = [vp, i32]
         L.spmv_test_rank_stream.argtypes = [vp, vp]
         L.spmv_test_corrupt_panel.argtypes = [vp, i32]
+        L.spmv_test_panel_stamps.argtypes = [vp, i32, vp, i64]
         for name in EXPORTED_TEST:
             getattr(L, name).restype = i32
         for name in EXPORTED:

@@ -135,6 +135,7 @@ struct spmv_plan_s {
     int32_t* d_rowptr = nullptr;      // [m_loc+1]
     int32_t* d_col = nullptr;         // [nnz_loc + pad] local column ids
     unsigned long long* d_dbg = nullptr;   // debug_checks: violation counters [3]
+    unsigned long long* d_stamps = nullptr;   // test hook spmv_test_panel_stamps: [panels * 8] or nullptr
     uint16_t* d_col16 = nullptr;      // f3: [nnz_loc + pad] 16-bit tile-local column ids (or nullptr)
     uint16_t* d_colx = nullptr;       // x-staged kernel: [nnz_loc + pad] 16-bit block-local ids
     spmvb::XsCta* d_xcta = nullptr;   // x-staged kernel: per CTA its tiles and x slices

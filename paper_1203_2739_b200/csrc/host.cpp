@@ -94,6 +94,7 @@ void free_plan(spmv_plan_s* h) {
     xchg_release(h);
     for (void* p : h->allocs) cudaFree(p);
     h->allocs.clear();
+    if (h->d_stamps) cudaFree(h->d_stamps);
     if (h->comm) ncclCommDestroy(h->comm);
     h->comm = nullptr;
     h->magic = 0;
@@ -1469,6 +1470,7 @@ spmv_status_t run(spmv_handle_t h, const double* x, double* y, uint32_t flags, c
         X.err = xv.err;
         X.herr = xv.herr;
         X.dbg = h->d_dbg;
+        X.stamps = h->d_stamps;
         X.x_cols = h->world > 1 ? h->x_int_len + h->border_total : h->n;
         CUDA_TRY(launch_panel(X, st));
     } else if (!split && h->kernel == 8) {

@@ -176,8 +176,11 @@ constexpr int kPnFoldSeq = 32;               // virtual rows a thread folds sequ
 #endif
 constexpr int kPnPend = SPMV_PN_PEND;        // planner: bank-blocked nonzeros an epoch keeps pending before
                                              // it closes a group early (y bank conflicts vs padding)
-constexpr int kPnSplitAt = 32;               // a row with more nonzeros is split into interleaved
-constexpr int kPnVMax = 32;                  // virtual rows of <= kPnVMax nonzeros (own y slots,
+#ifndef SPMV_PN_VMAX
+#define SPMV_PN_VMAX 32
+#endif
+constexpr int kPnSplitAt = SPMV_PN_VMAX;     // a row with more nonzeros is split into interleaved
+constexpr int kPnVMax = SPMV_PN_VMAX;        // virtual rows of <= kPnVMax nonzeros (own y slots,
                                              // folded in order in the epilogue)
 
 struct PnArgs {
@@ -218,6 +221,9 @@ struct PnArgs {
     // columns >= x_cols and rows updated twice in one epoch into dbg[0..2]
     unsigned long long* dbg;
     int64_t x_cols;
+    // test hook spmv_test_panel_stamps: per CTA 8 words (SM id, globaltimer at start and end,
+    // clock64 at start, after the prologue, after the epochs, at the end), or nullptr
+    unsigned long long* stamps;
 };
 // Dynamic shared memory of a panel CTA: its y slots (+ the padding lanes'
 // 16 scratch slots), the split rows' slot lists (u16) and their (first, count,

@@ -101,6 +101,16 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
         extern __shared__ __align__(16) double ys[];
         const PnPanel d = A.panel[p];
         const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+        unsigned long long* const stp = A.stamps ? A.stamps + (int64_t)p * 8 : nullptr;
+        if (stp && tid == 0) {
+            uint32_t sm;
+            unsigned long long gt;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+            stp[0] = sm;
+            stp[1] = gt;
+            stp[3] = clock64();
+        }
         for (int i = tid; i < ((d.nslots + 15) & ~15); i += kT) ys[i] = 0.0;   // the panel's y slots
         // virtual-row slot lists of the panel's split rows, copied to shared memory
         // once (the epilogue folds them)
@@ -117,6 +127,7 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
         if (CHK)
             for (int i = tid; i < A.max_rows + 16; i += kT) stamp[i] = 0;
         __syncthreads();
+        if (stp && tid == 0) stp[4] = clock64();
 
         const uint64_t pol = pol_evict_first();
         const uint64_t polx = pol_evict_last();   // x is the reused operand
@@ -296,6 +307,7 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
         };
         load_slots(tid);
         __syncthreads();
+        if (stp && tid == 0) stp[5] = clock64();
 
         // DB across GPUs: a panel of border-row temporaries writes them to y_hi
         const bool tpanel = d.row0 >= A.y_split;
@@ -345,6 +357,15 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
             if (lane == 0 && mx > 0.0)
                 atomicMax(A.maxabs_slots + ((p * NW + warp) & (kMaxSlots - 1)) * kSlotStride,
                           (unsigned long long)__double_as_longlong(mx));
+        }
+        if (stp) {
+            __syncthreads();
+            if (tid == 0) {
+                unsigned long long gt;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+                stp[6] = clock64();
+                stp[2] = gt;
+            }
         }
     }
 }

@@ -73,6 +73,7 @@ spmv_status_t spmv_pn_plan_check(int64_t m, int64_t n, const int64_t* row_ptr, c
         stats[3] = st.deferred; stats[4] = st.epochs; stats[5] = st.entries;
         stats[6] = (int64_t)(st.ywf0 * 1000.0); stats[7] = (int64_t)(st.ywf1 * 1000.0);
         stats[8] = smax; stats[9] = with_border; stats[10] = st.gsectors;
+        stats[11] = st.pads_drain; stats[12] = st.epochs_drain;
         if (st.entries != nnz) return fail(SPMV_ERR_INTERNAL, "pn_plan_check: plan holds %lld of %lld nonzeros",
                                            (long long)st.entries, (long long)nnz);
         if (smax > kPnSmemMax) return fail(SPMV_ERR_INTERNAL, "pn_plan_check: a panel needs %lld B of shared memory",
@@ -211,6 +212,25 @@ spmv_status_t spmv_test_corrupt_panel(spmv_handle_t h, int32_t kind) {
     if (kind == 2) blk[b] = ((uint32_t)(h->pn.max_rows + 100) << kPnDeltaBits) | (blk[b] & mask);   // slot
     if (kind == 3) blk[b] = (blk[b] & ~mask) | mask;                           // column delta 2^17 - 1
     CUDA_TRY(cudaMemcpy(dev, blk, sizeof blk, cudaMemcpyHostToDevice));
+    return SPMV_OK;
+}
+
+spmv_status_t spmv_test_panel_stamps(spmv_handle_t h, int32_t mode, uint64_t* out, int64_t cap) {
+    if (!valid(h) || mode < 0 || mode > 1 || (mode == 0 && (!out || cap < 0)))
+        return fail(SPMV_ERR_USAGE, "panel_stamps: bad arguments");
+    if (h->kernel != 7 || !h->pn.ok()) return fail(SPMV_ERR_UNSUPPORTED, "panel_stamps: not a panel handle");
+    DeviceGuard g(h->device);
+    const int64_t n = (int64_t)h->pn.panels * 8;
+    if (mode == 1) {
+        if (!h->d_stamps) CUDA_TRY(cudaMalloc(&h->d_stamps, n * sizeof(unsigned long long)));
+        CUDA_TRY(cudaMemset(h->d_stamps, 0, n * sizeof(unsigned long long)));
+        return SPMV_OK;
+    }
+    if (!h->d_stamps) return fail(SPMV_ERR_USAGE, "panel_stamps: not armed");
+    CUDA_TRY(cudaDeviceSynchronize());
+    CUDA_TRY(cudaMemcpy(out, h->d_stamps, std::min(n, cap) * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaFree(h->d_stamps));
+    h->d_stamps = nullptr;
     return SPMV_OK;
 }
 

@@ -32,7 +32,7 @@ def pn_plan_check(m: int, n: int, row_ptr, col, val, blocks, rows_target: int) -
     va = _np(val, np.float64)
     keep = []
     bptr = _blocks_struct(blocks, keep)
-    stats = np.zeros(11, dtype=np.int64)
+    stats = np.zeros(13, dtype=np.int64)
     _check(lib().spmv_pn_plan_check(m, n, _addr(rp), _addr(ci), _addr(va), bptr, rows_target, stats.ctypes.data),
            "spmv_pn_plan_check")
     d = dict(zip(("panels", "groups", "pads", "deferred", "epochs", "entries"), (int(v) for v in stats[:6])))
@@ -41,6 +41,8 @@ def pn_plan_check(m: int, n: int, row_ptr, col, val, blocks, rows_target: int) -
     d["smem_max"] = int(stats[8])
     d["panels_with_border"] = int(stats[9])
     d["gather_sectors"] = int(stats[10])
+    d["pads_drain"] = int(stats[11])
+    d["epochs_drain"] = int(stats[12])
     return d
 
 
@@ -85,3 +87,17 @@ def rank_stream(h):
 def corrupt_panel(h, kind: int) -> None:
     """Corrupt a panel handle's plan on the device (tests of debug_checks)."""
     _check(lib().spmv_test_corrupt_panel(_h(h), kind), "spmv_test_corrupt_panel")
+
+
+def panel_stamps_arm(h) -> None:
+    """Record the per-CTA timeline of the handle's next panel-kernel launches."""
+    _check(lib().spmv_test_panel_stamps(_h(h), 1, None, 0), "spmv_test_panel_stamps")
+
+
+def panel_stamps_read(h) -> np.ndarray:
+    """[panels, 8] uint64: SM id, globaltimer start/end (ns), clock64 at start, after the
+    prologue, after the epochs, at the end -- of the last launch; disarms."""
+    n = spmv_get_info(h)["panels"]
+    out = np.zeros((n, 8), np.uint64)
+    _check(lib().spmv_test_panel_stamps(_h(h), 0, _addr(out), out.size), "spmv_test_panel_stamps")
+    return out
