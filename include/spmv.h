@@ -252,6 +252,8 @@ typedef struct {
                                      shard; permutation of the rows; tiles + CSR upload; split layouts;
                                      panel plans + upload; maps and buffers (the ingest cost of Table 3's
                                      amortization) */
+    int64_t far_nonzeros;         /* panel kernel: nonzeros summed in the barrier-free far phase (those
+                                     still deferred when a panel's column sweep ends) */
 } spmv_info_t;
 
 spmv_status_t spmv_get_info(spmv_handle_t h, spmv_info_t* info);

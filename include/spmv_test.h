@@ -29,13 +29,14 @@ spmv_status_t spmv_debug_copy_csr(spmv_handle_t h, int64_t* row_ptr, int32_t* co
  * about rows_target rows, decodes the groups again and compares them with the
  * CSR bit for bit, checking that no row repeats within an epoch, that groups
  * never mix interior and border columns, that border groups come last and
- * that every panel fits shared memory.  stats[13] = panels, groups, padding
+ * that every panel fits shared memory.  stats[15] = panels, groups, padding
  * slots, deferred nonzeros, epochs, nonzeros packed, 1000 x the mean predicted
  * shared-memory wavefronts of a group's y access with natural / bank-coloured
  * y slots, the largest panel's shared memory bytes, panels with border
  * groups, distinct 32-byte x sectors over all groups' gathers, padding slots
  * and epochs of the drain (epochs that start after the panel's column sweep
- * has handed out its last nonzero: only deferred ones are left).  OK on an
+ * has handed out its last nonzero: only deferred ones are left), nonzeros in
+ * the far stream, and its steps per warp summed over the panels.  OK on an
  * exact round trip; INTERNAL otherwise. */
 spmv_status_t spmv_pn_plan_check(int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
                                  const spmv_blocks_t* blocks, int64_t rows_target, int64_t* stats);
@@ -93,8 +94,9 @@ spmv_status_t spmv_test_rank_stream(spmv_handle_t h, void** stream);
 /* Per-CTA timeline of the panel kernel (a measurement hook): mode 1 arms the
  * handle -- its next panel-kernel launches record, per CTA (panel), 8 words:
  * SM id, %globaltimer (ns) at start and end, clock64 at start, after the
- * prologue (y zeroed, fold lists copied), after the epochs, at the end (the
- * end adds one barrier per CTA); mode 0 copies the last launch's records into
+ * prologue (y zeroed, fold lists copied), after the far phase (and the
+ * epilogue's first slot loads), at the end (the end adds one barrier per
+ * CTA), after the epochs; mode 0 copies the last launch's records into
  * out[0 .. 8 * panels) (cap words at most; synchronises the device) and
  * disarms.  UNSUPPORTED for a handle without a panel plan. */
 spmv_status_t spmv_test_panel_stamps(spmv_handle_t h, int32_t mode, uint64_t* out, int64_t cap);

@@ -67,6 +67,10 @@ struct PanelPlan {
     int32_t* d_split_cnt = nullptr;
     uint16_t* d_split_slots = nullptr;
     int32_t* d_split_row = nullptr;
+    double* d_fval = nullptr;         // far stream (PnPanel::fs / fb)
+    uint32_t* d_fcol = nullptr;
+    uint16_t* d_fslot = nullptr;
+    int64_t far = 0, far_blocks = 0;
     int32_t max_sslots = 0, max_split_n = 0;
     int64_t panels = 0, groups = 0, pad = 0, gsectors = 0, deferred = 0;
     int32_t max_rows = 0;

@@ -249,7 +249,14 @@ spmv_status_t plan_pn(spmv_plan_s* h, PanelPlan& pl, const std::vector<int64_t>&
     const int64_t P = (int64_t)pd.size(), G = st.groups;
     std::vector<PnPanel> desc(P);
     int32_t max_rows = 0, max_ss = 0, max_sn = 0;
+    int64_t FB = 0;   // far-stream blocks (32 entries) of all panels
     for (int64_t p = 0; p < P; ++p) {
+        pd[p].desc.fb = (int32_t)FB;
+        FB += (int64_t)pd[p].desc.fs * kPnWarps;
+        if (FB >= INT32_MAX / 64) {
+            if (why_out) *why_out = "far stream beyond int32 blocks";
+            return SPMV_OK;
+        }
         desc[p] = pd[p].desc;
         max_rows = std::max(max_rows, (pd[p].nslots + 15) & ~15);
         max_ss = std::max(max_ss, (int32_t)pd[p].split_slots.size());
@@ -352,6 +359,30 @@ spmv_status_t plan_pn(spmv_plan_s* h, PanelPlan& pl, const std::vector<int64_t>&
             CUDA_TRY(cudaMemcpy(pl.d_gbase4 + gb, tb.data(), ng * 4, cudaMemcpyHostToDevice));
         }
         p0 = p1;
+    }
+    {   // far stream, + one ring turn of padding blocks (read-ahead past the last panel)
+        const int64_t FBp = FB + (int64_t)kPnFarRing * kPnWarps;
+        if ((s = dalloc(h, &pl.d_fval, FBp * 32))) return s;
+        if ((s = dalloc(h, &pl.d_fcol, FBp * 32))) return s;
+        if ((s = dalloc(h, &pl.d_fslot, FBp * 32))) return s;
+        CUDA_TRY(cudaMemset(pl.d_fval + FB * 32, 0, kPnFarRing * kPnWarps * 32 * sizeof(double)));
+        CUDA_TRY(cudaMemset(pl.d_fcol + FB * 32, 0, kPnFarRing * kPnWarps * 32 * sizeof(uint32_t)));
+        CUDA_TRY(cudaMemset(pl.d_fslot + FB * 32, 0, kPnFarRing * kPnWarps * 32 * sizeof(uint16_t)));
+        std::vector<uint32_t> fc;
+        for (int64_t p = 0; p < P; ++p) {
+            PnPanelData& D = pd[p];
+            const int64_t at = (int64_t)D.desc.fb * 32, ne = (int64_t)D.fval.size();
+            if (!ne) continue;
+            fc.assign(D.fcol.begin(), D.fcol.end());
+            CUDA_TRY(cudaMemcpy(pl.d_fval + at, D.fval.data(), ne * 8, cudaMemcpyHostToDevice));
+            CUDA_TRY(cudaMemcpy(pl.d_fcol + at, fc.data(), ne * 4, cudaMemcpyHostToDevice));
+            CUDA_TRY(cudaMemcpy(pl.d_fslot + at, D.fslot.data(), ne * 2, cudaMemcpyHostToDevice));
+            std::vector<double>().swap(D.fval);
+            std::vector<int32_t>().swap(D.fcol);
+            std::vector<uint16_t>().swap(D.fslot);
+        }
+        pl.far = st.far;
+        pl.far_blocks = FB;
     }
     pl.panels = P;
     pl.groups = G;
@@ -1144,7 +1175,7 @@ spmv_status_t create_impl(int64_t m, int64_t n, int64_t nnz, const int64_t* row_
                 return s;
             if (h->pn.ok()) {
                 h->kernel = 7;
-                h->bytes_stream = (12 * 32 + 4) * h->pn.groups + 8 * h->m_loc;
+                h->bytes_stream = (12 * 32 + 4) * h->pn.groups + 14 * 32 * h->pn.far_blocks + 8 * h->m_loc;
                 // the panel kernel reads only its group stream: the device CSR
                 // copy (and the row tiles' 16-bit ids) would double the
                 // handle's memory (C5: 13.7 GB) -- released unless asked for
@@ -1396,6 +1427,9 @@ void fill_pn_args(const PanelPlan& pl, PnArgs& X) {
     X.max_sslots = pl.max_sslots;
     X.max_split_n = pl.max_split_n;
     X.gather_na = pl.gather_na;
+    X.fval = pl.d_fval;
+    X.fcol = pl.d_fcol;
+    X.fslot = pl.d_fslot;
 }
 
 spmv_status_t run(spmv_handle_t h, const double* x, double* y, uint32_t flags, cudaStream_t st, bool split) {
@@ -1567,6 +1601,7 @@ spmv_status_t spmv_get_info(spmv_handle_t h, spmv_info_t* info) {
     info->has_owner_map = h->has_owner ? 1 : 0;
     info->panels = h->kernel == 7 ? h->pn.panels : 0;
     info->groups = h->kernel == 7 ? h->pn.groups : 0;
+    info->far_nonzeros = h->kernel == 7 ? h->pn.far : 0;
     info->pad_slots = h->kernel == 7 ? h->pn.pad : 0;
     info->deferred = h->kernel == 7 ? h->pn.deferred : 0;
     info->y_wavefronts_x1000 = h->kernel == 7 ? (int64_t)(h->pn.ywf * 1000.0) : 0;

@@ -166,11 +166,19 @@ struct PnPanel {
     int32_t sslot0;    // their virtual rows' slots: split_slots[sslot0, sslot0 + sslot_n)
     int32_t sslot_n;
     int32_t split_short; // split rows [0, split_short) have <= kPnFoldSeq virtual rows (folded by one thread)
+    int32_t fs;        // far-stream steps per warp (a multiple of kPnFarRing)
+    int32_t fb;        // first 32-entry block of the panel's far stream
     int32_t bepoch;    // first epoch with a border-column (x_split side) group; ne if none.  Interior
                        // groups come first (the planner's column order), so at world > 1 the border-x
                        // exchange overlaps epochs [0, bepoch) (a4)
 };
 constexpr int kPnFoldSeq = 32;               // virtual rows a thread folds sequentially
+// Far phase (plan_panel.cpp build_panel, panel.cu): the nonzeros still
+// deferred when a panel's column sweep ends are summed by one lane per y slot
+// after the epochs, barrier-free.
+constexpr int kPnFarRing = 8;                // far steps per ring turn (the stream is padded to whole turns)
+constexpr uint16_t kPnFarLast = 0x8000;      // fslot flag: the run's last entry (add the run's sum to y)
+constexpr uint16_t kPnFarPad = 0x7FFF;       // fslot of a padding entry (value 0, never stored)
 #ifndef SPMV_PN_PEND
 #define SPMV_PN_PEND 32
 #endif
@@ -224,6 +232,10 @@ struct PnArgs {
     // test hook spmv_test_panel_stamps: per CTA 8 words (SM id, globaltimer at start and end,
     // clock64 at start, after the prologue, after the epochs, at the end), or nullptr
     unsigned long long* stamps;
+    // far stream (PnPanel::fs / fb): [blocks * 32] (step, warp, lane) order
+    const double* fval;
+    const uint32_t* fcol;
+    const uint16_t* fslot;
 };
 // Dynamic shared memory of a panel CTA: its y slots (+ the padding lanes'
 // 16 scratch slots), the split rows' slot lists (u16) and their (first, count,

@@ -111,24 +111,6 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
             stp[1] = gt;
             stp[3] = clock64();
         }
-        for (int i = tid; i < ((d.nslots + 15) & ~15); i += kT) ys[i] = 0.0;   // the panel's y slots
-        // virtual-row slot lists of the panel's split rows, copied to shared memory
-        // once (the epilogue folds them)
-        uint16_t* ssl = reinterpret_cast<uint16_t*>(ys + A.max_rows + 16);
-        int32_t* sdesc = reinterpret_cast<int32_t*>(ssl + ((A.max_sslots + 7) & ~7));   // (first, count, row) per split row
-        for (int i = tid; i < d.sslot_n; i += kT) ssl[i] = A.split_slots[d.sslot0 + i];
-        for (int i = tid; i < d.split_n; i += kT) {
-            const int e = d.split_off + i;
-            sdesc[3 * i] = A.split_first[e] - d.sslot0;
-            sdesc[3 * i + 1] = A.split_cnt[e];
-            sdesc[3 * i + 2] = A.split_row[e];
-        }
-        int32_t* stamp = sdesc + 3 * A.max_split_n;   // CHK only: epoch + 1 of each slot's last update
-        if (CHK)
-            for (int i = tid; i < A.max_rows + 16; i += kT) stamp[i] = 0;
-        __syncthreads();
-        if (stp && tid == 0) stp[4] = clock64();
-
         const uint64_t pol = pol_evict_first();
         const uint64_t polx = pol_evict_last();   // x is the reused operand
         constexpr int PF = kPF;
@@ -158,6 +140,15 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
             ip += kPnWarps * 128;
             bp += kPnWarps;
         };
+        auto gather_col = [&](uint32_t c) -> double {
+            if (CHK && (int64_t)c >= A.x_cols) {
+                atomicAdd(A.dbg + 1, 1ull);
+                c = 0;
+            }
+            const double* xa = !XS ? A.x_lo + c
+                                   : (int32_t)c < A.x_split ? A.x_lo + c : A.x_hi + (c - (uint32_t)A.x_split);
+            return XS ? ld_x_co(xa, polx) : NA ? ld_x_na(xa, polx) : ld_x(xa, polx);
+        };
         auto gather = [&](uint32_t i, int32_t b) -> double {
             // unconditional: a padding lane reads x[base] (valid) and adds 0 * x into
             // the scratch y slot -- a predicated-off load behind a branch made the
@@ -166,14 +157,7 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
             // gathered border); world 1 reads one vector (no select per gather)
             // column = base + delta (non-negative, < 2^31): one unsigned 32-bit add
             // and one wide multiply-add form the address
-            uint32_t c = (uint32_t)b + (i & kDeltaMask);
-            if (CHK && (int64_t)c >= A.x_cols) {
-                atomicAdd(A.dbg + 1, 1ull);
-                c = 0;
-            }
-            const double* xa = !XS ? A.x_lo + c
-                                   : (int32_t)c < A.x_split ? A.x_lo + c : A.x_hi + (c - (uint32_t)A.x_split);
-            return XS ? ld_x_co(xa, polx) : NA ? ld_x_na(xa, polx) : ld_x(xa, polx);
+            return gather_col((uint32_t)b + (i & kDeltaMask));
         };
         // a4 (world > 1, P2P exchange): the border x(C_B) of this apply may
         // still be in flight over NVLink while the interior epochs run.  A
@@ -202,20 +186,29 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
         // prefetch per array per epoch, issued by thread 0): the register ring
         // then waits for L2, not HBM, latency -- the x gathers depend on the
         // loaded indices, so their distance is what bounds the pipeline.
-        // Past the panel's last epoch it prefetches the first epochs of panel
-        // p + gridDim.x -- about the panel the block scheduler starts next, on
-        // whichever SM frees first -- so a new CTA's ring does not fill from HBM.
-        int nx_g0 = 0, nx_ne = 0;
-        if (tid == 0 && p + (int)gridDim.x < A.n_panels) {
-            nx_g0 = A.panel[p + gridDim.x].g0;
-            nx_ne = A.panel[p + gridDim.x].ne;
-        }
+        // Past the panel's last epoch it prefetches the head of the panel's far
+        // stream (the phase after the epochs).
+        auto prefetch_far = [&](int s0) {   // far steps [s0, s0 + kPnFarRing) into L2
+            if (tid != 0 || s0 >= d.fs) return;
+            const int64_t b = ((int64_t)d.fb + (int64_t)s0 * NW) * 32;
+            constexpr uint32_t n = kPnFarRing * NW * 32;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.fval + b), "r"(n * 8) : "memory");
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.fcol + b), "r"(n * 4) : "memory");
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.fslot + b), "r"(n * 2) : "memory");
+        };
         auto prefetch_epoch = [&](int e) {
             if (tid != 0) return;
-            int64_t g;
-            if (e < d.ne) g = (int64_t)d.g0 + (int64_t)e * kPnEpoch;
-            else if (e - d.ne < nx_ne) g = (int64_t)nx_g0 + (int64_t)(e - d.ne) * kPnEpoch;
-            else return;
+            if (e >= d.ne) {
+                if (e == d.ne) {   // the epilogue's slot map of the panel's rows (16-byte granules)
+                    const uintptr_t a0 = reinterpret_cast<uintptr_t>(A.row2slot + d.row0) & ~uintptr_t(15);
+                    const uintptr_t a1 = (reinterpret_cast<uintptr_t>(A.row2slot + d.row0 + d.nrows) + 15) & ~uintptr_t(15);
+                    if (a1 > a0)
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0)) : "memory");
+                }
+                if (e - d.ne < 2) prefetch_far((e - d.ne) * kPnFarRing);
+                return;
+            }
+            const int64_t g = (int64_t)d.g0 + (int64_t)e * kPnEpoch;
             // normal priority: an evict_first prefetch is the first victim of the next one
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.gval + g * 32), "r"(kPnEpoch * 32 * 8)
                          : "memory");
@@ -240,6 +233,26 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
         }
     #pragma unroll
         for (int u = 0; u < kD; u += 4) load4(u);
+        // the ring's first loads are in flight while the CTA zeroes its y slots
+        // and copies the fold lists (C4: the prologue was 3.9 % of a CTA's clocks)
+        for (int i = tid; i < ((d.nslots + 15) & ~15); i += kT) ys[i] = 0.0;   // the panel's y slots
+        // virtual-row slot lists of the panel's split rows, copied to shared memory
+        // once (the epilogue folds them)
+        uint16_t* ssl = reinterpret_cast<uint16_t*>(ys + A.max_rows + 16);
+        int32_t* sdesc = reinterpret_cast<int32_t*>(ssl + ((A.max_sslots + 7) & ~7));   // (first, count, row) per split row
+        for (int i = tid; i < d.sslot_n; i += kT) ssl[i] = A.split_slots[d.sslot0 + i];
+        for (int i = tid; i < d.split_n; i += kT) {
+            const int e = d.split_off + i;
+            sdesc[3 * i] = A.split_first[e] - d.sslot0;
+            sdesc[3 * i + 1] = A.split_cnt[e];
+            sdesc[3 * i + 2] = A.split_row[e];
+        }
+        int32_t* stamp = sdesc + 3 * A.max_split_n;   // CHK only: epoch + 1 of each slot's last update
+        if (CHK)
+            for (int i = tid; i < A.max_rows + 16; i += kT) stamp[i] = 0;
+        __syncthreads();
+        if (stp && tid == 0) stp[4] = clock64();
+
         if (must_wait && d.bepoch == 0) {
             border_wait();
             __syncthreads();
@@ -294,10 +307,61 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
             if (u + kGD < kD) rx[u % kGD] = gather(ri[(u + kGD) % kD], rb[(u + kGD) % kD]);
             if (u % kPnB == kPnB - 1) epoch_end(t0 + u);
         }
+        // far phase (plan_panel.cpp): each lane sums its runs of far nonzeros in a
+        // register and adds a run's sum to its y slot at the run's last entry.
+        // A slot belongs to one lane and every epoch is done (the last epoch
+        // barrier), so nothing races and no barrier is needed until the
+        // epilogue's.  Loads kPnFarRing steps ahead, gathers kFG ahead.
+        if (stp && tid == 0) stp[7] = clock64();
+        if (d.fs > 0) {
+            if (XS && A.ready != nullptr && d.bepoch >= d.ne) {   // no border epoch waited for the exchange
+                border_wait();
+                __syncthreads();
+            }
+            constexpr int FR = kPnFarRing, kFG = 4;
+            static_assert(kFG < FR, "far ring geometry");
+            const int64_t fstep = (int64_t)NW * 32;
+            const int64_t f0 = ((int64_t)d.fb + warp) * 32 + lane;
+            double fv[FR], fx[kFG];
+            uint32_t fc[FR], fsl[FR];
+            auto fload = [&](int u, int st) {
+                const int64_t at = f0 + (int64_t)st * fstep;
+                asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+                             : "=d"(fv[u]) : "l"(A.fval + at), "l"(pol));
+                asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+                             : "=r"(fc[u]) : "l"(A.fcol + at), "l"(pol));
+                asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u16 %0, [%1], %2;"
+                             : "=r"(fsl[u]) : "l"(A.fslot + at), "l"(pol));
+            };
+    #pragma unroll
+            for (int u = 0; u < FR; ++u) fload(u, u);
+    #pragma unroll
+            for (int u = 0; u < kFG; ++u) fx[u] = gather_col(fc[u]);
+            double acc = 0.0;
+            for (int s0 = 0; s0 < d.fs; s0 += FR) {
+                prefetch_far(s0 + 2 * FR);
+    #pragma unroll
+                for (int u = 0; u < FR; ++u) {
+                    acc = fma(fv[u], fx[u % kFG], acc);
+                    const uint32_t sl = fsl[u];
+                    if (sl & kPnFarLast) {
+                        const int r = (int)(sl & (kPnFarLast - 1));
+                        if (CHK && r >= A.max_rows) {
+                            atomicAdd(A.dbg + 0, 1ull);
+                        } else {
+                            ys[r] += acc;
+                        }
+                        acc = 0.0;
+                    }
+                    fload(u, s0 + u + FR);
+                    fx[u % kFG] = gather_col(fc[(u + kFG) % FR]);
+                }
+            }
+        }
         // epilogue: y[row] = ys[slot(row)].  The slot loads are batched 16 per
         // thread (clamped addresses, no branch) and the first batch is issued
         // before the barrier, so their latency is not paid once per row.
-        constexpr int EB = 16;
+        constexpr int EB = 32;   // slot loads per thread and batch: panels of <= 16 K rows in one batch
         uint16_t sl[EB];
         const uint16_t* r2s = A.row2slot + d.row0;
         const int nrl = d.nrows;

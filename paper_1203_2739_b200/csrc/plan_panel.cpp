@@ -379,6 +379,16 @@ void build_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col
         }
     std::sort(keys.begin(), keys.end());
     P.entries = n;
+    // Sweep order; the far stream (the barrier-free phase after the epochs,
+    // panel.cu) takes what is still deferred when the sweep ends (below).
+    // Measured and not kept: also sending nonzeros with few
+    // others of the panel within +-128 columns, or sparse deferred ones, to the
+    // far stream -- C4 +2.5 %, C5 +3 % (the phase is short and its pipeline
+    // fill is paid at every CTA's end).
+    std::vector<int64_t> fars;   // far entries (entry ids)
+    std::vector<int64_t> order(n);
+    for (int64_t q = 0; q < n; ++q) order[q] = (int64_t)(keys[q] & 0xFFFFFFFFu);
+    const int64_t nn = (int64_t)order.size();
 
     const int64_t kMaxDelta = int64_t(1) << kPnDeltaBits;
     auto side = [&](int32_t c) { return (int64_t)c >= x_split; };
@@ -390,10 +400,18 @@ void build_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col
     int64_t pos = 0;
     int32_t epoch = 0;
     std::vector<uint8_t> drain_epoch;
-    while (pos < n || !deferred.empty()) {
+    while (pos < nn || !deferred.empty()) {
         int ng = 0;
         bool full = false;
-        drain_epoch.push_back(pos >= n);
+        if (pos >= nn) {
+            // the sweep is done: what is still deferred would fill near-empty
+            // epochs one nonzero per row at a time (C4: 14 % of all slots) --
+            // it goes to the far phase instead
+            fars.insert(fars.end(), deferred.begin(), deferred.end());
+            deferred.clear();
+            break;
+        }
+        drain_epoch.push_back(pos >= nn);
         // returns false when the epoch is full (entry not taken)
         auto take = [&](int64_t i) -> bool {
             const Ent& e = ents[i];
@@ -418,8 +436,8 @@ void build_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col
             }
         }
         deferred.swap(nd);
-        while (!full && pos < n) {
-            const int64_t i = (int64_t)(keys[pos] & 0xFFFFFFFFu);
+        while (!full && pos < nn) {
+            const int64_t i = order[pos];
             if (stamp[ents[i].row] == epoch) {
                 deferred.push_back(i);
                 ++P.deferred;
@@ -460,6 +478,57 @@ void build_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col
     }
     std::vector<uint16_t> v2s;
     colour_slots((int32_t)nr, gents, G, v2s, slot);
+    // Far stream: each virtual row's far nonzeros form one run, owned by one
+    // lane (runs balanced over the CTA's kPnWarps x 32 lanes, longest first);
+    // the lane sums a run in a register and adds it to the y slot once, at
+    // the run's last entry (slot | kPnFarLast).  No two lanes share a slot, so
+    // the phase needs no barrier.  Step s of warp w, lane l is entry
+    // (s * kPnWarps + w) * 32 + l; steps are padded to whole ring turns.
+    {
+        std::sort(fars.begin(), fars.end(), [&](int64_t u, int64_t v) {   // by row, then CSR position
+            return ents[u].row != ents[v].row ? ents[u].row < ents[v].row : u < v;
+        });
+        struct Run { int64_t b, e; };
+        std::vector<Run> runs;
+        for (int64_t q = 0; q < (int64_t)fars.size();) {
+            int64_t e = q;
+            while (e < (int64_t)fars.size() && ents[fars[e]].row == ents[fars[q]].row) ++e;
+            runs.push_back({q, e});
+            q = e;
+        }
+        std::stable_sort(runs.begin(), runs.end(), [](const Run& u, const Run& v) { return u.e - u.b > v.e - v.b; });
+        constexpr int kBins = kPnWarps * 32;
+        std::vector<int64_t> load(kBins, 0);
+        std::vector<std::vector<int32_t>> bin(kBins);   // run ids per lane
+        for (int32_t k = 0; k < (int32_t)runs.size(); ++k) {
+            int b = 0;
+            for (int j = 1; j < kBins; ++j)
+                if (load[j] < load[b]) b = j;
+            bin[b].push_back(k);
+            load[b] += runs[k].e - runs[k].b;
+        }
+        int64_t fs = 0;
+        for (int j = 0; j < kBins; ++j) fs = std::max(fs, load[j]);
+        fs = (fs + kPnFarRing - 1) / kPnFarRing * kPnFarRing;
+        P.desc.fs = (int32_t)fs;
+        P.far = (int64_t)fars.size();
+        const int32_t dcol = fars.empty() ? 0 : ents[fars[0]].col;   // padding: a valid x read, times 0
+        P.fval.assign(fs * kBins, 0.0);
+        P.fcol.assign(fs * kBins, dcol);
+        P.fslot.assign(fs * kBins, kPnFarPad);
+        for (int j = 0; j < kBins; ++j) {
+            const int w = j / 32, l = j % 32;
+            int64_t st = 0;
+            for (int32_t k : bin[j])
+                for (int64_t q = runs[k].b; q < runs[k].e; ++q, ++st) {
+                    const Ent& e = ents[fars[q]];
+                    const int64_t at = (st * kPnWarps + w) * 32 + l;
+                    P.fval[at] = e.v;
+                    P.fcol[at] = e.col;
+                    P.fslot[at] = (uint16_t)(slot[e.row] | (q + 1 == runs[k].e ? kPnFarLast : 0));
+                }
+        }
+    }
     // real rows -> slot, or -> split entry (virtual rows' slots in fold order)
     // split rows with <= kPnFoldSeq virtual rows first (the epilogue folds
     // those one thread per row, sequentially), then the longer ones (a warp each)
@@ -654,6 +723,8 @@ bool plan_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col,
         st.deferred += P.deferred;
         st.gsectors += P.gsectors;
         st.pads_drain += P.pads_drain;
+        st.far += P.far;
+        st.far_steps += P.desc.fs;
         st.epochs_drain += P.epochs_drain;
         st.epochs += P.desc.ne;
         st.ywf0 += P.ywf0 * (double)P.gbase.size();
@@ -768,6 +839,32 @@ bool verify_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& co
                     got[r].push_back({(int32_t)c, v});
                 }
             }
+        // far stream: runs owned by one lane each, the slot flagged at the run's end
+        if ((int64_t)P.fval.size() != (int64_t)d.fs * kPnWarps * 32 || P.fcol.size() != P.fval.size() ||
+            P.fslot.size() != P.fval.size())
+            e = "far stream size != fs * warps * 32";
+        {
+            std::vector<int32_t> owner(nsl, -1);
+            for (int64_t j = 0; j < (int64_t)kPnWarps * 32 && e.empty(); ++j) {
+                int32_t open = -1;   // slot of the lane's current run
+                for (int64_t st = 0; st < d.fs && e.empty(); ++st) {
+                    const int64_t at = (st * kPnWarps + j / 32) * 32 + j % 32;
+                    const int32_t sl = P.fslot[at] & (kPnFarLast - 1);
+                    const bool last = (P.fslot[at] & kPnFarLast) != 0;
+                    if (P.fslot[at] == kPnFarPad) {   // padding (after the lane's runs)
+                        if (open >= 0) { e = "far padding inside a run"; break; }
+                        continue;
+                    }
+                    if (sl >= nsl || row_of_slot[sl] < 0) { e = "far slot outside the panel"; break; }
+                    if (open >= 0 && sl != open) { e = "far run changes slot before its last entry"; break; }
+                    if (owner[sl] >= 0 && owner[sl] != j) { e = "far slot owned by two lanes"; break; }
+                    owner[sl] = (int32_t)j;
+                    got[row_of_slot[sl]].push_back({P.fcol[at], P.fval[at]});
+                    open = last ? -1 : sl;
+                }
+                if (e.empty() && open >= 0) e = "far run without a last entry";
+            }
+        }
         for (int64_t r = 0; r < d.nrows && e.empty(); ++r) {
             auto& gr = got[r];
             std::sort(gr.begin(), gr.end(),

@@ -24,6 +24,10 @@ struct PnPanelData {
     int32_t nslots = 0;             // y slots used (virtual rows), before rounding to 16
     int64_t entries = 0, pads = 0, deferred = 0;
     int64_t pads_drain = 0, epochs_drain = 0;   // padding / epochs after the sweep's last nonzero
+    int64_t far = 0;                // nonzeros in the far stream
+    std::vector<double> fval;       // [fs * kPnWarps * 32] far stream, (step, warp, lane) order
+    std::vector<int32_t> fcol;      //   column (the handle's local column ids)
+    std::vector<uint16_t> fslot;    //   y slot | kPnFarLast at a run's last entry
     int64_t gsectors = 0;          // distinct 32-byte x sectors over the groups' gathers
     int32_t rot = 0;               // the column sweep starts at this column (wraps around)
     double ywf0 = 0, ywf1 = 0;     // predicted y wavefronts per group access: natural slots / coloured
@@ -32,6 +36,7 @@ struct PnPanelData {
 struct PnPlanStats {
     int64_t panels = 0, groups = 0, entries = 0, pads = 0, deferred = 0, epochs = 0, gsectors = 0;
     int64_t pads_drain = 0, epochs_drain = 0;
+    int64_t far = 0, far_steps = 0;   // far-stream nonzeros, sum over panels of its steps per warp
     double ywf0 = 0, ywf1 = 0;     // mean predicted y wavefronts per group access, before / after colouring
 };
 

@@ -74,6 +74,7 @@ spmv_status_t spmv_pn_plan_check(int64_t m, int64_t n, const int64_t* row_ptr, c
         stats[6] = (int64_t)(st.ywf0 * 1000.0); stats[7] = (int64_t)(st.ywf1 * 1000.0);
         stats[8] = smax; stats[9] = with_border; stats[10] = st.gsectors;
         stats[11] = st.pads_drain; stats[12] = st.epochs_drain;
+        stats[13] = st.far; stats[14] = st.far_steps;
         if (st.entries != nnz) return fail(SPMV_ERR_INTERNAL, "pn_plan_check: plan holds %lld of %lld nonzeros",
                                            (long long)st.entries, (long long)nnz);
         if (smax > kPnSmemMax) return fail(SPMV_ERR_INTERNAL, "pn_plan_check: a panel needs %lld B of shared memory",

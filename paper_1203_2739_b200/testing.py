@@ -32,7 +32,7 @@ def pn_plan_check(m: int, n: int, row_ptr, col, val, blocks, rows_target: int) -
     va = _np(val, np.float64)
     keep = []
     bptr = _blocks_struct(blocks, keep)
-    stats = np.zeros(13, dtype=np.int64)
+    stats = np.zeros(15, dtype=np.int64)
     _check(lib().spmv_pn_plan_check(m, n, _addr(rp), _addr(ci), _addr(va), bptr, rows_target, stats.ctypes.data),
            "spmv_pn_plan_check")
     d = dict(zip(("panels", "groups", "pads", "deferred", "epochs", "entries"), (int(v) for v in stats[:6])))
@@ -43,6 +43,8 @@ def pn_plan_check(m: int, n: int, row_ptr, col, val, blocks, rows_target: int) -
     d["gather_sectors"] = int(stats[10])
     d["pads_drain"] = int(stats[11])
     d["epochs_drain"] = int(stats[12])
+    d["far"] = int(stats[13])
+    d["far_steps"] = int(stats[14])
     return d
 
 
@@ -96,7 +98,7 @@ def panel_stamps_arm(h) -> None:
 
 def panel_stamps_read(h) -> np.ndarray:
     """[panels, 8] uint64: SM id, globaltimer start/end (ns), clock64 at start, after the
-    prologue, after the epochs, at the end -- of the last launch; disarms."""
+    prologue, after the far phase, at the end, after the epochs -- of the last launch; disarms."""
     n = spmv_get_info(h)["panels"]
     out = np.zeros((n, 8), np.uint64)
     _check(lib().spmv_test_panel_stamps(_h(h), 0, _addr(out), out.size), "spmv_test_panel_stamps")

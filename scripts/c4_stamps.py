@@ -33,13 +33,14 @@ b.record()
 torch.cuda.synchronize()
 S = T.panel_stamps_read(h).astype(np.int64)
 ms = a.elapsed_time(b)
-sm, g0, g1, c0, c1, c2, c3 = S[:, 0], S[:, 1], S[:, 2], S[:, 3], S[:, 4], S[:, 5], S[:, 6]
+sm, g0, g1, c0, c1, c2, c3, ce = S[:, 0], S[:, 1], S[:, 2], S[:, 3], S[:, 4], S[:, 5], S[:, 6], S[:, 7]
 t0 = g0.min()
 dur = (g1 - g0) / 1e3
 pro, loop, epi = (c1 - c0), (c2 - c1), (c3 - c2)
 tot = c3 - c0
 print(f"{name} {opts}: event {ms * 1e3:.1f} us, panels {len(S)}, span {(g1.max() - t0) / 1e3:.1f} us")
 print(f"  CTA us: mean {dur.mean():.1f} min {dur.min():.1f} max {dur.max():.1f}")
+print(f"  far phase (+ first slot loads) share {(c2 - ce).sum() / tot.sum():.3f}")
 print(f"  phase share of CTA clocks: prologue {pro.sum() / tot.sum():.3f} epochs {loop.sum() / tot.sum():.3f} "
       f"epilogue {epi.sum() / tot.sum():.3f}; mean clocks pro {pro.mean():.0f} loop {loop.mean():.0f} epi {epi.mean():.0f}")
 # per SM: busy time vs span

@@ -1,0 +1,6 @@
+set -u
+run() { cp ablib/lib$1.so paper_1203_2739_b200/libspmv_b200.so; echo "== $1"; shift; timeout 900 python scripts/ab_opts.py "$@" 2>&1 | tail -4; }
+for c in c4 c3; do for r in 1 2 3; do for v in DRN PRO; do run $v $c '{}'; done; done; done
+for r in 1 2; do for v in DRN PRO; do run $v c5 '{}'; done; done
+cp ablib/libPRO.so paper_1203_2739_b200/libspmv_b200.so
+timeout 300 python scripts/c4_stamps.py c4

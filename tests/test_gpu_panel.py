@@ -203,3 +203,40 @@ def test_csr_released_on_panel_handles():
     sp.spmv_destroy(h)
     sp.spmv_destroy(h2)
     assert free0 > 0
+
+
+@pytest.mark.parametrize("variant", ["int", "real"])
+@pytest.mark.parametrize("checks", [0, 1])
+def test_far_stream_heavy_runs(variant, checks):
+    """Rows whose nonzeros all sit in one 40-column window: most of them are
+    still deferred when a small panel's sweep ends and run through the far
+    phase (one lane per y slot, register sums, barrier-free); parity with the
+    oracle (bit for bit on integer data), and the checked kernel variant sees
+    no out-of-bounds slot or column."""
+    rng = np.random.default_rng(7)
+    m = n = 3000
+    rows, cols = [], []
+    for r in range(m):
+        c0 = (r * 7) % (n - 40)
+        cs = np.sort(rng.choice(40, size=30, replace=False)) + c0
+        rows += [r] * len(cs)
+        cols += cs.tolist()
+    rp = np.zeros(m + 1, np.int64)
+    np.add.at(rp, np.asarray(rows) + 1, 1)
+    rp = np.cumsum(rp)
+    col = np.asarray(cols, np.int32)
+    if variant == "int":
+        val = rng.integers(-4, 5, len(col)).astype(np.float64)
+        x = rng.integers(-4, 5, n).astype(np.float64)
+    else:
+        val = rng.uniform(-1, 1, len(col))
+        x = rng.uniform(-1, 1, n)
+    st = T.pn_plan_check(m, n, rp, col, val, None, 1024)
+    assert st["far"] > len(col) // 20, st
+    yref, S = oracle.spmv(rp, col, val, x)
+    h = sp.spmv_create(m, n, rp, col, val, options=dict(kernel="panel", panel_rows=1024, debug_checks=checks))
+    assert sp.spmv_get_info(h)["kernel"] == 7
+    y = gpu_apply(h, x, m)
+    assert_parity(y, yref, S, exact=(variant == "int"), what=f"far_runs/{variant}")
+    if checks:
+        assert sp.spmv_get_info(h)["debug_violations"] == [0, 0, 0]

@@ -144,3 +144,38 @@ def test_border_groups_last():
     p = _c5_like()
     st = T.pn_plan_check(p.m, p.n, p.row_ptr, p.col, p.val, p.blocks, 7_000)
     assert st["panels_with_border"] == st["panels"]
+
+
+@pytest.mark.parametrize("name", ["c4s", "c3s"])
+def test_far_stream_takes_the_drain(name):
+    """Nonzeros still deferred when a panel's sweep ends go to the far stream
+    (panel.cu's barrier-free phase) instead of near-empty epochs: no drain
+    padding, and the round trip (runs owned by one lane each, flagged at their
+    last entry, every nonzero once) holds."""
+    p = synth.make(name)
+    blocks = p.blocks if name != "c4s" else None
+    st = T.pn_plan_check(p.m, p.n, p.row_ptr, p.col, p.val, blocks, 5000)
+    assert st["far"] > 0, st
+    assert st["pads_drain"] == 0 and st["epochs_drain"] == 0, st
+    assert st["entries"] == p.nnz
+
+
+def test_far_stream_heavy_column_runs():
+    """A panel whose rows all repeat one dense column window (every row's
+    nonzeros within 40 columns): deferrals pile up, the far stream carries
+    long runs, and the plan still round-trips bit for bit."""
+    rng = np.random.default_rng(5)
+    m = n = 3000
+    rows, cols = [], []
+    for r in range(m):
+        c0 = (r * 7) % (n - 40)
+        cs = np.sort(rng.choice(40, size=30, replace=False)) + c0
+        rows += [r] * len(cs)
+        cols += cs.tolist()
+    rp = np.zeros(m + 1, np.int64)
+    np.add.at(rp, np.asarray(rows) + 1, 1)
+    rp = np.cumsum(rp)
+    col = np.asarray(cols, np.int32)
+    val = rng.uniform(-1, 1, len(col))
+    st = T.pn_plan_check(m, n, rp, col, val, None, 1024)
+    assert st["entries"] == len(col) and st["pads_drain"] == 0, st
