@@ -1,4 +1,4 @@
-"""profiles/r02_panel_c5_c4.md from the round-2 ncu captures (gpurun_out/r2m_*)."""
+"""profiles/r02_panel_c5_c4*.md from the round-2 ncu captures (gpurun_out/<R>_*, R = argv[1], default r2m)."""
 import csv
 import io
 import os
@@ -32,16 +32,18 @@ def top_stalls(rep, n=12):
     return "\n".join(lines)
 
 
-c5 = os.path.join(G, "r2m_panel_c5.ncu-rep")
-c4 = os.path.join(G, "r2m_panel_c4.ncu-rep")
-print(f"""# Round 2 — ncu captures of the column-sorted panel kernel (C5 and C4)
+R = sys.argv[1] if len(sys.argv) > 1 else "r2m"
+NOTE = sys.argv[2] if len(sys.argv) > 2 else ""
+c5 = os.path.join(G, f"{R}_panel_c5.ncu-rep")
+c4 = os.path.join(G, f"{R}_panel_c4.ncu-rep")
+print(f"""# Round 2 — ncu captures of the column-sorted panel kernel (C5 and C4), {R}
+{NOTE}
 
 Command (bench launch configuration, `scripts/r2_profile.sh`): `python bench.py --workload c5|c4
 --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-parity --no-gather-peak --no-reorder-ref
 --no-cusparse --no-sbfs`, each ncu run after the same command exited 0 without ncu;
 `ncu --set full --clock-control none --import-source on -k regex:spmv_panel_kernel -s 3 -c 1`.
-The launch list of the C5 power step is `r02_launches_c5.csv` (panel kernel 92.9 % of the
-step, normalize 6.9 %, max finish 0.2 %).
+The launch list of the C5 power step is `r02_launches_c5{"_final" if R != "r2m" else ""}.csv`.
 
 ## C5
 
