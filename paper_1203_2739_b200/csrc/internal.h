@@ -158,8 +158,6 @@ struct PnPanel {
     int32_t nrows;     // rows (<= kPnRowsMax)
     int32_t g0;        // first group of the panel (groups of epoch e, step b, warp w: g0 + (e*kPnB + b)*16 + w)
     int32_t ne;        // epochs
-    int32_t pf_col;    // x_lo[pf_col, pf_col + pf_len) is prefetched into L2 at panel start
-    int32_t pf_len;    //   (a slice of the next block's interior columns, SB Eq.(1))
     int32_t split_off; // first entry of this panel in PnArgs::split_first / split_cnt / split_row
     int32_t nslots;    // y slots (virtual rows) of the panel
     int32_t split_n;   // rows of the panel split into virtual rows

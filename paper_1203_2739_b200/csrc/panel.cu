@@ -36,7 +36,9 @@ constexpr int kT = NW * 32;
 constexpr int kDefD = 8;    // steps (groups) in flight per warp, the launch default (8 beat 12 and 16 on C5
                             // by 2.5 % / 1 %, interleaved A/B; equal on C4 and C3)
 constexpr int kPF = 4;    // default: epochs of the group stream prefetched into L2 ahead (with the 8-deep
-                          // ring: 4 beat 2, 3, 5, 6, 8, 12 -- C5 -3.8 %, C4 -2.2 % vs 8, interleaved A/B)
+                          // ring: 4 beat 2, 3, 5, 6, 8, 12 -- C5 -3.8 %, C4 -2.2 % vs 8, interleaved A/B;
+                          // re-checked late round 2 under the power cap: 2 / 3 / 6 vs 4
+                          // = +9 / +1 / 0 %, profiles/r02_ab_stream_prefetch.txt)
 constexpr uint32_t kDeltaMask = (1u << kPnDeltaBits) - 1u;
 
 __device__ __forceinline__ uint64_t pol_evict_first() {
@@ -218,18 +220,6 @@ __global__ void __launch_bounds__(kT, 1) spmv_panel_kernel(const PnArgs A) {
         };
         {
             for (int e = 0; e < PF; ++e) prefetch_epoch(e);
-            // this panel's slice of the next SB block's x(C_k), kept in L2 (evict_last)
-            if (tid == 32 && d.pf_len > 0) {
-                const uint64_t pl = pol_evict_last();
-                // 16-byte aligned start and length (bulk prefetch granularity)
-                const uintptr_t a0 = reinterpret_cast<uintptr_t>(A.x_lo + d.pf_col) & ~uintptr_t(15);
-                const uintptr_t a1 = reinterpret_cast<uintptr_t>(A.x_lo + d.pf_col + d.pf_len) & ~uintptr_t(15);
-                for (uintptr_t a = a0; a < a1; a += 32768) {
-                    const uint32_t n = (uint32_t)(a1 - a < 32768 ? a1 - a : 32768);
-                    asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(a), "r"(n), "l"(pl)
-                                 : "memory");
-                }
-            }
         }
     #pragma unroll
         for (int u = 0; u < kD; u += 4) load4(u);

@@ -104,11 +104,14 @@ void colour_slots(int32_t nr, const std::vector<Ent>& ents, int64_t G, std::vect
 #ifndef SPMV_PN_WPOW
 #define SPMV_PN_WPOW 3
 #endif
+// 8 sweeps x 8 tries (was 2 x 3): predicted y wavefronts per access 4.02 ->
+// 3.79 on C5's geometry, C5 SpMxV -1.0 % in the sustained bench run (-1.5 %
+// under ncu), at ~2x the colouring time (profiles/r02_ab_stream_prefetch.txt)
 #ifndef SPMV_PN_SWEEPS
-#define SPMV_PN_SWEEPS 2
+#define SPMV_PN_SWEEPS 8
 #endif
 #ifndef SPMV_PN_TRIES
-#define SPMV_PN_TRIES 3
+#define SPMV_PN_TRIES 8
 #endif
     int64_t W[34];
     for (int c = 0; c < 34; ++c) {
@@ -666,14 +669,6 @@ bool plan_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col,
         std::vector<int64_t> cut = make_cuts(true);
         if ((int64_t)cut.size() - 1 > np0) cut = make_cuts(false);   // the cap added panels: cut by slots
         int64_t np = (int64_t)cut.size() - 1;
-        // L2 prefetch slice: the interior columns of the range that starts about
-        // one wave after this one (its panels then find x in L2), cut in np pieces
-        int64_t pf0 = 0, pf1 = 0;
-        const size_t ahead = (size_t)std::max<int64_t>(1, (pf_sms + np - 1) / np + 1);
-        if (xcols && k + ahead < xcols->size()) {
-            pf0 = (*xcols)[k + ahead].first;
-            pf1 = (*xcols)[k + ahead].second;
-        }
         for (int64_t p = 0; p < np; ++p) {
             const int64_t a = cut[p], e = cut[p + 1];
             int64_t ps = 0;
@@ -693,16 +688,6 @@ bool plan_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col,
             if (xcols && k < xcols->size()) {
                 const int64_t c0 = (*xcols)[k].first, c1 = (*xcols)[k].second;
                 d.rot = (int32_t)(c0 + (c1 - c0) * p / np);
-            }
-            if (pf1 > pf0) {
-                // 16-byte aligned slice boundaries (the bulk prefetch works in 16-byte units)
-                int64_t s0 = pf0 + (pf1 - pf0) * p / np, s1 = pf0 + (pf1 - pf0) * (p + 1) / np;
-                s0 &= ~int64_t(1);
-                s1 = std::min<int64_t>(s1 & ~int64_t(1), pf1 & ~int64_t(1));
-                if (s1 > s0) {
-                    d.desc.pf_col = (int32_t)s0;
-                    d.desc.pf_len = (int32_t)(s1 - s0);
-                }
             }
             out.push_back(std::move(d));
         }
