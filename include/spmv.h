@@ -254,6 +254,9 @@ typedef struct {
                                      amortization) */
     int64_t far_nonzeros;         /* panel kernel: nonzeros summed in the barrier-free far phase (those
                                      still deferred when a panel's column sweep ends) */
+    int64_t owner_runs;           /* spmv_normalize: > 0 when the column -> row owner map is held as this
+                                     many runs of consecutive rows (no per-column map is read), 0 when it
+                                     is a per-column array */
 } spmv_info_t;
 
 spmv_status_t spmv_get_info(spmv_handle_t h, spmv_info_t* info);

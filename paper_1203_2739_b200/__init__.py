@@ -80,7 +80,8 @@ class spmv_info_t(ctypes.Structure):
                                       "split_kernel", "exchange")] + [
         (k, ctypes.c_int64) for k in ("gather_sectors", "y_local_len", "y_border_begin", "y_border_len",
                                       "deferred", "y_wavefronts_x1000", "exchange_timeouts", "index_bytes")] + [
-        ("debug_violations", ctypes.c_int64 * 3), ("create_s", ctypes.c_double * 6), ("far_nonzeros", ctypes.c_int64)]
+        ("debug_violations", ctypes.c_int64 * 3), ("create_s", ctypes.c_double * 6), ("far_nonzeros", ctypes.c_int64),
+        ("owner_runs", ctypes.c_int64)]
 
     def as_dict(self) -> dict:
         d = {k: getattr(self, k) for k, _ in self._fields_}

@@ -168,7 +168,11 @@ struct spmv_plan_s {
     int32_t* d_rowperm = nullptr;     // ORIGINAL mode: y[i] = y^[row_perm[i]]
     double* d_xhat = nullptr;
     double* d_yhat = nullptr;
-    int32_t* d_owner = nullptr;       // [x_local_len] local col -> local y row
+    int32_t* d_owner = nullptr;       // [x_local_len] local col -> local y row (when not as runs)
+    int64_t owner_runs = 0;           // > 0: the owner map as runs of consecutive rows instead
+    int64_t* d_own_start = nullptr;   // [owner_runs + 1] first local column of each run (last = x_local_len)
+    int32_t* d_own_tgt = nullptr;     // [owner_runs] its local y row
+    int64_t* d_own_tdelta = nullptr;  // [tiles of kNormTileCols] tgt - start of the tile's run, or kNoDelta
     unsigned long long* d_slots = nullptr;
 
     // ---------------- world > 1

@@ -1228,7 +1228,32 @@ spmv_status_t create_impl(int64_t m, int64_t n, int64_t nnz, const int64_t* row_
                 else { outside = 1; owner[l] = 0; }
             }
             if (!outside) {
-                if ((s = upload(h, &h->d_owner, owner.data(), h->x_local_len))) return s;
+                // runs of consecutive rows (A17's owner-aligned layout: one per block's interior
+                // columns and one per owned border slice): the x-update then reads no map per column
+                std::vector<int64_t> rs;
+                std::vector<int32_t> rt;
+                for (int64_t l = 0; l < h->x_local_len; ++l)
+                    if (l == 0 || owner[l] != owner[l - 1] + 1) {
+                        rs.push_back(l);
+                        rt.push_back(owner[l]);
+                        if ((int64_t)rs.size() * kOwnerRunMin > h->x_local_len) break;
+                    }
+                if ((int64_t)rs.size() * kOwnerRunMin <= h->x_local_len) {
+                    h->owner_runs = (int64_t)rs.size();
+                    rs.push_back(h->x_local_len);
+                    const int64_t T = (h->x_local_len + kNormTileCols - 1) / kNormTileCols;
+                    std::vector<int64_t> td(T);
+                    for (int64_t t = 0, r = 0; t < T; ++t) {   // r: run of the tile's first column
+                        const int64_t a = t * kNormTileCols, b = std::min(a + kNormTileCols, h->x_local_len);
+                        while (rs[r + 1] <= a) ++r;
+                        td[t] = rs[r + 1] >= b ? (int64_t)rt[r] - rs[r] : kNoDelta;
+                    }
+                    if ((s = upload(h, &h->d_own_start, rs.data(), rs.size()))) return s;
+                    if ((s = upload(h, &h->d_own_tgt, rt.data(), rt.size()))) return s;
+                    if ((s = upload(h, &h->d_own_tdelta, td.data(), td.size()))) return s;
+                } else if ((s = upload(h, &h->d_owner, owner.data(), h->x_local_len))) {
+                    return s;
+                }
                 h->has_owner = true;
             }
         }
@@ -1599,6 +1624,7 @@ spmv_status_t spmv_get_info(spmv_handle_t h, spmv_info_t* info) {
     info->split_segments = h->n_seg;
     info->n_parts = h->n_parts; info->rank = h->rank; info->world = h->world; info->kind = h->kind;
     info->has_owner_map = h->has_owner ? 1 : 0;
+    info->owner_runs = h->owner_runs;
     info->panels = h->kernel == 7 ? h->pn.panels : 0;
     info->groups = h->kernel == 7 ? h->pn.groups : 0;
     info->far_nonzeros = h->kernel == 7 ? h->pn.far : 0;
@@ -1645,7 +1671,11 @@ spmv_status_t spmv_normalize(spmv_handle_t h, const double* y, const double* m_d
     if (!valid(h) || !y || !m_dev || !x_next) return fail(SPMV_ERR_USAGE, "invalid handle or pointer");
     if (!h->has_owner) return fail(SPMV_ERR_UNSUPPORTED, "no owner-aligned column->row map (A17)");
     DeviceGuard dg(h->device);
-    CUDA_TRY(launch_normalize(y, h->d_owner, m_dev, x_next, h->x_local_len, (cudaStream_t)stream));
+    if (h->owner_runs > 0)
+        CUDA_TRY(launch_normalize_runs(y, h->d_own_tdelta, h->d_own_start, h->d_own_tgt, h->owner_runs, m_dev, x_next,
+                                       h->x_local_len, (cudaStream_t)stream));
+    else
+        CUDA_TRY(launch_normalize(y, h->d_owner, m_dev, x_next, h->x_local_len, (cudaStream_t)stream));
     return SPMV_OK;
 }
 

@@ -19,6 +19,7 @@ constexpr int kTileShort = 1;      // >= 1: every row has <= kShortRow nonzeros;
 constexpr int kTileGeneral = 0;
 constexpr int kShortRow = 32;
 constexpr int kMaxDevices = 64;     // per-device caches (SM count, kernel attributes)
+constexpr int64_t kOwnerRunMin = 64;   // owner map kept as runs when they average >= this many columns
 constexpr int kMaxSlots = 1024;      // max-abs accumulator slots (spread atomics)
 constexpr int kSlotStride = 16;    // 16 x 8 B = 128 B apart
 
@@ -116,6 +117,12 @@ cudaError_t launch_maxabs_finish(const unsigned long long* slots, double* out, c
 // x_next[c] = y[owner[c]] / *m   (power-iteration glue, a9)
 cudaError_t launch_normalize(const double* y, const int32_t* owner, const double* m, double* x_next,
                              int64_t n, cudaStream_t s);
+// the same with the owner map as runs: x_next[l] = y[tgt[r] + l - start[r]], start[r] <= l < start[r+1];
+// tdelta[t] = tgt[r] - start[r] when tile t (kNormTileCols columns) lies in one run r, else kNoDelta
+constexpr int64_t kNormTileCols = 1024;
+constexpr int64_t kNoDelta = INT64_MIN;
+cudaError_t launch_normalize_runs(const double* y, const int64_t* tdelta, const int64_t* start, const int32_t* tgt,
+                                  int64_t runs, const double* m, double* x_next, int64_t n, cudaStream_t s);
 int kernel_num_sms();   // SMs of the current device
 // Eager loading of every SpMxV-path kernel on the current device (per .cu file)
 cudaError_t preload_kernels_misc();

@@ -19,18 +19,29 @@ __global__ void gather_kernel(const double* __restrict__ src, const int32_t* __r
         dst[i] = __ldg(src + idx[i]);
 }
 
-__global__ void maxabs_finish_kernel(const unsigned long long* __restrict__ slots, double* out) {
-    unsigned long long m = 0;
-    for (int i = threadIdx.x; i < kMaxSlots; i += blockDim.x) {
-        const unsigned long long v = slots[i * kSlotStride];
-        m = v > m ? v : m;
-    }
+// One thread per slot (a single load each, then a warp and a CTA fold): the
+// step's serial tail, so it is latency, not bytes (a one-warp loop over the
+// 1,024 slots measured 6.8 us under ncu).
+__global__ void __launch_bounds__(kMaxSlots) maxabs_finish_kernel(const unsigned long long* __restrict__ slots,
+                                                                  double* out) {
+    __shared__ unsigned long long wm[kMaxSlots / 32];
+    unsigned long long m = slots[threadIdx.x * kSlotStride];
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
         const unsigned long long o = __shfl_xor_sync(0xffffffffu, m, off);
         m = o > m ? o : m;
     }
-    if (threadIdx.x == 0) *out = __longlong_as_double((long long)m);
+    if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        m = wm[threadIdx.x];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const unsigned long long o = __shfl_xor_sync(0xffffffffu, m, off);
+            m = o > m ? o : m;
+        }
+        if (threadIdx.x == 0) *out = __longlong_as_double((long long)m);
+    }
 }
 
 // x_next[c] = y[owner[c]] / m, four columns per thread step: one 128-bit load
@@ -52,6 +63,51 @@ __global__ void __launch_bounds__(256) normalize_kernel(const double* __restrict
     }
     for (int64_t c = 4 * n4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n; c += stride)
         x[c] = __ldg(y + owner[c]) / mt;
+}
+
+// The same update with the owner map stored as runs (create: consecutive local
+// columns whose rows are consecutive too, A17's owner-aligned layout: C5 has
+// 128 runs for 64 M columns): x_next[l] = y[tgt[r] + l - start[r]] for the run
+// r holding l.  No 4-byte map per column is read (16 instead of 20 bytes per
+// column of HBM traffic).  Tiles of 1,024 columns; a tile inside one run has its
+// offset tgt[r] - start[r] precomputed at create (tdelta), loaded one tile ahead
+// so the y loads never wait on it; a tile that straddles runs (kNoDelta) finds
+// each column's run by binary search over the (few, L1-resident) run starts.
+constexpr int kNormTile = (int)kNormTileCols;
+__global__ void __launch_bounds__(256) normalize_runs_kernel(const double* __restrict__ y,
+                                                             const int64_t* __restrict__ tdelta,
+                                                             const int64_t* __restrict__ start,
+                                                             const int32_t* __restrict__ tgt, int64_t R,
+                                                             const double* __restrict__ m, double* __restrict__ x,
+                                                             int64_t n) {
+    const double mt = *m;
+    const int64_t T = (n + kNormTile - 1) / kNormTile;
+    int64_t t = blockIdx.x;
+    int64_t dnext = t < T ? __ldg(tdelta + t) : 0;
+    for (; t < T; t += gridDim.x) {
+        const int64_t delta = dnext;
+        if (t + gridDim.x < T) dnext = __ldg(tdelta + t + gridDim.x);
+        const int64_t t0 = t * kNormTile + threadIdx.x;
+        double v[4];
+        if (delta != kNoDelta && t0 + 3 * 256 < n) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) v[k] = __ldg(y + t0 + k * 256 + delta);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) x[t0 + k * 256] = v[k] / mt;
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int64_t l = t0 + k * 256;
+                if (l >= n) break;
+                int64_t lo = 0, hi = R - 1;   // last run with start <= l
+                while (lo < hi) {
+                    const int64_t mid = (lo + hi + 1) >> 1;
+                    if (__ldg(start + mid) <= l) lo = mid; else hi = mid - 1;
+                }
+                x[l] = __ldg(y + __ldg(tgt + lo) + (l - __ldg(start + lo))) / mt;
+            }
+        }
+    }
 }
 
 __global__ void normalize_scalar_kernel(const double* __restrict__ y, const int32_t* __restrict__ owner,
@@ -144,7 +200,7 @@ cudaError_t launch_fold(const double* tin, const int32_t* fptr, const int32_t* f
 }
 
 cudaError_t launch_maxabs_finish(const unsigned long long* slots, double* out, cudaStream_t s) {
-    maxabs_finish_kernel<<<1, 32, 0, s>>>(slots, out);
+    maxabs_finish_kernel<<<1, kMaxSlots, 0, s>>>(slots, out);
     return cudaGetLastError();
 }
 
@@ -159,6 +215,14 @@ cudaError_t launch_normalize(const double* y, const int32_t* owner, const double
     return cudaGetLastError();
 }
 
+cudaError_t launch_normalize_runs(const double* y, const int64_t* tdelta, const int64_t* start, const int32_t* tgt,
+                                  int64_t runs, const double* m, double* x_next, int64_t n, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    normalize_runs_kernel<<<grid_for((n + kNormTile - 1) / kNormTile, 1), 256, 0, s>>>(y, tdelta, start, tgt, runs,
+                                                                                       m, x_next, n);
+    return cudaGetLastError();
+}
+
 
 // Loads this file's kernels now (cudaFuncGetAttributes forces the lazy loader):
 // a kernel first launched while a peer rank's kernel spins on an exchange flag
@@ -167,6 +231,7 @@ cudaError_t launch_normalize(const double* y, const int32_t* owner, const double
 cudaError_t preload_kernels_misc() {
     cudaFuncAttributes fa;
     for (const void* k : {(const void*)gather_kernel, (const void*)maxabs_finish_kernel, (const void*)normalize_kernel,
+                          (const void*)normalize_runs_kernel,
                           (const void*)normalize_scalar_kernel, (const void*)fold_kernel}) {
         const cudaError_t e = cudaFuncGetAttributes(&fa, k);
         if (e != cudaSuccess) return e;

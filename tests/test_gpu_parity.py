@@ -2,6 +2,8 @@
 element by element on the same seeded inputs (north_star tolerance
 |y - y_ref| <= 1e-12 * sum_j |a_ij x_j|; integer/dyadic variants and all
 index work bit-exact)."""
+import dataclasses
+
 import numpy as np
 import pytest
 
@@ -209,7 +211,7 @@ def _c5_like(seed=3):
     return synth.make("_c5like_pi", scramble=0, seed=seed)
 
 
-def _teacher_forced(p, opts, steps, split=False, expect_kernel=None):
+def _teacher_forced(p, opts, steps, split=False, expect_kernel=None, expect_runs=None):
     """Teacher-forced power iteration: at every step the
     oracle recomputes A x_t (or the split sum) from the GPU's own x_t and
     checks y_t within the north_star tolerance; m_t must equal the oracle's
@@ -220,6 +222,8 @@ def _teacher_forced(p, opts, steps, split=False, expect_kernel=None):
     assert info["has_owner_map"] == 1
     if expect_kernel is not None:
         assert (info["split_kernel"] if split else info["kernel"]) == expect_kernel
+    if expect_runs is not None:
+        assert info["owner_runs"] == expect_runs
     x = p.x()
     xh = torch.from_numpy(oracle.permute_x(p.col_perm, x) if p.col_perm is not None else x.copy()).cuda()
     yh = torch.empty(p.m, dtype=torch.float64, device="cuda")
@@ -268,6 +272,22 @@ def test_power_iteration_panel_c4_virtual_rows():
     p = synth.make("c4s")
     assert int(np.diff(p.row_ptr).max()) > 32 * 32   # some rows get > 32 virtual rows (warp fold)
     _teacher_forced(p, panel(2000), 4, expect_kernel=7)
+
+
+def test_power_iteration_owner_map_forms():
+    """The x-update's two owner-map forms (a9): A17's owner-aligned SB layout
+    held as runs (c5s: one run per block's interior columns and one per owned
+    border slice; c4s: identity, one run), and a per-column array when the
+    runs are short (independent random row and column permutations)."""
+    p = synth.make("c5s")
+    K = p.blocks["K"]
+    _teacher_forced(p, None, 3, expect_runs=2 * K)
+    q = synth.make("c4s")
+    _teacher_forced(q, None, 2, expect_runs=1)
+    rng = np.random.default_rng(11)
+    q = dataclasses.replace(q, row_perm=rng.permutation(q.m).astype(np.int32),
+                            col_perm=rng.permutation(q.n).astype(np.int32))
+    _teacher_forced(q, None, 3, expect_runs=0)
 
 
 def test_power_iteration_split_fused_maxabs():
