@@ -441,8 +441,15 @@ cudaError_t launch_panel_t(const PnArgs& a, cudaStream_t s, int64_t smem) {
         const int smax = (int)kPnSmemMax;
         for (const void* k : {(const void*)spmv_panel_kernel<false, false, CHK>, (const void*)spmv_panel_kernel<false, true, CHK>,
                               (const void*)spmv_panel_kernel<true, false, CHK>, (const void*)spmv_panel_kernel<true, true, CHK>})
+        {
             if ((r = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smax)) != cudaSuccess)
                 return r;
+#ifdef SPMV_PN_CARVEOUT   // build-time experiment: shared-memory carveout hint (% of the maximum)
+            if ((r = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, SPMV_PN_CARVEOUT)) !=
+                cudaSuccess)
+                return r;
+#endif
+        }
         ready[di].store(1, std::memory_order_release);
     }
     const bool xs = a.x_split != INT32_MAX;
