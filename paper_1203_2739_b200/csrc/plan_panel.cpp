@@ -104,14 +104,20 @@ void colour_slots(int32_t nr, const std::vector<Ent>& ents, int64_t G, std::vect
 #ifndef SPMV_PN_WPOW
 #define SPMV_PN_WPOW 3
 #endif
-// 8 sweeps x 8 tries (was 2 x 3): predicted y wavefronts per access 4.02 ->
-// 3.79 on C5's geometry, C5 SpMxV -1.0 % in the sustained bench run (-1.5 %
-// under ncu), at ~2x the colouring time (profiles/r02_ab_stream_prefetch.txt)
+// Round 2, first form: 8 sweeps x 8 random (bank, partner) tries per row --
+// predicted y wavefronts per access 4.02 -> 3.79 on C5's geometry (C5 SpMxV
+// -1.0 % sustained) but three quarters of spmv_create's planning time.  Now
+// directed (below): 4 sweeps x 2 best banks x 3 partners reach 3.75 (C4: 3.42
+// against 3.45) in 0.3x the colouring time; 8 such sweeps give 3.70, the
+// plateau 32 sweeps of the random form reached (3.695).
 #ifndef SPMV_PN_SWEEPS
-#define SPMV_PN_SWEEPS 8
+#define SPMV_PN_SWEEPS 4
 #endif
 #ifndef SPMV_PN_TRIES
-#define SPMV_PN_TRIES 8
+#define SPMV_PN_TRIES 3
+#endif
+#ifndef SPMV_PN_CBANKS
+#define SPMV_PN_CBANKS 2
 #endif
     int64_t W[34];
     for (int c = 0; c < 34; ++c) {
@@ -144,26 +150,57 @@ void colour_slots(int32_t nr, const std::vector<Ent>& ents, int64_t G, std::vect
             cnt[g * 16 + b2]++;
         }
     };
-    constexpr int kSweeps = SPMV_PN_SWEEPS, kTries = SPMV_PN_TRIES;
+    // Directed swaps: one pass over r's groups gives the cost change of moving
+    // r to each of the 16 banks (add[b]) and of leaving its own (rem); the
+    // kPnColBanks best target banks are tried with kPnColTries random partners
+    // each, whose own move back to r's bank is evaluated the same way.  These
+    // estimates ignore groups holding both rows (their moves cancel there), so
+    // the chosen swap is re-evaluated exactly (group marks) before it is applied.
+    int64_t DA[34], DR[34];   // DA[c] = W[c+1] - W[c] (c <= 32), DR[c] = W[c-1] - W[c] (c >= 1)
+    for (int c = 0; c < 33; ++c) DA[c] = W[c + 1] - W[c];
+    for (int c = 1; c < 34; ++c) DR[c] = W[c - 1] - W[c];
+    DA[33] = 0;
+    DR[0] = 0;
+    constexpr int kSweeps = SPMV_PN_SWEEPS, kTries = SPMV_PN_TRIES, kBanks = SPMV_PN_CBANKS;
     for (int sw = 0; sw < kSweeps; ++sw)
         for (int32_t i = 0; i < nr; ++i) {
             const int32_t r = (int32_t)((i * 40503ull + sw * 7919ull) % (uint64_t)nr);   // fixed visiting order
             if (rg_ptr[r + 1] == rg_ptr[r]) continue;
             const int b1 = bank[r];
+            int64_t add[16] = {0}, rem = 0;
+            for (int32_t q = rg_ptr[r]; q < rg_ptr[r + 1]; ++q) {
+                const uint8_t* c = &cnt[(int64_t)rg[q] * 16];
+                for (int b = 0; b < 16; ++b) add[b] += DA[c[b]];
+                rem += DR[c[b1]];
+            }
+            add[b1] = INT64_MAX;
             int64_t best = 0;
             int32_t bs = -1;
-            for (int k = 0; k < kTries; ++k) {
-                const int b2 = (b1 + 1 + (int)(rnd() % 15)) & 15;
+            for (int kb = 0; kb < kBanks; ++kb) {
+                int b2 = 0;
+                for (int b = 1; b < 16; ++b)
+                    if (add[b] < add[b2]) b2 = b;
+                if (add[b2] == INT64_MAX) break;
+                const int64_t d1 = rem + add[b2];
+                add[b2] = INT64_MAX;
                 if (of_bank[b2].empty()) continue;
-                const int32_t s2 = of_bank[b2][rnd() % of_bank[b2].size()];
-                mark_groups(s2);
-                int64_t d = gain_move(r, b1, b2);
-                mark_groups(r);
-                d += gain_move(s2, b2, b1);
-                if (d < best) { best = d; bs = s2; }
+                for (int k = 0; k < kTries; ++k) {
+                    const int32_t s2 = of_bank[b2][rnd() % of_bank[b2].size()];
+                    int64_t d = d1;
+                    for (int32_t q = rg_ptr[s2]; q < rg_ptr[s2 + 1]; ++q) {
+                        const uint8_t* c = &cnt[(int64_t)rg[q] * 16];
+                        d += DA[c[b1]] + DR[c[b2]];
+                    }
+                    if (d < best) { best = d; bs = s2; }
+                }
             }
             if (bs >= 0) {
                 const int b2 = bank[bs];
+                mark_groups(bs);
+                int64_t d = gain_move(r, b1, b2);
+                mark_groups(r);
+                d += gain_move(bs, b2, b1);
+                if (d >= 0) continue;
                 apply_move(r, b1, b2);
                 apply_move(bs, b2, b1);
                 std::swap(of_bank[b1][pos[r]], of_bank[b2][pos[bs]]);
@@ -380,7 +417,23 @@ void build_panel(const std::vector<int64_t>& rp, const std::vector<int32_t>& col
                                               : (uint64_t)(c >= P.rot ? c - P.rot : c - P.rot + x_split);
             keys[i] = (rel << 32) | (uint64_t)i;
         }
-    std::sort(keys.begin(), keys.end());
+    if (n > 1) {
+        // keys are unique and were built in ascending entry id: a stable LSD
+        // radix sort on the upper 32 bits (3 passes of 11 bits) is the full
+        // sort (std::sort here was a fifth of the planning time)
+        std::vector<uint64_t> tmp(n);
+        std::vector<int64_t> h(2049);
+        uint64_t *src = keys.data(), *dst = tmp.data();
+        for (int sh = 32; sh < 64; sh += 11) {
+            std::fill(h.begin(), h.end(), 0);
+            for (int64_t i = 0; i < n; ++i) h[((src[i] >> sh) & 2047) + 1]++;
+            if (h[((src[0] >> sh) & 2047) + 1] == n) continue;   // one bucket: the pass is the identity
+            for (int b = 0; b < 2048; ++b) h[b + 1] += h[b];
+            for (int64_t i = 0; i < n; ++i) dst[h[(src[i] >> sh) & 2047]++] = src[i];
+            std::swap(src, dst);
+        }
+        if (src != keys.data()) keys.swap(tmp);
+    }
     P.entries = n;
     // Sweep order; the far stream (the barrier-free phase after the epochs,
     // panel.cu) takes what is still deferred when the sweep ends (below).
