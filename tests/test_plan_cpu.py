@@ -179,3 +179,17 @@ def test_far_stream_heavy_column_runs():
     val = rng.uniform(-1, 1, len(col))
     st = T.pn_plan_check(m, n, rp, col, val, None, 1024)
     assert st["entries"] == len(col) and st["pads_drain"] == 0, st
+
+
+def test_bank_colouring_lowers_predicted_y_wavefronts():
+    """The y-slot colouring (plan_panel.cpp colour_slots, directed bank swaps):
+    on C5-like panels (12-20 nonzeros per row, columns random inside the
+    block) the predicted wavefronts of a warp-wide 64-bit y access must fall
+    well below the slot = row layout's (4.84 -> 3.75 at the
+    production panel size); both are at least 2 (two half-warps)."""
+    p = _c5_like()
+    st = T.pn_plan_check(p.m, p.n, p.row_ptr, p.col, p.val, p.blocks, 16384)
+    nat, colr = st["y_wavefronts_natural"], st["y_wavefronts_coloured"]
+    assert 2.0 <= colr < nat
+    assert colr <= nat - 0.8, (nat, colr)
+    assert colr <= 3.9, colr
